@@ -1,0 +1,312 @@
+"""bench.py — J.v residual evaluations per second on the 1M-cell config (BASELINE configs[1]),
+achieved HBM GB/s against the measured B200 peak, the end-to-end J.v through the C-ABI
+with host buffers, the device JFNK solve time at 1M cells, and the reference CPU solver
+timed on this box's host cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2] [--no-jfnk] [--no-cpu]
+
+One step = one J.v = (R(u + eps v) - R(u)) / eps over the whole mesh (inputs resident in
+HBM).  The J.v working set (~0.45-0.65 GB at 1M cells) exceeds the 126 MB L2, so no L2
+flush is needed between steps.  Multi-GPU (torchrun): the path does not shard with parity
+ — N independent replicas, value = total J.v/s over ranks, max-over-ranks
+device time ("replicas only").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "J·v residual evals/s + achieved HBM GB/s; JFNK solve time at 1M cells"
+UNIT = "J·v/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_jv(case, mesh, u, r_u, v, seconds_budget=20.0, threads=None):
+    """The reference's own jacobian_vector_product (oracle/_ref) on host threads; falls
+    back to the C restatement when the reference build is absent."""
+    from oracle.bind import OracleCase, RefCase, ref_available
+    threads = threads or min(os.cpu_count() or 1, 32)
+    if ref_available():
+        rc = RefCase(mesh, case.physics)
+        rc.set_time(1.0)
+        t1 = rc.time_jv(u, r_u, v, 1, 1)  # one J.v on one core, to size the sample
+        reps = max(1, int(seconds_budget / max(t1, 1e-6) / 2))
+        reps = min(reps, 8)
+        secs = rc.time_jv(u, r_u, v, reps, threads)
+        total = reps * threads
+        return {"value": total / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"{total} J.v ({threads} threads x {reps}) of the reference's jacobian_vector_product "
+                          f"on the full {mesh.n_cells}-cell mesh; single-core J.v {t1:.3f} s",
+                "single_core_jv_s": t1}
+    oc = OracleCase(mesh, case.physics)
+    oc.set_time(1.0)
+    t1 = oc.time_jv(u, r_u, v, 1)
+    reps = max(1, min(8, int(seconds_budget / max(t1, 1e-6))))
+    secs = oc.time_jv(u, r_u, v, reps)
+    return {"value": reps / secs, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{reps} J.v of the C restatement (oracle/sfv_oracle.c) on the full mesh, 1 core",
+            "single_core_jv_s": t1}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from paper_2502_17217_b200 import cases
+    from paper_2502_17217_b200.solver import box_mesh  # host-only mesh generator
+    case = cases.config(args.config)
+    mesh = case.mesh()
+    u, v = cases.jv_inputs(mesh, extent=case.mesh_args.get("extents"))
+    from oracle.bind import RefCase, OracleCase, ref_available
+    Cls = RefCase if ref_available() else OracleCase
+    ref = Cls(mesh, case.physics)
+    ref.set_time(1.0)
+    r_u = ref.residual(u)
+    threads = min(os.cpu_count() or 1, 32)
+    step_times = []
+    for i in range(args.warmup + args.steps):
+        if ref_available():
+            dt = ref.time_jv(u, r_u, v, 1, threads)
+        else:
+            dt = ref.time_jv(u, r_u, v, 1)
+        if i >= args.warmup:
+            step_times.append(dt)
+    per_step = (threads if ref_available() else 1)
+    total_t = sum(step_times)
+    value = per_step * len(step_times) / total_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_t / len(step_times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {case.notes}", "cells": mesh.n_cells, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": per_step,
+                         "kind": "reference" if ref_available() else "port",
+                         "sample": f"each step = {per_step} concurrent J.v of the full {mesh.n_cells}-cell mesh"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2502_17217_b200 import cases
+    from paper_2502_17217_b200 import solver as sv
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    case = cases.config(args.config)
+    t_setup = time.time()
+    mesh = case.mesh()
+    ev = sv.ResidualEvaluator(mesh, case.physics)
+    ev.set_time(1.0)
+    t_setup = time.time() - t_setup
+    u_h, v_h = cases.jv_inputs(mesh, extent=case.mesh_args.get("extents"))
+    u = sv.to_device(u_h)
+    v = sv.to_device(v_h)
+    r_u = ev.residual(u)
+    out = ev.empty()
+    L, h = ev.L, ev.h
+    stream = torch.cuda.current_stream()
+
+    def jv_step():
+        rc = L.sfv_jv_async(h, u.data_ptr(), r_u.data_ptr(), v.data_ptr(), out.data_ptr())
+        if rc:
+            ev._check(rc)
+
+    for _ in range(args.warmup):
+        jv_step()
+    ev._check(L.sfv_check_errors(h, None))
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = ev.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.05)
+        e0.record(stream)
+        for _ in range(args.steps):
+            jv_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = ev.launch_count - l0
+    ms = e0.elapsed_time(e1)
+    ev._check(L.sfv_check_errors(h, None))
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        if ws > 1:
+            torch.distributed.barrier()
+    ms_per = ms / args.steps
+    value = ws * args.steps / (ms / 1e3)
+    peak, peak_kind = _peaks()
+    jv_bytes = ev.jv_bytes
+    achieved = jv_bytes / (ms_per / 1e3) / 1e9
+
+    # end to end through the C-ABI with pinned host buffers: H2D u, r_u, v; J.v; D2H out
+    n = ev.n
+    hu = torch.from_numpy(u_h).pin_memory()
+    hr = r_u.cpu().pin_memory()
+    hv = torch.from_numpy(v_h).pin_memory()
+    ho = torch.empty(n, dtype=torch.float64).pin_memory()
+    import ctypes as C
+    dp = C.POINTER(C.c_double)
+
+    def e2e_step():
+        rc = L.sfv_jv_host(h, C.cast(hu.data_ptr(), dp), C.cast(hr.data_ptr(), dp), C.cast(hv.data_ptr(), dp),
+                           C.cast(ho.data_ptr(), dp), None)
+        ev._check(rc)
+
+    for _ in range(2):
+        e2e_step()
+    e2e_n = max(3, min(args.steps, 20))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_n):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_n
+    if ws > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_jv")
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {case.notes}", "cells": mesh.n_cells, "faces": mesh.n_faces,
+                   "parallelism": "replicas only" if ws > 1 else "single GPU",
+                   "l2": "J.v working set > 126 MB L2 (no flush needed)", "setup_s": round(t_setup, 2)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_kind": peak_kind, "traffic": traffic, "algorithmic_bytes_per_jv": jv_bytes,
+                     "kernel": "J.v (eps reduction + gradient pass + flux pass)"},
+        "cell_dof_per_s": 3 * mesh.n_cells * value,
+        "e2e": {"value": ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 3 * 8 * n, "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_jfnk:
+        f0 = case.initial_field(mesh)
+        cfg = case.solver()
+        f, reps, wall = sv.run_steps_host(ev, f0, cfg, 1 if case.n_steps == 1 else min(case.n_steps, args.jfnk_steps))
+        s = [r.summary() for r in reps]
+        line["jfnk"] = {"solve_seconds": wall, "steps": len(s), "status": [x["status"] for x in s],
+                        "newton": [x["outer_iters"] for x in s], "krylov_per_newton": [x["krylov_per_newton"] for x in s],
+                        "final_rel_residual": [x["final_residual"] / x["initial_residual"] for x in s],
+                        "path": "sfv_run_steps_host (host buffers; includes preconditioner setup)"}
+    if rank == 0 and not args.no_cpu and ws == 1:
+        try:
+            line["cpu_baseline"] = cpu_reference_jv(case, mesh, u_h, r_u.cpu().numpy(), v_h)
+        except Exception as exc:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "error": str(exc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-jfnk", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--jfnk-steps", type=int, default=1)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

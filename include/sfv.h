@@ -1,0 +1,124 @@
+/* sfv.h — C-ABI of the B200-native JFNK hot path (libsfv.so).
+ *
+ * Plain pointers and sizes only.  "_dev" arguments are CUDA device pointers of
+ * 3*n_cells doubles in the reference's interleaved layout [3c + k]
+ * (/root/reference/proj/src/fields.cpp:20-25); the *_host variants take host
+ * buffers and do the H2D/D2H copies themselves.  All calls are stream-ordered on
+ * the context's stream (sfv_set_stream), default the legacy default stream.
+ *
+ * Each entry point replaces one reference interface (file:line under
+ * /root/reference/proj):
+ *
+ *   sfv_mesh_box            <- generate_box_hex + distort_mesh   include/solidfv/mesh.hpp:77-86
+ *   sfv_create              <- compute_geometry + ResidualEvaluator ctor
+ *                                                                mesh.hpp:89, discretisation.hpp:51-52
+ *   sfv_set_time            <- ResidualEvaluator::set_time       discretisation.hpp:59
+ *   sfv_set_history         <- ResidualEvaluator::set_history    discretisation.hpp:63
+ *   sfv_residual            <- ResidualEvaluator::residual       discretisation.hpp:55
+ *   sfv_stabilisation       <- ResidualEvaluator::stabilisation  discretisation.hpp:57
+ *   sfv_jv                  <- jacobian_vector_product           nonlinear.hpp:74-77
+ *   sfv_precond_create      <- assemble_approximate_jacobian + make_preconditioner
+ *                                                                discretisation.hpp:98, nonlinear.hpp:122
+ *   sfv_precond_apply       <- Preconditioner::solve             linalg.hpp:55-59
+ *   sfv_gmres_jv            <- gmres_solve(op = J.v at u)        linalg.hpp:94-97
+ *   sfv_jfnk_solve          <- jfnk_solve                        nonlinear.hpp:96-97
+ *   sfv_run_steps           <- run_steps                         nonlinear.hpp:117-118
+ *
+ * Errors: every call returns SFV_OK or one SFV_ERR_* code (include/sfv_case.h), one
+ * per solidfv exception type; *cell receives the offending cell where the reference
+ * exception carries one (errors.hpp:18-37).  Non-convergence is a status in
+ * sfv_solve_report, never an error, as in the reference.
+ */
+#ifndef SFV_H
+#define SFV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "sfv_case.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sfv_mesh sfv_mesh;
+typedef struct sfv_ctx sfv_ctx;
+
+/* ---- mesh generators (host) ---- */
+sfv_mesh* sfv_mesh_box(const double extents[3], const int divisions[3], const int patch_kinds[6],
+                       double distort_factor, uint64_t seed, char* err, int errlen);
+sfv_mesh* sfv_mesh_kuhn_tets(const double extents[3], int n, const int patch_kinds[6], uint64_t perm_seed,
+                             int permute, int rcm, char* err, int errlen);
+/* counts = {n_points, n_faces, n_face_points, n_cells, n_internal, n_patches} */
+void sfv_mesh_counts(const sfv_mesh* m, int counts[6]);
+void sfv_mesh_export(const sfv_mesh* m, double* points, int* face_offsets, int* face_points, int* owner,
+                     int* neighbour, int* patch_kind, int* patch_start, int* patch_count);
+void sfv_mesh_free(sfv_mesh* m);
+
+/* ---- evaluator context ---- */
+sfv_ctx* sfv_create(const sfv_mesh_desc* mesh, const sfv_physics* phys, char* err, int errlen);
+void sfv_destroy(sfv_ctx* ctx);
+int sfv_set_stream(sfv_ctx* ctx, void* cuda_stream);
+int sfv_n_cells(const sfv_ctx* ctx);
+const char* sfv_last_error(const sfv_ctx* ctx);
+/* number of device kernels this context has launched so far */
+long long sfv_launch_count(const sfv_ctx* ctx);
+/* bytes of device memory held by the context */
+size_t sfv_device_bytes(const sfv_ctx* ctx);
+/* compulsory HBM bytes of one J.v (SURVEY.md §8d byte model) */
+double sfv_jv_bytes(const sfv_ctx* ctx);
+
+/* host copies of the geometry, same layout as the oracle's orc_geometry */
+int sfv_geometry(const sfv_ctx* ctx, double* volume, double* centroid, double* face_centroid, double* area,
+                 double* d, double* d_mag, double* w, double* delta, double* g_inv, signed char* g_singular,
+                 int* cf_offsets, int* cf_faces, double* ls_vec);
+
+/* compute_geometry on the host only (no device needed) */
+int sfv_mesh_geometry(const sfv_mesh_desc* mesh, double* volume, double* centroid, double* face_centroid,
+                      double* area, double* d, double* d_mag, double* w, double* delta, double* g_inv,
+                      signed char* g_singular, int* cf_offsets, int* cf_faces, double* ls_vec, char* err,
+                      int errlen);
+
+int sfv_set_time(sfv_ctx* ctx, double t);
+int sfv_set_history(sfv_ctx* ctx, const double* u_old_dev, const double* u_old_old_dev, const double* v_old_dev,
+                    const double* v_old_old_dev);
+
+int sfv_residual(sfv_ctx* ctx, const double* u_dev, double* r_dev, int* cell);
+int sfv_stabilisation(sfv_ctx* ctx, const double* u_dev, double* r_dev, int* cell);
+/* cell_gradients (discretisation.hpp:29-30): G_dev is 9*n_cells, SoA [(3i+j)*n_cells + c] */
+int sfv_gradients(sfv_ctx* ctx, const double* u_dev, double* G_dev, int* cell);
+int sfv_jv(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* v_dev, double* out_dev,
+           int* cell);
+/* J.v with a caller-supplied eps (parity harness: isolates the kernel from the norm
+ * reduction order); eps = 0 returns zeros */
+int sfv_jv_eps(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* v_dev, double eps,
+               double* out_dev, int* cell);
+/* Asynchronous J.v for throughput runs: no host synchronisation, errors accumulate
+ * on the device until sfv_check_errors. */
+int sfv_jv_async(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* v_dev, double* out_dev);
+int sfv_check_errors(sfv_ctx* ctx, int* cell);
+
+/* host-buffer conveniences (copies inside the call) */
+int sfv_residual_host(sfv_ctx* ctx, const double* u, double* r, int* cell);
+int sfv_jv_host(sfv_ctx* ctx, const double* u, const double* r_u, const double* v, double* out, int* cell);
+
+int sfv_precond_create(sfv_ctx* ctx, int kind);
+int sfv_precond_apply(sfv_ctx* ctx, const double* r_dev, double* z_dev);
+/* preconditioner facts: {kind_resolved, n_levels_fwd, n_levels_bwd, nnz_L, nnz_U} */
+int sfv_precond_info(const sfv_ctx* ctx, int info[5]);
+
+int sfv_gmres_jv(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* b_dev, double* x_dev,
+                 int restart, double rel_reduction, int max_iters, int* iters, int* status, double* rel_residual);
+int sfv_jfnk_solve(sfv_ctx* ctx, double* u_dev, const sfv_solver_cfg* cfg, sfv_solve_report* report);
+/* field_dev: 6 consecutive device arrays of 3*n_cells doubles:
+ * u, u_old, u_old_old, v_old, v_old_old, a_old (VectorField, fields.hpp:29-42) */
+int sfv_run_steps(sfv_ctx* ctx, double* field_dev, const sfv_solver_cfg* cfg, int n_steps,
+                  sfv_solve_report* reports, int cap, int* n_reports, double* wall_seconds);
+int sfv_run_steps_host(sfv_ctx* ctx, double* field, const sfv_solver_cfg* cfg, int n_steps,
+                       sfv_solve_report* reports, int cap, int* n_reports, double* wall_seconds);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFV_H */

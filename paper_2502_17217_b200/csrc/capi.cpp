@@ -1,0 +1,1075 @@
+// capi.cpp — libsfv.so: context, device layout, preconditioner setup and the
+// device-resident GMRES / JFNK / stepping drivers behind the C-ABI of include/sfv.h.
+//
+// Control flow restates the reference line for line (cited per function); all vector
+// work stays on the device, and the host sees only the scalars the reference's control
+// decisions need (norms, Hessenberg columns) — one small D2H per Arnoldi step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device.h"
+#include "host_mesh.h"
+#include "precond_host.h"
+#include "sfv.h"
+
+using namespace sfv;
+
+namespace {
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    bool alloc(size_t count) {
+        release();
+        n = count;
+        if (count == 0) return true;
+        return cudaMalloc(&p, sizeof(T) * count) == cudaSuccess;
+    }
+    bool upload(const std::vector<T>& h) {
+        if (!alloc(h.size())) return false;
+        return h.empty() || cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+    size_t bytes() const { return sizeof(T) * n; }
+};
+
+struct Status {  // pinned host mirror of the device scalars read per control decision
+    ErrWords err;
+    double h[72];
+};
+
+struct TriDev {
+    DevBuf<int> order, rp, col;
+    DevBuf<double> val, diag;
+    DevTri view;
+    int n_levels = 0;
+    size_t nnz = 0;
+    bool upload(const TriSchedule& t, int n_rows) {
+        bool ok = order.upload(t.order) && rp.upload(t.rp) && col.upload(t.col) && val.upload(t.val) &&
+                  diag.upload(t.diag);
+        view.n = t.n_pos;
+        view.n_rows = n_rows;
+        view.n_levels = t.n_levels;
+        view.order = order.p;
+        view.rp = rp.p;
+        view.col = col.p;
+        view.val = val.p;
+        view.diag = diag.p;
+        n_levels = t.n_levels;
+        nnz = t.col.size();
+        return ok;
+    }
+};
+
+struct SfvError {
+    int code;
+    int cell;
+    std::string msg;
+};
+
+}  // namespace
+
+struct sfv_mesh {
+    HostMesh m;
+};
+
+struct sfv_ctx {
+    HostMesh mesh;
+    HostGeometry geom;
+    int nc = 0, n = 0;
+    int singular_cell = -1;
+    DevMesh dm;
+    Physics ph{};
+    PatchTable pt{};
+    std::vector<double> bc_raw;  // per patch, unscaled
+    std::vector<int> bc_ramp;
+    double time = 0.0;
+    cudaStream_t stream = nullptr;
+    // owned layout buffers
+    DevBuf<int> slot_face, slot_other;
+    DevBuf<double> slot_ls, gam, del, dmag, w, volume;
+    // scratch
+    DevBuf<double> grad, red, scal;  // scal: [0]=eps [1]=u_norm [2..] misc
+    DevBuf<unsigned> counter;
+    DevBuf<ErrWords> err;
+    Status* st = nullptr;  // pinned
+    History hist{};
+    DevBuf<double> hist_own;  // zero history when none supplied
+    // preconditioner
+    int pc_kind = SFV_PRECOND_NONE;
+    int pc_ncomp = 1;
+    TriDev L[3], U[3];
+    DevBuf<double> ily;  // forward-sweep scratch
+    int tri_grid = 0;
+    int tri_sleep = 0;
+    DevBuf<double> dense_w[3];
+    DevBuf<int> dense_perm[3];
+    // krylov workspace
+    DevBuf<double> V, wv, rv, tv, xv, bv, hdev, ydev, ucand, rcand, uscratch, rscratch, dzero;
+    int v_cap = 0;
+    long long launches = 0;
+    SfvError last{0, -1, ""};
+
+    int fail(int code, int cell, const std::string& msg) {
+        last = {code, cell, msg};
+        return code;
+    }
+    int cuda_check(const char* where) {
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(SFV_ERR_CUDA, -1, std::string(where) + ": " + cudaGetErrorString(e));
+        return SFV_OK;
+    }
+};
+
+namespace {
+
+constexpr int kNone = 0x7f7f7f7f;
+
+void update_patch_values(sfv_ctx* c) {
+    // config-built BC: ramp ? v * t : v (io.cpp:278-279)
+    for (int p = 0; p < c->pt.n; ++p)
+        for (int k = 0; k < 3; ++k)
+            c->pt.value[p][k] = c->bc_ramp[p] ? c->bc_raw[3 * p + k] * c->time : c->bc_raw[3 * p + k];
+}
+
+std::string build_layout(sfv_ctx* c) {
+    const HostMesh& m = c->mesh;
+    const HostGeometry& g = c->geom;
+    const int nc = m.n_cells, nf = m.n_faces();
+    int slots = 0;
+    for (int i = 0; i < nc; ++i) slots = std::max(slots, m.cf_off[i + 1] - m.cf_off[i]);
+    if (slots > kMaxSlots) return "mesh: cells with more than 8 faces are not supported by the device layout";
+    std::vector<int> sf(static_cast<size_t>(slots) * nc, -1), so(static_cast<size_t>(slots) * nc, -1);
+    std::vector<double> sl(static_cast<size_t>(3) * slots * nc, 0.0);
+    for (int i = 0; i < nc; ++i) {
+        int s = 0;
+        for (int q = m.cf_off[i]; q < m.cf_off[i + 1]; ++q, ++s) {
+            const int f = m.cf[q];
+            const size_t si = static_cast<size_t>(s) * nc + i;
+            const bool nb = f < m.n_internal && m.neighbour[f] == i;
+            sf[si] = f | (nb ? static_cast<int>(0x80000000u) : 0);
+            so[si] = f < m.n_internal ? (nb ? m.owner[f] : m.neighbour[f]) : -(2 + m.face_patch[f]);
+            sl[(3 * static_cast<size_t>(s)) * nc + i] = g.ls[q].x;
+            sl[(3 * static_cast<size_t>(s) + 1) * nc + i] = g.ls[q].y;
+            sl[(3 * static_cast<size_t>(s) + 2) * nc + i] = g.ls[q].z;
+        }
+    }
+    std::vector<double> gm(3 * static_cast<size_t>(nf)), de(3 * static_cast<size_t>(nf)), dmg(nf), ww(nf);
+    for (int f = 0; f < nf; ++f) {
+        gm[f] = g.area[f].x;
+        gm[nf + f] = g.area[f].y;
+        gm[2 * static_cast<size_t>(nf) + f] = g.area[f].z;
+        de[f] = g.delta[f].x;
+        de[nf + f] = g.delta[f].y;
+        de[2 * static_cast<size_t>(nf) + f] = g.delta[f].z;
+        dmg[f] = g.d_mag[f];
+        ww[f] = g.w[f];
+    }
+    if (!c->slot_face.upload(sf) || !c->slot_other.upload(so) || !c->slot_ls.upload(sl) || !c->gam.upload(gm) ||
+        !c->del.upload(de) || !c->dmag.upload(dmg) || !c->w.upload(ww))
+        return "cuda: out of device memory for the mesh layout";
+    if (c->ph.transient && !c->volume.upload(g.volume)) return "cuda: out of device memory";
+    DevMesh& d = c->dm;
+    d.nc = nc;
+    d.nf = nf;
+    d.nint = m.n_internal;
+    d.slots = slots;
+    d.slot_face = c->slot_face.p;
+    d.slot_other = c->slot_other.p;
+    d.slot_ls = c->slot_ls.p;
+    d.gam = c->gam.p;
+    d.del = c->del.p;
+    d.dmag = c->dmag.p;
+    d.w = c->w.p;
+    d.volume = c->volume.p;
+    return "";
+}
+
+void reset_err(sfv_ctx* c) { cudaMemsetAsync(c->err.p, 0x7f, sizeof(ErrWords), c->stream); }
+
+// read the error words (and optionally k doubles from hdev) in one D2H + sync
+int fetch(sfv_ctx* c, int k) {
+    cudaMemcpyAsync(&c->st->err, c->err.p, sizeof(ErrWords), cudaMemcpyDeviceToHost, c->stream);
+    if (k > 0) cudaMemcpyAsync(c->st->h, c->hdev.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream);
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return c->fail(SFV_ERR_CUDA, -1, std::string("cuda: ") + cudaGetErrorString(e));
+    return SFV_OK;
+}
+
+// Map device error words to the reference's exception, in the order the reference
+// would raise them (stress loop, then face loop, then the NaN scan).
+int decode_residual_errors(sfv_ctx* c, bool jv) {
+    const ErrWords& e = c->st->err;
+    if (e.inverted_cell != kNone)
+        return jv ? c->fail(SFV_ERR_JVP_NAN, -1, "jvp: kinematics: det F <= 0")
+                  : c->fail(SFV_ERR_INVERTED_ELEMENT, e.inverted_cell, "kinematics: det F <= 0");
+    if (e.inverted_face != kNone)
+        return jv ? c->fail(SFV_ERR_JVP_NAN, -1, "jvp: face deformation gradient is not invertible")
+                  : c->fail(SFV_ERR_INVERTED_ELEMENT, c->mesh.owner[e.inverted_face],
+                            "face deformation gradient is not invertible");
+    if (e.nan_cell != kNone)
+        return jv ? c->fail(SFV_ERR_JVP_NAN, -1, "jvp: residual: non-finite entry")
+                  : c->fail(SFV_ERR_RESIDUAL_NAN, e.nan_cell, "residual: non-finite entry");
+    if (jv && e.nan_jv != kNone) return c->fail(SFV_ERR_JVP_NAN, -1, "jvp: non-finite difference quotient");
+    return SFV_OK;
+}
+
+int gradient_failure(sfv_ctx* c) {
+    return c->fail(SFV_ERR_GRADIENT_FAILURE, c->singular_cell, "cell_gradients: singular least-squares stencil");
+}
+
+// R(u) into r (async; caller fetches + decodes)
+void residual_async(sfv_ctx* c, const double* u, double* r) {
+    launch_residual(c->dm, c->ph, c->pt, c->hist, u, nullptr, nullptr, nullptr, r, c->grad.p, c->err.p, c->stream);
+    c->launches += 2;
+}
+
+// J.v (async).  u_norm_cached: *scal[1] already holds |u| for this u.
+void jv_async(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out, bool u_norm_cached) {
+    launch_jv_eps(u, v, c->n, c->red.p, c->counter.p, c->scal.p, c->scal.p + 1, u_norm_cached, c->stream);
+    launch_residual(c->dm, c->ph, c->pt, c->hist, u, v, c->scal.p, r_u, out, c->grad.p, c->err.p, c->stream);
+    c->launches += 3;
+}
+
+int residual_sync(sfv_ctx* c, const double* u, double* r) {
+    if (c->singular_cell >= 0) return gradient_failure(c);
+    reset_err(c);
+    residual_async(c, u, r);
+    if (int e = c->cuda_check("residual")) return e;
+    if (int e = fetch(c, 0)) return e;
+    return decode_residual_errors(c, false);
+}
+
+// squared-norm on the device, returned on the host (one sync)
+int norm_host(sfv_ctx* c, const double* a, double* out) {
+    launch_dot(a, a, c->n, c->hdev.p, c->red.p, c->counter.p, c->stream);
+    c->launches += 1;
+    if (int e = fetch(c, 1)) return e;
+    *out = std::sqrt(c->st->h[0]);
+    return SFV_OK;
+}
+
+int precond_apply_async(sfv_ctx* c, const double* r, double* z) {
+    const int n = c->n;
+    switch (c->pc_kind) {
+        case SFV_PRECOND_ILU0:
+        case SFV_PRECOND_ILU1:
+        case SFV_PRECOND_ILU2:
+        {
+            TriSet Ls, Us;
+            for (int a = 0; a < 3; ++a) {
+                Ls.t[a] = c->L[a].view;
+                Us.t[a] = c->U[a].view;
+            }
+            launch_ilu_apply(Ls, Us, c->pc_ncomp, r, c->ily.p, z, c->tri_grid, c->tri_sleep, c->stream);
+            c->launches += 4;
+            return SFV_OK;
+        }
+        case SFV_PRECOND_LU:
+            for (int a = 0; a < c->pc_ncomp; ++a) {
+                launch_dense_apply_perm(c->dense_w[a].p, c->nc, c->dense_perm[a].p, r, z, c->pc_ncomp == 1 ? -1 : a,
+                                        c->stream);
+                c->launches += 1;
+            }
+            return SFV_OK;
+        default:
+            if (r != z) cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
+            return SFV_OK;
+    }
+}
+
+bool ensure_krylov(sfv_ctx* c, int restart) {
+    const size_t n = static_cast<size_t>(c->n);
+    if (c->v_cap >= restart + 1 && c->wv.p) return true;
+    bool ok = c->V.alloc(n * (restart + 1)) && c->wv.alloc(n) && c->rv.alloc(n) && c->tv.alloc(n) &&
+              c->xv.alloc(n) && c->bv.alloc(n) && c->ydev.alloc(64) && c->ucand.alloc(n) && c->rcand.alloc(n) &&
+              c->uscratch.alloc(n) && c->rscratch.alloc(n);
+    c->v_cap = ok ? restart + 1 : 0;
+    return ok;
+}
+
+enum { G_CONVERGED = 0, G_MAX_ITERS = 1, G_STAGNATED = 2 };
+
+// gmres_solve, left preconditioned (/root/reference/proj/src/linalg.cpp:423-538), with
+// op = J.v at (u, r_u).  x_zero: x0 is all zeros, so op(x0) = 0 without evaluation
+// (jacobian_vector_product short-circuits |v| = 0, nonlinear.cpp:110).
+int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, double* x, bool x_zero, int restart,
+          double rel_reduction, int max_iters, int* iters_out, int* status_out, double* rel_out) {
+    const int n = c->n;
+    if (restart > 64) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "gmres: restart > 64 unsupported");
+    if (!ensure_krylov(c, restart)) return c->fail(SFV_ERR_CUDA, -1, "gmres: out of device memory");
+    double* V = c->V.p;
+    double* w = c->wv.p;
+    double* r = c->rv.p;
+    double* tmp = c->tv.p;
+    bool unorm_cached = false;
+    auto op = [&](const double* v, double* out) -> int {
+        reset_err(c);
+        jv_async(c, u, r_u, v, out, unorm_cached);
+        unorm_cached = true;
+        return SFV_OK;
+    };
+    // residual(x): r = M^-1 (b - op(x))  (linalg.cpp:434-439)
+    auto residual_of_x = [&](bool zero) -> int {
+        if (zero) {
+            cudaMemcpyAsync(tmp, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
+        } else {
+            op(x, tmp);
+            launch_sub_from(b, tmp, n, c->stream);
+            ++c->launches;
+        }
+        if (int e = precond_apply_async(c, tmp, r)) return e;
+        launch_dot(r, r, n, c->hdev.p, c->red.p, c->counter.p, c->stream);
+        ++c->launches;
+        if (int e = fetch(c, 1)) return e;
+        if (!zero)
+            if (int e = decode_residual_errors(c, true)) return e;
+        return SFV_OK;
+    };
+    int total = 0, status = G_MAX_ITERS;
+    double rel = 1.0;
+    *iters_out = 0;
+    if (int e = residual_of_x(x_zero)) return e;
+    const double r0 = std::sqrt(c->st->h[0]);
+    if (r0 == 0.0) {
+        *status_out = G_CONVERGED;
+        *rel_out = 0.0;
+        return SFV_OK;
+    }
+    const double target = rel_reduction * r0;
+    double beta = r0;
+    std::vector<std::vector<double>> H;
+    std::vector<double> cs, sn, g, y;
+    while (total < max_iters) {
+        const double cycle_start = beta;
+        launch_scale_div_host(r, beta, V, n, c->stream);  // v0 = r / beta
+        ++c->launches;
+        H.clear();
+        cs.clear();
+        sn.clear();
+        g.assign(1, beta);
+        int j = 0;
+        bool happy = false;
+        while (j < restart && total < max_iters) {
+            double* vj = V + static_cast<size_t>(j) * n;
+            op(vj, tmp);
+            if (int e = precond_apply_async(c, tmp, w)) return e;
+            // modified Gram-Schmidt (linalg.cpp:469-473): h_0 = w.v_0, then
+            // w -= h_i v_i fused with h_{i+1} = w.v_{i+1}; the last pass yields w.w
+            launch_dot(w, V, n, c->hdev.p, c->red.p, c->counter.p, c->stream);
+            ++c->launches;
+            for (int i = 0; i <= j; ++i) {
+                const double* vnext = i < j ? V + static_cast<size_t>(i + 1) * n : nullptr;
+                launch_axpy_dot(w, V + static_cast<size_t>(i) * n, c->hdev.p + i, vnext, n, c->hdev.p + i + 1,
+                                c->red.p, c->counter.p, c->stream);
+                ++c->launches;
+            }
+            if (int e = c->cuda_check("arnoldi")) return e;
+            if (int e = fetch(c, j + 2)) return e;
+            if (int e = decode_residual_errors(c, true)) return e;
+            std::vector<double> hj(j + 2, 0.0);
+            for (int i = 0; i <= j; ++i) hj[i] = c->st->h[i];
+            hj[j + 1] = std::sqrt(c->st->h[j + 1]);
+            for (int i = 0; i < j; ++i) {  // apply stored rotations
+                const double t = cs[i] * hj[i] + sn[i] * hj[i + 1];
+                hj[i + 1] = -sn[i] * hj[i] + cs[i] * hj[i + 1];
+                hj[i] = t;
+            }
+            const double denom = std::hypot(hj[j], hj[j + 1]);
+            const double cc = denom == 0.0 ? 1.0 : hj[j] / denom;
+            const double ss = denom == 0.0 ? 0.0 : hj[j + 1] / denom;
+            cs.push_back(cc);
+            sn.push_back(ss);
+            g.push_back(-ss * g[j]);
+            g[j] = cc * g[j];
+            hj[j] = denom;
+            const double subdiag = hj[j + 1];
+            hj[j + 1] = 0.0;
+            H.push_back(std::move(hj));
+            ++total;
+            ++j;
+            if (subdiag <= 1e-14 * std::max(denom, 1e-300)) {  // happy breakdown
+                happy = true;
+                break;
+            }
+            if (std::abs(g[j]) <= target) break;
+            if (j < restart) {
+                launch_scale_div_host(w, subdiag, V + static_cast<size_t>(j) * n, n, c->stream);
+                ++c->launches;
+            }
+        }
+        // back substitution, then x += V y (linalg.cpp:505-515)
+        y.assign(j, 0.0);
+        for (int i = j - 1; i >= 0; --i) {
+            double s = g[i];
+            for (int k = i + 1; k < j; ++k) s -= H[k][i] * y[k];
+            y[i] = s / H[i][i];
+        }
+        cudaMemcpyAsync(c->ydev.p, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, c->stream);
+        launch_update(x, V, c->ydev.p, j, n, c->stream);
+        ++c->launches;
+        x_zero = false;
+        if (int e = residual_of_x(false)) return e;  // explicit restart residual (:518-519)
+        beta = std::sqrt(c->st->h[0]);
+        rel = beta / r0;
+        if (beta <= target || (happy && std::abs(g[j]) <= target)) {
+            status = G_CONVERGED;
+            break;
+        }
+        if (happy || beta >= cycle_start * (1.0 - 1e-12)) {
+            status = G_STAGNATED;
+            break;
+        }
+    }
+    *iters_out = total;
+    *status_out = status;
+    *rel_out = rel;
+    return SFV_OK;
+}
+
+void push_record(sfv_solve_report* rep, int iter, double r_norm, int kry, double s) {
+    const int cap = static_cast<int>(sizeof(rep->records) / sizeof(rep->records[0]));
+    if (rep->n_records < cap) rep->records[rep->n_records] = {0, iter, r_norm, kry, s};
+    ++rep->n_records;
+}
+
+// jfnk_solve (nonlinear.cpp:173-266) with line_search (:140-163) and check_convergence
+// (:97-103).  Returns an error only where the reference lets an exception escape.
+int jfnk(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int n = c->n;
+    const int max_outer = cfg->max_outer > 0 ? cfg->max_outer : 50;
+    const double inner = cfg->inner_reduction > 0.0 ? cfg->inner_reduction : 1e-3;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->status = SFV_MAX_ITERS;
+    auto wall = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    if (!ensure_krylov(c, std::max(cfg->restart, 1))) return c->fail(SFV_ERR_CUDA, -1, "jfnk: out of device memory");
+    double* r = c->rscratch.p;  // residual at the current iterate
+    double* rhs = c->bv.p;
+    double* x = c->xv.p;
+    int e = residual_sync(c, u, r);
+    if (e) {
+        rep->wall_seconds = wall();
+        return e;
+    }
+    double r_norm;
+    if ((e = norm_host(c, r, &r_norm))) return e;
+    const double r_norm0 = r_norm;
+    rep->initial_residual = r_norm0;
+    rep->final_residual = r_norm;
+    push_record(rep, 0, r_norm, 0, 0.0);
+    if (r_norm <= cfg->a_tol || r_norm <= cfg->r_tol * r_norm0) {
+        rep->status = SFV_CONVERGED;
+        rep->wall_seconds = wall();
+        return SFV_OK;
+    }
+    int stag = 0;
+    for (int k = 0; k < max_outer; ++k) {
+        launch_negate(r, rhs, n, c->stream);
+        cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream);
+        ++c->launches;
+        int iters = 0, status = 0;
+        double rel = 0.0;
+        e = gmres(c, u, r, rhs, x, true, cfg->restart, inner, cfg->max_krylov, &iters, &status, &rel);
+        if (e == SFV_ERR_JVP_NAN) {
+            rep->status = SFV_DIVERGED;
+            std::snprintf(rep->detail, SFV_DETAIL_LEN, "%s", c->last.msg.c_str());
+            e = SFV_OK;
+            break;
+        }
+        if (e) {
+            rep->wall_seconds = wall();
+            return e;
+        }
+        rep->krylov_iters += iters;
+        if (status == G_STAGNATED) {
+            if (++stag >= 2) {
+                rep->status = SFV_DIVERGED;
+                std::snprintf(rep->detail, SFV_DETAIL_LEN, "gmres stagnated on two consecutive outer iterations");
+                break;
+            }
+        } else {
+            stag = 0;
+        }
+        double s = 1.0;
+        if (cfg->line_search) {
+            bool ok = false;
+            double ss = 1.0, rn = 0.0;
+            for (int attempt = 0; attempt < 6; ++attempt, ss *= 0.5) {
+                launch_lincomb(c->ucand.p, u, ss, x, n, c->stream);
+                ++c->launches;
+                if (residual_sync(c, c->ucand.p, c->rcand.p)) continue;  // invalid trial state rejects the step
+                if ((e = norm_host(c, c->rcand.p, &rn))) return e;
+                if (rn < r_norm) {
+                    ok = true;
+                    break;
+                }
+            }
+            if (!ok) {
+                rep->status = SFV_DIVERGED;
+                std::snprintf(rep->detail, SFV_DETAIL_LEN, "line search found no residual decrease");
+                break;
+            }
+            s = ss;
+            // u += s du reproduces the accepted candidate bit for bit; r is its residual
+            cudaMemcpyAsync(u, c->ucand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
+            cudaMemcpyAsync(r, c->rcand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
+            r_norm = rn;
+        } else {
+            launch_lincomb(u, u, 1.0, x, n, c->stream);
+            ++c->launches;
+            if (residual_sync(c, u, r)) {
+                rep->status = SFV_DIVERGED;
+                std::snprintf(rep->detail, SFV_DETAIL_LEN, "%s", c->last.msg.c_str());
+                rep->outer_iters = k + 1;
+                break;
+            }
+            if ((e = norm_host(c, r, &r_norm))) return e;
+        }
+        rep->outer_iters = k + 1;
+        push_record(rep, k + 1, r_norm, iters, s);
+        rep->final_residual = r_norm;
+        bool conv = r_norm <= cfg->a_tol || r_norm <= cfg->r_tol * r_norm0;
+        if (!conv && cfg->s_tol > 0.0) {
+            double dn, un;
+            if ((e = norm_host(c, x, &dn)) || (e = norm_host(c, u, &un))) return e;
+            conv = s * dn <= cfg->s_tol * un;
+        }
+        if (conv) {
+            rep->status = SFV_CONVERGED;
+            break;
+        }
+    }
+    if (rep->status == SFV_MAX_ITERS && rep->outer_iters == max_outer)
+        std::snprintf(rep->detail, SFV_DETAIL_LEN, "outer iteration limit reached");
+    cudaStreamSynchronize(c->stream);
+    rep->wall_seconds = wall();
+    return SFV_OK;
+}
+
+int precond_create(sfv_ctx* c, int kind) {
+    c->pc_kind = SFV_PRECOND_NONE;
+    if (kind == SFV_PRECOND_AUTO) kind = 3 * c->nc <= 30000 ? SFV_PRECOND_LU : SFV_PRECOND_ILU1;  // nonlinear.cpp:355-356
+    if (kind == SFV_PRECOND_NONE) return SFV_OK;
+    std::vector<ScalarCsr> comps;
+    const std::string msg = cell_jacobian(c->mesh, c->geom, c->ph.kbar, c->ph.transient != 0, c->ph.rho, c->ph.dt, comps);
+    if (!msg.empty()) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, msg);
+    c->pc_ncomp = static_cast<int>(comps.size());
+    if (kind == SFV_PRECOND_LU) {
+        for (size_t a = 0; a < comps.size(); ++a) {
+            BandChol bc;
+            const std::string m2 = band_cholesky_neg(comps[a], bc);
+            if (!m2.empty()) return c->fail(SFV_ERR_LU_SINGULAR, -1, m2);
+            DevBuf<double> band;
+            if (!band.upload(bc.l) || !c->dense_perm[a].upload(bc.perm) ||
+                !c->dense_w[a].alloc(static_cast<size_t>(bc.n) * bc.n))
+                return c->fail(SFV_ERR_CUDA, -1, "lu: out of device memory");
+            launch_band_inverse(band.p, bc.n, bc.bw, c->dense_w[a].p, c->stream);
+            ++c->launches;
+            if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->cuda_check("lu setup");
+        }
+        c->pc_kind = SFV_PRECOND_LU;
+        return SFV_OK;
+    }
+    const int level = kind == SFV_PRECOND_ILU0 ? 0 : kind == SFV_PRECOND_ILU1 ? 1 : 2;
+    std::vector<ScalarCsr> lus(comps.size());
+    bool broke = false;
+    for (size_t a = 0; a < comps.size(); ++a)
+        if (!iluk_factor(comps[a], level, lus[a]).empty()) broke = true;
+    if (broke) {  // one retry with a 1e-12 |diag| shift over the expanded diagonal (nonlinear.cpp:357-369)
+        double dn = 0.0;
+        for (int i = 0; i < c->nc; ++i)
+            for (int a = 0; a < 3; ++a) {
+                const ScalarCsr& s = comps[comps.size() == 1 ? 0 : a];
+                const int q = static_cast<int>(std::lower_bound(s.col.begin() + s.rp[i], s.col.begin() + s.rp[i + 1], i) -
+                                               s.col.begin());
+                dn += s.val[q] * s.val[q];
+            }
+        dn = std::sqrt(dn);
+        for (auto& s : comps)
+            for (int i = 0; i < c->nc; ++i) {
+                const int q = static_cast<int>(std::lower_bound(s.col.begin() + s.rp[i], s.col.begin() + s.rp[i + 1], i) -
+                                               s.col.begin());
+                s.val[q] += 1e-12 * dn;
+            }
+        for (size_t a = 0; a < comps.size(); ++a) {
+            const std::string m3 = iluk_factor(comps[a], level, lus[a]);
+            if (!m3.empty()) return c->fail(SFV_ERR_ILU_BREAKDOWN, -1, m3);
+        }
+    }
+    for (size_t a = 0; a < lus.size(); ++a) {
+        TriSchedule tl, tu;
+        schedule_lower(lus[a], tl);
+        schedule_upper(lus[a], tu);
+        if (!c->L[a].upload(tl, c->nc) || !c->U[a].upload(tu, c->nc))
+            return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
+    }
+    if (!c->ily.alloc(c->n)) return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
+    // persistent grid: every CTA resident (<= 8 CTAs of 256 threads per SM fit), so each
+    // awaited row belongs to a running thread.  Knobs for tuning: SFV_TRI_CTAS_PER_SM,
+    // SFV_TRI_SLEEP_NS.
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = 2;
+    if (const char* e = std::getenv("SFV_TRI_CTAS_PER_SM")) per_sm = std::max(1, std::min(8, std::atoi(e)));
+    c->tri_sleep = 0;
+    if (const char* e = std::getenv("SFV_TRI_SLEEP_NS")) c->tri_sleep = std::max(0, std::atoi(e));
+    c->tri_grid = std::max(1, sms * per_sm);
+    c->pc_kind = kind;
+    return c->cuda_check("ilu setup");
+}
+
+}  // namespace
+
+// ================================================================ C-ABI
+
+extern "C" {
+
+sfv_mesh* sfv_mesh_box(const double extents[3], const int divisions[3], const int patch_kinds[6],
+                       double distort_factor, uint64_t seed, char* err, int errlen) {
+    for (int a = 0; a < 3; ++a)
+        if (divisions[a] < 1 || !(extents[a] > 0.0)) {
+            if (err) std::snprintf(err, errlen, "generate_box_hex: bad divisions or extents");
+            return nullptr;
+        }
+    auto* m = new sfv_mesh{box_hex(extents, divisions, patch_kinds)};
+    const std::string e = distort(m->m, distort_factor, seed);
+    if (!e.empty()) {
+        if (err) std::snprintf(err, errlen, "%s", e.c_str());
+        delete m;
+        return nullptr;
+    }
+    return m;
+}
+
+sfv_mesh* sfv_mesh_kuhn_tets(const double extents[3], int n, const int patch_kinds[6], uint64_t perm_seed, int permute,
+                             int rcm, char* err, int errlen) {
+    if (n < 1) {
+        if (err) std::snprintf(err, errlen, "kuhn_tets: n must be >= 1");
+        return nullptr;
+    }
+    return new sfv_mesh{kuhn_tets(extents, n, patch_kinds, perm_seed, permute != 0, rcm != 0)};
+}
+
+void sfv_mesh_counts(const sfv_mesh* mm, int counts[6]) {
+    const HostMesh& m = mm->m;
+    counts[0] = static_cast<int>(m.points.size());
+    counts[1] = m.n_faces();
+    counts[2] = static_cast<int>(m.face_pts.size());
+    counts[3] = m.n_cells;
+    counts[4] = m.n_internal;
+    counts[5] = static_cast<int>(m.patches.size());
+}
+
+void sfv_mesh_export(const sfv_mesh* mm, double* points, int* face_offsets, int* face_points, int* owner,
+                     int* neighbour, int* patch_kind, int* patch_start, int* patch_count) {
+    const HostMesh& m = mm->m;
+    for (size_t i = 0; i < m.points.size(); ++i) {
+        points[3 * i] = m.points[i].x;
+        points[3 * i + 1] = m.points[i].y;
+        points[3 * i + 2] = m.points[i].z;
+    }
+    std::memcpy(face_offsets, m.face_off.data(), sizeof(int) * m.face_off.size());
+    std::memcpy(face_points, m.face_pts.data(), sizeof(int) * m.face_pts.size());
+    std::memcpy(owner, m.owner.data(), sizeof(int) * m.owner.size());
+    std::memcpy(neighbour, m.neighbour.data(), sizeof(int) * m.neighbour.size());
+    for (size_t p = 0; p < m.patches.size(); ++p) {
+        patch_kind[p] = m.patches[p].kind;
+        patch_start[p] = m.patches[p].start;
+        patch_count[p] = m.patches[p].count;
+    }
+}
+
+void sfv_mesh_free(sfv_mesh* m) { delete m; }
+
+sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, int errlen) {
+    auto fail = [&](const std::string& m) -> sfv_ctx* {
+        if (err) std::snprintf(err, errlen, "%s", m.c_str());
+        return nullptr;
+    };
+    if (md->dim != 3) return fail("sfv: only 3-D meshes are on the hot path");
+    if (md->n_patches > kMaxPatches) return fail("sfv: too many patches");
+    auto c = std::make_unique<sfv_ctx>();
+    HostMesh& m = c->mesh;
+    m.points.resize(md->n_points);
+    for (int i = 0; i < md->n_points; ++i)
+        m.points[i] = {md->points[3 * i], md->points[3 * i + 1], md->points[3 * i + 2]};
+    m.face_off.assign(md->face_offsets, md->face_offsets + md->n_faces + 1);
+    m.face_pts.assign(md->face_points, md->face_points + md->face_offsets[md->n_faces]);
+    m.owner.assign(md->owner, md->owner + md->n_faces);
+    m.neighbour.assign(md->neighbour, md->neighbour + md->n_faces);
+    for (int p = 0; p < md->n_patches; ++p) m.patches.push_back({md->patch_kind[p], md->patch_start[p], md->patch_count[p]});
+    m.n_cells = md->n_cells;
+    m.n_internal = md->n_internal;
+    std::string e = m.finalise();
+    if (!e.empty()) return fail(e);
+    e = compute_geometry(m, c->geom);
+    if (!e.empty()) return fail(e);
+    // ResidualEvaluator ctor checks (discretisation.cpp:64-67)
+    if (!(ph->alpha > 0.0)) return fail("discretisation: alpha must be positive");
+    if (ph->transient && !(ph->dt > 0.0)) return fail("discretisation: transient mode needs dt > 0");
+    c->nc = m.n_cells;
+    c->n = 3 * m.n_cells;
+    for (int i = 0; i < c->nc; ++i)
+        if (c->geom.g_singular[i]) {
+            c->singular_cell = i;
+            break;
+        }
+    Physics& p = c->ph;
+    p.law = ph->law;
+    p.tl = ph->total_lagrangian;
+    p.transient = ph->transient;
+    p.mu = ph->mu;
+    p.lam = ph->lambda;
+    p.alpha = ph->alpha;
+    p.kbar = ph->law == SFV_LAW_NEO_HOOKEAN ? 4.0 / 3.0 * ph->mu + ph->lambda : 2.0 * ph->mu + ph->lambda;
+    p.rho = ph->rho;
+    p.dt = ph->dt;
+    c->pt.n = md->n_patches;
+    c->bc_raw.assign(ph->bc_value, ph->bc_value + 3 * md->n_patches);
+    c->bc_ramp.assign(ph->bc_ramp, ph->bc_ramp + md->n_patches);
+    for (int q = 0; q < md->n_patches; ++q) c->pt.kind[q] = md->patch_kind[q];
+    update_patch_values(c.get());
+    e = build_layout(c.get());
+    if (!e.empty()) return fail(e);
+    const size_t n = static_cast<size_t>(c->n);
+    if (!c->grad.alloc(9 * static_cast<size_t>(c->nc)) || !c->red.alloc(2 * 148 * 8 + 64) || !c->scal.alloc(8) ||
+        !c->counter.alloc(1) || !c->err.alloc(1) || !c->hdev.alloc(72) || !c->dzero.alloc(n))
+        return fail("cuda: out of device memory");
+    cudaMemset(c->counter.p, 0, sizeof(unsigned));
+    cudaMemset(c->dzero.p, 0, sizeof(double) * n);
+    if (c->ph.transient) {
+        c->hist.u_old = c->hist.u_old_old = c->hist.v_old = c->hist.v_old_old = c->dzero.p;
+    }
+    if (cudaMallocHost(&c->st, sizeof(Status)) != cudaSuccess) return fail("cuda: pinned allocation failed");
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail("cuda: setup failed");
+    return c.release();
+}
+
+void sfv_destroy(sfv_ctx* c) {
+    if (!c) return;
+    if (c->st) cudaFreeHost(c->st);
+    delete c;
+}
+
+int sfv_set_stream(sfv_ctx* c, void* s) {
+    c->stream = static_cast<cudaStream_t>(s);
+    return SFV_OK;
+}
+
+int sfv_n_cells(const sfv_ctx* c) { return c->nc; }
+const char* sfv_last_error(const sfv_ctx* c) { return c->last.msg.c_str(); }
+long long sfv_launch_count(const sfv_ctx* c) { return c->launches; }
+
+size_t sfv_device_bytes(const sfv_ctx* c) {
+    return c->slot_face.bytes() + c->slot_other.bytes() + c->slot_ls.bytes() + c->gam.bytes() + c->del.bytes() +
+           c->dmag.bytes() + c->w.bytes() + c->volume.bytes() + c->grad.bytes() + c->V.bytes() + c->dense_w[0].bytes() + c->dense_w[1].bytes() + c->dense_w[2].bytes();
+}
+
+double sfv_jv_bytes(const sfv_ctx* c) {
+    // B = 96 N_c + 120 N_f + 60 N_d + 12 N_t (+104 N_c transient)
+    const HostMesh& m = c->mesh;
+    double nd = 0, nt = 0, ns = 0;
+    for (int f = m.n_internal; f < m.n_faces(); ++f) {
+        const int k = m.patches[m.face_patch[f]].kind;
+        if (k == SFV_PATCH_DISPLACEMENT) nd += 1;
+        else if (k == SFV_PATCH_TRACTION) nt += 1;
+        else ns += 1;
+    }
+    return 96.0 * c->nc + 120.0 * m.n_internal + 60.0 * nd + 12.0 * nt + 84.0 * ns +
+           (c->ph.transient ? 104.0 * c->nc : 0.0);
+}
+
+int sfv_geometry(const sfv_ctx* c, double* volume, double* centroid, double* face_centroid, double* area, double* d,
+                 double* d_mag, double* w, double* delta, double* g_inv, signed char* g_singular, int* cf_offsets,
+                 int* cf_faces, double* ls_vec) {
+    const HostMesh& m = c->mesh;
+    const HostGeometry& g = c->geom;
+    for (int i = 0; i < m.n_cells; ++i) {
+        volume[i] = g.volume[i];
+        centroid[3 * i] = g.centroid[i].x;
+        centroid[3 * i + 1] = g.centroid[i].y;
+        centroid[3 * i + 2] = g.centroid[i].z;
+        for (int k = 0; k < 9; ++k) g_inv[9 * i + k] = g.g_inv[9 * static_cast<size_t>(i) + k];
+        g_singular[i] = g.g_singular[i];
+    }
+    for (int f = 0; f < m.n_faces(); ++f) {
+        const V3* src[4] = {&g.face_centroid[f], &g.area[f], &g.d[f], &g.delta[f]};
+        double* dst[4] = {face_centroid, area, d, delta};
+        for (int a = 0; a < 4; ++a) {
+            dst[a][3 * f] = src[a]->x;
+            dst[a][3 * f + 1] = src[a]->y;
+            dst[a][3 * f + 2] = src[a]->z;
+        }
+        d_mag[f] = g.d_mag[f];
+        w[f] = g.w[f];
+    }
+    std::memcpy(cf_offsets, m.cf_off.data(), sizeof(int) * m.cf_off.size());
+    std::memcpy(cf_faces, m.cf.data(), sizeof(int) * m.cf.size());
+    for (size_t q = 0; q < g.ls.size(); ++q) {
+        ls_vec[3 * q] = g.ls[q].x;
+        ls_vec[3 * q + 1] = g.ls[q].y;
+        ls_vec[3 * q + 2] = g.ls[q].z;
+    }
+    return SFV_OK;
+}
+
+int sfv_set_time(sfv_ctx* c, double t) {
+    c->time = t;
+    update_patch_values(c);
+    return SFV_OK;
+}
+
+int sfv_set_history(sfv_ctx* c, const double* uo, const double* uoo, const double* vo, const double* voo) {
+    c->hist.u_old = uo;
+    c->hist.u_old_old = uoo;
+    c->hist.v_old = vo;
+    c->hist.v_old_old = voo;
+    return SFV_OK;
+}
+
+int sfv_residual(sfv_ctx* c, const double* u, double* r, int* cell) {
+    const int e = residual_sync(c, u, r);
+    if (cell) *cell = e ? c->last.cell : -1;
+    return e;
+}
+
+int sfv_stabilisation(sfv_ctx* c, const double* u, double* r, int* cell) {
+    if (cell) *cell = -1;
+    if (c->singular_cell >= 0) {
+        if (cell) *cell = c->singular_cell;
+        return gradient_failure(c);
+    }
+    reset_err(c);
+    Physics ph = c->ph;
+    ph.stab_only = 1;
+    launch_residual(c->dm, ph, c->pt, c->hist, u, nullptr, nullptr, nullptr, r, c->grad.p, c->err.p, c->stream);
+    c->launches += 2;
+    if (int e = c->cuda_check("stabilisation")) return e;
+    return fetch(c, 0);
+}
+
+int sfv_gradients(sfv_ctx* c, const double* u, double* G, int* cell) {
+    if (cell) *cell = -1;
+    if (c->singular_cell >= 0) {
+        if (cell) *cell = c->singular_cell;
+        return gradient_failure(c);
+    }
+    launch_gradients(c->dm, c->pt, u, G, c->stream);
+    c->launches += 1;
+    if (int e = c->cuda_check("gradients")) return e;
+    return cudaStreamSynchronize(c->stream) == cudaSuccess ? SFV_OK : c->cuda_check("gradients");
+}
+
+int sfv_mesh_geometry(const sfv_mesh_desc* md, double* volume, double* centroid, double* face_centroid,
+                      double* area, double* d, double* d_mag, double* w, double* delta, double* g_inv,
+                      signed char* g_singular, int* cf_offsets, int* cf_faces, double* ls_vec, char* err,
+                      int errlen) {
+    sfv_ctx tmp;
+    HostMesh& m = tmp.mesh;
+    m.points.resize(md->n_points);
+    for (int i = 0; i < md->n_points; ++i)
+        m.points[i] = {md->points[3 * i], md->points[3 * i + 1], md->points[3 * i + 2]};
+    m.face_off.assign(md->face_offsets, md->face_offsets + md->n_faces + 1);
+    m.face_pts.assign(md->face_points, md->face_points + md->face_offsets[md->n_faces]);
+    m.owner.assign(md->owner, md->owner + md->n_faces);
+    m.neighbour.assign(md->neighbour, md->neighbour + md->n_faces);
+    for (int p = 0; p < md->n_patches; ++p) m.patches.push_back({md->patch_kind[p], md->patch_start[p], md->patch_count[p]});
+    m.n_cells = md->n_cells;
+    m.n_internal = md->n_internal;
+    std::string e = m.finalise();
+    if (e.empty()) e = compute_geometry(m, tmp.geom);
+    if (!e.empty()) {
+        if (err) std::snprintf(err, errlen, "%s", e.c_str());
+        return SFV_ERR_GEOMETRY;
+    }
+    tmp.nc = m.n_cells;
+    return sfv_geometry(&tmp, volume, centroid, face_centroid, area, d, d_mag, w, delta, g_inv, g_singular,
+                        cf_offsets, cf_faces, ls_vec);
+}
+
+int sfv_jv(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out, int* cell) {
+    if (cell) *cell = -1;
+    if (c->singular_cell >= 0) {  // GradientFailure escapes J.v unless v == 0 (nonlinear.cpp:110)
+        double vn;
+        if (int e = norm_host(c, v, &vn)) return e;
+        if (vn != 0.0) {
+            if (cell) *cell = c->singular_cell;
+            return gradient_failure(c);
+        }
+        cudaMemsetAsync(out, 0, sizeof(double) * c->n, c->stream);
+        return SFV_OK;
+    }
+    reset_err(c);
+    jv_async(c, u, r_u, v, out, false);
+    if (int e = c->cuda_check("jv")) return e;
+    if (int e = fetch(c, 0)) return e;
+    return decode_residual_errors(c, true);
+}
+
+int sfv_jv_eps(sfv_ctx* c, const double* u, const double* r_u, const double* v, double eps, double* out, int* cell) {
+    if (cell) *cell = -1;
+    if (c->singular_cell >= 0) return gradient_failure(c);
+    reset_err(c);
+    cudaMemcpyAsync(c->scal.p, &eps, sizeof(double), cudaMemcpyHostToDevice, c->stream);
+    cudaStreamSynchronize(c->stream);
+    launch_residual(c->dm, c->ph, c->pt, c->hist, u, v, c->scal.p, r_u, out, c->grad.p, c->err.p, c->stream);
+    c->launches += 2;
+    if (int e = c->cuda_check("jv_eps")) return e;
+    if (int e = fetch(c, 0)) return e;
+    return decode_residual_errors(c, true);
+}
+
+int sfv_jv_async(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out) {
+    if (c->singular_cell >= 0) return gradient_failure(c);
+    jv_async(c, u, r_u, v, out, false);
+    return c->cuda_check("jv_async");
+}
+
+int sfv_check_errors(sfv_ctx* c, int* cell) {
+    if (int e = fetch(c, 0)) return e;
+    const int e = decode_residual_errors(c, true);
+    if (cell) *cell = e ? c->last.cell : -1;
+    reset_err(c);
+    return e;
+}
+
+int sfv_residual_host(sfv_ctx* c, const double* u, double* r, int* cell) {
+    const size_t bytes = sizeof(double) * c->n;
+    if (!ensure_krylov(c, 1)) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
+    cudaMemcpyAsync(c->ucand.p, u, bytes, cudaMemcpyHostToDevice, c->stream);
+    const int e = residual_sync(c, c->ucand.p, c->rcand.p);
+    if (cell) *cell = e ? c->last.cell : -1;
+    if (e) return e;
+    cudaMemcpyAsync(r, c->rcand.p, bytes, cudaMemcpyDeviceToHost, c->stream);
+    return cudaStreamSynchronize(c->stream) == cudaSuccess ? SFV_OK : c->cuda_check("residual_host");
+}
+
+int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out, int* cell) {
+    const size_t bytes = sizeof(double) * c->n;
+    if (!ensure_krylov(c, 1)) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
+    cudaMemcpyAsync(c->ucand.p, u, bytes, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(c->rcand.p, r_u, bytes, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(c->tv.p, v, bytes, cudaMemcpyHostToDevice, c->stream);
+    const int e = sfv_jv(c, c->ucand.p, c->rcand.p, c->tv.p, c->wv.p, cell);
+    if (e) return e;
+    cudaMemcpyAsync(out, c->wv.p, bytes, cudaMemcpyDeviceToHost, c->stream);
+    return cudaStreamSynchronize(c->stream) == cudaSuccess ? SFV_OK : c->cuda_check("jv_host");
+}
+
+int sfv_precond_create(sfv_ctx* c, int kind) { return precond_create(c, kind); }
+
+int sfv_precond_apply(sfv_ctx* c, const double* r, double* z) {
+    if (int e = precond_apply_async(c, r, z)) return e;
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->cuda_check("precond_apply");
+    return c->cuda_check("precond_apply");
+}
+
+int sfv_precond_info(const sfv_ctx* c, int info[5]) {
+    info[0] = c->pc_kind;
+    info[1] = c->L[0].n_levels;
+    info[2] = c->U[0].n_levels;
+    info[3] = static_cast<int>(c->L[0].nnz);
+    info[4] = static_cast<int>(c->U[0].nnz);
+    return SFV_OK;
+}
+
+int sfv_gmres_jv(sfv_ctx* c, const double* u, const double* r_u, const double* b, double* x, int restart,
+                 double rel_reduction, int max_iters, int* iters, int* status, double* rel_residual) {
+    if (c->singular_cell >= 0) return gradient_failure(c);
+    // x is the initial guess; a nonzero guess costs one extra J.v as in the reference
+    return gmres(c, u, r_u, b, x, false, restart, rel_reduction, max_iters, iters, status, rel_residual);
+}
+
+int sfv_jfnk_solve(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep) {
+    return jfnk(c, u, cfg, rep);
+}
+
+// run_steps (nonlinear.cpp:382-446)
+int sfv_run_steps(sfv_ctx* c, double* field, const sfv_solver_cfg* cfg, int n_steps, sfv_solve_report* reports,
+                  int cap, int* n_reports, double* wall_seconds) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (n_steps < 1) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "run_steps: need at least one step");
+    const int n = c->n;
+    *n_reports = 0;
+    if (int e = precond_create(c, cfg->preconditioner)) return e;
+    if (!ensure_krylov(c, std::max(cfg->restart, 1))) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
+    double* fu = field;
+    double* fuo = field + n;
+    double* fuoo = field + 2 * static_cast<size_t>(n);
+    double* fvo = field + 3 * static_cast<size_t>(n);
+    double* fvoo = field + 4 * static_cast<size_t>(n);
+    double* fao = field + 5 * static_cast<size_t>(n);
+    double* u = c->uscratch.p;
+    const bool transient = c->ph.transient != 0;
+    const double dt = c->ph.dt;
+    for (int step = 1; step <= n_steps; ++step) {
+        sfv_set_time(c, transient ? step * dt : static_cast<double>(step) / n_steps);
+        if (transient) {
+            sfv_set_history(c, fuo, fuoo, fvo, fvoo);
+            launch_predict(u, fuo, fvo, fao, dt, n, c->stream);
+            ++c->launches;
+        } else {
+            cudaMemcpyAsync(u, fu, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
+        }
+        sfv_solve_report rep;
+        const int e = jfnk(c, u, cfg, &rep);
+        if (e) {
+            std::memset(&rep, 0, sizeof(rep));
+            rep.status = SFV_DIVERGED;
+            std::snprintf(rep.detail, SFV_DETAIL_LEN, "%s", c->last.msg.c_str());
+        }
+        rep.step = step;
+        for (int i = 0; i < std::min(rep.n_records, 64); ++i) rep.records[i].step = step;
+        if (*n_reports < cap) reports[*n_reports] = rep;
+        ++*n_reports;
+        if (rep.status != SFV_CONVERGED) break;
+        if (transient) {
+            launch_bdf2_rotate(fuo, fuoo, fvo, fvoo, fao, u, dt, n, c->stream);
+            ++c->launches;
+        } else {
+            cudaMemcpyAsync(fuo, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
+        }
+        cudaMemcpyAsync(fu, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
+    }
+    if (*n_reports > cap) *n_reports = cap;
+    if (transient) sfv_set_history(c, c->dzero.p, c->dzero.p, c->dzero.p, c->dzero.p);
+    cudaStreamSynchronize(c->stream);
+    *wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return c->cuda_check("run_steps");
+}
+
+int sfv_run_steps_host(sfv_ctx* c, double* field, const sfv_solver_cfg* cfg, int n_steps, sfv_solve_report* reports,
+                       int cap, int* n_reports, double* wall_seconds) {
+    const size_t bytes = sizeof(double) * 6 * c->n;
+    double* d = nullptr;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
+    cudaMemcpyAsync(d, field, bytes, cudaMemcpyHostToDevice, c->stream);
+    const int e = sfv_run_steps(c, d, cfg, n_steps, reports, cap, n_reports, wall_seconds);
+    cudaMemcpyAsync(field, d, bytes, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(d);
+    return e;
+}
+
+}  // extern "C"

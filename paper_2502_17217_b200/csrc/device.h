@@ -1,0 +1,132 @@
+// device.h — device-resident layout of the JFNK hot path (B200 / sm_100a).
+//
+// HBM layout:
+//   * cell vectors u, v, R(u), J.v are the reference's interleaved [3c + k] doubles
+//     (fields.cpp:20-25) — a cell's three components are one 24-byte record, and a
+//     warp of 32 consecutive cells reads 768 contiguous bytes;
+//   * per-cell face slots in ELL (slot-major) form: slot s of cell c at s*nc + c, in
+//     ascending face index (Mesh::cell_faces order, mesh.cpp:55-59), so slot loads
+//     are fully coalesced; each slot carries the face index (bit 31 = this cell is
+//     the face's neighbour), the other cell (or -(2+patch) on a boundary face) and
+//     the cell's least-squares vector for that face (mesh.cpp:493-507);
+//   * per-face geometry SoA: Gamma (area vector), Delta (over-relaxed orthogonal
+//     vector), |d|, w — |Gamma| and |Delta| are recomputed exactly as the reference
+//     does (norm(), mesh.cpp:386 / discretisation.cpp:35);
+//   * per-patch BC values (already multiplied by t when ramped) are kernel arguments.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace sfv {
+
+constexpr int kMaxPatches = 16;
+constexpr int kMaxSlots = 8;
+
+struct PatchTable {
+    int n;
+    int kind[kMaxPatches];
+    double value[kMaxPatches][3];
+};
+
+struct DevMesh {
+    int nc = 0, nf = 0, nint = 0, slots = 0;
+    const int* slot_face = nullptr;   // [slots*nc]; -1 = padding
+    const int* slot_other = nullptr;  // [slots*nc]
+    const double* slot_ls = nullptr;  // [3*slots*nc], (3*s + k)*nc + c
+    const double* gam = nullptr;      // [3*nf], k*nf + f
+    const double* del = nullptr;      // [3*nf]
+    const double* dmag = nullptr;     // [nf]
+    const double* w = nullptr;        // [nf]
+    const double* volume = nullptr;   // [nc]
+};
+
+struct Physics {
+    int law;  // SFV_LAW_*
+    int tl;
+    int transient;
+    double mu, lam, alpha, kbar;
+    double rho, dt;
+    int stab_only;  // ResidualEvaluator::stabilisation (discretisation.cpp:210-214)
+};
+
+// Error words written by kernels (atomicMin of the first offending index; INT_MAX = none).
+struct ErrWords {
+    int inverted_cell;  // law stress: det F <= 0 (laws.cpp:14)
+    int inverted_face;  // transform_area: det F_f <= 0 (discretisation.cpp:102)
+    int nan_cell;       // residual: non-finite entry (discretisation.cpp:171-172)
+    int nan_jv;         // J.v: non-finite difference quotient (nonlinear.cpp:135)
+};
+
+// History for the BDF2 inertia term (interleaved [3c+k]).
+struct History {
+    const double* u_old = nullptr;
+    const double* u_old_old = nullptr;
+    const double* v_old = nullptr;
+    const double* v_old_old = nullptr;
+};
+
+// ---- residual.cu
+// R(u) (jv_eps == nullptr) or the fused J.v epilogue (R(u + eps v) - r_u) / eps with
+// eps read from *jv_eps (a zero eps means v == 0: out is zero, nonlinear.cpp:110).
+void launch_residual(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist,
+                     const double* u, const double* v, const double* jv_eps, const double* r_u,
+                     double* out, double* grad_scratch, ErrWords* err, cudaStream_t s);
+// cell_gradients only (discretisation.cpp:10-31), SoA [k*nc + c], k = 3i + j
+void launch_gradients(const DevMesh& m, const PatchTable& pt, const double* u, double* G, cudaStream_t s);
+// eps = sqrt(DBL_EPSILON) sqrt(1 + |u|) / |v| into *eps (nonlinear.cpp:109-115), with
+// |u| taken from *u_norm when u_norm_cached is set.
+void launch_jv_eps(const double* u, const double* v, int n, double* scratch, unsigned* counter,
+                   double* eps_out, double* u_norm_inout, bool u_norm_cached, cudaStream_t s);
+
+// ---- krylov.cu (deterministic fixed-order reductions)
+int reduce_blocks(int n);
+void launch_dot(const double* a, const double* b, int n, double* out, double* scratch, unsigned* counter,
+                cudaStream_t s);
+// w -= (*h) * vi ; then *out = dot(w, vnext) (vnext == nullptr: *out = dot(w, w))
+void launch_axpy_dot(double* w, const double* vi, const double* h, const double* vnext, int n, double* out,
+                     double* scratch, unsigned* counter, cudaStream_t s);
+void launch_scale_div(const double* in, const double* divisor, double* out, int n, cudaStream_t s);
+void launch_scale_div_host(const double* in, double divisor, double* out, int n, cudaStream_t s);
+void launch_update(double* x, const double* V, const double* y, int j, int n, cudaStream_t s);
+void launch_sub_from(const double* b, double* r, int n, cudaStream_t s);  // r = b - r
+void launch_negate(const double* a, double* out, int n, cudaStream_t s);
+void launch_axpy_host(double* y, double alpha, const double* x, int n, cudaStream_t s);  // y += alpha x
+void launch_lincomb(double* out, const double* u, double s, const double* du, int n,
+                    cudaStream_t st);  // out = u + s*du
+void launch_bdf2_rotate(double* uo, double* uoo, double* vo, double* voo, double* ao, const double* u, double dt,
+                        int n, cudaStream_t s);
+void launch_predict(double* u, const double* uo, const double* vo, const double* ao, double dt, int n,
+                    cudaStream_t s);
+
+// ---- precond.cu
+struct DevTri {  // one triangular factor in level (processing) order
+    int n = 0;       // positions (rows + per-level padding)
+    int n_rows = 0;  // matrix rows
+    int n_levels = 0;
+    const int* order = nullptr;   // [n] row processed at position p
+    const int* rp = nullptr;      // [n+1] entries of the row at position p
+    const int* col = nullptr;     // [nnz]
+    const double* val = nullptr;  // [nnz]
+    const double* diag = nullptr; // [n] (upper only; per position)
+};
+// ILU apply on the cell graph, 3 interleaved right-hand sides (finding 4):
+// forward unit-lower then backward upper, row arithmetic in the reference's order.
+struct TriSet {
+    DevTri t[3];
+};
+// y is the forward-sweep scratch vector (3n); z receives M^{-1} r.  ncomp = 1: one
+// factor for all three components; ncomp = 3: factor t[k] for component k.
+void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double* r, double* y, double* z, int grid,
+                      int sleep_ns, cudaStream_t s);
+// Exact dense apply z = A^{-1} r for the small-system LU path (3 interleaved RHS).
+void launch_dense_apply(const double* inv, int n, const double* r, double* z, cudaStream_t s);
+// Small-system exact preconditioner: W = (L L^T)^{-1} from a band Cholesky of -K, and
+// z = K^{-1} r = -P W P^T r applied to 3 interleaved components.
+void launch_band_inverse(const double* l, int n, int bw, double* W, cudaStream_t s);
+// comp < 0: all three components with one W; comp = k: component k only
+void launch_dense_apply_perm(const double* W, int n, const int* perm, const double* r, double* z, int comp,
+                             cudaStream_t s);
+
+}  // namespace sfv

@@ -1,0 +1,194 @@
+// krylov.cu — GMRES Arnoldi vector work and Newton vector ops (FP64, sm_100a).
+//
+// Restates the vector kernels of gmres_solve (/root/reference/proj/src/linalg.cpp:423-538):
+// modified Gram-Schmidt (:469-473) as a chain of fused "w -= h_i v_i ; h_{i+1} = w.v_{i+1}"
+// passes, the basis normalisation (:500-501), the correction x += V y (:512-515), and the
+// Newton/stepping vector updates of nonlinear.cpp.  Every reduction is a fixed-order
+// two-level tree (block partials, then one last block in block order), so results are
+// run-to-run deterministic; the scalar h_i never leaves the device between passes.
+#include "device.h"
+
+namespace sfv {
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = kT / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    return sh[0];
+}
+
+// last-block finalisation: returns true in the block that must sum the partials
+__device__ __forceinline__ bool publish_partial(double part, double* partial, unsigned* counter) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        partial[blockIdx.x] = part;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    return last;
+}
+
+__device__ __forceinline__ void finish_sum(const double* partial, unsigned* counter, double* out, double* sh) {
+    __threadfence();
+    double t = 0.0;
+    for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(&partial[b]);
+    const double tot = block_sum(t, sh);
+    if (threadIdx.x == 0) {
+        *out = tot;
+        *counter = 0u;
+    }
+}
+
+__global__ void __launch_bounds__(kT) dot_kernel(const double* __restrict__ a, const double* __restrict__ b, int n,
+                                                 double* __restrict__ out, double* partial, unsigned* counter) {
+    __shared__ double sh[kT];
+    double acc = 0.0;
+    for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += gridDim.x * kT) acc += a[i] * b[i];
+    const double part = block_sum(acc, sh);
+    if (publish_partial(part, partial, counter)) finish_sum(partial, counter, out, sh);
+}
+
+__global__ void __launch_bounds__(kT) axpy_dot_kernel(double* __restrict__ w, const double* __restrict__ vi,
+                                                      const double* __restrict__ h, const double* __restrict__ vnext,
+                                                      int n, double* __restrict__ out, double* partial,
+                                                      unsigned* counter) {
+    __shared__ double sh[kT];
+    const double hi = *h;
+    double acc = 0.0;
+    for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += gridDim.x * kT) {
+        const double wn = w[i] + (-hi) * vi[i];  // axpy(-h_i, v_i, w): w += (-h_i) v_i
+        w[i] = wn;
+        acc += vnext ? wn * vnext[i] : wn * wn;
+    }
+    const double part = block_sum(acc, sh);
+    if (publish_partial(part, partial, counter)) finish_sum(partial, counter, out, sh);
+}
+
+__global__ void scale_div_kernel(const double* __restrict__ in, const double* __restrict__ d, double dh,
+                                 double* __restrict__ out, int n) {
+    const double s = d ? *d : dh;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i] / s;
+}
+
+// dx = sum_i y_i v_i accumulated in i order from zero, then x += dx (linalg.cpp:512-515)
+__global__ void update_kernel(double* __restrict__ x, const double* __restrict__ V, const double* __restrict__ y, int j,
+                              int n) {
+    __shared__ double ys[64];
+    for (int i = threadIdx.x; i < j; i += blockDim.x) ys[i] = y[i];
+    __syncthreads();
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        double dx = 0.0;
+        for (int i = 0; i < j; ++i) dx += ys[i] * V[static_cast<size_t>(i) * n + e];
+        x[e] += 1.0 * dx;
+    }
+}
+
+__global__ void sub_from_kernel(const double* __restrict__ b, double* __restrict__ r, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) r[i] = b[i] - r[i];
+}
+
+__global__ void negate_kernel(const double* __restrict__ a, double* __restrict__ o, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) o[i] = -a[i];
+}
+
+__global__ void axpy_kernel(double* __restrict__ y, double alpha, const double* __restrict__ x, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] += alpha * x[i];
+}
+
+__global__ void lincomb_kernel(double* __restrict__ o, const double* __restrict__ u, double s,
+                               const double* __restrict__ du, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) o[i] = u[i] + du[i] * s;
+}
+
+// run_steps history rotation (nonlinear.cpp:427-437): v_new, a_new by BDF2 then shift
+__global__ void bdf2_rotate_kernel(double* uo, double* uoo, double* vo, double* voo, double* ao,
+                                   const double* __restrict__ u, double dt, int n) {
+    const double idt = 1.0 / (2.0 * dt);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double un = u[i], ut = uo[i], utm1 = uoo[i], vt = vo[i], vtm1 = voo[i];
+        const double vn = ((un * 3.0 - ut * 4.0) + utm1) * idt;
+        const double an = ((vn * 3.0 - vt * 4.0) + vtm1) * idt;
+        uoo[i] = ut;
+        uo[i] = un;
+        voo[i] = vt;
+        vo[i] = vn;
+        ao[i] = an;
+    }
+}
+
+// predict_step_start, transient branch (nonlinear.cpp:165-171)
+__global__ void predict_kernel(double* __restrict__ u, const double* __restrict__ uo, const double* __restrict__ vo,
+                               const double* __restrict__ ao, double dt, int n) {
+    const double h = 0.5 * dt * dt;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        u[i] = (uo[i] + vo[i] * dt) + ao[i] * h;
+}
+
+int grid_for(int n) {
+    const int b = (n + 255) / 256;
+    return b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16;
+}
+
+}  // namespace
+
+int reduce_blocks(int n) {
+    const int b = (n + kT * 4 - 1) / (kT * 4);
+    return b < 1 ? 1 : (b > 148 * 8 ? 148 * 8 : b);
+}
+
+void launch_dot(const double* a, const double* b, int n, double* out, double* scratch, unsigned* counter,
+                cudaStream_t s) {
+    dot_kernel<<<reduce_blocks(n), kT, 0, s>>>(a, b, n, out, scratch, counter);
+}
+
+void launch_axpy_dot(double* w, const double* vi, const double* h, const double* vnext, int n, double* out,
+                     double* scratch, unsigned* counter, cudaStream_t s) {
+    axpy_dot_kernel<<<reduce_blocks(n), kT, 0, s>>>(w, vi, h, vnext, n, out, scratch, counter);
+}
+
+void launch_scale_div(const double* in, const double* divisor, double* out, int n, cudaStream_t s) {
+    scale_div_kernel<<<grid_for(n), 256, 0, s>>>(in, divisor, 0.0, out, n);
+}
+
+void launch_scale_div_host(const double* in, double divisor, double* out, int n, cudaStream_t s) {
+    scale_div_kernel<<<grid_for(n), 256, 0, s>>>(in, nullptr, divisor, out, n);
+}
+
+void launch_update(double* x, const double* V, const double* y, int j, int n, cudaStream_t s) {
+    update_kernel<<<grid_for(n), 256, 0, s>>>(x, V, y, j, n);
+}
+
+void launch_sub_from(const double* b, double* r, int n, cudaStream_t s) {
+    sub_from_kernel<<<grid_for(n), 256, 0, s>>>(b, r, n);
+}
+
+void launch_negate(const double* a, double* out, int n, cudaStream_t s) {
+    negate_kernel<<<grid_for(n), 256, 0, s>>>(a, out, n);
+}
+
+void launch_axpy_host(double* y, double alpha, const double* x, int n, cudaStream_t s) {
+    axpy_kernel<<<grid_for(n), 256, 0, s>>>(y, alpha, x, n);
+}
+
+void launch_lincomb(double* out, const double* u, double s, const double* du, int n, cudaStream_t st) {
+    lincomb_kernel<<<grid_for(n), 256, 0, st>>>(out, u, s, du, n);
+}
+
+void launch_bdf2_rotate(double* uo, double* uoo, double* vo, double* voo, double* ao, const double* u, double dt,
+                        int n, cudaStream_t s) {
+    bdf2_rotate_kernel<<<grid_for(n), 256, 0, s>>>(uo, uoo, vo, voo, ao, u, dt, n);
+}
+
+void launch_predict(double* u, const double* uo, const double* vo, const double* ao, double dt, int n,
+                    cudaStream_t s) {
+    predict_kernel<<<grid_for(n), 256, 0, s>>>(u, uo, vo, ao, dt, n);
+}
+
+}  // namespace sfv

@@ -1,0 +1,313 @@
+// precond_host.cpp — preconditioner setup on the host (once per run, as in the reference:
+// run_steps factors once and reuses the factor for every step, nonlinear.cpp:390-400).
+#include "precond_host.h"
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <numeric>
+
+#include "sfv_case.h"
+
+namespace sfv {
+
+std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar, bool transient, double rho,
+                          double dt, std::vector<ScalarCsr>& comps) {
+    const int nc = m.n_cells;
+    // pattern: diagonal plus one entry per internal face side, columns sorted (discretisation.cpp:223-236)
+    std::vector<int> rp(nc + 1, 1);
+    rp[0] = 0;
+    for (int f = 0; f < m.n_internal; ++f) {
+        ++rp[m.owner[f] + 1];
+        ++rp[m.neighbour[f] + 1];
+    }
+    for (int c = 0; c < nc; ++c) rp[c + 1] += rp[c];
+    std::vector<int> col(rp[nc]);
+    std::vector<int> fill(rp.begin(), rp.end() - 1);
+    for (int c = 0; c < nc; ++c) col[fill[c]++] = c;
+    for (int f = 0; f < m.n_internal; ++f) {
+        col[fill[m.owner[f]]++] = m.neighbour[f];
+        col[fill[m.neighbour[f]]++] = m.owner[f];
+    }
+    for (int c = 0; c < nc; ++c) std::sort(col.begin() + rp[c], col.begin() + rp[c + 1]);
+    bool sym = false;
+    for (int f = m.n_internal; f < m.n_faces(); ++f)
+        if (m.patches[m.face_patch[f]].kind == SFV_PATCH_SYMMETRY) {
+            sym = true;
+            const V3 n = g.normal[f];
+            if (n.x * n.y != 0.0 || n.x * n.z != 0.0 || n.y * n.z != 0.0)
+                return "preconditioner: symmetry plane not axis-aligned couples the displacement components";
+        }
+    const int ncomp = sym ? 3 : 1;
+    comps.assign(ncomp, ScalarCsr{});
+    auto find = [&](int i, int j) {
+        return static_cast<int>(std::lower_bound(col.begin() + rp[i], col.begin() + rp[i + 1], j) - col.begin());
+    };
+    for (int a = 0; a < ncomp; ++a) {
+        ScalarCsr& s = comps[a];
+        s.n = nc;
+        s.rp = rp;
+        s.col = col;
+        s.val.assign(col.size(), 0.0);
+        for (int f = 0; f < m.n_faces(); ++f) {
+            // alpha is unity in the matrix (discretisation.cpp:239-240)
+            const double coeff = kbar * g.delta_mag[f] / g.d_mag[f] * g.area_mag[f];
+            const int p = m.owner[f];
+            if (f < m.n_internal) {
+                const int n = m.neighbour[f];
+                s.val[find(p, n)] += coeff * 1.0;
+                s.val[find(n, p)] += coeff * 1.0;
+                s.val[find(p, p)] += -coeff * 1.0;
+                s.val[find(n, n)] += -coeff * 1.0;
+            } else {
+                const int kind = m.patches[m.face_patch[f]].kind;
+                if (kind == SFV_PATCH_DISPLACEMENT) {
+                    s.val[find(p, p)] += -coeff * 1.0;
+                } else if (kind == SFV_PATCH_SYMMETRY) {
+                    const double na = a == 0 ? g.normal[f].x : (a == 1 ? g.normal[f].y : g.normal[f].z);
+                    s.val[find(p, p)] += (na * na) * -coeff;
+                }
+            }
+        }
+        if (transient)
+            for (int c = 0; c < nc; ++c) s.val[find(c, c)] += (-2.25 * rho * g.volume[c] / (dt * dt)) * 1.0;
+    }
+    return "";
+}
+
+std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& out) {
+    const int n = a.n;
+    // symbolic phase: level-of-fill row merge in ascending column order (linalg.cpp:252-269)
+    out.n = n;
+    out.rp.assign(n + 1, 0);
+    out.col.clear();
+    std::vector<int> levs;
+    out.col.reserve(a.col.size() * 2);
+    levs.reserve(a.col.size() * 2);
+    std::vector<int> pos(n, 0), wcol, wlev;
+    for (int i = 0; i < n; ++i) {
+        wcol.clear();
+        wlev.clear();
+        for (int p = a.rp[i]; p < a.rp[i + 1]; ++p) {
+            wcol.push_back(a.col[p]);
+            wlev.push_back(0);
+        }
+        if (!std::binary_search(a.col.begin() + a.rp[i], a.col.begin() + a.rp[i + 1], i)) {
+            wcol.insert(std::lower_bound(wcol.begin(), wcol.end(), i), i);
+            wlev.push_back(0);
+        }
+        for (std::size_t x = 0; x < wcol.size(); ++x) pos[wcol[x]] = static_cast<int>(x) + 1;
+        for (std::size_t it = 0; it < wcol.size() && wcol[it] < i; ++it) {
+            const int k = wcol[it], lev_ik = wlev[it];
+            if (lev_ik >= level) continue;
+            for (int q = out.rp[k]; q < out.rp[k + 1]; ++q) {
+                const int j = out.col[q];
+                if (j <= k) continue;
+                const int lev = lev_ik + levs[q] + 1;
+                if (lev > level) continue;
+                if (pos[j]) {
+                    if (wlev[pos[j] - 1] > lev) wlev[pos[j] - 1] = lev;
+                } else {
+                    const std::size_t at = static_cast<std::size_t>(
+                        std::lower_bound(wcol.begin() + it + 1, wcol.end(), j) - wcol.begin());
+                    wcol.insert(wcol.begin() + at, j);
+                    wlev.insert(wlev.begin() + at, lev);
+                    for (std::size_t y = at; y < wcol.size(); ++y) pos[wcol[y]] = static_cast<int>(y) + 1;
+                }
+            }
+        }
+        for (std::size_t x = 0; x < wcol.size(); ++x) {
+            out.col.push_back(wcol[x]);
+            levs.push_back(wlev[x]);
+            pos[wcol[x]] = 0;
+        }
+        out.rp[i + 1] = static_cast<int>(out.col.size());
+    }
+    out.val.assign(out.col.size(), 0.0);
+    std::vector<int> diag(n, -1);
+    for (int i = 0; i < n; ++i) {
+        for (int q = out.rp[i]; q < out.rp[i + 1]; ++q) {
+            pos[out.col[q]] = q + 1;
+            if (out.col[q] == i) diag[i] = q;
+        }
+        for (int p = a.rp[i]; p < a.rp[i + 1]; ++p) out.val[pos[a.col[p]] - 1] = a.val[p];
+        for (int q = out.rp[i]; q < out.rp[i + 1]; ++q) pos[out.col[q]] = 0;
+    }
+    // numeric phase, IKJ on the fixed pattern (linalg.cpp:283-299)
+    for (int i = 0; i < n; ++i) {
+        for (int q = out.rp[i]; q < out.rp[i + 1]; ++q) pos[out.col[q]] = q + 1;
+        for (int p = out.rp[i]; p < out.rp[i + 1] && out.col[p] < i; ++p) {
+            const int k = out.col[p];
+            const double pivot = out.val[diag[k]];
+            if (pivot == 0.0 || !std::isfinite(pivot)) {
+                for (int q = out.rp[i]; q < out.rp[i + 1]; ++q) pos[out.col[q]] = 0;
+                return "ilu: zero pivot in row " + std::to_string(k);
+            }
+            const double lik = (out.val[p] /= pivot);
+            for (int q = out.rp[k]; q < out.rp[k + 1]; ++q) {
+                if (out.col[q] <= k) continue;
+                if (pos[out.col[q]]) out.val[pos[out.col[q]] - 1] -= lik * out.val[q];
+            }
+        }
+        for (int q = out.rp[i]; q < out.rp[i + 1]; ++q) pos[out.col[q]] = 0;
+        const double d = out.val[diag[i]];
+        if (d == 0.0 || !std::isfinite(d)) return "ilu: zero pivot in row " + std::to_string(i);
+    }
+    return "";
+}
+
+namespace {
+
+// rows grouped by dependency level, each level padded to a multiple of 32 positions
+void pack(const std::vector<int>& level, int n_levels, TriSchedule& t,
+          const std::function<void(int, std::vector<int>&, std::vector<double>&, double&)>& row_entries) {
+    const int n = static_cast<int>(level.size());
+    std::vector<int> count(n_levels, 0);
+    for (int i = 0; i < n; ++i) ++count[level[i]];
+    std::vector<int> start(n_levels + 1, 0);
+    for (int l = 0; l < n_levels; ++l) start[l + 1] = start[l] + (count[l] + 31) / 32 * 32;
+    t.n_pos = start[n_levels];
+    t.n_levels = n_levels;
+    t.order.assign(t.n_pos, -1);
+    std::vector<int> fill(start.begin(), start.end() - 1);
+    for (int i = 0; i < n; ++i) t.order[fill[level[i]]++] = i;
+    t.rp.assign(t.n_pos + 1, 0);
+    t.col.clear();
+    t.val.clear();
+    t.diag.assign(t.n_pos, 1.0);
+    std::vector<int> c;
+    std::vector<double> v;
+    for (int p = 0; p < t.n_pos; ++p) {
+        const int i = t.order[p];
+        if (i >= 0) {
+            c.clear();
+            v.clear();
+            double d = 1.0;
+            row_entries(i, c, v, d);
+            t.col.insert(t.col.end(), c.begin(), c.end());
+            t.val.insert(t.val.end(), v.begin(), v.end());
+            t.diag[p] = d;
+        }
+        t.rp[p + 1] = static_cast<int>(t.col.size());
+    }
+}
+
+}  // namespace
+
+void schedule_lower(const ScalarCsr& lu, TriSchedule& t) {
+    const int n = lu.n;
+    std::vector<int> level(n, 0);
+    int n_levels = 0;
+    for (int i = 0; i < n; ++i) {
+        int l = 0;
+        for (int p = lu.rp[i]; p < lu.rp[i + 1] && lu.col[p] < i; ++p) l = std::max(l, level[lu.col[p]] + 1);
+        level[i] = l;
+        n_levels = std::max(n_levels, l + 1);
+    }
+    // forward row: entries col < i in ascending column order (linalg.cpp:304-306)
+    pack(level, n_levels, t, [&](int i, std::vector<int>& c, std::vector<double>& v, double&) {
+        for (int p = lu.rp[i]; p < lu.rp[i + 1] && lu.col[p] < i; ++p) {
+            c.push_back(lu.col[p]);
+            v.push_back(lu.val[p]);
+        }
+    });
+}
+
+void schedule_upper(const ScalarCsr& lu, TriSchedule& t) {
+    const int n = lu.n;
+    std::vector<int> level(n, 0);
+    int n_levels = 0;
+    for (int i = n - 1; i >= 0; --i) {
+        int l = 0;
+        for (int p = lu.rp[i + 1] - 1; p >= lu.rp[i] && lu.col[p] > i; --p) l = std::max(l, level[lu.col[p]] + 1);
+        level[i] = l;
+        n_levels = std::max(n_levels, l + 1);
+    }
+    // backward row: entries col > i in descending column order, then the pivot (linalg.cpp:307-314)
+    pack(level, n_levels, t, [&](int i, std::vector<int>& c, std::vector<double>& v, double& d) {
+        d = 0.0;
+        for (int p = lu.rp[i + 1] - 1; p >= lu.rp[i] && lu.col[p] >= i; --p) {
+            if (lu.col[p] == i)
+                d = lu.val[p];
+            else {
+                c.push_back(lu.col[p]);
+                v.push_back(lu.val[p]);
+            }
+        }
+    });
+}
+
+std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out) {
+    const int n = a.n;
+    // reverse Cuthill-McKee ordering of the symmetric pattern
+    std::vector<int> deg(n);
+    for (int i = 0; i < n; ++i) deg[i] = a.rp[i + 1] - a.rp[i];
+    std::vector<int> by_deg(n);
+    std::iota(by_deg.begin(), by_deg.end(), 0);
+    std::stable_sort(by_deg.begin(), by_deg.end(), [&](int x, int y) { return deg[x] < deg[y]; });
+    std::vector<char> seen(n, 0);
+    std::vector<int> order;
+    order.reserve(n);
+    std::vector<int> nb;
+    for (int s0 : by_deg) {
+        if (seen[s0]) continue;
+        const std::size_t base = order.size();
+        order.push_back(s0);
+        seen[s0] = 1;
+        for (std::size_t h = base; h < order.size(); ++h) {
+            const int u = order[h];
+            nb.clear();
+            for (int p = a.rp[u]; p < a.rp[u + 1]; ++p)
+                if (!seen[a.col[p]] && a.val[p] != 0.0) {
+                    seen[a.col[p]] = 1;
+                    nb.push_back(a.col[p]);
+                }
+            std::stable_sort(nb.begin(), nb.end(), [&](int x, int y) { return deg[x] < deg[y]; });
+            order.insert(order.end(), nb.begin(), nb.end());
+        }
+    }
+    std::reverse(order.begin(), order.end());
+    auto bandwidth = [&](const std::vector<int>& inv_) {
+        int b = 0;
+        for (int i = 0; i < n; ++i)
+            for (int p = a.rp[i]; p < a.rp[i + 1]; ++p)
+                if (a.val[p] != 0.0) b = std::max(b, std::abs(inv_[i] - inv_[a.col[p]]));
+        return b;
+    };
+    std::vector<int> inv(n), ident(n);
+    for (int i = 0; i < n; ++i) inv[order[i]] = i;
+    std::iota(ident.begin(), ident.end(), 0);
+    int bw = bandwidth(inv);
+    if (const int bw0 = bandwidth(ident); bw0 <= bw) {  // keep the natural order when it is as narrow
+        bw = bw0;
+        order = ident;
+        inv = ident;
+    }
+    out.n = n;
+    out.bw = bw;
+    out.perm = order;
+    const int w = bw + 1;
+    out.l.assign(static_cast<std::size_t>(n) * w, 0.0);
+    auto L = [&](int i, int j) -> double& { return out.l[static_cast<std::size_t>(i) * w + (j - i + bw)]; };
+    for (int i = 0; i < n; ++i)
+        for (int p = a.rp[i]; p < a.rp[i + 1]; ++p) {
+            const int bi = inv[i], bj = inv[a.col[p]];
+            if (bj <= bi) L(bi, bj) = -a.val[p];  // -A is symmetric positive definite
+        }
+    for (int i = 0; i < n; ++i) {
+        const int j0 = std::max(0, i - bw);
+        for (int j = j0; j < i; ++j) {
+            double s = L(i, j);
+            const int k0 = std::max(j0, std::max(0, j - bw));
+            for (int k = k0; k < j; ++k) s -= L(i, k) * L(j, k);
+            L(i, j) = s / L(j, j);
+        }
+        double d = L(i, i);
+        for (int k = j0; k < i; ++k) d -= L(i, k) * L(i, k);
+        if (!(d > 0.0) || !std::isfinite(d)) return "lu: factorisation failed";
+        L(i, i) = std::sqrt(d);
+    }
+    return "";
+}
+
+}  // namespace sfv

@@ -1,0 +1,46 @@
+// precond_host.h — host setup of the reference's preconditioners on the cell graph.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "host_mesh.h"
+
+namespace sfv {
+
+struct ScalarCsr {
+    int n = 0;
+    std::vector<int> rp, col;  // columns ascending per row
+    std::vector<double> val;
+};
+
+// Per-component scalar matrices of assemble_approximate_jacobian
+// (/root/reference/proj/src/discretisation.cpp:216-262), accumulated entry by entry in
+// the reference's face order.  ncomp = 1 when every block is c*I (no symmetry faces),
+// 3 when blocks are diagonal (axis-aligned symmetry faces).  Returns "" or an error.
+std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar, bool transient, double rho,
+                          double dt, std::vector<ScalarCsr>& comps);
+
+// IlukPrecond ctor (linalg.cpp:251-300) on a scalar matrix: returns "" or the
+// IluBreakdown message.  The factor is the combined LU in one CSR pattern.
+std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& lu);
+
+// One triangular sweep in dependency-level order, levels padded to whole warps.
+struct TriSchedule {
+    int n_pos = 0, n_levels = 0;
+    std::vector<int> order, rp, col;
+    std::vector<double> val, diag;
+};
+void schedule_lower(const ScalarCsr& lu, TriSchedule& t);
+void schedule_upper(const ScalarCsr& lu, TriSchedule& t);
+
+// Banded Cholesky of -A after reverse Cuthill-McKee (A symmetric negative definite);
+// returns "" or "lu: factorisation failed".  Band row i holds L(i, i-bw .. i).
+struct BandChol {
+    int n = 0, bw = 0;
+    std::vector<int> perm;  // band index -> original row
+    std::vector<double> l;  // n * (bw + 1), l[i*(bw+1) + (j - i + bw)]
+};
+std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out);
+
+}  // namespace sfv

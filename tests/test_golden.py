@@ -1,0 +1,87 @@
+"""The C oracle (and, on a GPU box, the CUDA path) against the golden fixtures generated
+from the reference itself by tests/golden/make_golden.py."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from oracle.bind import OracleCase
+from paper_2502_17217_b200.abi import Mesh, Physics, solver_cfg
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+NAMES = [os.path.basename(p)[:-4] for p in GOLDEN]
+
+
+def load(path):
+    z = np.load(path)
+    m = Mesh(z["points"], z["face_offsets"], z["face_points"], z["owner"], z["neighbour"], int(z["n_cells"]),
+             int(z["n_internal"]), z["patch_kind"], z["patch_start"], z["patch_count"])
+    ph = Physics(int(z["law"]), float(z["mu"]), float(z["lam"]), total_lagrangian=bool(z["tl"]),
+                 transient=bool(z["transient"]), dt=float(z["dt"]), rho=float(z["rho"]), bc_value=z["bc_value"],
+                 bc_ramp=z["bc_ramp"])
+    return z, m, ph
+
+
+def test_fixtures_present():
+    assert len(GOLDEN) >= 5
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=NAMES)
+def test_oracle_matches_reference_golden(path):
+    z, m, ph = load(path)
+    o = OracleCase(m, ph)
+    o.set_time(float(z["time"]))
+    if ph.transient:
+        o.set_history(*z["hist"])
+    u, v = z["u"], z["v"]
+    r = o.residual(u)
+    assert np.array_equal(r, z["residual"])
+    assert np.array_equal(o.jv(u, r, v), z["jv"])
+    assert np.array_equal(o.stabilisation(u), z["stabilisation"])
+    if "ilu1_out" in z:
+        o.precond_create(3)
+        assert np.array_equal(o.precond_apply(z["ilu1_in"]), z["ilu1_out"])
+    o.precond_create(5)
+    lu = o.precond_apply(z["lu_in"])
+    assert np.linalg.norm(lu - z["lu_out"]) <= 1e-12 * np.linalg.norm(z["lu_out"])
+    o2 = OracleCase(m, ph)
+    f, reps, _ = o2.run_steps(z["steps_field0"], solver_cfg(r_tol=1e-8), len(z["steps_newton"]))
+    assert [r.outer_iters for r in reps] == list(z["steps_newton"])
+    assert [sum(r.summary()["krylov_per_newton"]) for r in reps] == list(z["steps_krylov"])
+    assert np.abs(f - z["steps_field"]).max() <= 1e-12 * max(np.abs(z["steps_field"]).max(), 1e-300)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", GOLDEN, ids=NAMES)
+def test_gpu_matches_reference_golden(path):
+    from paper_2502_17217_b200 import solver as sv
+    z, m, ph = load(path)
+    ev = sv.ResidualEvaluator(m, ph)
+    ev.set_time(float(z["time"]))
+    if ph.transient:
+        ev.set_history(*z["hist"])
+    u, v = z["u"], z["v"]
+    r = ev.residual(u).cpu().numpy()
+    tol = 0.0 if ph.law == 0 else 1e-12  # neo-Hookean: pow() is not correctly rounded
+    assert np.abs(r - z["residual"]).max() <= tol * np.abs(z["residual"]).max()
+    jv = sv.jacobian_vector_product(ev, u, z["residual"], v).cpu().numpy()
+    assert np.linalg.norm(jv - z["jv"]) <= 1e-6 * np.linalg.norm(z["jv"])
+    st = np.zeros_like(u)
+    import ctypes as C
+    ud, sd = sv.to_device(u), ev.empty()
+    ev._check(ev.L.sfv_stabilisation(ev.h, ud.data_ptr(), sd.data_ptr(), None))
+    assert np.abs(sd.cpu().numpy() - z["stabilisation"]).max() <= tol * np.abs(z["stabilisation"]).max() + 0.0
+    if "ilu1_out" in z:
+        pc = sv.make_preconditioner(ev, "ilu1")
+        assert np.array_equal(pc.solve(z["ilu1_in"]).cpu().numpy(), z["ilu1_out"])
+    pc = sv.make_preconditioner(ev, "lu")
+    lu = pc.solve(z["lu_in"]).cpu().numpy()
+    assert np.linalg.norm(lu - z["lu_out"]) <= 1e-10 * np.linalg.norm(z["lu_out"])
+    ev2 = sv.ResidualEvaluator(m, ph)
+    f, reps, _ = sv.run_steps(ev2, z["steps_field0"], solver_cfg(r_tol=1e-8), len(z["steps_newton"]))
+    assert [r.outer_iters for r in reps] == list(z["steps_newton"])
+    for a, b in zip([sum(r.summary()["krylov_per_newton"]) for r in reps], z["steps_krylov"]):
+        assert abs(a - b) <= max(1, r.outer_iters)  # +-1 per Newton step
+    f = f.cpu().numpy()
+    assert np.abs(f[0] - z["steps_field"][0]).max() <= 1e-8 * np.abs(z["steps_field"][0]).max()

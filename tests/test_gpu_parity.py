@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the C oracle on identical
+seeded inputs.  Bar (BASELINE.json north_star): R within 1e-12 relative L-inf (we
+hold bit-identity where the arithmetic allows), Newton-converged u within 1e-8,
+per-Newton GMRES counts within +-1."""
+import numpy as np
+import pytest
+
+from oracle.bind import OracleCase
+from paper_2502_17217_b200 import cases
+from paper_2502_17217_b200.abi import (LAW_HOOKE, LAW_NEO_HOOKEAN, PATCH_DISPLACEMENT as D, PATCH_SYMMETRY as S,
+                                       PATCH_TRACTION as T, Physics, solver_cfg)
+
+pytestmark = pytest.mark.gpu
+
+
+def _sv():
+    from paper_2502_17217_b200 import solver
+    return solver
+
+
+def _pair(mesh, phys, t=0.7):
+    sv = _sv()
+    ev = sv.ResidualEvaluator(mesh, phys)
+    orc = OracleCase(mesh, phys)
+    ev.set_time(t)
+    orc.set_time(t)
+    return ev, orc
+
+
+def _phys(law=LAW_HOOKE, tl=False, transient=False, npatch=6, **kw):
+    bv = np.zeros((npatch, 3))
+    bv[1] = (1e6, 2e5, -1e5)
+    bv[3] = (0.5e6, 0.0, 0.0)
+    if law == LAW_HOOKE:
+        mu, lam = cases.mu_from(200e9, 0.3), cases.lambda_from(200e9, 0.3)
+    else:
+        mu, lam = 0.4e6, 2e6
+    return Physics(law, mu, lam, total_lagrangian=tl, transient=transient, dt=1e-5, rho=7800.0, bc_value=bv,
+                   bc_ramp=np.ones(npatch, dtype=np.int32), **kw)
+
+
+BOX_CASES = {
+    "hooke_mixed": (dict(extents=(1.0, 1.2, 0.8), divisions=(9, 7, 6), kinds=[D, T, T, T, T, T], distort=0.15, seed=42),
+                    dict()),
+    "hooke_symmetry": (dict(extents=(1.0, 1.0, 1.0), divisions=(8, 6, 5), kinds=[D, T, S, T, S, T], distort=0.1,
+                            seed=3), dict()),
+    "neohookean_tl": (dict(extents=(4.0, 1.0, 1.0), divisions=(16, 5, 5), kinds=[D, D, T, T, T, T], distort=0.05,
+                           seed=42), dict(law=LAW_NEO_HOOKEAN, tl=True)),
+    "transient": (dict(extents=(1.0, 1.0, 1.0), divisions=(8, 8, 8), kinds=[D, T, T, T, T, T], distort=0.15, seed=42),
+                  dict(transient=True)),
+    "alpha": (dict(extents=(1.0, 1.0, 1.0), divisions=(6, 6, 6), kinds=[D, T, T, T, T, T], distort=0.2, seed=5),
+              dict(alpha=0.8)),
+}
+
+
+@pytest.mark.parametrize("name", list(BOX_CASES))
+def test_residual_bitwise(name):
+    margs, pargs = BOX_CASES[name]
+    sv = _sv()
+    mesh = sv.box_mesh(**margs)
+    phys = _phys(**pargs)
+    ev, orc = _pair(mesh, phys)
+    u, v = cases.jv_inputs(mesh, seed=11)
+    if pargs.get("law") == LAW_NEO_HOOKEAN:
+        u = u * 1e4  # O(1e-2) strains: genuinely nonlinear
+    if pargs.get("transient"):
+        rng = np.random.default_rng(1)
+        hist = [rng.uniform(-1e-6, 1e-6, 3 * mesh.n_cells) for _ in range(4)]
+        ev.set_history(*hist)
+        orc.set_history(*hist)
+    r_gpu = ev.residual(u).cpu().numpy()
+    r_orc = orc.residual(u)
+    err = np.abs(r_gpu - r_orc).max() / np.abs(r_orc).max()
+    assert err <= 1e-12
+    if pargs.get("law") != LAW_NEO_HOOKEAN:  # pow() is not correctly rounded on either side
+        assert np.array_equal(r_gpu, r_orc)
+
+
+@pytest.mark.parametrize("name", list(BOX_CASES))
+def test_jv_fixed_eps_and_fd(name):
+    margs, pargs = BOX_CASES[name]
+    sv = _sv()
+    mesh = sv.box_mesh(**margs)
+    phys = _phys(**pargs)
+    ev, orc = _pair(mesh, phys)
+    u, v = cases.jv_inputs(mesh, seed=5)
+    if pargs.get("law") == LAW_NEO_HOOKEAN:
+        u = u * 1e4
+    r_u = orc.residual(u)
+    eps = 3e-8
+    jv_gpu = sv.jacobian_vector_product(ev, u, r_u, v, eps=eps).cpu().numpy()
+    jv_orc = (orc.residual(u + eps * v) - r_u) / eps
+    if pargs.get("law") != LAW_NEO_HOOKEAN:
+        assert np.array_equal(jv_gpu, jv_orc)
+    else:
+        assert np.linalg.norm(jv_gpu - jv_orc) / np.linalg.norm(jv_orc) < 1e-6
+    # reference eps rule: only the norm reductions differ in order -> FD-noise-level agreement
+    jv = sv.jacobian_vector_product(ev, u, r_u, v).cpu().numpy()
+    ref = orc.jv(u, r_u, v)
+    assert np.linalg.norm(jv - ref) / np.linalg.norm(ref) < 1e-6
+    # zero direction short-circuits to exactly zero (nonlinear.cpp:110)
+    z = sv.jacobian_vector_product(ev, u, r_u, np.zeros_like(v)).cpu().numpy()
+    assert not z.any()
+
+
+def test_tets_residual_and_geometry():
+    sv = _sv()
+    case = cases.config("c5", n=6)
+    mesh = case.mesh()
+    ev, orc = _pair(mesh, case.physics, t=1.0)
+    g1, g2 = ev.geometry(), orc.geometry()
+    for k in g1:
+        assert np.array_equal(g1[k], g2[k]), k
+    u, v = cases.jv_inputs(mesh)
+    assert np.array_equal(ev.residual(u).cpu().numpy(), orc.residual(u))
+
+
+def test_geometry_bitwise_box():
+    sv = _sv()
+    case = cases.config("c2", n=10)
+    mesh = case.mesh()
+    ev, orc = _pair(mesh, case.physics)
+    g1, g2 = ev.geometry(), orc.geometry()
+    for k in g1:
+        assert np.array_equal(g1[k], g2[k]), k
+
+
+@pytest.mark.parametrize("kind,level", [("ilu0", 2), ("ilu1", 3), ("ilu2", 4)])
+def test_ilu_apply_bitwise(kind, level):
+    sv = _sv()
+    case = cases.config("c2", n=9)
+    mesh = case.mesh()
+    ev, orc = _pair(mesh, case.physics)
+    pc = sv.make_preconditioner(ev, kind)
+    orc.precond_create(level)
+    r = cases.uniform(9, 3 * mesh.n_cells)
+    z_gpu = pc.solve(r).cpu().numpy()
+    z_orc = orc.precond_apply(r)
+    assert np.array_equal(z_gpu, z_orc)  # equal up to the sign of zero
+    info = pc.info()
+    assert info["levels_fwd"] > 1 and info["nnz_L"] > 0
+
+
+def test_ilu_apply_transient_bitwise():
+    sv = _sv()
+    case = cases.config("c4", n=8)
+    mesh = case.mesh()
+    ev, orc = _pair(mesh, case.physics)
+    pc = sv.make_preconditioner(ev, "ilu1")
+    orc.precond_create(3)
+    r = cases.uniform(3, 3 * mesh.n_cells)
+    assert np.array_equal(pc.solve(r).cpu().numpy(), orc.precond_apply(r))
+
+
+def test_lu_apply_exact():
+    sv = _sv()
+    case = cases.config("c1", n=8)
+    mesh = case.mesh()
+    ev, orc = _pair(mesh, case.physics)
+    pc = sv.make_preconditioner(ev, "auto")  # 3*512 rows <= 30000 -> LU
+    orc.precond_create(0)
+    r = cases.uniform(4, 3 * mesh.n_cells)
+    z_gpu = pc.solve(r).cpu().numpy()
+    z_orc = orc.precond_apply(r)
+    assert np.linalg.norm(z_gpu - z_orc) / np.linalg.norm(z_orc) < 1e-11
+
+
+def _counts(reps):
+    return [r.summary()["krylov_per_newton"] for r in reps]
+
+
+@pytest.mark.parametrize("cfgname,n,pc", [("c1", 8, "auto"), ("c2", 10, "ilu1"), ("c3", 16, "ilu1"),
+                                          ("c4", 8, "ilu1")])
+def test_run_steps_parity(cfgname, n, pc):
+    sv = _sv()
+    case = cases.config(cfgname, n=n)
+    mesh = case.mesh()
+    ev = sv.ResidualEvaluator(mesh, case.physics)
+    orc = OracleCase(mesh, case.physics)
+    steps = min(case.n_steps, 3)
+    cfg = case.solver(preconditioner=pc)
+    f0 = case.initial_field(mesh)
+    fg, rg, _ = sv.run_steps(ev, f0, cfg, steps)
+    fo, ro, _ = orc.run_steps(f0, cfg, steps)
+    assert [r.status for r in rg] == [r.status for r in ro] == [0] * steps
+    cg, co = _counts(rg), _counts(ro)
+    for a, b in zip(cg, co):
+        assert len(a) == len(b), (cg, co)
+        assert all(abs(x - y) <= 1 for x, y in zip(a, b)), (cg, co)
+    u_g, u_o = fg.cpu().numpy()[0], fo[0]
+    assert np.abs(u_g - u_o).max() <= 1e-8 * np.abs(u_o).max()
+
+
+def test_gradient_failure_reported():
+    sv = _sv()
+    mesh = sv.box_mesh((2.0, 1.0, 1.0), (2, 1, 1), [T] * 6)
+    ev = sv.ResidualEvaluator(mesh, _phys())
+    with pytest.raises(sv.SolidfvError) as e:
+        ev.residual(np.zeros(6))
+    assert e.value.kind == "GradientFailure" and e.value.cell == 0
+    # J.v with v == 0 returns zeros before evaluating anything (nonlinear.cpp:110)
+    out = sv.jacobian_vector_product(ev, np.zeros(6), np.zeros(6), np.zeros(6)).cpu().numpy()
+    assert not out.any()
+
+
+def test_nan_and_inverted_errors():
+    sv = _sv()
+    mesh = sv.box_mesh((1.0, 1.0, 1.0), (4, 4, 4), [D, T, T, T, T, T])
+    ev = sv.ResidualEvaluator(mesh, _phys())
+    u = np.zeros(3 * mesh.n_cells)
+    u[3 * 17 + 1] = np.nan
+    with pytest.raises(sv.SolidfvError) as e:
+        ev.residual(u)
+    assert e.value.kind == "ResidualNan"
+    orc = OracleCase(mesh, _phys())
+    with pytest.raises(Exception) as e2:
+        orc.residual(u)
+    assert e.value.cell == e2.value.cell
+    with pytest.raises(sv.SolidfvError) as e3:
+        sv.jacobian_vector_product(ev, np.zeros_like(u), np.zeros_like(u), u)
+    assert e3.value.kind == "JvpNan"
+    ev2 = sv.ResidualEvaluator(mesh, _phys(law=LAW_NEO_HOOKEAN, tl=True))
+    u2 = np.zeros_like(u)
+    x = cases.cell_centres(mesh)
+    u2[0::3] = -2.0 * x[:, 0] * (x[:, 1] > 0.5)  # d(u_x)/dx = -2 in the upper half: det F < 0
+    orc2 = OracleCase(mesh, _phys(law=LAW_NEO_HOOKEAN, tl=True))
+    with pytest.raises(sv.SolidfvError) as e4:
+        ev2.residual(u2)
+    with pytest.raises(Exception) as e5:
+        orc2.residual(u2)
+    assert e4.value.kind == "InvertedElement" and e4.value.cell == e5.value.cell
