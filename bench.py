@@ -87,6 +87,22 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def max_over_ranks(x: float, device: str = "cuda") -> float:
+    """Max of a per-rank scalar over all ranks (identity when not distributed)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(steps_per_rank: int, ms_max: float, world: int) -> float:
+    """Whole-job J.v/s of N independent replicas timed by the slowest rank."""
+    return world * steps_per_rank / (ms_max / 1e3)
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -126,11 +142,14 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_2502_17217_b200 import cases
-    from paper_2502_17217_b200.solver import box_mesh  # host-only mesh generator
+    from oracle.bind import RefCase, OracleCase, ref_available, ref_box_mesh
     case = cases.config(args.config)
-    mesh = case.mesh()
+    if ref_available() and case.kind == "box":  # the reference's own generate_box_hex + distort_mesh
+        ma = case.mesh_args
+        mesh = ref_box_mesh(ma["extents"], ma["divisions"], ma["kinds"], ma.get("distort", 0.0), ma.get("seed", 0))
+    else:
+        mesh = case.mesh()
     u, v = cases.jv_inputs(mesh, extent=case.mesh_args.get("extents"))
-    from oracle.bind import RefCase, OracleCase, ref_available
     Cls = RefCase if ref_available() else OracleCase
     ref = Cls(mesh, case.physics)
     ref.set_time(1.0)
@@ -209,14 +228,9 @@ def run_ours(args):
     launches = ev.launch_count - l0
     ms = e0.elapsed_time(e1)
     ev._check(L.sfv_check_errors(h, None))
-    if ws > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-        if ws > 1:
-            torch.distributed.barrier()
+    ms = max_over_ranks(ms)
     ms_per = ms / args.steps
-    value = ws * args.steps / (ms / 1e3)
+    value = replica_throughput(args.steps, ms, ws)
     peak, peak_kind = _peaks()
     jv_bytes = ev.jv_bytes
     achieved = jv_bytes / (ms_per / 1e3) / 1e9
@@ -244,10 +258,7 @@ def run_ours(args):
         e2e_step()
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_n
-    if ws > 1:
-        t = torch.tensor([e2e_s], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(e2e_s)
 
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")

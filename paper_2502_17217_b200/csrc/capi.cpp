@@ -58,14 +58,19 @@ struct Status {  // pinned host mirror of the device scalars read per control de
 };
 
 struct TriDev {
-    DevBuf<int> order, rp, col;
-    DevBuf<double> val, diag;
+    DevBuf<int> order, rp, col, level_ptr, ell_col;
+    DevBuf<double> val, diag, ell_val;
     DevTri view;
     int n_levels = 0;
     size_t nnz = 0;
     bool upload(const TriSchedule& t, int n_rows) {
         bool ok = order.upload(t.order) && rp.upload(t.rp) && col.upload(t.col) && val.upload(t.val) &&
-                  diag.upload(t.diag);
+                  diag.upload(t.diag) && level_ptr.upload(t.level_ptr) && ell_col.upload(t.ell_col) &&
+                  ell_val.upload(t.ell_val);
+        view.level_ptr = level_ptr.p;
+        view.maxd = t.maxd;
+        view.ell_col = ell_col.p;
+        view.ell_val = ell_val.p;
         view.n = t.n_pos;
         view.n_rows = n_rows;
         view.n_levels = t.n_levels;
@@ -121,8 +126,15 @@ struct sfv_ctx {
     DevBuf<double> ily;  // forward-sweep scratch
     int tri_grid = 0;
     int tri_sleep = 0;
+    int tri_cluster = 16;
     DevBuf<double> dense_w[3];
     DevBuf<int> dense_perm[3];
+    // fused J.v kernel (jv_fused.cu)
+    bool use_fused = false;
+    FusedLayout fl;
+    DevBuf<int> f_tfp, f_own, f_oth, f_slots, f_index, f_flags, f_ticket;
+    DevBuf<double> f_geo, f_gring, f_fring;
+    int f_epoch = 0, f_grid = 0;
     // krylov workspace
     DevBuf<double> V, wv, rv, tv, xv, bv, hdev, ydev, ucand, rcand, uscratch, rscratch, dzero;
     int v_cap = 0;
@@ -204,6 +216,103 @@ std::string build_layout(sfv_ctx* c) {
     return "";
 }
 
+// Layout of the fused kernel: faces regrouped by the tile of their lower cell (sorted by
+// the slot they occupy there, then by cell, so ring writes of a warp are contiguous),
+// rings sized to the pipeline depth.  Returns "" when the fused path is unusable (too
+// wide a bandwidth for L2-resident rings), and the two-pass kernels are used instead.
+std::string build_fused_layout(sfv_ctx* c) {
+    const HostMesh& m = c->mesh;
+    const HostGeometry& g = c->geom;
+    const int nc = m.n_cells, nf = m.n_faces();
+    int bw = 0;
+    for (int f = 0; f < m.n_internal; ++f) bw = std::max(bw, std::abs(m.neighbour[f] - m.owner[f]));
+    std::vector<int> slot_of_owner(nf, 0), slot_of_nb(nf, 0);
+    for (int i = 0; i < nc; ++i)
+        for (int q = m.cf_off[i]; q < m.cf_off[i + 1]; ++q) {
+            const int f = m.cf[q];
+            if (m.owner[f] == i) slot_of_owner[f] = q - m.cf_off[i];
+            else slot_of_nb[f] = q - m.cf_off[i];
+        }
+    FusedLayout& L = c->fl;
+    L.ntiles = (nc + kTile - 1) / kTile;
+    L.lag = (bw + kTile - 1) / kTile + 1;
+    const int ctas = fused_resident_ctas(c->ph.law != SFV_LAW_HOOKE || c->ph.tl != 0);
+    c->f_grid = std::max(1, std::min(ctas, L.ntiles + L.lag));
+    L.ring_tiles = std::min(L.ntiles + L.lag + 1, L.lag + c->f_grid + 4);
+    L.ring_cells = L.ring_tiles * kTile;
+    const double ring_bytes = 8.0 * L.ring_cells * (9.0 + 6.0 * c->dm.slots);
+    if (ring_bytes > 96e6) return "rings exceed the L2 budget";
+    std::vector<int> order(nf);
+    for (int f = 0; f < nf; ++f) order[f] = f;
+    auto low = [&](int f) { return f < m.n_internal ? std::min(m.owner[f], m.neighbour[f]) : m.owner[f]; };
+    auto low_slot = [&](int f) {
+        return f < m.n_internal && m.neighbour[f] < m.owner[f] ? slot_of_nb[f] : slot_of_owner[f];
+    };
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        const int ta = low(a) / kTile, tb = low(b) / kTile;
+        if (ta != tb) return ta < tb;
+        const int sa = low_slot(a), sb = low_slot(b);
+        if (sa != sb) return sa < sb;
+        return low(a) < low(b);
+    });
+    std::vector<int> tfp(L.ntiles + 1, 0), own(nf), oth(nf), sl(nf), idx(nf);
+    std::vector<double> geo(8 * static_cast<size_t>(nf));
+    for (int x = 0; x < nf; ++x) {
+        const int f = order[x];
+        ++tfp[low(f) / kTile + 1];
+        own[x] = m.owner[f];
+        oth[x] = f < m.n_internal ? m.neighbour[f] : -(2 + m.face_patch[f]);
+        sl[x] = slot_of_owner[f] | ((f < m.n_internal ? slot_of_nb[f] : 0) << 8);
+        idx[x] = f;
+        const double vals[8] = {g.area[f].x, g.area[f].y, g.area[f].z, g.delta[f].x,
+                                g.delta[f].y, g.delta[f].z, g.d_mag[f], g.w[f]};
+        for (int k = 0; k < 8; ++k) geo[static_cast<size_t>(k) * nf + x] = vals[k];
+    }
+    for (int t = 0; t < L.ntiles; ++t) tfp[t + 1] += tfp[t];
+    if (!c->f_tfp.upload(tfp) || !c->f_own.upload(own) || !c->f_oth.upload(oth) || !c->f_slots.upload(sl) ||
+        !c->f_index.upload(idx) || !c->f_geo.upload(geo) || !c->f_gring.alloc(9 * static_cast<size_t>(L.ring_cells)) ||
+        !c->f_fring.alloc(6 * static_cast<size_t>(c->dm.slots) * L.ring_cells) ||
+        !c->f_flags.alloc(3 * static_cast<size_t>(L.ntiles)) || !c->f_ticket.alloc(1))
+        return "cuda: out of device memory for the fused layout";
+    cudaMemset(c->f_flags.p, 0, sizeof(int) * 3 * static_cast<size_t>(L.ntiles));
+    L.nfl = nf;
+    L.tile_face_ptr = c->f_tfp.p;
+    L.f_owner = c->f_own.p;
+    L.f_other = c->f_oth.p;
+    L.f_slots = c->f_slots.p;
+    L.f_index = c->f_index.p;
+    L.f_geo = c->f_geo.p;
+    L.gring = c->f_gring.p;
+    L.fring = c->f_fring.p;
+    c->use_fused = true;
+    if (const char* e = std::getenv("SFV_FUSED")) c->use_fused = std::atoi(e) != 0;
+    return "";
+}
+
+void launch_fused_pass(sfv_ctx* c, const Physics& ph, const double* u, const double* v, const double* eps,
+                       const double* r_u, double* out) {
+    FusedArgs a;
+    a.m = c->dm;
+    a.L = c->fl;
+    a.ph = ph;
+    a.pt = c->pt;
+    a.hist = c->hist;
+    a.u = u;
+    a.v = v ? v : u;
+    a.eps = eps;
+    a.r_u = r_u;
+    a.out = out;
+    a.err = c->err.p;
+    a.ticket = c->f_ticket.p;
+    a.a_done = c->f_flags.p;
+    a.b1_done = c->f_flags.p + c->fl.ntiles;
+    a.b2_done = c->f_flags.p + 2 * static_cast<size_t>(c->fl.ntiles);
+    a.epoch = ++c->f_epoch;
+    cudaMemsetAsync(c->f_ticket.p, 0, sizeof(int), c->stream);
+    launch_fused(a, c->f_grid, c->stream);
+    c->launches += 1;
+}
+
 void reset_err(sfv_ctx* c) { cudaMemsetAsync(c->err.p, 0x7f, sizeof(ErrWords), c->stream); }
 
 // read the error words (and optionally k doubles from hdev) in one D2H + sync
@@ -238,16 +347,25 @@ int gradient_failure(sfv_ctx* c) {
 }
 
 // R(u) into r (async; caller fetches + decodes)
-void residual_async(sfv_ctx* c, const double* u, double* r) {
-    launch_residual(c->dm, c->ph, c->pt, c->hist, u, nullptr, nullptr, nullptr, r, c->grad.p, c->err.p, c->stream);
+void residual_pass(sfv_ctx* c, const Physics& ph, const double* u, const double* v, const double* eps,
+                   const double* r_u, double* out) {
+    if (c->use_fused) {
+        launch_fused_pass(c, ph, u, v, eps, r_u, out);
+        return;
+    }
+    launch_residual(c->dm, ph, c->pt, c->hist, u, v, eps, r_u, out, c->grad.p, c->err.p, c->stream);
     c->launches += 2;
+}
+
+void residual_async(sfv_ctx* c, const double* u, double* r) {
+    residual_pass(c, c->ph, u, nullptr, nullptr, nullptr, r);
 }
 
 // J.v (async).  u_norm_cached: *scal[1] already holds |u| for this u.
 void jv_async(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out, bool u_norm_cached) {
     launch_jv_eps(u, v, c->n, c->red.p, c->counter.p, c->scal.p, c->scal.p + 1, u_norm_cached, c->stream);
-    launch_residual(c->dm, c->ph, c->pt, c->hist, u, v, c->scal.p, r_u, out, c->grad.p, c->err.p, c->stream);
-    c->launches += 3;
+    residual_pass(c, c->ph, u, v, c->scal.p, r_u, out);
+    c->launches += 1;
 }
 
 int residual_sync(sfv_ctx* c, const double* u, double* r) {
@@ -280,8 +398,8 @@ int precond_apply_async(sfv_ctx* c, const double* r, double* z) {
                 Ls.t[a] = c->L[a].view;
                 Us.t[a] = c->U[a].view;
             }
-            launch_ilu_apply(Ls, Us, c->pc_ncomp, r, c->ily.p, z, c->tri_grid, c->tri_sleep, c->stream);
-            c->launches += 4;
+            launch_ilu_apply(Ls, Us, c->pc_ncomp, r, c->ily.p, z, c->tri_grid, c->tri_sleep, c->tri_cluster, c->stream);
+            c->launches += c->tri_cluster > 0 ? 2 : 4;
             return SFV_OK;
         }
         case SFV_PRECOND_LU:
@@ -635,6 +753,10 @@ int precond_create(sfv_ctx* c, int kind) {
     c->tri_sleep = 0;
     if (const char* e = std::getenv("SFV_TRI_SLEEP_NS")) c->tri_sleep = std::max(0, std::atoi(e));
     c->tri_grid = std::max(1, sms * per_sm);
+    c->tri_cluster = 16;
+    if (const char* e = std::getenv("SFV_TRI_CLUSTER")) c->tri_cluster = std::max(0, std::min(16, std::atoi(e)));
+    for (int a = 0; a < c->pc_ncomp; ++a)  // the ELL cluster sweep holds rows of up to 32 entries
+        if (c->L[a].view.maxd > 32 || c->U[a].view.maxd > 32) c->tri_cluster = 0;
     c->pc_kind = kind;
     return c->cuda_check("ilu setup");
 }
@@ -752,6 +874,7 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     update_patch_values(c.get());
     e = build_layout(c.get());
     if (!e.empty()) return fail(e);
+    if (build_fused_layout(c.get()).rfind("cuda", 0) == 0) return fail("cuda: out of device memory");
     const size_t n = static_cast<size_t>(c->n);
     if (!c->grad.alloc(9 * static_cast<size_t>(c->nc)) || !c->red.alloc(2 * 148 * 8 + 64) || !c->scal.alloc(8) ||
         !c->counter.alloc(1) || !c->err.alloc(1) || !c->hdev.alloc(72) || !c->dzero.alloc(n))
@@ -863,8 +986,7 @@ int sfv_stabilisation(sfv_ctx* c, const double* u, double* r, int* cell) {
     reset_err(c);
     Physics ph = c->ph;
     ph.stab_only = 1;
-    launch_residual(c->dm, ph, c->pt, c->hist, u, nullptr, nullptr, nullptr, r, c->grad.p, c->err.p, c->stream);
-    c->launches += 2;
+    residual_pass(c, ph, u, nullptr, nullptr, nullptr, r);
     if (int e = c->cuda_check("stabilisation")) return e;
     return fetch(c, 0);
 }
@@ -933,8 +1055,7 @@ int sfv_jv_eps(sfv_ctx* c, const double* u, const double* r_u, const double* v, 
     reset_err(c);
     cudaMemcpyAsync(c->scal.p, &eps, sizeof(double), cudaMemcpyHostToDevice, c->stream);
     cudaStreamSynchronize(c->stream);
-    launch_residual(c->dm, c->ph, c->pt, c->hist, u, v, c->scal.p, r_u, out, c->grad.p, c->err.p, c->stream);
-    c->launches += 2;
+    residual_pass(c, c->ph, u, v, c->scal.p, r_u, out);
     if (int e = c->cuda_check("jv_eps")) return e;
     if (int e = fetch(c, 0)) return e;
     return decode_residual_errors(c, true);

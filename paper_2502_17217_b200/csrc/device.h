@@ -80,6 +80,40 @@ void launch_gradients(const DevMesh& m, const PatchTable& pt, const double* u, d
 void launch_jv_eps(const double* u, const double* v, int n, double* scratch, unsigned* counter,
                    double* eps_out, double* u_norm_inout, bool u_norm_cached, cudaStream_t s);
 
+// ---- jv_fused.cu: one persistent kernel per residual / J.v (see the file header)
+constexpr int kTile = 256;
+struct FusedLayout {
+    int ntiles = 0, lag = 0, ring_tiles = 0, ring_cells = 0, nfl = 0;
+    const int* tile_face_ptr = nullptr;  // [ntiles+1] faces computed by each tile (lower cell in tile)
+    const int* f_owner = nullptr;        // [nfl] reference owner
+    const int* f_other = nullptr;        // [nfl] neighbour, or -(2+patch) on a boundary face
+    const int* f_slots = nullptr;        // [nfl] slot in owner list | slot in neighbour list << 8
+    const int* f_index = nullptr;        // [nfl] reference face index
+    const double* f_geo = nullptr;       // [8*nfl] Gamma xyz, Delta xyz, |d|, w in processing order
+    double* gring = nullptr;             // [9*ring_cells]
+    double* fring = nullptr;             // [6*slots*ring_cells]
+};
+struct FusedArgs {
+    DevMesh m;
+    FusedLayout L;
+    Physics ph;
+    PatchTable pt;
+    History hist;
+    const double* u;
+    const double* v;
+    const double* eps;  // nullptr: plain residual
+    const double* r_u;
+    double* out;
+    ErrWords* err;
+    int* ticket;
+    int* a_done;
+    int* b1_done;
+    int* b2_done;
+    int epoch;
+};
+int fused_resident_ctas(bool general);  // resident CTAs of the persistent grid
+void launch_fused(const FusedArgs& a, int grid, cudaStream_t s);
+
 // ---- krylov.cu (deterministic fixed-order reductions)
 int reduce_blocks(int n);
 void launch_dot(const double* a, const double* b, int n, double* out, double* scratch, unsigned* counter,
@@ -106,10 +140,14 @@ struct DevTri {  // one triangular factor in level (processing) order
     int n_rows = 0;  // matrix rows
     int n_levels = 0;
     const int* order = nullptr;   // [n] row processed at position p
+    const int* level_ptr = nullptr;  // [n_levels+1] first position of each level
     const int* rp = nullptr;      // [n+1] entries of the row at position p
     const int* col = nullptr;     // [nnz]
     const double* val = nullptr;  // [nnz]
     const double* diag = nullptr; // [n] (upper only; per position)
+    int maxd = 0;                     // widest row
+    const int* ell_col = nullptr;     // [maxd*n] k-th entry of the row at position p, -1 = none
+    const double* ell_val = nullptr;  // [maxd*n]
 };
 // ILU apply on the cell graph, 3 interleaved right-hand sides (finding 4):
 // forward unit-lower then backward upper, row arithmetic in the reference's order.
@@ -118,8 +156,10 @@ struct TriSet {
 };
 // y is the forward-sweep scratch vector (3n); z receives M^{-1} r.  ncomp = 1: one
 // factor for all three components; ncomp = 3: factor t[k] for component k.
+// cluster > 0: level-synchronous sweep by one cluster of that many CTAs per component;
+// cluster == 0: sync-free sentinel polling on a persistent grid of `grid` CTAs.
 void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double* r, double* y, double* z, int grid,
-                      int sleep_ns, cudaStream_t s);
+                      int sleep_ns, int cluster, cudaStream_t s);
 // Exact dense apply z = A^{-1} r for the small-system LU path (3 interleaved RHS).
 void launch_dense_apply(const double* inv, int n, const double* r, double* z, cudaStream_t s);
 // Small-system exact preconditioner: W = (L L^T)^{-1} from a band Cholesky of -K, and

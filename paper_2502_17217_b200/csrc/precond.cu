@@ -16,9 +16,13 @@
 //
 // Dense apply: exact A^{-1} for the small-system "lu" path (make_preconditioner picks LU
 // at <= 30000 rows, nonlinear.cpp:355-356), a warp per row over 3 interleaved RHS.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "device.h"
+
+namespace cg = cooperative_groups;
 
 namespace sfv {
 namespace {
@@ -88,6 +92,89 @@ __global__ void __launch_bounds__(256) tri_kernel(TriSet set, const double* __re
         }
 #pragma unroll
         for (int k = 0; k < NRHS; ++k) __stcg(&dst[3 * i + comp + k], publish(z[k]));
+    }
+}
+
+// Level-synchronous sweep run by ONE thread-block cluster (up to 16 CTAs on 16 SMs):
+// the rows of a level are spread over the cluster's threads, then one
+// barrier.cluster (release/acquire at cluster scope, ~0.2 us) publishes them to the
+// next level.  Nothing spins, so no L2 bandwidth is burnt on polling.  Rows are stored
+// per level in ELL form and the NEXT level's matrix entries and right-hand side are
+// loaded into registers before the barrier, so the only loads left on the critical
+// path are the dependency values themselves (one L2 round trip per level).
+constexpr int kLvlChunk = 1024;
+
+template <bool UPPER, int NRHS, int MAXD>
+__global__ void __launch_bounds__(512) tri_cluster_kernel(TriSet set, const double* __restrict__ src, double* dst) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int comp = NRHS == 3 ? 0 : static_cast<int>(blockIdx.x / cluster.dim_blocks().x);
+    const DevTri& t = set.t[comp];
+    const int nthr = static_cast<int>(cluster.num_threads());
+    const int tid = static_cast<int>(cluster.block_rank()) * blockDim.x + threadIdx.x;
+    const int np = t.n;
+    // prefetched row (first row of this thread in the upcoming level)
+    int pi = -1;
+    int pc[MAXD];
+    double pv[MAXD], pz[NRHS], pd = 1.0;
+    auto fetch = [&](int p) {
+        pi = t.order[p];
+        if (pi < 0) return;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            pc[k] = k < t.maxd ? t.ell_col[static_cast<size_t>(k) * np + p] : -1;
+            pv[k] = pc[k] >= 0 ? t.ell_val[static_cast<size_t>(k) * np + p] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < NRHS; ++k) pz[k] = src[3 * pi + comp + k];
+        if (UPPER) pd = t.diag[p];
+    };
+    auto solve = [&]() {
+        double z[NRHS];
+#pragma unroll
+        for (int k = 0; k < NRHS; ++k) z[k] = pz[k];
+        double dv[MAXD][NRHS];
+#pragma unroll
+        for (int q = 0; q < MAXD; ++q)  // all dependency loads in flight together
+            if (pc[q] >= 0)
+#pragma unroll
+                for (int k = 0; k < NRHS; ++k) dv[q][k] = __ldcg(&dst[3 * pc[q] + comp + k]);
+#pragma unroll
+        for (int q = 0; q < MAXD; ++q)  // then the reference's order of subtraction
+            if (pc[q] >= 0)
+#pragma unroll
+                for (int k = 0; k < NRHS; ++k) z[k] -= pv[q] * dv[q][k];
+        if (UPPER)
+#pragma unroll
+            for (int k = 0; k < NRHS; ++k) z[k] /= pd;
+#pragma unroll
+        for (int k = 0; k < NRHS; ++k) __stcg(&dst[3 * pi + comp + k], z[k]);
+    };
+    // level boundaries staged once in shared memory (chunks of kLvlChunk levels)
+    __shared__ int lp[kLvlChunk + 2];
+    auto stage_levels = [&](int base) {
+        __syncthreads();
+        for (int x = threadIdx.x; x < kLvlChunk + 2; x += blockDim.x)
+            lp[x] = base + x <= t.n_levels ? t.level_ptr[base + x] : t.level_ptr[t.n_levels];
+        __syncthreads();
+    };
+    stage_levels(0);
+    if (t.n_levels > 0 && lp[0] + tid < lp[1]) fetch(lp[0] + tid);
+    for (int l = 0; l < t.n_levels; ++l) {
+        const int ll = l % kLvlChunk;
+        const int p0 = lp[ll] + tid, pend = lp[ll + 1];
+        if (p0 < pend && pi >= 0) solve();
+        for (int p = p0 + nthr; p < pend; p += nthr) {  // levels wider than the cluster
+            fetch(p);
+            if (pi >= 0) solve();
+        }
+        pi = -1;
+        // split-phase barrier: publish this level (release), prefetch the next level's
+        // rows while the other CTAs arrive, then acquire.
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        const int q0 = lp[ll + 1] + tid;
+        if (l + 1 < t.n_levels && q0 < lp[ll + 2]) fetch(q0);
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (ll == kLvlChunk - 1) stage_levels(l + 1);
     }
 }
 
@@ -185,9 +272,48 @@ void launch_dense_apply_perm(const double* W, int n, const int* perm, const doub
         dense_apply_perm_kernel<1><<<(n + 7) / 8, 256, 0, s>>>(W, n, perm, r, z, comp);
 }
 
+template <bool UPPER, int NRHS, int MAXD>
+static cudaError_t launch_cluster_w(const TriSet& set, int ncomp, int csize, const double* src, double* dst,
+                                    cudaStream_t s) {
+    auto kern = tri_cluster_kernel<UPPER, NRHS, MAXD>;
+    if (csize > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csize * (NRHS == 3 ? 1 : ncomp));
+    cfg.blockDim = dim3(512);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, set, src, dst);
+}
+
+template <bool UPPER, int NRHS>
+static cudaError_t launch_cluster(const TriSet& set, int ncomp, int csize, const double* src, double* dst,
+                                  cudaStream_t s) {
+    int maxd = 0;
+    for (int a = 0; a < (NRHS == 3 ? 1 : ncomp); ++a) maxd = std::max(maxd, set.t[a].maxd);
+    if (maxd <= 8) return launch_cluster_w<UPPER, NRHS, 8>(set, ncomp, csize, src, dst, s);
+    if (maxd <= 16) return launch_cluster_w<UPPER, NRHS, 16>(set, ncomp, csize, src, dst, s);
+    return launch_cluster_w<UPPER, NRHS, 32>(set, ncomp, csize, src, dst, s);
+}
+
 void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double* r, double* y, double* z, int grid,
-                      int sleep_ns, cudaStream_t s) {
-    const int n3 = 3 * L.t[0].n_rows;
+                      int sleep_ns, int cluster, cudaStream_t s) {
+    if (cluster > 0) {  // level-synchronous cluster sweep (default)
+        if (ncomp == 1) {
+            launch_cluster<false, 3>(L, 1, cluster, r, y, s);
+            launch_cluster<true, 3>(U, 1, cluster, y, z, s);
+        } else {
+            launch_cluster<false, 1>(L, 3, cluster, r, y, s);
+            launch_cluster<true, 1>(U, 3, cluster, y, z, s);
+        }
+        return;
+    }
+    const int n3 = 3 * L.t[0].n_rows;  // sync-free sentinel polling (SFV_TRI_CLUSTER=0)
     fill_sentinel_kernel<<<592, 256, 0, s>>>(y, n3);
     fill_sentinel_kernel<<<592, 256, 0, s>>>(z, n3);
     if (ncomp == 1) {

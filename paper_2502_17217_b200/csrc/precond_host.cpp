@@ -168,6 +168,7 @@ void pack(const std::vector<int>& level, int n_levels, TriSchedule& t,
     for (int l = 0; l < n_levels; ++l) start[l + 1] = start[l] + (count[l] + 31) / 32 * 32;
     t.n_pos = start[n_levels];
     t.n_levels = n_levels;
+    t.level_ptr = start;
     t.order.assign(t.n_pos, -1);
     std::vector<int> fill(start.begin(), start.end() - 1);
     for (int i = 0; i < n; ++i) t.order[fill[level[i]]++] = i;
@@ -190,6 +191,15 @@ void pack(const std::vector<int>& level, int n_levels, TriSchedule& t,
         }
         t.rp[p + 1] = static_cast<int>(t.col.size());
     }
+    t.maxd = 0;
+    for (int p = 0; p < t.n_pos; ++p) t.maxd = std::max(t.maxd, t.rp[p + 1] - t.rp[p]);
+    t.ell_col.assign(static_cast<size_t>(t.maxd) * t.n_pos, -1);
+    t.ell_val.assign(static_cast<size_t>(t.maxd) * t.n_pos, 0.0);
+    for (int p = 0; p < t.n_pos; ++p)
+        for (int q = t.rp[p]; q < t.rp[p + 1]; ++q) {
+            t.ell_col[static_cast<size_t>(q - t.rp[p]) * t.n_pos + p] = t.col[q];
+            t.ell_val[static_cast<size_t>(q - t.rp[p]) * t.n_pos + p] = t.val[q];
+        }
 }
 
 }  // namespace

@@ -28,8 +28,11 @@ std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& lu);
 // One triangular sweep in dependency-level order, levels padded to whole warps.
 struct TriSchedule {
     int n_pos = 0, n_levels = 0;
-    std::vector<int> order, rp, col;
+    std::vector<int> order, rp, col, level_ptr;
     std::vector<double> val, diag;
+    int maxd = 0;
+    std::vector<int> ell_col;  // [maxd * n_pos], entry k of position p at k * n_pos + p
+    std::vector<double> ell_val;
 };
 void schedule_lower(const ScalarCsr& lu, TriSchedule& t);
 void schedule_upper(const ScalarCsr& lu, TriSchedule& t);
