@@ -58,7 +58,7 @@ struct Status {  // pinned host mirror of the device scalars read per control de
 };
 
 struct TriDev {
-    DevBuf<int> order, rp, col, level_ptr, ell_col;
+    DevBuf<int> order, rp, col, level_ptr, ell_col, ell_pcol, u2l;
     DevBuf<double> val, diag, ell_val;
     DevTri view;
     int n_levels = 0;
@@ -66,7 +66,8 @@ struct TriDev {
     bool upload(const TriSchedule& t, int n_rows) {
         bool ok = order.upload(t.order) && rp.upload(t.rp) && col.upload(t.col) && val.upload(t.val) &&
                   diag.upload(t.diag) && level_ptr.upload(t.level_ptr) && ell_col.upload(t.ell_col) &&
-                  ell_val.upload(t.ell_val);
+                  ell_val.upload(t.ell_val) && ell_pcol.upload(t.ell_pcol);
+        view.ell_pcol = ell_pcol.p;
         view.level_ptr = level_ptr.p;
         view.maxd = t.maxd;
         view.ell_col = ell_col.p;
@@ -123,10 +124,14 @@ struct sfv_ctx {
     int pc_kind = SFV_PRECOND_NONE;
     int pc_ncomp = 1;
     TriDev L[3], U[3];
-    DevBuf<double> ily;  // forward-sweep scratch
+    DevBuf<double> ily, ipa, ipb;  // forward-sweep scratch, position-space scratch
     int tri_grid = 0;
     int tri_sleep = 0;
     int tri_cluster = 16;
+    bool ring_ok = false;
+    bool stream_ok = false;
+    StreamSet sL{}, sU{};
+    DevBuf<unsigned char> srec[6];  // streamed-sweep records: L0..L2, U0..U2
     DevBuf<double> dense_w[3];
     DevBuf<int> dense_perm[3];
     // fused J.v kernel (jv_fused.cu)
@@ -398,7 +403,8 @@ int precond_apply_async(sfv_ctx* c, const double* r, double* z) {
                 Ls.t[a] = c->L[a].view;
                 Us.t[a] = c->U[a].view;
             }
-            launch_ilu_apply(Ls, Us, c->pc_ncomp, r, c->ily.p, z, c->tri_grid, c->tri_sleep, c->tri_cluster, c->stream);
+            launch_ilu_apply(Ls, Us, c->pc_ncomp, r, c->ily.p, z, c->tri_grid, c->tri_sleep, c->tri_cluster, c->ipa.p,
+                             c->ipb.p, &c->sL, &c->sU, c->stream);
             c->launches += c->tri_cluster > 0 ? 2 : 4;
             return SFV_OK;
         }
@@ -734,14 +740,76 @@ int precond_create(sfv_ctx* c, int kind) {
             if (!m3.empty()) return c->fail(SFV_ERR_ILU_BREAKDOWN, -1, m3);
         }
     }
+    int max_pos = 0;
+    bool ring_ok_all = true, stream_ok_all = true;
+    std::vector<TriSchedule> scheds;  // L0, U0, L1, U1, ...
     for (size_t a = 0; a < lus.size(); ++a) {
         TriSchedule tl, tu;
         schedule_lower(lus[a], tl);
         schedule_upper(lus[a], tu);
-        if (!c->L[a].upload(tl, c->nc) || !c->U[a].upload(tu, c->nc))
+        std::vector<int> u2l(tu.n_pos, -1);  // backward-sweep position -> forward-sweep position
+        for (int p = 0; p < tu.n_pos; ++p)
+            if (tu.order[p] >= 0) u2l[p] = tl.pos[tu.order[p]];
+        if (!c->L[a].upload(tl, c->nc) || !c->U[a].upload(tu, c->nc) || !c->U[a].u2l.upload(u2l))
             return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
+        c->U[a].view.u2l = c->U[a].u2l.p;
+        max_pos = std::max(max_pos, std::max(tl.n_pos, tu.n_pos));
+        for (const TriSchedule* ts : {&tl, &tu}) {  // DSMEM ring admissibility
+            int dist = 0, width = 0;
+            for (int l = 0; l < ts->n_levels; ++l) width = std::max(width, ts->level_ptr[l + 1] - ts->level_ptr[l]);
+            for (size_t q = 0; q < ts->ell_pcol.size(); ++q)
+                if (ts->ell_pcol[q] >= 0) dist = std::max(dist, static_cast<int>(q % ts->n_pos) - ts->ell_pcol[q]);
+            if (dist + 2 * width + 64 > ilu_ring_window()) ring_ok_all = false;
+        }
+        scheds.push_back(std::move(tl));
+        scheds.push_back(std::move(tu));
     }
-    if (!c->ily.alloc(c->n)) return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
+    // streamed sweep (precond_stream.cu): rows per CTA-slice, the smallest safe value ring,
+    // and as many cp.async stages as the remaining shared memory holds
+    {
+        int max_rows = 32;
+        for (const TriSchedule& ts : scheds)
+            for (int l = 0; l < ts.n_levels; ++l) {
+                const int nch = (ts.level_ptr[l + 1] - ts.level_ptr[l]) / 32;
+                max_rows = std::max(max_rows, (nch + kStreamCluster - 1) / kStreamCluster * 32);
+            }
+        std::vector<std::vector<StreamRecord>> recs(scheds.size());
+        int ring = 0;
+        if (max_rows <= kStreamMaxRows)
+            for (int cand : {1024, 2048, 3072, 4096}) {
+                bool ok = true;
+                for (size_t x = 0; x < scheds.size() && ok; ++x)
+                    ok = build_stream_records(scheds[x], kStreamCluster, cand, max_rows, recs[x]);
+                if (ok) {
+                    ring = cand;
+                    break;
+                }
+            }
+        const int smem_cap = 232448;
+        const int stages = ring ? std::min(8, (smem_cap - ring * 32 - 4200) / (max_rows * 120)) : 0;
+        stream_ok_all = ring > 0 && stages >= 3;
+        if (stream_ok_all) {
+            for (size_t x = 0; x < scheds.size(); ++x) {
+                DevBuf<unsigned char>& b = c->srec[(x % 2) * 3 + x / 2];
+                if (!b.alloc(recs[x].size() * sizeof(StreamRecord)) ||
+                    cudaMemcpy(b.p, recs[x].data(), b.bytes(), cudaMemcpyHostToDevice) != cudaSuccess)
+                    return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
+                const int a = static_cast<int>(x / 2);
+                DevStream ds{scheds[x].n_levels, x % 2 ? c->U[a].view.level_ptr : c->L[a].view.level_ptr, b.p};
+                (x % 2 ? c->sU : c->sL).t[a] = ds;
+            }
+            for (StreamSet* ss : {&c->sL, &c->sU}) {
+                ss->ring = ring;
+                ss->max_rows = max_rows;
+                ss->stages = stages;
+            }
+        }
+    }
+    c->ring_ok = ring_ok_all;
+    c->stream_ok = stream_ok_all;
+    if (!c->ily.alloc(c->n) || !c->ipa.alloc(3 * static_cast<size_t>(max_pos)) ||
+        !c->ipb.alloc(3 * static_cast<size_t>(max_pos)))
+        return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
     // persistent grid: every CTA resident (<= 8 CTAs of 256 threads per SM fit), so each
     // awaited row belongs to a running thread.  Knobs for tuning: SFV_TRI_CTAS_PER_SM,
     // SFV_TRI_SLEEP_NS.
@@ -753,8 +821,17 @@ int precond_create(sfv_ctx* c, int kind) {
     c->tri_sleep = 0;
     if (const char* e = std::getenv("SFV_TRI_SLEEP_NS")) c->tri_sleep = std::max(0, std::atoi(e));
     c->tri_grid = std::max(1, sms * per_sm);
-    c->tri_cluster = 16;
-    if (const char* e = std::getenv("SFV_TRI_CLUSTER")) c->tri_cluster = std::max(0, std::min(16, std::atoi(e)));
+    if (const char* e = std::getenv("SFV_TRI_CTAS")) c->tri_grid = std::max(1, std::atoi(e));
+    // default: the DSMEM-ring sweep when its window covers every dependency distance plus
+    // two levels (so no ring slot is overwritten before its last reader ran); else the
+    // L2 cluster sweep
+    c->tri_cluster = c->stream_ok ? kStreamMode : (c->ring_ok ? kDsRingMode : 16);
+    if (const char* e = std::getenv("SFV_TRI_CLUSTER")) {
+        const int v = std::atoi(e);
+        c->tri_cluster = (v == kDsRingMode && c->ring_ok) || (v == kStreamMode && c->stream_ok)
+                             ? v
+                             : std::max(0, std::min(16, v));
+    }
     for (int a = 0; a < c->pc_ncomp; ++a)  // the ELL cluster sweep holds rows of up to 32 entries
         if (c->L[a].view.maxd > 32 || c->U[a].view.maxd > 32) c->tri_cluster = 0;
     c->pc_kind = kind;

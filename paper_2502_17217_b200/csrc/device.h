@@ -147,6 +147,8 @@ struct DevTri {  // one triangular factor in level (processing) order
     const double* diag = nullptr; // [n] (upper only; per position)
     int maxd = 0;                     // widest row
     const int* ell_col = nullptr;     // [maxd*n] k-th entry of the row at position p, -1 = none
+    const int* ell_pcol = nullptr;    // [maxd*n] the same entries as positions (position-space sweeps)
+    const int* u2l = nullptr;         // [n] (upper only) lower-sweep position of the row at position p
     const double* ell_val = nullptr;  // [maxd*n]
 };
 // ILU apply on the cell graph, 3 interleaved right-hand sides (finding 4):
@@ -158,8 +160,34 @@ struct TriSet {
 // factor for all three components; ncomp = 3: factor t[k] for component k.
 // cluster > 0: level-synchronous sweep by one cluster of that many CTAs per component;
 // cluster == 0: sync-free sentinel polling on a persistent grid of `grid` CTAs.
+// pa, pb: position-space scratch vectors of 3 * max positions (cluster > 0 path).
+// cluster == kDsRingMode selects the DSMEM-ring sweep (needs ring_window() >= largest
+// dependency distance + 2 x widest level, checked at setup).
+constexpr int kDsRingMode = 100;
+int ilu_ring_window();
+
+// ---- precond_stream.cu: streamed sweep (default; records built by build_stream_records)
+constexpr int kStreamMode = 200;
+constexpr int kStreamCluster = 16;
+constexpr int kStreamRing = 3072;    // 32-byte value slots per CTA
+constexpr int kStreamMaxRows = 256;  // positions per CTA per level
+struct DevStream {
+    int n_levels = 0;
+    const int* level_ptr = nullptr;  // position-space level boundaries (same as DevTri)
+    const void* rec = nullptr;       // [n_pos] 96-byte records
+};
+struct StreamSet {
+    DevStream t[3];
+    int ring = 0;      // value slots per CTA
+    int max_rows = 0;  // positions per CTA per level (multiple of 32)
+    int stages = 3;    // cp.async pipeline depth (levels in flight + 1)
+};
+int stream_smem_bytes(int ring, int max_rows, int stages);
+cudaError_t launch_tri_stream(const StreamSet& set, bool upper, int ncomp, const double* src, double* dst,
+                              cudaStream_t s);
 void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double* r, double* y, double* z, int grid,
-                      int sleep_ns, int cluster, cudaStream_t s);
+                      int sleep_ns, int cluster, double* pa, double* pb, const struct StreamSet* SL,
+                      const struct StreamSet* SU, cudaStream_t s);
 // Exact dense apply z = A^{-1} r for the small-system LU path (3 interleaved RHS).
 void launch_dense_apply(const double* inv, int n, const double* r, double* z, cudaStream_t s);
 // Small-system exact preconditioner: W = (L L^T)^{-1} from a band Cholesky of -K, and

@@ -24,6 +24,17 @@
 
 namespace cg = cooperative_groups;
 
+// Timing probes (scripts/probes): build with -DSFV_PROBE_MASK=m to drop parts of the DSMEM
+// sweep (1: dependency loads, 2: pivot divide, 4: HBM copies).  Results are then wrong;
+// production builds use 0.
+#ifndef SFV_PROBE_MASK
+#define SFV_PROBE_MASK 0
+#endif
+#define SFV_PROBE(b) (!(SFV_PROBE_MASK & (b)))
+#ifndef SFV_DS_MODE
+#define SFV_DS_MODE 0
+#endif
+
 namespace sfv {
 namespace {
 
@@ -95,37 +106,44 @@ __global__ void __launch_bounds__(256) tri_kernel(TriSet set, const double* __re
     }
 }
 
-// Level-synchronous sweep run by ONE thread-block cluster (up to 16 CTAs on 16 SMs):
-// the rows of a level are spread over the cluster's threads, then one
-// barrier.cluster (release/acquire at cluster scope, ~0.2 us) publishes them to the
-// next level.  Nothing spins, so no L2 bandwidth is burnt on polling.  Rows are stored
-// per level in ELL form and the NEXT level's matrix entries and right-hand side are
-// loaded into registers before the barrier, so the only loads left on the critical
-// path are the dependency values themselves (one L2 round trip per level).
+// Level-synchronous sweep in POSITION space, run by one thread-block cluster (or one CTA):
+// rows are renumbered in dependency-level order at setup (columns too), the right-hand
+// side is gathered into that order once, and the result scattered back once, so every
+// load a row needs except its dependency values is contiguous, coalesced and independent
+// of the sweep.  The next level's rows are loaded into registers between the arrive and
+// the wait of a split-phase barrier.cluster (release/acquire at cluster scope); the only
+// loads on the critical path are the dependency values (one L2 round trip per level).
 constexpr int kLvlChunk = 1024;
 
-template <bool UPPER, int NRHS, int MAXD>
-__global__ void __launch_bounds__(512) tri_cluster_kernel(TriSet set, const double* __restrict__ src, double* dst) {
-    cg::cluster_group cluster = cg::this_cluster();
-    const int comp = NRHS == 3 ? 0 : static_cast<int>(blockIdx.x / cluster.dim_blocks().x);
+template <bool UPPER, int NRHS, int MAXD, bool SOLO>
+__global__ void __launch_bounds__(SOLO ? 1024 : 512) tri_cluster_kernel(TriSet set, const double* __restrict__ src,
+                                                                         double* dst) {
+    int comp, nthr, tid;
+    if (SOLO) {  // one CTA per component
+        comp = NRHS == 3 ? 0 : static_cast<int>(blockIdx.x);
+        nthr = blockDim.x;
+        tid = threadIdx.x;
+    } else {
+        cg::cluster_group cluster = cg::this_cluster();
+        comp = NRHS == 3 ? 0 : static_cast<int>(blockIdx.x / cluster.dim_blocks().x);
+        nthr = static_cast<int>(cluster.num_threads());
+        tid = static_cast<int>(cluster.block_rank()) * blockDim.x + threadIdx.x;
+    }
     const DevTri& t = set.t[comp];
-    const int nthr = static_cast<int>(cluster.num_threads());
-    const int tid = static_cast<int>(cluster.block_rank()) * blockDim.x + threadIdx.x;
     const int np = t.n;
-    // prefetched row (first row of this thread in the upcoming level)
-    int pi = -1;
+    // the prefetched row (this thread's first position in the upcoming level)
+    int pp = -1;
     int pc[MAXD];
     double pv[MAXD], pz[NRHS], pd = 1.0;
     auto fetch = [&](int p) {
-        pi = t.order[p];
-        if (pi < 0) return;
+        pp = p;
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) {
-            pc[k] = k < t.maxd ? t.ell_col[static_cast<size_t>(k) * np + p] : -1;
-            pv[k] = pc[k] >= 0 ? t.ell_val[static_cast<size_t>(k) * np + p] : 0.0;
+            pc[k] = k < t.maxd ? t.ell_pcol[static_cast<size_t>(k) * np + p] : -1;
+            pv[k] = k < t.maxd ? t.ell_val[static_cast<size_t>(k) * np + p] : 0.0;
         }
 #pragma unroll
-        for (int k = 0; k < NRHS; ++k) pz[k] = src[3 * pi + comp + k];
+        for (int k = 0; k < NRHS; ++k) pz[k] = src[3 * static_cast<size_t>(p) + comp + k];
         if (UPPER) pd = t.diag[p];
     };
     auto solve = [&]() {
@@ -137,7 +155,10 @@ __global__ void __launch_bounds__(512) tri_cluster_kernel(TriSet set, const doub
         for (int q = 0; q < MAXD; ++q)  // all dependency loads in flight together
             if (pc[q] >= 0)
 #pragma unroll
-                for (int k = 0; k < NRHS; ++k) dv[q][k] = __ldcg(&dst[3 * pc[q] + comp + k]);
+                for (int k = 0; k < NRHS; ++k) {
+                    const size_t a = 3 * static_cast<size_t>(pc[q]) + comp + k;
+                    dv[q][k] = SOLO ? dst[a] : __ldcg(&dst[a]);
+                }
 #pragma unroll
         for (int q = 0; q < MAXD; ++q)  // then the reference's order of subtraction
             if (pc[q] >= 0)
@@ -147,9 +168,13 @@ __global__ void __launch_bounds__(512) tri_cluster_kernel(TriSet set, const doub
 #pragma unroll
             for (int k = 0; k < NRHS; ++k) z[k] /= pd;
 #pragma unroll
-        for (int k = 0; k < NRHS; ++k) __stcg(&dst[3 * pi + comp + k], z[k]);
+        for (int k = 0; k < NRHS; ++k) {
+            const size_t a = 3 * static_cast<size_t>(pp) + comp + k;
+            if (SOLO) dst[a] = z[k];
+            else __stcg(&dst[a], z[k]);
+        }
     };
-    // level boundaries staged once in shared memory (chunks of kLvlChunk levels)
+    // level boundaries staged in shared memory (chunks of kLvlChunk levels)
     __shared__ int lp[kLvlChunk + 2];
     auto stage_levels = [&](int base) {
         __syncthreads();
@@ -162,19 +187,236 @@ __global__ void __launch_bounds__(512) tri_cluster_kernel(TriSet set, const doub
     for (int l = 0; l < t.n_levels; ++l) {
         const int ll = l % kLvlChunk;
         const int p0 = lp[ll] + tid, pend = lp[ll + 1];
-        if (p0 < pend && pi >= 0) solve();
+        if (p0 < pend && pp >= 0) solve();
         for (int p = p0 + nthr; p < pend; p += nthr) {  // levels wider than the cluster
             fetch(p);
-            if (pi >= 0) solve();
+            solve();
         }
-        pi = -1;
-        // split-phase barrier: publish this level (release), prefetch the next level's
-        // rows while the other CTAs arrive, then acquire.
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        pp = -1;
         const int q0 = lp[ll + 1] + tid;
-        if (l + 1 < t.n_levels && q0 < lp[ll + 2]) fetch(q0);
-        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        const bool more = l + 1 < t.n_levels && q0 < lp[ll + 2];
+        if (SOLO) {
+            if (more) fetch(q0);
+            __syncthreads();  // one CTA: bar.sync orders its global writes for all its threads
+        } else {
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+            if (more) fetch(q0);
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        }
         if (ll == kLvlChunk - 1) stage_levels(l + 1);
+    }
+}
+
+// DSMEM sweep: the same position-space level sweep, but the values the next levels read
+// live in a ring in the cluster's distributed shared memory.  Positions are dealt to the
+// cluster's CTAs in warp-sized chunks (chunk c -> CTA c % CS); each CTA keeps its chunks'
+// values in a ring of kRingPerCta 32-byte slots, so a dependency is one or two
+// ld.shared::cluster (~200 cycles) instead of an L2 round trip, and the split-phase
+// barrier.cluster per level only orders shared-memory writes.  Each thread keeps the
+// matrix rows of the next TWO levels in registers (two register sets used alternately,
+// refilled right after each arrive), so the HBM latency of the streamed factor is hidden behind two
+// barrier periods.  Results go to HBM with plain stores issued after the arrive, so the
+// release never waits for them.  The host selects this path only when the ring window
+// exceeds the largest dependency distance plus twice the widest level.
+constexpr int kDsCluster = 16;
+constexpr int kRingPerCta = 4096;  // 32-byte slots per CTA: 128 KB
+constexpr int kDsThreads = 256;
+
+template <int MAXD, int NRHS>
+struct RowRegs {
+    int p;
+    int pc[MAXD];
+    double pv[MAXD];
+    double pz[NRHS];
+    double pd;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ double2 ld_dsmem2(uint32_t addr) {
+    double2 v;
+#if SFV_DS_MODE == 0
+    asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+#else
+    asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+#endif
+    return v;
+}
+__device__ __forceinline__ double ld_dsmem(uint32_t addr) {
+    double v;
+#if SFV_DS_MODE == 0
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+#else
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+#endif
+    return v;
+}
+
+// Level hand-over of the DSMEM sweep.  The values a level publishes live in exactly one
+// physical shared memory (the owning CTA's); a CTA-scope fence (MEMBAR.ALL.CTA) makes the
+// writing thread's STS complete, and the relaxed cluster barrier orders every later DSMEM
+// read after it.  A cluster-scope release would compile to MEMBAR.ALL.GPU, which also
+// waits for the level's outstanding HBM stores (~1 us per level); SFV_DS_STRICT=1 builds
+// the strict form for comparison.
+#ifndef SFV_DS_STRICT
+#define SFV_DS_STRICT 0
+#endif
+__device__ __forceinline__ void ds_arrive() {
+#if SFV_DS_STRICT
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#else
+    asm volatile("fence.acq_rel.cta;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void ds_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
+template <bool UPPER, int NRHS, int MAXD>
+__global__ void __launch_bounds__(kDsThreads, 1) tri_dsmem_kernel(TriSet set, const double* __restrict__ src,
+                                                                  double* dst) {
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) double ring[];  // [kRingPerCta][4]
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int comp = NRHS == 3 ? 0 : static_cast<int>(blockIdx.x / kDsCluster);
+    const DevTri& t = set.t[comp];
+    const int np = t.n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int nwarps = kDsThreads / 32;
+    const uint32_t ring_base = smem_u32(ring);
+    __shared__ int lp[kLvlChunk + 3];
+    int lbase = 0;
+    auto stage_levels = [&](int base) {
+        __syncthreads();
+        lbase = base;
+        for (int x = threadIdx.x; x < kLvlChunk + 3; x += blockDim.x)
+            lp[x] = base + x <= t.n_levels ? t.level_ptr[base + x] : t.level_ptr[t.n_levels];
+        __syncthreads();
+    };
+    // the k-th position of this thread in level l (-1 if none); levels start on chunk boundaries
+    auto my_pos = [&](int l, int k) {
+        const int ll = l - lbase;
+        const int c0 = lp[ll] >> 5;
+        const int c = c0 + (rank - c0 % kDsCluster + kDsCluster) % kDsCluster + kDsCluster * (warp + nwarps * k);
+        const int p = c * 32 + lane;
+        return p < lp[ll + 1] ? p : -1;
+    };
+    auto slot_addr = [&](int p, int& owner) {
+        const int c = p >> 5;
+        owner = c % kDsCluster;
+        return ring_base + static_cast<uint32_t>(((c / kDsCluster) % (kRingPerCta / 32)) * 32 + (p & 31)) * 32u;
+    };
+    auto fetch = [&](RowRegs<MAXD, NRHS>& r, int p) {
+        r.p = p;
+        if (p < 0 || !SFV_PROBE(8)) return;
+#pragma unroll
+        for (int k = 0; k < MAXD; ++k) {
+            r.pc[k] = k < t.maxd ? t.ell_pcol[static_cast<size_t>(k) * np + p] : -1;
+            r.pv[k] = k < t.maxd ? t.ell_val[static_cast<size_t>(k) * np + p] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < NRHS; ++k) r.pz[k] = src[3 * static_cast<size_t>(p) + comp + k];
+        r.pd = UPPER ? t.diag[p] : 1.0;
+    };
+    auto solve = [&](const RowRegs<MAXD, NRHS>& r, double* z) {
+#pragma unroll
+        for (int k = 0; k < NRHS; ++k) z[k] = r.pz[k];
+        double dv[MAXD][NRHS];
+#pragma unroll
+        for (int q = 0; q < MAXD; ++q)  // all dependency loads in flight together
+            if (r.pc[q] >= 0) {
+                int owner;
+                const uint32_t a = mapa(slot_addr(r.pc[q], owner), owner);
+                if (NRHS == 3) {
+                    const double2 v01 = ld_dsmem2(a);
+                    dv[q][0] = v01.x;
+                    if (NRHS > 1) dv[q][NRHS > 1 ? 1 : 0] = v01.y;
+                    if (NRHS > 2) dv[q][NRHS > 2 ? 2 : 0] = ld_dsmem(a + 16);
+                } else {
+                    dv[q][0] = ld_dsmem(a);
+                }
+            }
+#pragma unroll
+        for (int q = 0; q < MAXD; ++q)  // then the reference's order of subtraction
+            if (r.pc[q] >= 0)
+#pragma unroll
+                for (int k = 0; k < NRHS; ++k) z[k] -= r.pv[q] * dv[q][k];
+        if (UPPER)
+#pragma unroll
+            for (int k = 0; k < NRHS; ++k) z[k] /= r.pd;
+        int owner;
+        double* slot = ring + (slot_addr(r.p, owner) - ring_base) / 8;  // owner == rank by construction
+#pragma unroll
+        for (int k = 0; k < NRHS; ++k) slot[k] = z[k];
+    };
+    auto store = [&](int p, const double* z) {
+#pragma unroll
+        for (int k = 0; k < NRHS; ++k) dst[3 * static_cast<size_t>(p) + comp + k] = z[k];
+    };
+    RowRegs<MAXD, NRHS> R0, R1;  // level l in R0 (l even) / R1 (l odd); the other holds l+1
+    stage_levels(0);
+    fetch(R0, t.n_levels > 0 ? my_pos(0, 0) : -1);
+    fetch(R1, t.n_levels > 1 ? my_pos(1, 0) : -1);
+    // one level: solve `cur`, extra positions of wide levels, barrier, refill `cur` with level l+3
+    auto level = [&](RowRegs<MAXD, NRHS>& cur, int l) {
+        double z[NRHS];
+        int done_p = -1;
+        if (cur.p >= 0) {
+            solve(cur, z);
+            done_p = cur.p;
+        }
+        for (int k = 1;; ++k) {  // levels wider than the cluster's first round
+            const int p = my_pos(l, k);
+            if (p < 0) break;
+            if (done_p >= 0) store(done_p, z);
+            RowRegs<MAXD, NRHS> w;
+            fetch(w, p);
+            solve(w, z);
+            done_p = p;
+        }
+        ds_arrive();
+        if (done_p >= 0) store(done_p, z);  // HBM copy, outside the release
+        const bool restage = l + 3 - lbase > kLvlChunk;
+        if (!restage) fetch(cur, l + 2 < t.n_levels ? my_pos(l + 2, 0) : -1);
+        ds_wait();
+        if (restage) {
+            stage_levels(l + 1);
+            fetch(cur, l + 2 < t.n_levels ? my_pos(l + 2, 0) : -1);
+        }
+    };
+    for (int l = 0; l < t.n_levels; l += 2) {
+        level(R0, l);
+        if (l + 1 < t.n_levels) level(R1, l + 1);
+    }
+}
+
+// position-space gathers / scatters around the sweeps (padding positions get zeros)
+__global__ void gather_pos_kernel(const int* __restrict__ order, int np, int comp, int ncomp,
+                                  const double* __restrict__ in, double* __restrict__ out) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+        const int i = order[p];
+        for (int k = comp; k < comp + ncomp; ++k) out[3 * static_cast<size_t>(p) + k] = i >= 0 ? in[3 * static_cast<size_t>(i) + k] : 0.0;
+    }
+}
+__global__ void scatter_pos_kernel(const int* __restrict__ order, int np, int comp, int ncomp,
+                                   const double* __restrict__ in, double* __restrict__ out) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+        const int i = order[p];
+        if (i >= 0)
+            for (int k = comp; k < comp + ncomp; ++k) out[3 * static_cast<size_t>(i) + k] = in[3 * static_cast<size_t>(p) + k];
+    }
+}
+// y_U[p'] = y_L[map[p']] (map: U position -> L position, -1 on padding)
+__global__ void permute_pos_kernel(const int* __restrict__ map, int np, int comp, int ncomp,
+                                   const double* __restrict__ in, double* __restrict__ out) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+        const int q = map[p];
+        for (int k = comp; k < comp + ncomp; ++k) out[3 * static_cast<size_t>(p) + k] = q >= 0 ? in[3 * static_cast<size_t>(q) + k] : 0.0;
     }
 }
 
@@ -275,7 +517,11 @@ void launch_dense_apply_perm(const double* W, int n, const int* perm, const doub
 template <bool UPPER, int NRHS, int MAXD>
 static cudaError_t launch_cluster_w(const TriSet& set, int ncomp, int csize, const double* src, double* dst,
                                     cudaStream_t s) {
-    auto kern = tri_cluster_kernel<UPPER, NRHS, MAXD>;
+    if (csize == 1) {  // single-CTA sweep: bar.sync per level, 1024 threads
+        tri_cluster_kernel<UPPER, NRHS, MAXD, true><<<NRHS == 3 ? 1 : ncomp, 1024, 0, s>>>(set, src, dst);
+        return cudaGetLastError();
+    }
+    auto kern = tri_cluster_kernel<UPPER, NRHS, MAXD, false>;
     if (csize > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(csize * (NRHS == 3 ? 1 : ncomp));
@@ -291,26 +537,59 @@ static cudaError_t launch_cluster_w(const TriSet& set, int ncomp, int csize, con
     return cudaLaunchKernelEx(&cfg, kern, set, src, dst);
 }
 
+template <bool UPPER, int NRHS, int MAXD>
+static cudaError_t launch_dsmem_w(const TriSet& set, int ncomp, const double* src, double* dst, cudaStream_t s) {
+    auto kern = tri_dsmem_kernel<UPPER, NRHS, MAXD>;
+    const int smem = kRingPerCta * 4 * static_cast<int>(sizeof(double));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kDsCluster * (NRHS == 3 ? 1 : ncomp));
+    cfg.blockDim = dim3(kDsThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kDsCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, set, src, dst);
+}
+
 template <bool UPPER, int NRHS>
 static cudaError_t launch_cluster(const TriSet& set, int ncomp, int csize, const double* src, double* dst,
                                   cudaStream_t s) {
     int maxd = 0;
     for (int a = 0; a < (NRHS == 3 ? 1 : ncomp); ++a) maxd = std::max(maxd, set.t[a].maxd);
+    if (csize == kDsRingMode) {  // values in distributed shared memory
+        if (maxd <= 8) return launch_dsmem_w<UPPER, NRHS, 8>(set, ncomp, src, dst, s);
+        if (maxd <= 16) return launch_dsmem_w<UPPER, NRHS, 16>(set, ncomp, src, dst, s);
+        return launch_dsmem_w<UPPER, NRHS, 32>(set, ncomp, src, dst, s);
+    }
     if (maxd <= 8) return launch_cluster_w<UPPER, NRHS, 8>(set, ncomp, csize, src, dst, s);
     if (maxd <= 16) return launch_cluster_w<UPPER, NRHS, 16>(set, ncomp, csize, src, dst, s);
     return launch_cluster_w<UPPER, NRHS, 32>(set, ncomp, csize, src, dst, s);
 }
 
 void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double* r, double* y, double* z, int grid,
-                      int sleep_ns, int cluster, cudaStream_t s) {
-    if (cluster > 0) {  // level-synchronous cluster sweep (default)
-        if (ncomp == 1) {
-            launch_cluster<false, 3>(L, 1, cluster, r, y, s);
-            launch_cluster<true, 3>(U, 1, cluster, y, z, s);
-        } else {
-            launch_cluster<false, 1>(L, 3, cluster, r, y, s);
-            launch_cluster<true, 1>(U, 3, cluster, y, z, s);
-        }
+                      int sleep_ns, int cluster, double* pa, double* pb, const StreamSet* SL, const StreamSet* SU,
+                      cudaStream_t s) {
+    if (cluster > 0) {  // level-synchronous position-space sweeps (default)
+        const int per = ncomp == 1 ? 3 : 1;
+        for (int c = 0; c < ncomp; ++c)  // r -> L positions
+            gather_pos_kernel<<<592, 256, 0, s>>>(L.t[c].order, L.t[c].n, c, per, r, pa);
+        if (cluster == kStreamMode) launch_tri_stream(*SL, false, ncomp, pa, pb, s);
+        else if (ncomp == 1) launch_cluster<false, 3>(L, 1, cluster, pa, pb, s);
+        else launch_cluster<false, 1>(L, 3, cluster, pa, pb, s);
+        for (int c = 0; c < ncomp; ++c)  // y: L positions -> U positions
+            permute_pos_kernel<<<592, 256, 0, s>>>(U.t[c].u2l, U.t[c].n, c, per, pb, pa);
+        if (cluster == kStreamMode) launch_tri_stream(*SU, true, ncomp, pa, pb, s);
+        else if (ncomp == 1) launch_cluster<true, 3>(U, 1, cluster, pa, pb, s);
+        else launch_cluster<true, 1>(U, 3, cluster, pa, pb, s);
+        for (int c = 0; c < ncomp; ++c)  // U positions -> rows
+            scatter_pos_kernel<<<592, 256, 0, s>>>(U.t[c].order, U.t[c].n, c, per, pb, z);
         return;
     }
     const int n3 = 3 * L.t[0].n_rows;  // sync-free sentinel polling (SFV_TRI_CLUSTER=0)
@@ -331,4 +610,8 @@ void launch_dense_apply(const double* inv, int n, const double* r, double* z, cu
     dense_apply_kernel<<<(n + warps_per_block - 1) / warps_per_block, 256, 0, s>>>(inv, n, r, z);
 }
 
+}  // namespace sfv
+
+namespace sfv {
+int ilu_ring_window() { return kRingPerCta * kDsCluster; }
 }  // namespace sfv

@@ -195,10 +195,15 @@ void pack(const std::vector<int>& level, int n_levels, TriSchedule& t,
     for (int p = 0; p < t.n_pos; ++p) t.maxd = std::max(t.maxd, t.rp[p + 1] - t.rp[p]);
     t.ell_col.assign(static_cast<size_t>(t.maxd) * t.n_pos, -1);
     t.ell_val.assign(static_cast<size_t>(t.maxd) * t.n_pos, 0.0);
+    t.pos.assign(n, -1);
+    for (int p = 0; p < t.n_pos; ++p)
+        if (t.order[p] >= 0) t.pos[t.order[p]] = p;
+    t.ell_pcol.assign(static_cast<size_t>(t.maxd) * t.n_pos, -1);
     for (int p = 0; p < t.n_pos; ++p)
         for (int q = t.rp[p]; q < t.rp[p + 1]; ++q) {
             t.ell_col[static_cast<size_t>(q - t.rp[p]) * t.n_pos + p] = t.col[q];
             t.ell_val[static_cast<size_t>(q - t.rp[p]) * t.n_pos + p] = t.val[q];
+            t.ell_pcol[static_cast<size_t>(q - t.rp[p]) * t.n_pos + p] = t.pos[t.col[q]];
         }
 }
 
@@ -318,6 +323,50 @@ std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out) {
         L(i, i) = std::sqrt(d);
     }
     return "";
+}
+
+}  // namespace sfv
+
+namespace sfv {
+
+bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, std::vector<StreamRecord>& out) {
+    if (t.maxd > 8) return false;
+    const int np = t.n_pos;
+    std::vector<int> owner(np, 0), ordinal(np, 0), level_of(np, 0);
+    std::vector<int> count(cs, 0);
+    std::vector<std::vector<int>> ord_level(cs);  // per CTA: level of its k-th position
+    for (int l = 0; l < t.n_levels; ++l) {
+        const int a = t.level_ptr[l], b = t.level_ptr[l + 1];
+        const int nch = (b - a) / 32, per = (nch + cs - 1) / cs;
+        if (per * 32 > max_rows) return false;
+        for (int p = a; p < b; ++p) {
+            const int r = ((p - a) / 32) / std::max(per, 1);
+            owner[p] = r;
+            ordinal[p] = count[r]++;
+            ord_level[r].push_back(l);
+            level_of[p] = l;
+        }
+    }
+    out.assign(np, StreamRecord{});
+    for (int p = 0; p < np; ++p) {
+        StreamRecord& rec = out[p];
+        rec.own = static_cast<uint16_t>(ordinal[p] % ring);
+        rec.diag = t.diag[p];
+        for (int k = 0; k < 8; ++k) {
+            rec.dep[k] = 0xffff;
+            rec.val[k] = 0.0;
+            if (k >= t.maxd) continue;
+            const int q = t.ell_pcol[static_cast<size_t>(k) * np + p];
+            if (q < 0) continue;
+            // the slot of q is rewritten by its owner's (ordinal + ring)-th position: that
+            // position must lie in a strictly later level than the reader p
+            const int r = owner[q], o = ordinal[q] + ring;
+            if (o < static_cast<int>(ord_level[r].size()) && ord_level[r][o] <= level_of[p]) return false;
+            rec.dep[k] = static_cast<uint16_t>((r << 12) | (ordinal[q] % ring));
+            rec.val[k] = t.ell_val[static_cast<size_t>(k) * np + p];
+        }
+    }
+    return true;
 }
 
 }  // namespace sfv

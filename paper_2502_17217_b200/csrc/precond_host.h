@@ -1,6 +1,7 @@
 // precond_host.h — host setup of the reference's preconditioners on the cell graph.
 #pragma once
 
+#include <cstdint>
 #include <string>
 #include <vector>
 
@@ -31,11 +32,29 @@ struct TriSchedule {
     std::vector<int> order, rp, col, level_ptr;
     std::vector<double> val, diag;
     int maxd = 0;
-    std::vector<int> ell_col;  // [maxd * n_pos], entry k of position p at k * n_pos + p
+    std::vector<int> ell_col;   // [maxd * n_pos], entry k of position p at k * n_pos + p
+    std::vector<int> ell_pcol;  // the same columns as positions of this schedule
     std::vector<double> ell_val;
+    std::vector<int> pos;       // row -> position
 };
 void schedule_lower(const ScalarCsr& lu, TriSchedule& t);
 void schedule_upper(const ScalarCsr& lu, TriSchedule& t);
+
+// Streamed-sweep records (precond.cu, tri_stream_kernel): one 96-byte record per position,
+// position order.  Level l's positions are split into `cs` contiguous chunk-aligned slices
+// (CTA r of the cluster owns slice r); each CTA stores its positions' values in a ring of
+// `ring` slots in its shared memory, and every dependency is recorded as its DSMEM address
+// (owner << 12 | slot).  Returns false when a ring slot would be overwritten before its
+// last reader (then the caller keeps another sweep), or a slice exceeds max_rows.
+struct StreamRecord {
+    uint16_t dep[8];  // owner << 12 | slot, 0xffff = none; at most 8 entries per row
+    uint16_t own;     // this position's slot in its owner's ring
+    uint16_t pad[3];
+    double val[8];
+    double diag;
+};
+static_assert(sizeof(StreamRecord) == 96, "record layout");
+bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, std::vector<StreamRecord>& out);
 
 // Banded Cholesky of -A after reverse Cuthill-McKee (A symmetric negative definite);
 // returns "" or "lu: factorisation failed".  Band row i holds L(i, i-bw .. i).

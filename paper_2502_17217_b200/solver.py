@@ -31,7 +31,7 @@ import numpy as np
 from .abi import ERR, Mesh, MeshDesc, Physics, PhysicsDesc, SolveReport, SolverCfg, dptr, iptr, solver_cfg
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsfv.so")
+LIB_PATH = os.environ.get("SFV_LIB") or os.path.join(HERE, "libsfv.so")
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
