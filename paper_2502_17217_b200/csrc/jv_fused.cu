@@ -25,6 +25,13 @@
 #include "device.h"
 #include "sfv_case.h"
 
+// timing probes (scripts/probes): -DSFV_FPROBE=m drops 1: stage waits, 2: face stage, 4: gradient
+// stage, 8: per-cell sums.  Results are then wrong; production builds use 0.
+#ifndef SFV_FPROBE
+#define SFV_FPROBE 0
+#endif
+#define FPROBE(b) (!(SFV_FPROBE & (b)))
+
 namespace sfv {
 namespace {
 
@@ -183,9 +190,15 @@ __device__ __forceinline__ d3 ld3(const double* __restrict__ p, int c) { return 
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// Flag polls are relaxed on purpose: an acquire load compiles to LDG.STRONG + CCTL.IVALL,
+// i.e. it invalidates the whole SM's L1 on every poll and destroys the neighbour reuse
+// of every co-resident CTA.  The data a stage hands over (the two rings) is only ever read
+// with ld.global.cg (LDG.STRONG.GPU, served by L2, the coherence point) and only after the
+// poll loop has observed the flag; the producer publishes with st.release.gpu
+// (MEMBAR.ALL.GPU before the flag store), so the ring lines are in L2 before the flag.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
     int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -193,7 +206,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void wait_range(const int* flags, int lo, int hi, int epoch) {
     if (lo < 0) lo = 0;
     for (int i = lo + static_cast<int>(threadIdx.x); i <= hi; i += blockDim.x)
-        while (ld_acquire(&flags[i]) != epoch) __nanosleep(64);
+        while (FPROBE(1) && ld_relaxed(&flags[i]) != epoch) __nanosleep(32);
     __syncthreads();
 }
 
@@ -202,7 +215,6 @@ __device__ __forceinline__ void wait_range(const int* flags, int lo, int hi, int
 __device__ __forceinline__ void publish(int* flag, int epoch) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
         st_release(flag, epoch);
     }
 }
@@ -270,7 +282,7 @@ __global__ void __launch_bounds__(kTile, GEN ? 2 : 3) fused_kernel(FusedArgs a) 
             // the ring slots of tile k last held tile k - RT, read by B1/B2 of [k-RT-lag+1, k-RT]
             wait_range(a.b2_done, k - L.ring_tiles - L.lag + 1, k - L.ring_tiles, a.epoch);
             const int c = k * kTile + tid;
-            if (c < m.nc && !zero) {
+            if (c < m.nc && !zero && FPROBE(4)) {
                 const d3 uc = load_u<PERT>(a.u, a.v, eps, c);
                 dm3 g;
 #pragma unroll
@@ -313,7 +325,7 @@ __global__ void __launch_bounds__(kTile, GEN ? 2 : 3) fused_kernel(FusedArgs a) 
         // ---------------- B1(t): faces whose lower cell is in tile t, each computed once
         wait_range(a.a_done, t, min(t + L.lag - 1, L.ntiles - 1), a.epoch);
         wait_range(a.b2_done, t - L.ring_tiles, t + L.lag - 1 - L.ring_tiles, a.epoch);
-        if (!zero) {
+        if (!zero && FPROBE(2)) {
             const int fend = L.tile_face_ptr[t + 1];
             for (int fi = L.tile_face_ptr[t] + tid; fi < fend; fi += kTile) {
                 const int p = L.f_owner[fi], o = L.f_other[fi];
@@ -425,7 +437,7 @@ __global__ void __launch_bounds__(kTile, GEN ? 2 : 3) fused_kernel(FusedArgs a) 
         wait_range(a.b1_done, t - L.lag + 1, t - 1, a.epoch);
         {
             const int c = t * kTile + tid;
-            if (c < m.nc) {
+            if (c < m.nc && FPROBE(8)) {
                 if (zero) {
                     a.out[3 * c] = 0.0;
                     a.out[3 * c + 1] = 0.0;
