@@ -111,8 +111,11 @@ struct sfv_ctx {
     double time = 0.0;
     cudaStream_t stream = nullptr;
     // owned layout buffers
-    DevBuf<int> slot_face, slot_other;
+    DevBuf<int> slot_face, slot_other, bnd_si;  // bnd_si: slot index of each boundary face
     DevBuf<double> slot_ls, gam, del, dmag, w, volume;
+    // jv_pair.cu scratch + face records
+    DevBuf<double> pw, pG, face9, bres;
+    PairScratch ps;
     // scratch
     DevBuf<double> grad, red, scal;  // scal: [0]=eps [1]=u_norm [2..] misc
     DevBuf<unsigned> counter;
@@ -134,7 +137,8 @@ struct sfv_ctx {
     DevBuf<unsigned char> srec[6];  // streamed-sweep records: L0..L2, U0..U2
     DevBuf<double> dense_w[3];
     DevBuf<int> dense_perm[3];
-    // fused J.v kernel (jv_fused.cu)
+    // residual / J.v kernels: 0 = jv_pair.cu (default), 1 = jv_fused.cu, 2 = residual.cu
+    int jv_path = 0;
     bool use_fused = false;
     FusedLayout fl;
     DevBuf<int> f_tfp, f_own, f_oth, f_slots, f_index, f_flags, f_ticket;
@@ -177,6 +181,9 @@ std::string build_layout(sfv_ctx* c) {
     if (slots > kMaxSlots) return "mesh: cells with more than 8 faces are not supported by the device layout";
     std::vector<int> sf(static_cast<size_t>(slots) * nc, -1), so(static_cast<size_t>(slots) * nc, -1);
     std::vector<double> sl(static_cast<size_t>(3) * slots * nc, 0.0);
+    std::vector<int> bsi(std::max(1, nf - m.n_internal), 0);
+    if (static_cast<size_t>(slots) * nc > static_cast<size_t>(INT_MAX))
+        return "mesh: too many cells for 32-bit slot indices";
     for (int i = 0; i < nc; ++i) {
         int s = 0;
         for (int q = m.cf_off[i]; q < m.cf_off[i + 1]; ++q, ++s) {
@@ -188,10 +195,20 @@ std::string build_layout(sfv_ctx* c) {
             sl[(3 * static_cast<size_t>(s)) * nc + i] = g.ls[q].x;
             sl[(3 * static_cast<size_t>(s) + 1) * nc + i] = g.ls[q].y;
             sl[(3 * static_cast<size_t>(s) + 2) * nc + i] = g.ls[q].z;
+            if (f >= m.n_internal) bsi[f - m.n_internal] = static_cast<int>(si);
         }
     }
     std::vector<double> gm(3 * static_cast<size_t>(nf)), de(3 * static_cast<size_t>(nf)), dmg(nf), ww(nf);
+    std::vector<double> f9(9 * static_cast<size_t>(nf));
     for (int f = 0; f < nf; ++f) {
+        // per-face constants of rhie_chow(): |Delta| / |d| and |Gamma| (discretisation.cpp:176-208),
+        // same IEEE operations as the reference (sqrt of the left-to-right dot, then divide)
+        const double* a = &g.area[f].x;
+        const double* d = &g.delta[f].x;
+        const double rec[9] = {a[0], a[1], a[2], d[0], d[1], d[2],
+                               std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]) / g.d_mag[f],
+                               std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]), g.w[f]};
+        for (int q = 0; q < 9; ++q) f9[static_cast<size_t>(q) * nf + f] = rec[q];
         gm[f] = g.area[f].x;
         gm[nf + f] = g.area[f].y;
         gm[2 * static_cast<size_t>(nf) + f] = g.area[f].z;
@@ -202,7 +219,9 @@ std::string build_layout(sfv_ctx* c) {
         ww[f] = g.w[f];
     }
     if (!c->slot_face.upload(sf) || !c->slot_other.upload(so) || !c->slot_ls.upload(sl) || !c->gam.upload(gm) ||
-        !c->del.upload(de) || !c->dmag.upload(dmg) || !c->w.upload(ww))
+        !c->del.upload(de) || !c->dmag.upload(dmg) || !c->w.upload(ww) || !c->bnd_si.upload(bsi) ||
+        !c->bres.alloc(6 * bsi.size()) || !c->face9.upload(f9) || !c->pw.alloc(3 * static_cast<size_t>(nc)) ||
+        !c->pG.alloc(9 * static_cast<size_t>(nc)))
         return "cuda: out of device memory for the mesh layout";
     if (c->ph.transient && !c->volume.upload(g.volume)) return "cuda: out of device memory";
     DevMesh& d = c->dm;
@@ -218,6 +237,11 @@ std::string build_layout(sfv_ctx* c) {
     d.dmag = c->dmag.p;
     d.w = c->w.p;
     d.volume = c->volume.p;
+    c->ps.w = c->pw.p;
+    c->ps.G = c->pG.p;
+    c->ps.face9 = c->face9.p;
+    c->ps.bnd_si = c->bnd_si.p;
+    c->ps.bres = c->bres.p;
     return "";
 }
 
@@ -290,7 +314,6 @@ std::string build_fused_layout(sfv_ctx* c) {
     L.gring = c->f_gring.p;
     L.fring = c->f_fring.p;
     c->use_fused = true;
-    if (const char* e = std::getenv("SFV_FUSED")) c->use_fused = std::atoi(e) != 0;
     return "";
 }
 
@@ -356,6 +379,11 @@ void residual_pass(sfv_ctx* c, const Physics& ph, const double* u, const double*
                    const double* r_u, double* out) {
     if (c->use_fused) {
         launch_fused_pass(c, ph, u, v, eps, r_u, out);
+        return;
+    }
+    if (c->jv_path == 0) {
+        launch_residual_pair(c->dm, ph, c->pt, c->hist, u, v, eps, r_u, out, c->ps, c->err.p, c->stream);
+        c->launches += c->dm.nf > c->dm.nint ? 4 : 3;
         return;
     }
     launch_residual(c->dm, ph, c->pt, c->hist, u, v, eps, r_u, out, c->grad.p, c->err.p, c->stream);
@@ -951,7 +979,12 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     update_patch_values(c.get());
     e = build_layout(c.get());
     if (!e.empty()) return fail(e);
-    if (build_fused_layout(c.get()).rfind("cuda", 0) == 0) return fail("cuda: out of device memory");
+    if (const char* j = std::getenv("SFV_JV")) {  // kernel-path override (scripts/microbench.py)
+        const std::string js(j);
+        c->jv_path = js == "fused" ? 1 : js == "twopass" ? 2 : 0;
+    }
+    if (c->jv_path == 1 && build_fused_layout(c.get()).rfind("cuda", 0) == 0)
+        return fail("cuda: out of device memory");
     const size_t n = static_cast<size_t>(c->n);
     if (!c->grad.alloc(9 * static_cast<size_t>(c->nc)) || !c->red.alloc(2 * 148 * 8 + 64) || !c->scal.alloc(8) ||
         !c->counter.alloc(1) || !c->err.alloc(1) || !c->hdev.alloc(72) || !c->dzero.alloc(n))

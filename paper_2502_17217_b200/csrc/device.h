@@ -73,6 +73,18 @@ struct History {
 void launch_residual(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist,
                      const double* u, const double* v, const double* jv_eps, const double* r_u,
                      double* out, double* grad_scratch, ErrWords* err, cudaStream_t s);
+// ---- jv_pair.cu: same contract as launch_residual; perturb + gradient + boundary-face +
+// per-(cell, face slot) flux kernels
+struct PairScratch {
+    double* w = nullptr;            // [3*nc] perturbed state u + eps v, SoA
+    double* G = nullptr;            // [9*nc] cell gradients, row-major entries, SoA
+    const double* face9 = nullptr;  // [9*nf] Gamma xyz, Delta xyz, |Delta|/|d|, |Gamma|, w; SoA
+    const int* bnd_si = nullptr;  // [nf-nint] slot index (s*nc + cell) of boundary face nint+fb
+    double* bres = nullptr;       // [6*(nf-nint)] boundary-face flux + stabilisation
+};
+void launch_residual_pair(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist,
+                          const double* u, const double* v, const double* jv_eps, const double* r_u, double* out,
+                          const PairScratch& ps, ErrWords* err, cudaStream_t s);
 // cell_gradients only (discretisation.cpp:10-31), SoA [k*nc + c], k = 3i + j
 void launch_gradients(const DevMesh& m, const PatchTable& pt, const double* u, double* G, cudaStream_t s);
 // eps = sqrt(DBL_EPSILON) sqrt(1 + |u|) / |v| into *eps (nonlinear.cpp:109-115), with

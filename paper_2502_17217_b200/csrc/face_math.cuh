@@ -1,0 +1,202 @@
+// face_math.cuh — the per-cell / per-face arithmetic of the residual, shared by the
+// device kernels.  Every helper performs exactly the operations (and operation order) of
+// the reference's small-matrix code (/root/reference/proj/src/laws.cpp,
+// discretisation.cpp:33-106), so kernels built on them are bit-identical to
+// ResidualEvaluator::residual when compiled with -fmad=false.
+#pragma once
+
+#include <cmath>
+
+#include "device.h"
+#include "sfv_case.h"
+
+namespace sfv {
+namespace fm {
+
+struct d3 {
+    double x, y, z;
+};
+struct dm3 {
+    double a[3][3];
+};
+
+__device__ __forceinline__ d3 add(d3 a, d3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ d3 sub(d3 a, d3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ d3 scl(d3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ d3 neg(d3 a) { return {-a.x, -a.y, -a.z}; }
+__device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ double nrm(d3 a) { return sqrt(dot(a, a)); }
+__device__ __forceinline__ double cmp(d3 a, int i) { return i == 0 ? a.x : (i == 1 ? a.y : a.z); }
+
+__device__ __forceinline__ dm3 madd(const dm3& a, const dm3& b) {
+    dm3 r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) r.a[i][j] = a.a[i][j] + b.a[i][j];
+    return r;
+}
+__device__ __forceinline__ dm3 mscl(const dm3& a, double s) {
+    dm3 r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) r.a[i][j] = a.a[i][j] * s;
+    return r;
+}
+__device__ __forceinline__ dm3 mmul(const dm3& a, const dm3& b) {
+    dm3 r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) s += a.a[i][k] * b.a[k][j];
+            r.a[i][j] = s;
+        }
+    return r;
+}
+__device__ __forceinline__ dm3 mtr(const dm3& a) {
+    dm3 r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) r.a[i][j] = a.a[j][i];
+    return r;
+}
+__device__ __forceinline__ d3 mv(const dm3& a, d3 v) {
+    return {a.a[0][0] * v.x + a.a[0][1] * v.y + a.a[0][2] * v.z, a.a[1][0] * v.x + a.a[1][1] * v.y + a.a[1][2] * v.z,
+            a.a[2][0] * v.x + a.a[2][1] * v.y + a.a[2][2] * v.z};
+}
+// v . A (row vector times matrix)
+__device__ __forceinline__ d3 dot_left(d3 v, const dm3& a) {
+    return {v.x * a.a[0][0] + v.y * a.a[1][0] + v.z * a.a[2][0], v.x * a.a[0][1] + v.y * a.a[1][1] + v.z * a.a[2][1],
+            v.x * a.a[0][2] + v.y * a.a[1][2] + v.z * a.a[2][2]};
+}
+__device__ __forceinline__ double det(const dm3& a) {
+    return a.a[0][0] * (a.a[1][1] * a.a[2][2] - a.a[1][2] * a.a[2][1]) -
+           a.a[0][1] * (a.a[1][0] * a.a[2][2] - a.a[1][2] * a.a[2][0]) +
+           a.a[0][2] * (a.a[1][0] * a.a[2][1] - a.a[1][1] * a.a[2][0]);
+}
+__device__ __forceinline__ dm3 inverse(const dm3& a) {
+    const double id = 1.0 / det(a);
+    dm3 r;
+    r.a[0][0] = (a.a[1][1] * a.a[2][2] - a.a[1][2] * a.a[2][1]) * id;
+    r.a[0][1] = (a.a[0][2] * a.a[2][1] - a.a[0][1] * a.a[2][2]) * id;
+    r.a[0][2] = (a.a[0][1] * a.a[1][2] - a.a[0][2] * a.a[1][1]) * id;
+    r.a[1][0] = (a.a[1][2] * a.a[2][0] - a.a[1][0] * a.a[2][2]) * id;
+    r.a[1][1] = (a.a[0][0] * a.a[2][2] - a.a[0][2] * a.a[2][0]) * id;
+    r.a[1][2] = (a.a[0][2] * a.a[1][0] - a.a[0][0] * a.a[1][2]) * id;
+    r.a[2][0] = (a.a[1][0] * a.a[2][1] - a.a[1][1] * a.a[2][0]) * id;
+    r.a[2][1] = (a.a[0][1] * a.a[2][0] - a.a[0][0] * a.a[2][1]) * id;
+    r.a[2][2] = (a.a[0][0] * a.a[1][1] - a.a[0][1] * a.a[1][0]) * id;
+    return r;
+}
+// w P + (1 - w) N (discretisation.cpp:33)
+__device__ __forceinline__ dm3 interp(const dm3& p, const dm3& n, double w) { return madd(mscl(p, w), mscl(n, 1.0 - w)); }
+// F = I + grad(u)^T (laws.cpp:5-9)
+__device__ __forceinline__ dm3 defgrad(const dm3& g) {
+    dm3 r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) r.a[i][j] = (i == j ? 1.0 : 0.0) + g.a[j][i];
+    return r;
+}
+// I - 2 n n^T (discretisation.cpp:60-66)
+__device__ __forceinline__ dm3 reflection(d3 gamma) {
+    const d3 n = scl(gamma, 1.0 / nrm(gamma));
+    dm3 r;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) r.a[i][j] = (i == j ? 1.0 : 0.0) - (cmp(n, i) * cmp(n, j)) * 2.0;
+    return r;
+}
+__device__ __forceinline__ dm3 mirror_avg(const dm3& a, const dm3& R) { return mscl(madd(a, mmul(mmul(R, a), R)), 0.5); }
+// linear elastic (laws.cpp:21-27)
+__device__ __forceinline__ dm3 hooke(const dm3& g, double mu, double lam) {
+    dm3 s;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s.a[i][j] = (g.a[i][j] + g.a[j][i]) * mu;
+    const double t = lam * ((g.a[0][0] + g.a[1][1]) + g.a[2][2]);
+    s.a[0][0] += t;
+    s.a[1][1] += t;
+    s.a[2][2] += t;
+    return s;
+}
+// compressible neo-Hookean, Cauchy stress (laws.cpp:29-45)
+__device__ __forceinline__ dm3 neo_hookean(const dm3& g, double mu, double kappa, bool& ok) {
+    const dm3 F = defgrad(g);
+    const double J = det(F);
+    ok = J > 0.0;
+    const dm3 bb = mscl(mmul(F, mtr(F)), pow(J, -2.0 / 3.0));
+    const double t = ((bb.a[0][0] + bb.a[1][1]) + bb.a[2][2]) / 3.0;
+    dm3 dv = bb;
+    dv.a[0][0] -= t;
+    dv.a[1][1] -= t;
+    dv.a[2][2] -= t;
+    dm3 s = mscl(dv, mu / J);
+    const double p = 0.5 * kappa * (J * J - 1.0) / J;
+    s.a[0][0] += p;
+    s.a[1][1] += p;
+    s.a[2][2] += p;
+    return s;
+}
+__device__ __forceinline__ dm3 stress(const Physics& ph, const dm3& g, bool& ok) {
+    if (ph.law == SFV_LAW_NEO_HOOKEAN) return neo_hookean(g, ph.mu, ph.lam, ok);
+    ok = true;
+    return hooke(g, ph.mu, ph.lam);
+}
+// Rhie-Chow term (discretisation.cpp:176-208)
+__device__ __forceinline__ d3 rhie_chow(d3 up, d3 uo, const dm3& gf, d3 delta, double d_mag, double area_mag,
+                                        double alpha, double kbar) {
+    const d3 compact = scl(sub(uo, up), nrm(delta) / d_mag);
+    return scl(sub(compact, dot_left(delta, gf)), alpha * kbar * area_mag);
+}
+// Nanson: J Gamma . F^{-1} (discretisation.cpp:96-106)
+__device__ __forceinline__ d3 transform_area(d3 gamma, const dm3& ff, bool& ok) {
+    const double j = det(ff);
+    ok = j > 0.0;
+    return scl(dot_left(gamma, inverse(ff)), j);
+}
+
+// Hooke, small strain: flux = Gamma . interp(sigma_P, sigma_N, w) and the Rhie-Chow term
+// with grad_f = interp(G_P, G_N, w), element by element with exactly the operations of
+// hooke(), interp(), dot_left() and rhie_chow() (bit-identical) but without materialising
+// the four 3x3 matrices.  gp, gn: row-major 3x3 gradients.
+// cfac = |Delta| / |d| and gmag = |Gamma| are the per-face constants of rhie_chow().
+__device__ __forceinline__ void hooke_face(const double* gp, const double* gn, double w, double mu, double lam, d3 gam,
+                                           d3 del, d3 up, d3 un, double cfac, double gmag, double alpha, double kbar,
+                                           d3& flux, d3& st) {
+    const double tp = lam * ((gp[0] + gp[4]) + gp[8]);
+    const double tn = lam * ((gn[0] + gn[4]) + gn[8]);
+    const double wn = 1.0 - w;
+    double f[3], dg[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        double a[3], g[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            double sp = (gp[3 * i + j] + gp[3 * j + i]) * mu;
+            double sn = (gn[3 * i + j] + gn[3 * j + i]) * mu;
+            if (i == j) {
+                sp += tp;
+                sn += tn;
+            }
+            a[i] = sp * w + sn * wn;
+            g[i] = gp[3 * i + j] * w + gn[3 * i + j] * wn;
+        }
+        f[j] = gam.x * a[0] + gam.y * a[1] + gam.z * a[2];
+        dg[j] = del.x * g[0] + del.y * g[1] + del.z * g[2];
+    }
+    flux = {f[0], f[1], f[2]};
+    const d3 compact = scl(sub(un, up), cfac);
+    st = scl(sub(compact, d3{dg[0], dg[1], dg[2]}), alpha * kbar * gmag);
+}
+
+}  // namespace fm
+}  // namespace sfv

@@ -1,0 +1,367 @@
+// jv_pair.cu — residual / J.v as two sync-free kernels with one thread per (cell, face slot).
+//
+// The reference evaluates R(u) cell by cell: gradients (discretisation.cpp:10-31), then
+// for every face the interpolated-stress flux (:121-156) and, after the whole face loop,
+// the Rhie-Chow terms (:158, :176-208), then the BDF2 inertia and the NaN scan
+// (:163-172).  Here a CTA owns kCells consecutive cells and runs one warp per face slot:
+// lane l of warp s evaluates slot s of cell (base + l).  Every per-face load of a thread
+// is independent of the others (only the slot's face index and other cell come first),
+// so a warp keeps ~40 loads in flight with no cross-CTA synchronisation at all.  The
+// per-face results go to shared memory and the ordered per-cell sums — fluxes in
+// ascending face order, then stabilisation terms in the same order, exactly the
+// reference's summation order — are done by 3 x kCells threads, one per (component,
+// cell), whose output stores are fully coalesced.
+//
+// Internal faces are evaluated from both sides with the operands in (owner, neighbour)
+// order and the result negated on the neighbour side, which is bit-identical to the
+// reference's r[N] -= flux.  Compiled with -fmad=false (see residual.cu).
+#include <cfloat>
+#include <climits>
+
+#include "device.h"
+#include "face_math.cuh"
+#include "sfv_case.h"
+
+namespace sfv {
+namespace {
+
+using namespace fm;
+
+constexpr int kCells = 32;  // cells per CTA (one warp-width); CTA = kCells x S threads
+constexpr int kSign = static_cast<int>(0x80000000u);
+
+__device__ __forceinline__ d3 ldsoa(const double* __restrict__ p, int n, int i) {
+    return {p[i], p[n + i], p[2 * static_cast<size_t>(n) + i]};
+}
+// All gathered arrays are SoA so that the 32 lanes of a warp (32 consecutive cells, one
+// face slot) load 32 consecutive doubles per instruction: the L1 wavefront queue, not DRAM,
+// limits a gather kernel whose loads each touch many 128-byte lines.
+// perturbed state w[k * nc + c] = u + eps v
+__device__ __forceinline__ d3 ldw(const double* __restrict__ w, int nc, int c) {
+    return {w[c], w[nc + c], w[2 * nc + c]};
+}
+// cell gradient G[q * nc + c], q = 3 i + j (row-major)
+__device__ __forceinline__ void ldg9(const double* __restrict__ G, int nc, int c, double* g) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) g[q] = G[q * nc + c];
+}
+__device__ __forceinline__ dm3 ldG(const double* __restrict__ G, int nc, int c) {
+    dm3 r;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) r.a[q / 3][q % 3] = G[q * nc + c];
+    return r;
+}
+
+// ---------------------------------------------------------------- perturbed state
+// w = u + eps v, formed once per J.v exactly as the reference forms u_pert
+// (nonlinear.cpp:116-118); plain residual: w = u.
+template <bool PERT>
+__global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __restrict__ u, const double* __restrict__ v,
+                                                      const double* __restrict__ eps_p, double* __restrict__ w) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    double x = u[3 * c], y = u[3 * c + 1], z = u[3 * c + 2];
+    if (PERT) {
+        const double eps = *eps_p;
+        x = x + eps * v[3 * c];
+        y = y + eps * v[3 * c + 1];
+        z = z + eps * v[3 * c + 2];
+    }
+    w[c] = x;
+    w[nc + c] = y;
+    w[2 * nc + c] = z;
+}
+
+// ---------------------------------------------------------------- gradients
+// one thread per cell, slots unrolled so the neighbour loads are all in flight together
+// (discretisation.cpp:10-31: g += ls_f (x) (u_N - u_P), faces in cell order)
+template <int S>
+__global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt, const double* __restrict__ w,
+                                                        double* __restrict__ G) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= m.nc) return;
+    int o[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) o[s] = s < m.slots ? m.slot_other[s * m.nc + c] : -1;
+    const d3 wc = ldw(w, m.nc, c);
+    d3 wn[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) wn[s] = o[s] >= 0 ? ldw(w, m.nc, o[s]) : d3{0.0, 0.0, 0.0};
+    double g[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) g[q] = 0.0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        d3 du;
+        if (o[s] >= 0) {
+            du = sub(wn[s], wc);
+        } else if (o[s] <= -2 && pt.kind[-o[s] - 2] == SFV_PATCH_SYMMETRY) {
+            const dm3 R = reflection(ldsoa(m.gam, m.nf, m.slot_face[s * m.nc + c] & ~kSign));
+            du = sub(mv(R, wc), wc);
+        } else {
+            continue;  // traction / displacement faces are not in the stencil; padding
+        }
+        const d3 ls = {m.slot_ls[(3 * s) * m.nc + c], m.slot_ls[(3 * s + 1) * m.nc + c],
+                       m.slot_ls[(3 * s + 2) * m.nc + c]};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) g[3 * i + j] += cmp(ls, i) * cmp(du, j);
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) G[q * m.nc + c] = g[q];
+}
+
+// ---------------------------------------------------------------- boundary faces
+// One thread per boundary face (face f = nint + fb, slot index bnd_si[fb] = s * nc + cell):
+// flux and stabilisation term into bres[q * nbf + fb] (discretisation.cpp:128-154, :186-205).
+// Kept out of the per-slot kernel so its register budget is set by the internal faces.
+__global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, PatchTable pt,
+                                                       const int* __restrict__ bnd_si, const double* __restrict__ w,
+                                                       const double* __restrict__ eps_p,
+                                                       const double* __restrict__ G, double* __restrict__ bres,
+                                                       ErrWords* __restrict__ err) {
+    const int nbf = m.nf - m.nint;
+    const int fb = blockIdx.x * blockDim.x + threadIdx.x;
+    if (fb >= nbf) return;
+    if (eps_p && *eps_p == 0.0) return;
+    const int si = bnd_si[fb];
+    const int c = si % m.nc;
+    const int f = m.nint + fb;
+    const int patch = -m.slot_other[si] - 2;
+    const int pk = pt.kind[patch];
+    const d3 bc = {pt.value[patch][0], pt.value[patch][1], pt.value[patch][2]};
+    const d3 gam = ldsoa(m.gam, m.nf, f);
+    d3 flux, st{0.0, 0.0, 0.0};
+    if (pk == SFV_PATCH_TRACTION) {  // nominal load |Gamma| T (discretisation.cpp:151-154)
+        flux = scl(bc, nrm(gam));
+    } else {
+        const dm3 gc = ldG(G, m.nc, c);
+        const d3 uc = ldw(w, m.nc, c);
+        const d3 del = ldsoa(m.del, m.nf, f);
+        const double dmag = m.dmag[f];
+        bool okc;
+        const dm3 sc = stress(ph, gc, okc);
+        if (pk == SFV_PATCH_DISPLACEMENT) {
+            d3 gm = gam;
+            if (ph.tl) {
+                bool ok;
+                gm = transform_area(gam, defgrad(gc), ok);
+                if (!ok) atomicMin(&err->inverted_face, f);
+            }
+            flux = dot_left(gm, sc);
+            st = rhie_chow(uc, bc, gc, del, dmag, nrm(gam), ph.alpha, ph.kbar);
+        } else {  // symmetry plane (discretisation.cpp:138-150, :194-203)
+            const dm3 R = reflection(gam);
+            d3 gm = gam;
+            if (ph.tl) {
+                bool ok;
+                gm = transform_area(gam, mirror_avg(defgrad(gc), R), ok);
+                if (!ok) atomicMin(&err->inverted_face, f);
+            }
+            flux = dot_left(gm, mirror_avg(sc, R));
+            st = rhie_chow(uc, mv(R, uc), mirror_avg(gc, R), del, dmag, nrm(gam), ph.alpha, ph.kbar);
+        }
+    }
+    bres[fb] = flux.x;
+    bres[nbf + fb] = flux.y;
+    bres[2 * static_cast<size_t>(nbf) + fb] = flux.z;
+    bres[3 * static_cast<size_t>(nbf) + fb] = st.x;
+    bres[4 * static_cast<size_t>(nbf) + fb] = st.y;
+    bres[5 * static_cast<size_t>(nbf) + fb] = st.z;
+}
+
+// ---------------------------------------------------------------- fluxes + epilogue
+// face9[q * nf + f], q = Gamma xyz, Delta xyz, |Delta| / |d|, |Gamma|, w (the two ratios are
+// the per-face constants of rhie_chow(), precomputed with the same IEEE operations).
+// kind of a slot's contribution: 0 none (padding), 1 flux only (traction), 2 flux + stabilisation
+template <bool PERT, int S, bool GEN>
+__global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
+    flux_pair_kernel(DevMesh m, Physics ph, PatchTable pt, History hist, const double* __restrict__ w,
+                     const double* __restrict__ eps_p, const double* __restrict__ G,
+                     const double* __restrict__ face9, const double* __restrict__ bres,
+                     const double* __restrict__ r_u, double* __restrict__ out, ErrWords* __restrict__ err) {
+    __shared__ double res[S][6][kCells];
+    __shared__ unsigned char kind[S][kCells];
+    const int lane = threadIdx.x % kCells, s = threadIdx.x / kCells;
+    const double eps = PERT ? *eps_p : 0.0;
+    const bool zero = PERT && eps == 0.0;  // |v| = 0 short-circuit (nonlinear.cpp:110)
+    const int ntiles = (m.nc + kCells - 1) / kCells;
+    // Persistent grid-stride loop over tiles of kCells cells.  The slot indices of a tile
+    // and the epilogue operand r_u of (component s, cell) — threads s < 3 do the per-cell
+    // sums — are loaded one iteration ahead, so a tile's dependent chain is one gather.
+    auto fetch = [&](int t, int& fr, int& o, double& ru) {
+        const int cc = t * kCells + lane;
+        fr = -1;
+        o = -1;
+        ru = 0.0;
+        if (t < ntiles && cc < m.nc) {
+            if (s < m.slots) {
+                fr = m.slot_face[s * m.nc + cc];
+                o = m.slot_other[s * m.nc + cc];
+            }
+            if (PERT && s < 3) ru = r_u[3 * cc + s];
+        }
+    };
+    int fr_next, o_next;
+    double ru_next;
+    fetch(blockIdx.x, fr_next, o_next, ru_next);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int fr = fr_next, o = o_next;
+        const double ru = ru_next;
+        fetch(tile + gridDim.x, fr_next, o_next, ru_next);
+        const int c = tile * kCells + lane;
+        unsigned char kd = 0;
+        if (fr != -1 && !zero) {
+            const int f = fr & ~kSign;
+            d3 flux, st;
+            if (o >= 0) {
+                const bool nb = (fr & kSign) != 0;
+                const int ip = nb ? o : c, in = nb ? c : o;  // reference owner / neighbour
+                const int nf = m.nf;
+                const d3 gam = {face9[f], face9[nf + f], face9[2 * nf + f]};
+                const d3 del = {face9[3 * nf + f], face9[4 * nf + f], face9[5 * nf + f]};
+                const double cfac = face9[6 * nf + f], gmag = face9[7 * nf + f], wf = face9[8 * nf + f];
+                const d3 up = ldw(w, m.nc, ip), un = ldw(w, m.nc, in);
+                if (!GEN) {
+                    double gp[9], gn[9];
+                    ldg9(G, m.nc, ip, gp);
+                    ldg9(G, m.nc, in, gn);
+                    hooke_face(gp, gn, wf, ph.mu, ph.lam, gam, del, up, un, cfac, gmag, ph.alpha, ph.kbar, flux, st);
+                } else {
+                    const dm3 gp = ldG(G, m.nc, ip), gn = ldG(G, m.nc, in);
+                    bool okp, okn;
+                    const dm3 sp = stress(ph, gp, okp), sn = stress(ph, gn, okn);
+                    d3 gm = gam;
+                    if (ph.tl) {
+                        bool ok;
+                        gm = transform_area(gam, interp(defgrad(gp), defgrad(gn), wf), ok);
+                        if (!ok) atomicMin(&err->inverted_face, f);
+                    }
+                    flux = dot_left(gm, interp(sp, sn, wf));
+                    // rhie_chow() with its per-face constants precomputed
+                    const d3 compact = scl(sub(un, up), cfac);
+                    st = scl(sub(compact, dot_left(del, interp(gp, gn, wf))), ph.alpha * ph.kbar * gmag);
+                }
+                if (nb) {
+                    flux = neg(flux);
+                    st = neg(st);
+                }
+                kd = 2;
+            } else {
+                // boundary face: evaluated by boundary_kernel; traction faces carry no
+                // stabilisation term (discretisation.cpp:204-205)
+                const int fb = f - m.nint;
+                const int nbf = m.nf - m.nint;
+                flux = {bres[fb], bres[nbf + fb], bres[2 * nbf + fb]};
+                st = {bres[3 * nbf + fb], bres[4 * nbf + fb], bres[5 * nbf + fb]};
+                kd = pt.kind[-o - 2] == SFV_PATCH_TRACTION ? 1 : 2;
+            }
+            res[s][0][lane] = flux.x;
+            res[s][1][lane] = flux.y;
+            res[s][2][lane] = flux.z;
+            res[s][3][lane] = st.x;
+            res[s][4][lane] = st.y;
+            res[s][5][lane] = st.z;
+        }
+        kind[s][lane] = kd;
+        __syncthreads();
+        // (component k = s, cell c): the reference's per-cell summation order
+        if (s < 3 && c < m.nc) {
+            const int k = s;
+            const int ik = 3 * c + k;
+            if (zero) {
+                out[ik] = 0.0;
+            } else {
+                if (GEN && k == 0 && ph.law == SFV_LAW_NEO_HOOKEAN) {  // the stress loop visits every cell
+                    bool ok;
+                    (void)stress(ph, ldG(G, m.nc, c), ok);
+                    if (!ok) atomicMin(&err->inverted_cell, c);
+                }
+                double r = 0.0;
+                if (!ph.stab_only) {
+#pragma unroll
+                    for (int t = 0; t < S; ++t)
+                        if (kind[t][lane] != 0) r += res[t][k][lane];
+                }
+#pragma unroll
+                for (int t = 0; t < S; ++t)
+                    if (kind[t][lane] == 2) r += res[t][3 + k][lane];
+                if (ph.transient && !ph.stab_only) {  // BDF2 inertia (discretisation.cpp:48-57, :163-169)
+                    const double uc = w[k * m.nc + c];
+                    const double idt = 1.0 / (2.0 * ph.dt);
+                    const double vn = ((uc * 3.0 - hist.u_old[ik] * 4.0) + hist.u_old_old[ik]) * idt;
+                    const double ac = ((vn * 3.0 - hist.v_old[ik] * 4.0) + hist.v_old_old[ik]) * idt;
+                    r = r - ac * (ph.rho * m.volume[c]);
+                }
+                if (!ph.stab_only && !isfinite(r)) atomicMin(&err->nan_cell, c);
+                if constexpr (PERT) {  // (R(u + eps v) - R(u)) / eps (nonlinear.cpp:132-136)
+                    const double q = (r - ru) / eps;
+                    if (!isfinite(q)) atomicMin(&err->nan_jv, c);
+                    out[ik] = q;
+                } else {
+                    out[ik] = r;
+                }
+            }
+        }
+        __syncthreads();  // res / kind are rewritten by the next tile
+    }
+}
+
+template <bool PERT, int S, bool GEN>
+int flux_grid(int ntiles) {
+    static int per_sm = -1;
+    static int sms = 0;
+    if (per_sm < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flux_pair_kernel<PERT, S, GEN>, kCells * S, 0);
+        per_sm = per_sm < 1 ? 1 : per_sm;
+    }
+    const int g = per_sm * sms;
+    return ntiles < g ? ntiles : g;
+}
+
+template <bool PERT, int S>
+void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist, const double* u,
+              const double* v, const double* eps, const double* r_u, double* out, const PairScratch& ps,
+              ErrWords* err, cudaStream_t st) {
+    double* w = ps.w;
+    double* G = ps.G;
+    const int cb = (m.nc + 255) / 256;
+    perturb_kernel<PERT><<<cb, 256, 0, st>>>(m.nc, u, v, eps, w);
+    grad_cell_kernel<S><<<cb, 256, 0, st>>>(m, pt, w, G);
+    const int nbf = m.nf - m.nint;
+    if (nbf > 0)
+        boundary_kernel<<<(nbf + 127) / 128, 128, 0, st>>>(m, ph, pt, ps.bnd_si, w, PERT ? eps : nullptr, G, ps.bres,
+                                                           err);
+    const int ntiles = (m.nc + kCells - 1) / kCells;
+    const double* f9 = ps.face9;
+    if (ph.law != SFV_LAW_HOOKE || ph.tl)
+        flux_pair_kernel<PERT, S, true>
+            <<<flux_grid<PERT, S, true>(ntiles), kCells * S, 0, st>>>(m, ph, pt, hist, w, eps, G, f9, ps.bres, r_u, out, err);
+    else
+        flux_pair_kernel<PERT, S, false>
+            <<<flux_grid<PERT, S, false>(ntiles), kCells * S, 0, st>>>(m, ph, pt, hist, w, eps, G, f9, ps.bres, r_u, out, err);
+}
+
+}  // namespace
+
+void launch_residual_pair(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist,
+                          const double* u, const double* v, const double* jv_eps, const double* r_u, double* out,
+                          const PairScratch& ps, ErrWords* err, cudaStream_t s) {
+    const bool pert = jv_eps != nullptr;
+    if (m.slots <= 4) {
+        if (pert) launch_s<true, 4>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
+        else launch_s<false, 4>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
+    } else if (m.slots <= 6) {
+        if (pert) launch_s<true, 6>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
+        else launch_s<false, 6>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
+    } else {
+        if (pert) launch_s<true, 8>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
+        else launch_s<false, 8>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
+    }
+}
+
+}  // namespace sfv
