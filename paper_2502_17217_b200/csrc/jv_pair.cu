@@ -33,9 +33,21 @@ constexpr int kSign = static_cast<int>(0x80000000u);
 __device__ __forceinline__ d3 ldsoa(const double* __restrict__ p, int n, int i) {
     return {p[i], p[n + i], p[2 * static_cast<size_t>(n) + i]};
 }
+// Streams read once per pass (slot tables, least-squares vectors, r_u) are loaded with
+// evict-first (ld.global.cs) so that the gathered w and G (~96 MB at 1M cells) stay in L2.
 // All gathered arrays are SoA so that the 32 lanes of a warp (32 consecutive cells, one
 // face slot) load 32 consecutive doubles per instruction: the L1 wavefront queue, not DRAM,
 // limits a gather kernel whose loads each touch many 128-byte lines.
+// w and G are written with an L2 evict-last policy: their consumers gather them within
+// the next two kernels, after ~170 MB of streamed least-squares vectors and slot tables.
+__device__ __forceinline__ unsigned long long evict_last_policy() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_keep(double* a, double v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
 // perturbed state w[k * nc + c] = u + eps v
 __device__ __forceinline__ d3 ldw(const double* __restrict__ w, int nc, int c) {
     return {w[c], w[nc + c], w[2 * nc + c]};
@@ -67,9 +79,10 @@ __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __re
         y = y + eps * v[3 * c + 1];
         z = z + eps * v[3 * c + 2];
     }
-    w[c] = x;
-    w[nc + c] = y;
-    w[2 * nc + c] = z;
+    const unsigned long long pol = evict_last_policy();
+    st_keep(&w[c], x, pol);
+    st_keep(&w[nc + c], y, pol);
+    st_keep(&w[2 * nc + c], z, pol);
 }
 
 // ---------------------------------------------------------------- gradients
@@ -82,7 +95,7 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
     if (c >= m.nc) return;
     int o[S];
 #pragma unroll
-    for (int s = 0; s < S; ++s) o[s] = s < m.slots ? m.slot_other[s * m.nc + c] : -1;
+    for (int s = 0; s < S; ++s) o[s] = s < m.slots ? __ldcs(&m.slot_other[s * m.nc + c]) : -1;
     const d3 wc = ldw(w, m.nc, c);
     d3 wn[S];
 #pragma unroll
@@ -101,15 +114,16 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
         } else {
             continue;  // traction / displacement faces are not in the stencil; padding
         }
-        const d3 ls = {m.slot_ls[(3 * s) * m.nc + c], m.slot_ls[(3 * s + 1) * m.nc + c],
-                       m.slot_ls[(3 * s + 2) * m.nc + c]};
+        const d3 ls = {__ldcs(&m.slot_ls[(3 * s) * m.nc + c]), __ldcs(&m.slot_ls[(3 * s + 1) * m.nc + c]),
+                       __ldcs(&m.slot_ls[(3 * s + 2) * m.nc + c])};
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int j = 0; j < 3; ++j) g[3 * i + j] += cmp(ls, i) * cmp(du, j);
     }
+    const unsigned long long pol = evict_last_policy();
 #pragma unroll
-    for (int q = 0; q < 9; ++q) G[q * m.nc + c] = g[q];
+    for (int q = 0; q < 9; ++q) st_keep(&G[q * m.nc + c], g[q], pol);
 }
 
 // ---------------------------------------------------------------- boundary faces
@@ -181,8 +195,11 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
                      const double* __restrict__ eps_p, const double* __restrict__ G,
                      const double* __restrict__ face9, const double* __restrict__ bres,
                      const double* __restrict__ r_u, double* __restrict__ out, ErrWords* __restrict__ err) {
-    __shared__ double res[S][6][kCells];
-    __shared__ unsigned char kind[S][kCells];
+    // double-buffered per-slot results: one barrier per tile; the sums of tile i (warps
+    // s < 3) overlap the face work of tile i + 1, and the barrier of tile i + 1 orders
+    // them before buffer i & 1 is rewritten by tile i + 2
+    __shared__ double res_buf[2][S][6][kCells];
+    __shared__ unsigned char kind_buf[2][S][kCells];
     const int lane = threadIdx.x % kCells, s = threadIdx.x / kCells;
     const double eps = PERT ? *eps_p : 0.0;
     const bool zero = PERT && eps == 0.0;  // |v| = 0 short-circuit (nonlinear.cpp:110)
@@ -197,16 +214,19 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
         ru = 0.0;
         if (t < ntiles && cc < m.nc) {
             if (s < m.slots) {
-                fr = m.slot_face[s * m.nc + cc];
-                o = m.slot_other[s * m.nc + cc];
+                fr = __ldcs(&m.slot_face[s * m.nc + cc]);
+                o = __ldcs(&m.slot_other[s * m.nc + cc]);
             }
-            if (PERT && s < 3) ru = r_u[3 * cc + s];
+            if (PERT && s < 3) ru = __ldcs(&r_u[3 * cc + s]);
         }
     };
     int fr_next, o_next;
     double ru_next;
     fetch(blockIdx.x, fr_next, o_next, ru_next);
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        double(*res)[6][kCells] = res_buf[it & 1];
+        unsigned char(*kind)[kCells] = kind_buf[it & 1];
         const int fr = fr_next, o = o_next;
         const double ru = ru_next;
         fetch(tile + gridDim.x, fr_next, o_next, ru_next);
@@ -304,7 +324,6 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
                 }
             }
         }
-        __syncthreads();  // res / kind are rewritten by the next tile
     }
 }
 
