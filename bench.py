@@ -184,6 +184,8 @@ def run_reference(args):
 
 
 def run_ours(args):
+    import ctypes as C
+
     import torch
 
     from paper_2502_17217_b200 import cases
@@ -245,7 +247,6 @@ def run_ours(args):
     hr = r_u.cpu().pin_memory()
     hv = torch.from_numpy(v_h).pin_memory()
     ho = torch.empty(n, dtype=torch.float64).pin_memory()
-    import ctypes as C
     dp = C.POINTER(C.c_double)
 
     def e2e_step():
@@ -264,11 +265,23 @@ def run_ours(args):
     e2e_s = (time.perf_counter() - t0) / e2e_n
     e2e_s = max_over_ranks(e2e_s)
 
+    # per-stage device times of the same J.v (CUDA events on the context stream), and the
+    # algorithmic bytes of each stage: the roofline is quoted for the dominant kernel
+    import ctypes as C
+    names = ["jv_eps_kernel", "perturb_kernel", "grad_cell_kernel", "boundary_kernel", "flux_pair_kernel"]
+    st_ms = (C.c_double * 5)()
+    st_b = (C.c_double * 5)()
+    L.sfv_jv_stage_bytes(h, st_b)
+    ev._check(L.sfv_jv_stage_times(h, u.data_ptr(), r_u.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                   max(5, min(args.steps, 50)), st_ms))
+    stages = [{"kernel": names[k], "ms": st_ms[k], "bytes": st_b[k],
+               "GBps": st_b[k] / (st_ms[k] / 1e3) / 1e9 if st_ms[k] > 0 else None} for k in range(5)]
+    top = max(range(5), key=lambda k: st_ms[k])
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(prof):
         with open(prof) as f:
-            traffic = json.load(f).get("dram_bytes_per_jv")
+            traffic = json.load(f).get("dram_bytes_per_launch", {}).get(names[top])
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -277,9 +290,13 @@ def run_ours(args):
         "config": {"workload": f"{args.config}: {case.notes}", "cells": mesh.n_cells, "faces": mesh.n_faces,
                    "parallelism": "replicas only" if ws > 1 else "single GPU",
                    "l2": "J.v working set > 126 MB L2 (no flush needed)", "setup_s": round(t_setup, 2)},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_kind": peak_kind, "traffic": traffic, "algorithmic_bytes_per_jv": jv_bytes,
-                     "kernel": "J.v (eps reduction + gradient pass + flux pass)"},
+        "roofline": {"bound": "hbm", "achieved": stages[top]["GBps"], "peak": peak, "unit": "GB/s",
+                     "frac": stages[top]["GBps"] / peak, "peak_kind": peak_kind, "traffic": traffic,
+                     "kernel": names[top], "algorithmic_bytes_per_launch": st_b[top],
+                     "launch_ms": st_ms[top], "share_of_jv": st_ms[top] / sum(st_ms)},
+        "jv_roofline": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                        "algorithmic_bytes_per_jv": jv_bytes, "model": "SURVEY.md 8d: 96Nc+120Nf+60Nd+12Nt"},
+        "stages": stages,
         "cell_dof_per_s": 3 * mesh.n_cells * value,
         "e2e": {"value": ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 3 * 8 * n, "d2h_bytes_per_step": 8 * n},
         "gpu_launches": launches,

@@ -97,6 +97,14 @@ int sfv_jv_eps(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const d
  * on the device until sfv_check_errors. */
 int sfv_jv_async(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* v_dev, double* out_dev);
 int sfv_check_errors(sfv_ctx* ctx, int* cell);
+/* Measurement only (bench.py): average device time in ms of each stage of `reps`
+ * J.v calls, timed with CUDA events on the context stream: ms[0] |u|,|v| + eps,
+ * ms[1] perturbed state, ms[2] gradients, ms[3] boundary faces, ms[4] face fluxes +
+ * per-cell sums.  Returns SFV_ERR_INVALID_ARGUMENT unless the default (jv_pair.cu) path is active. */
+int sfv_jv_stage_times(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* v_dev,
+                       double* out_dev, int reps, double* ms);
+/* The bytes each of those five stages moves at least once (its algorithmic traffic). */
+void sfv_jv_stage_bytes(const sfv_ctx* ctx, double* bytes);
 
 /* host-buffer conveniences (copies inside the call) */
 int sfv_residual_host(sfv_ctx* ctx, const double* u, double* r, int* cell);

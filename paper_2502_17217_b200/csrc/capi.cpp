@@ -1033,6 +1033,18 @@ double sfv_jv_bytes(const sfv_ctx* c) {
            (c->ph.transient ? 104.0 * c->nc : 0.0);
 }
 
+void sfv_jv_stage_bytes(const sfv_ctx* c, double* b) {
+    // bytes each stage of the default J.v path must move at least once:
+    // N_c cells, S face slots per cell, N_f faces, N_b boundary faces
+    const double nc = c->nc, S = c->dm.slots, nf = c->dm.nf, nb = c->dm.nf - c->dm.nint;
+    const double tr = c->ph.transient ? 104.0 * nc : 0.0;  // volume + 4 history vectors
+    b[0] = 48.0 * nc;                                       // u, v
+    b[1] = 72.0 * nc;                                       // u, v -> w
+    b[2] = (4.0 * S + 24.0 * S + 24.0 + 72.0) * nc;         // slot_other, ls, w, G
+    b[3] = 208.0 * nb;                                      // slot, geometry, G, w -> 6 results
+    b[4] = (8.0 * S + 72.0 + 24.0 + 24.0 + 24.0) * nc + 72.0 * nf + 48.0 * nb + tr;  // slots, G, w, r_u, out, faces
+}
+
 int sfv_geometry(const sfv_ctx* c, double* volume, double* centroid, double* face_centroid, double* area, double* d,
                  double* d_mag, double* w, double* delta, double* g_inv, signed char* g_singular, int* cf_offsets,
                  int* cf_faces, double* ls_vec) {
@@ -1175,6 +1187,34 @@ int sfv_jv_async(sfv_ctx* c, const double* u, const double* r_u, const double* v
     if (c->singular_cell >= 0) return gradient_failure(c);
     jv_async(c, u, r_u, v, out, false);
     return c->cuda_check("jv_async");
+}
+
+int sfv_jv_stage_times(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out, int reps,
+                       double* ms) {
+    if (c->jv_path != 0 || reps <= 0 || !ms) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "jv_stage_times: default path only");
+    if (c->singular_cell >= 0) return gradient_failure(c);
+    cudaEvent_t ev[6];
+    for (auto& e : ev) cudaEventCreate(&e);
+    double acc[5] = {0, 0, 0, 0, 0};
+    for (int r = 0; r < reps; ++r) {
+        cudaEventRecord(ev[0], c->stream);
+        launch_jv_eps(u, v, c->n, c->red.p, c->counter.p, c->scal.p, c->scal.p + 1, false, c->stream);
+        cudaEventRecord(ev[1], c->stream);
+        c->ps.marks = ev + 2;
+        launch_residual_pair(c->dm, c->ph, c->pt, c->hist, u, v, c->scal.p, r_u, out, c->ps, c->err.p, c->stream);
+        c->ps.marks = nullptr;
+        cudaEventRecord(ev[5], c->stream);
+        if (cudaEventSynchronize(ev[5]) != cudaSuccess) break;
+        for (int k = 0; k < 5; ++k) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, ev[k], ev[k + 1]);
+            acc[k] += t;
+        }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (int k = 0; k < 5; ++k) ms[k] = acc[k] / reps;
+    c->launches += static_cast<long long>(reps) * (c->dm.nf > c->dm.nint ? 5 : 4);
+    return c->cuda_check("jv_stage_times");
 }
 
 int sfv_check_errors(sfv_ctx* c, int* cell) {

@@ -81,6 +81,7 @@ struct PairScratch {
     const double* face9 = nullptr;  // [9*nf] Gamma xyz, Delta xyz, |Delta|/|d|, |Gamma|, w; SoA
     const int* bnd_si = nullptr;  // [nf-nint] slot index (s*nc + cell) of boundary face nint+fb
     double* bres = nullptr;       // [6*(nf-nint)] boundary-face flux + stabilisation
+    cudaEvent_t* marks = nullptr;  // optional: recorded after the perturb, gradient, boundary passes
 };
 void launch_residual_pair(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist,
                           const double* u, const double* v, const double* jv_eps, const double* r_u, double* out,

@@ -350,11 +350,14 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     double* G = ps.G;
     const int cb = (m.nc + 255) / 256;
     perturb_kernel<PERT><<<cb, 256, 0, st>>>(m.nc, u, v, eps, w);
+    if (ps.marks) cudaEventRecord(ps.marks[0], st);
     grad_cell_kernel<S><<<cb, 256, 0, st>>>(m, pt, w, G);
+    if (ps.marks) cudaEventRecord(ps.marks[1], st);
     const int nbf = m.nf - m.nint;
     if (nbf > 0)
         boundary_kernel<<<(nbf + 127) / 128, 128, 0, st>>>(m, ph, pt, ps.bnd_si, w, PERT ? eps : nullptr, G, ps.bres,
                                                            err);
+    if (ps.marks) cudaEventRecord(ps.marks[2], st);
     const int ntiles = (m.nc + kCells - 1) / kCells;
     const double* f9 = ps.face9;
     if (ph.law != SFV_LAW_HOOKE || ph.tl)

@@ -79,6 +79,8 @@ def lib():
         "sfv_jv_eps": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _vp, _ip]),
         "sfv_jv_async": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
         "sfv_check_errors": (C.c_int, [_vp, _ip]),
+        "sfv_jv_stage_times": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _dp]),
+        "sfv_jv_stage_bytes": (None, [_vp, _dp]),
         "sfv_residual_host": (C.c_int, [_vp, _dp, _dp, _ip]),
         "sfv_jv_host": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _ip]),
         "sfv_precond_create": (C.c_int, [_vp, C.c_int]),
