@@ -814,13 +814,15 @@ int precond_create(sfv_ctx* c, int kind) {
                 }
             }
         const int smem_cap = 232448;
-        const int stages = ring ? std::min(8, (smem_cap - ring * 32 - 4200) / (max_rows * 120)) : 0;
+        const int stages = ring ? std::min(8, (smem_cap - stream_smem_bytes(ring, max_rows, 0)) / (max_rows * 120)) : 0;
         stream_ok_all = ring > 0 && stages >= 3;
         if (stream_ok_all) {
             for (size_t x = 0; x < scheds.size(); ++x) {
                 DevBuf<unsigned char>& b = c->srec[(x % 2) * 3 + x / 2];
-                if (!b.alloc(recs[x].size() * sizeof(StreamRecord)) ||
-                    cudaMemcpy(b.p, recs[x].data(), b.bytes(), cudaMemcpyHostToDevice) != cudaSuccess)
+                std::vector<unsigned char> packed;
+                pack_stream_chunks(recs[x], packed);
+                if (!b.alloc(packed.size()) ||
+                    cudaMemcpy(b.p, packed.data(), b.bytes(), cudaMemcpyHostToDevice) != cudaSuccess)
                     return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
                 const int a = static_cast<int>(x / 2);
                 DevStream ds{scheds[x].n_levels, x % 2 ? c->U[a].view.level_ptr : c->L[a].view.level_ptr, b.p};

@@ -3,6 +3,9 @@
 #include "precond_host.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <functional>
 #include <numeric>
@@ -348,6 +351,7 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
         }
     }
     out.assign(np, StreamRecord{});
+    long long n_dep = 0, n_local = 0;
     for (int p = 0; p < np; ++p) {
         StreamRecord& rec = out[p];
         rec.own = static_cast<uint16_t>(ordinal[p] % ring);
@@ -364,9 +368,36 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
             if (o < static_cast<int>(ord_level[r].size()) && ord_level[r][o] <= level_of[p]) return false;
             rec.dep[k] = static_cast<uint16_t>((r << 12) | (ordinal[q] % ring));
             rec.val[k] = t.ell_val[static_cast<size_t>(k) * np + p];
+            ++n_dep;
+            if (r == owner[p]) ++n_local;
         }
     }
+    if (std::getenv("SFV_STREAM_STATS"))
+        std::fprintf(stderr, "stream records: %d positions, %d levels, %lld deps, %.1f%% in the reading CTA\n", np,
+                     t.n_levels, n_dep, 100.0 * n_local / std::max(1LL, n_dep));
     return true;
+}
+
+void pack_stream_chunks(const std::vector<StreamRecord>& recs, std::vector<unsigned char>& out) {
+    const size_t nchunk = (recs.size() + 31) / 32;
+    out.assign(nchunk * kChunkBytes, 0);
+    for (size_t p = 0; p < recs.size(); ++p) {
+        const StreamRecord& r = recs[p];
+        unsigned char* c = out.data() + (p / 32) * kChunkBytes;
+        const size_t l = p % 32;
+        for (int q = 0; q < 8; ++q) {
+            std::memcpy(c + (q * 32 + l) * 8, &r.val[q], 8);
+            std::memcpy(c + 2304 + (q * 32 + l) * 2, &r.dep[q], 2);
+        }
+        std::memcpy(c + 2048 + l * 8, &r.diag, 8);
+        std::memcpy(c + 2816 + l * 2, &r.own, 2);
+    }
+    for (size_t p = recs.size(); p < nchunk * 32; ++p) {  // padding rows: no dependencies
+        unsigned char* c = out.data() + (p / 32) * kChunkBytes;
+        const size_t l = p % 32;
+        const uint16_t none = 0xffff;
+        for (int q = 0; q < 8; ++q) std::memcpy(c + 2304 + (q * 32 + l) * 2, &none, 2);
+    }
 }
 
 }  // namespace sfv

@@ -55,6 +55,12 @@ struct StreamRecord {
 };
 static_assert(sizeof(StreamRecord) == 96, "record layout");
 bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, std::vector<StreamRecord>& out);
+// Device layout of the records: per chunk of 32 positions (levels are padded to 32), the
+// fields as arrays over the 32 positions — val[8][32], diag[32], dep[8][32], own[32],
+// 3072 bytes — so that a warp reading one field of 32 consecutive rows from shared
+// memory is bank-conflict free (the 96-byte AoS record was read at a 96-byte lane stride).
+constexpr int kChunkBytes = 3072;
+void pack_stream_chunks(const std::vector<StreamRecord>& recs, std::vector<unsigned char>& out);
 
 // Banded Cholesky of -A after reverse Cuthill-McKee (A symmetric negative definite);
 // returns "" or "lu: factorisation failed".  Band row i holds L(i, i-bw .. i).

@@ -9,9 +9,12 @@
 //     them; their values go into CTA r's shared-memory ring, from where later levels read
 //     them over DSMEM (one ld.shared::cluster pair per dependency, ~200 cycles);
 //   * each position's factor row is a 96-byte record (16-bit DSMEM address of every
-//     dependency, its value, the pivot), streamed kStages-1 levels ahead with cp.async into
-//     shared-memory stages — the dependent chain per level is only DSMEM loads + FMA-free
-//     FP64 arithmetic, never an HBM round trip;
+//     dependency, its value, the pivot), stored field-major per chunk of 32 positions
+//     (pack_stream_chunks: bank-conflict-free shared-memory reads) and streamed kStages-1
+//     levels ahead with cp.async into shared-memory stages — the dependent chain per level
+//     is only DSMEM loads + FMA-free FP64 arithmetic, never an HBM round trip;
+//   * the value ring is one array per right-hand side ([NRHS][ring] doubles), so the 32
+//     lanes of a warp store consecutive doubles;
 //   * one CTA-scope fence + relaxed cluster barrier hands the level over (a cluster-scope
 //     release compiles to MEMBAR.ALL.GPU and would wait for the HBM stores of the results).
 //
@@ -19,10 +22,20 @@
 // reader and that no level slice exceeds kMaxRows (build_stream_records); otherwise the
 // other sweeps in precond.cu are used.  Compiled with -fmad=false: bit-identical results.
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include "device.h"
 
 namespace cg = cooperative_groups;
+
+// timing probes (scripts/build_variant.py): -DSFV_TS_PROBE=m drops 1: the CTA fence,
+// 2: the result stores to HBM, 4: the record prefetch, 8: the dependency loads,
+// 16: the whole row loop (results are then wrong); 32: per-phase clock64 totals of
+// CTA 0 / CTA 15 printed at exit (results stay right).
+#ifndef SFV_TS_PROBE
+#define SFV_TS_PROBE 0
+#endif
+#define TSP(b) (!(SFV_TS_PROBE & (b)))
 
 namespace sfv {
 namespace {
@@ -30,14 +43,8 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kLvl = 1024;
 
-struct Rec {
-    unsigned short dep[8];
-    unsigned short own;
-    unsigned short pad[3];
-    double val[8];
-    double diag;
-};
-static_assert(sizeof(Rec) == 96, "record layout");
+// field offsets inside a 3072-byte chunk of 32 records (precond_host.h: pack_stream_chunks)
+constexpr int kChunk = 3072, kOffDiag = 2048, kOffDep = 2304, kOffOwn = 2816;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
@@ -49,25 +56,53 @@ __device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
+__device__ __forceinline__ void mbar_init(uint32_t a, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+// one TMA bulk copy global -> own shared memory, completing `bytes` on the mbarrier
+__device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+// kThreads compute threads + one producer warp whose lane 0 streams the records kStages - 1
+// levels ahead: a CTA's slice of a level is contiguous in position space, so it is two TMA
+// bulk copies (records, right-hand side) completing on the stage's mbarrier (expect_tx).
+// The per-level critical path is: wait stage -> rows -> cluster barrier.
 template <bool UPPER, int NRHS, int kStages>
-__global__ void __launch_bounds__(kThreads, 1) tri_stream_kernel(StreamSet set, const double* __restrict__ src,
-                                                                 double* __restrict__ dst) {
+__global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet set, const double* __restrict__ src,
+                                                                      double* __restrict__ dst) {
     const int kMaxRows = set.max_rows;  // rows per CTA per level (stage stride)
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = static_cast<int>(cluster.block_rank());
     const int comp = NRHS == 3 ? 0 : static_cast<int>(blockIdx.x / kStreamCluster);
     const DevStream& t = set.t[comp];
+    const bool producer = threadIdx.x >= kThreads;
+    const int ptid = threadIdx.x - kThreads;
     extern __shared__ __align__(16) unsigned char smem[];
-    double* ring = reinterpret_cast<double*>(smem);                               // [ring][4]
-    Rec* stage_rec = reinterpret_cast<Rec*>(smem + static_cast<size_t>(set.ring) * 32);  // [kStages][kMaxRows]
-    double* stage_src = reinterpret_cast<double*>(stage_rec + kStages * kMaxRows);  // [kStages][kMaxRows*3]
-    int* lp = reinterpret_cast<int*>(stage_src + kStages * kMaxRows * 3);          // [kLvl + 2]
+    const int ring_n = set.ring;
+    double* ring = reinterpret_cast<double*>(smem);  // [NRHS][ring_n]
+    unsigned char* stage_rec = smem + static_cast<size_t>(ring_n) * 24;  // [kStages][kMaxRows / 32 chunks]
+    double* stage_src = reinterpret_cast<double*>(stage_rec + static_cast<size_t>(kStages) * kMaxRows * 96);  // [kStages][kMaxRows*3]
+    int* lp = reinterpret_cast<int*>(stage_src + kStages * kMaxRows * 3);  // [kLvl + 2]
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(lp + kLvl + 2);  // [kStages], 8-aligned
     const uint32_t ring_base = smem_u32(ring);
+    const uint32_t mbar_base = smem_u32(mbar);
     int lbase = 0;
     auto stage_levels = [&](int base) {
         __syncthreads();
         lbase = base;
-        for (int x = threadIdx.x; x < kLvl + 2; x += kThreads)
+        for (int x = threadIdx.x; x < kLvl + 2; x += blockDim.x)
             lp[x] = base + x <= t.n_levels ? t.level_ptr[base + x] : t.level_ptr[t.n_levels];
         __syncthreads();
     };
@@ -77,72 +112,117 @@ __global__ void __launch_bounds__(kThreads, 1) tri_stream_kernel(StreamSet set, 
         a = min(lb, la + rank * per * 32);
         b = min(lb, a + per * 32);
     };
-    auto issue = [&](int l) {  // async copy of level l's records and right-hand side
-        if (l < t.n_levels) {
+    auto issue = [&](int l) {  // producer lane 0: level l's records and right-hand side
+        if (l >= t.n_levels || ptid != 0) return;
+        const int s = l % kStages;
+        int a, b;
+        slice(l, a, b);
+        if (!TSP(4)) b = a;
+        const uint32_t bar = mbar_base + 8u * s;
+        // positions are chunk (32) aligned: both copies are 16-byte multiples at 16-byte addresses
+        mbar_expect(bar, static_cast<uint32_t>(b - a) * 120u);
+        if (b > a) {
+            bulk_copy(smem_u32(stage_rec + static_cast<size_t>(s) * kMaxRows * 96),
+                      reinterpret_cast<const unsigned char*>(t.rec) + static_cast<size_t>(a) * 96,
+                      static_cast<uint32_t>(b - a) * 96u, bar);
+            bulk_copy(smem_u32(stage_src + s * kMaxRows * 3), src + 3 * static_cast<size_t>(a),
+                      static_cast<uint32_t>(b - a) * 24u, bar);
+        }
+    };
+    if (threadIdx.x < kStages) mbar_init(mbar_base + 8u * threadIdx.x, 1);
+    stage_levels(0);  // its __syncthreads also publishes the mbarrier init
+    if (producer)
+        for (int l = 0; l < kStages - 1; ++l) issue(l);
+    long long ph[5] = {0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
+    (void)ph;
+    (void)t0;
+    (void)t1;
+    for (int l = 0; l < t.n_levels; ++l) {
+        if (!TSP(32)) t0 = clock64();
+        if (l + kStages - 1 + 1 - lbase > kLvl) stage_levels(l);  // keep lp[] covering the issue window
+        if (producer) {
+            // stage (l - 1) % kStages was consumed before the barrier that ended level l - 1
+            issue(l + kStages - 1);
+        } else {
+            mbar_wait(mbar_base + 8u * (l % kStages), static_cast<uint32_t>((l / kStages) & 1));
+            if (!TSP(32)) {
+                t1 = clock64();
+                ph[1] += t1 - t0;
+                t0 = t1;
+            }
             int a, b;
             slice(l, a, b);
             const int s = l % kStages;
-            const uint32_t rdst = smem_u32(stage_rec + s * kMaxRows);
-            const unsigned char* rsrc = reinterpret_cast<const unsigned char*>(t.rec) + static_cast<size_t>(a) * 96;
-            for (int u = threadIdx.x; u < (b - a) * 6; u += kThreads) cp16(rdst + u * 16, rsrc + u * 16);
-            const uint32_t sdst = smem_u32(stage_src + s * kMaxRows * 3);
-            const double* ssrc = src + 3 * static_cast<size_t>(a);
-            for (int u = threadIdx.x; u < ((b - a) * 3) / 2; u += kThreads) cp16(sdst + u * 16, ssrc + 2 * u);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    stage_levels(0);
-    for (int l = 0; l < kStages - 1; ++l) issue(l);
-    for (int l = 0; l < t.n_levels; ++l) {
-        if (l + kStages - 1 + 1 - lbase > kLvl) stage_levels(l);  // keep lp[] covering the issue window
-        issue(l + kStages - 1);
-        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
-        __syncthreads();
-        int a, b;
-        slice(l, a, b);
-        const int s = l % kStages;
-        for (int j = threadIdx.x; j < b - a; j += kThreads) {
-            const Rec& r = stage_rec[s * kMaxRows + j];
-            double z[NRHS];
+            for (int j = threadIdx.x; TSP(16) && j < b - a; j += kThreads) {
+                const unsigned char* ch = stage_rec + static_cast<size_t>(s) * kMaxRows * 96 + (j / 32) * kChunk;
+                const int ln = j % 32;
+                const double* rval = reinterpret_cast<const double*>(ch) + ln;  // [q * 32]
+                const unsigned short* rdep = reinterpret_cast<const unsigned short*>(ch + kOffDep) + ln;  // [q * 32]
+                unsigned short dep[8];
 #pragma unroll
-            for (int k = 0; k < NRHS; ++k) z[k] = stage_src[(s * kMaxRows + j) * 3 + comp + k];
-            double dv[8][NRHS];
+                for (int q = 0; q < 8; ++q) dep[q] = rdep[q * 32];
+                double z[NRHS];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {  // all dependency loads in flight together
-                const unsigned d = r.dep[q];
-                if (d != 0xffffu) {
-                    const uint32_t ad = mapa(ring_base + (d & 0xfffu) * 32u, static_cast<int>(d >> 12));
-                    if (NRHS == 3) {
-                        asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];"
-                                     : "=d"(dv[q][0]), "=d"(dv[q][NRHS > 1 ? 1 : 0])
-                                     : "r"(ad));
-                        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(dv[q][NRHS > 2 ? 2 : 0]) : "r"(ad + 16));
-                    } else {
-                        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(dv[q][0]) : "r"(ad));
+                for (int k = 0; k < NRHS; ++k) z[k] = stage_src[(s * kMaxRows + j) * 3 + comp + k];
+                double dv[8][NRHS];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {  // all dependency loads in flight together
+                    const unsigned d = dep[q];
+#pragma unroll
+                    for (int k = 0; k < NRHS; ++k) dv[q][k] = 0.0;
+                    if (d != 0xffffu && TSP(8)) {
+                        const uint32_t ad = mapa(ring_base + (d & 0xfffu) * 8u, static_cast<int>(d >> 12));
+#pragma unroll
+                        for (int k = 0; k < NRHS; ++k)
+                            asm volatile("ld.shared::cluster.f64 %0, [%1];"
+                                         : "=d"(dv[q][k])
+                                         : "r"(ad + static_cast<uint32_t>(k * ring_n * 8)));
                     }
                 }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)  // the reference's order of subtraction
+                    if (dep[q] != 0xffffu) {
+                        const double vq = rval[q * 32];
+#pragma unroll
+                        for (int k = 0; k < NRHS; ++k) z[k] -= vq * dv[q][k];
+                    }
+                if (UPPER) {
+                    const double dg = reinterpret_cast<const double*>(ch + kOffDiag)[ln];
+#pragma unroll
+                    for (int k = 0; k < NRHS; ++k) z[k] /= dg;
+                }
+                const int own = reinterpret_cast<const unsigned short*>(ch + kOffOwn)[ln];
+#pragma unroll
+                for (int k = 0; k < NRHS; ++k) {
+                    ring[k * ring_n + own] = z[k];
+                    if (TSP(2)) dst[3 * static_cast<size_t>(a + j) + comp + k] = z[k];
+                }
             }
-#pragma unroll
-            for (int q = 0; q < 8; ++q)  // the reference's order of subtraction
-                if (r.dep[q] != 0xffffu)
-#pragma unroll
-                    for (int k = 0; k < NRHS; ++k) z[k] -= r.val[q] * dv[q][k];
-            if (UPPER)
-#pragma unroll
-                for (int k = 0; k < NRHS; ++k) z[k] /= r.diag;
-            double* slot = ring + static_cast<size_t>(r.own) * 4;
-#pragma unroll
-            for (int k = 0; k < NRHS; ++k) {
-                slot[k] = z[k];
-                dst[3 * static_cast<size_t>(a + j) + comp + k] = z[k];
+            if (!TSP(32)) {
+                t1 = clock64();
+                ph[2] += t1 - t0;
+                t0 = t1;
             }
+            // hand the level over: CTA-scope fence (the values live in this CTA's shared memory)
+            if (TSP(1)) asm volatile("fence.acq_rel.cta;" ::: "memory");
         }
-        // hand the level over: CTA-scope fence (the values live in this CTA's shared memory)
-        asm volatile("fence.acq_rel.cta;" ::: "memory");
         asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+        if (!TSP(32)) {
+            t1 = clock64();
+            ph[3] += t1 - t0;
+            t0 = t1;
+        }
         asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+        if (!TSP(32)) {
+            t1 = clock64();
+            ph[4] += t1 - t0;
+        }
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (!TSP(32) && (threadIdx.x == 0 || threadIdx.x == kThreads) && (rank == 0 || rank == 15))
+        printf("tri_stream U=%d rank %d thr %d levels %d: stage-wait %lld rows %lld fence+arrive %lld "
+               "barrier-wait %lld cycles/level\n",
+               UPPER ? 1 : 0, rank, threadIdx.x, t.n_levels, ph[1] / t.n_levels, ph[2] / t.n_levels,
+               ph[3] / t.n_levels, ph[4] / t.n_levels);
 }
 
 template <bool UPPER, int NRHS, int ST>
@@ -153,7 +233,7 @@ cudaError_t launch_st(const StreamSet& set, int ncomp, const double* src, double
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kStreamCluster * (NRHS == 3 ? 1 : ncomp));
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(kThreads + 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -181,7 +261,7 @@ cudaError_t launch_one(const StreamSet& set, int ncomp, const double* src, doubl
 }  // namespace
 
 int stream_smem_bytes(int ring, int max_rows, int stages) {
-    return ring * 32 + stages * max_rows * (96 + 24) + (kLvl + 2) * 4;
+    return ring * 24 + stages * max_rows * (96 + 24) + (kLvl + 2) * 4 + 8 * 8;
 }
 
 cudaError_t launch_tri_stream(const StreamSet& set, bool upper, int ncomp, const double* src, double* dst,
