@@ -23,6 +23,7 @@
 // other sweeps in precond.cu are used.  Compiled with -fmad=false: bit-identical results.
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.h"
 
@@ -266,6 +267,18 @@ int stream_smem_bytes(int ring, int max_rows, int stages) {
 
 cudaError_t launch_tri_stream(const StreamSet& set, bool upper, int ncomp, const double* src, double* dst,
                               cudaStream_t s) {
+    // one 16-CTA cluster per component also for the shared factor: three concurrent sweeps
+    // with a third of the DSMEM loads each beat one sweep carrying three right-hand sides
+    // (0.86 vs 1.28 ms per apply at 1M cells).  SFV_STREAM_SPLIT=0 restores the latter.
+    static const bool split = [] {
+        const char* e = std::getenv("SFV_STREAM_SPLIT");
+        return !e || std::atoi(e) != 0;
+    }();
+    if (ncomp == 1 && split) {
+        StreamSet s3 = set;
+        s3.t[1] = s3.t[2] = set.t[0];
+        return upper ? launch_one<true, 1>(s3, 3, src, dst, s) : launch_one<false, 1>(s3, 3, src, dst, s);
+    }
     if (upper) return ncomp == 1 ? launch_one<true, 3>(set, 1, src, dst, s) : launch_one<true, 1>(set, 3, src, dst, s);
     return ncomp == 1 ? launch_one<false, 3>(set, 1, src, dst, s) : launch_one<false, 1>(set, 3, src, dst, s);
 }
