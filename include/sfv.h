@@ -114,6 +114,10 @@ int sfv_precond_create(sfv_ctx* ctx, int kind);
 int sfv_precond_apply(sfv_ctx* ctx, const double* r_dev, double* z_dev);
 /* preconditioner facts: {kind_resolved, n_levels_fwd, n_levels_bwd, nnz_L, nnz_U} */
 int sfv_precond_info(const sfv_ctx* ctx, int info[5]);
+/* Device sweep of the ILU apply: 200 streamed level-synchronous (default), 300 block-
+ * pipelined (SFV_PIPE=1), 100 DSMEM ring, 1..16 ELL cluster, 0 sentinel polling; -1 when
+ * the preconditioner is not ILU. */
+int sfv_precond_sweep(const sfv_ctx* ctx);
 
 int sfv_gmres_jv(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* b_dev, double* x_dev,
                  int restart, double rel_reduction, int max_iters, int* iters, int* status, double* rel_residual);

@@ -134,6 +134,10 @@ struct sfv_ctx {
     bool ring_ok = false;
     bool stream_ok = false;
     StreamSet sL{}, sU{};
+    bool pipe_ok = false;
+    PipeSet pL{}, pU{};
+    DevBuf<int> pint[6 * 6];          // per (component, sweep): step_off, step_ptr, need, guard, order, to_lower
+    DevBuf<unsigned char> prec[6];    // per (component, sweep) records
     DevBuf<unsigned char> srec[6];  // streamed-sweep records: L0..L2, U0..U2
     DevBuf<double> dense_w[3];
     DevBuf<int> dense_perm[3];
@@ -432,8 +436,8 @@ int precond_apply_async(sfv_ctx* c, const double* r, double* z) {
                 Us.t[a] = c->U[a].view;
             }
             launch_ilu_apply(Ls, Us, c->pc_ncomp, r, c->ily.p, z, c->tri_grid, c->tri_sleep, c->tri_cluster, c->ipa.p,
-                             c->ipb.p, &c->sL, &c->sU, c->stream);
-            c->launches += c->tri_cluster > 0 ? 2 : 4;
+                             c->ipb.p, &c->sL, &c->sU, c->stream, &c->pL, &c->pU);
+            c->launches += c->tri_cluster == kPipeMode ? 11 : c->tri_cluster > 0 ? 2 : 4;
             return SFV_OK;
         }
         case SFV_PRECOND_LU:
@@ -855,15 +859,76 @@ int precond_create(sfv_ctx* c, int kind) {
     // default: the DSMEM-ring sweep when its window covers every dependency distance plus
     // two levels (so no ring slot is overwritten before its last reader ran); else the
     // L2 cluster sweep
-    c->tri_cluster = c->stream_ok ? kStreamMode : (c->ring_ok ? kDsRingMode : 16);
+    // block-pipelined sweeps (precond_pipe.cu), opt-in with SFV_PIPE=1: bit-identical, but
+    // slower than the streamed level-synchronous sweep at every size measured
+    c->pipe_ok = false;
+    if (const char* pe = std::getenv("SFV_PIPE"); pe && std::atoi(pe) != 0) {
+        bool ok = true;
+        int ring = 0;
+        std::vector<PipeSchedule> ps(2 * lus.size());
+        int min_ring = 4096;
+        if (const char* e = std::getenv("SFV_PIPE_RING")) min_ring = std::atoi(e);
+        for (int cand : {4096, 8192, 16384}) {
+            if (cand < min_ring) continue;
+            ok = true;
+            for (size_t x = 0; x < ps.size() && ok; ++x)
+                ok = build_pipe(lus[x / 2], x % 2 == 1, kPipeCluster, cand, ps[x], nullptr);
+            if (ok) {
+                ring = cand;
+                break;
+            }
+        }
+        if (ok) {
+            for (size_t a = 0; a < lus.size() && ok; ++a) {
+                const PipeSchedule& pl = ps[2 * a];
+                const PipeSchedule& pu = ps[2 * a + 1];
+                std::vector<int> to_lower(pu.n_pos, -1);
+                for (int p = 0; p < pu.n_pos; ++p)
+                    if (pu.order[p] >= 0) to_lower[p] = pl.pos[pu.order[p]];
+                for (int w = 0; w < 2; ++w) {
+                    const PipeSchedule& q = w ? pu : pl;
+                    DevBuf<int>* ib = c->pint + (2 * a + w) * 6;
+                    if (!ib[0].upload(q.step_off) || !ib[1].upload(q.step_ptr) || !ib[2].upload(q.need) ||
+                        !ib[3].upload(q.guard) || !ib[4].upload(q.order) ||
+                        (w && !ib[5].upload(to_lower)) || !c->prec[2 * a + w].alloc(q.rec.size()) ||
+                        cudaMemcpy(c->prec[2 * a + w].p, q.rec.data(), q.rec.size(), cudaMemcpyHostToDevice) !=
+                            cudaSuccess)
+                        return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
+                    max_pos = std::max(max_pos, q.n_pos);
+                }
+            }
+            for (int a = 0; a < 3; ++a) {
+                const int src = c->pc_ncomp == 1 ? 0 : a;
+                for (int w = 0; w < 2; ++w) {
+                    DevBuf<int>* ib = c->pint + (2 * src + w) * 6;
+                    DevPipe d;
+                    d.step_off = ib[0].p;
+                    d.step_ptr = ib[1].p;
+                    d.need = ib[2].p;
+                    d.guard = ib[3].p;
+                    d.order = ib[4].p;
+                    d.to_lower = w ? ib[5].p : nullptr;
+                    d.rec = c->prec[2 * src + w].p;
+                    d.n_pos = ps[2 * src + w].n_pos;
+                    (w ? c->pU : c->pL).t[a] = d;
+                }
+            }
+            c->pL.ring = c->pU.ring = ring;
+            c->pipe_ok = true;
+            if (!c->ipa.alloc(3 * static_cast<size_t>(max_pos)) || !c->ipb.alloc(3 * static_cast<size_t>(max_pos)))
+                return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
+        }
+    }
+    c->tri_cluster = c->pipe_ok ? kPipeMode : c->stream_ok ? kStreamMode : (c->ring_ok ? kDsRingMode : 16);
     if (const char* e = std::getenv("SFV_TRI_CLUSTER")) {
         const int v = std::atoi(e);
-        c->tri_cluster = (v == kDsRingMode && c->ring_ok) || (v == kStreamMode && c->stream_ok)
+        c->tri_cluster = (v == kDsRingMode && c->ring_ok) || (v == kStreamMode && c->stream_ok) ||
+                                 (v == kPipeMode && c->pipe_ok)
                              ? v
                              : std::max(0, std::min(16, v));
     }
     for (int a = 0; a < c->pc_ncomp; ++a)  // the ELL cluster sweep holds rows of up to 32 entries
-        if (c->L[a].view.maxd > 32 || c->U[a].view.maxd > 32) c->tri_cluster = 0;
+        if (c->tri_cluster != kPipeMode && (c->L[a].view.maxd > 32 || c->U[a].view.maxd > 32)) c->tri_cluster = 0;
     c->pc_kind = kind;
     return c->cuda_check("ilu setup");
 }
@@ -1265,6 +1330,11 @@ int sfv_precond_info(const sfv_ctx* c, int info[5]) {
     info[3] = static_cast<int>(c->L[0].nnz);
     info[4] = static_cast<int>(c->U[0].nnz);
     return SFV_OK;
+}
+
+int sfv_precond_sweep(const sfv_ctx* c) {
+    const bool ilu = c->pc_kind == SFV_PRECOND_ILU0 || c->pc_kind == SFV_PRECOND_ILU1 || c->pc_kind == SFV_PRECOND_ILU2;
+    return ilu ? c->tri_cluster : -1;
 }
 
 int sfv_gmres_jv(sfv_ctx* c, const double* u, const double* r_u, const double* b, double* x, int restart,

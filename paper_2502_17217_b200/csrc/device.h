@@ -198,9 +198,32 @@ struct StreamSet {
 int stream_smem_bytes(int ring, int max_rows, int stages);
 cudaError_t launch_tri_stream(const StreamSet& set, bool upper, int ncomp, const double* src, double* dst,
                               cudaStream_t s);
+// ---- precond_pipe.cu: block-pipelined sweep (default when build_pipe accepts the factor)
+constexpr int kPipeMode = 300;
+constexpr int kPipeCluster = 16;
+constexpr int kPipeThreads = 512;  // consumer threads per CTA (+ producer and publisher warps)
+constexpr int kPipeChunk = 3328;   // bytes per 32 records (precond_host.h: kPipeChunkBytes)
+struct DevPipe {
+    const int* step_off = nullptr;  // [blocks + 1]
+    const int* step_ptr = nullptr;  // [total steps + blocks]
+    const int* need = nullptr;      // [total steps]
+    const int* guard = nullptr;     // [total steps]
+    const unsigned char* rec = nullptr;
+    const int* order = nullptr;     // position -> row (-1 padding)
+    const int* to_lower = nullptr;  // upper sweep only: position -> lower-sweep position
+    int n_pos = 0;
+};
+struct PipeSet {
+    DevPipe t[3];  // per component (the same factor three times when shared)
+    int ring = 0;
+};
+int pipe_smem_bytes(int ring);
+cudaError_t launch_tri_pipe(const PipeSet& set, bool upper, const double* src, double* dst, cudaStream_t s);
+
 void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double* r, double* y, double* z, int grid,
                       int sleep_ns, int cluster, double* pa, double* pb, const struct StreamSet* SL,
-                      const struct StreamSet* SU, cudaStream_t s);
+                      const struct StreamSet* SU, cudaStream_t s, const PipeSet* PL = nullptr,
+                      const PipeSet* PU = nullptr);
 // Exact dense apply z = A^{-1} r for the small-system LU path (3 interleaved RHS).
 void launch_dense_apply(const double* inv, int n, const double* r, double* z, cudaStream_t s);
 // Small-system exact preconditioner: W = (L L^T)^{-1} from a band Cholesky of -K, and

@@ -575,7 +575,18 @@ static cudaError_t launch_cluster(const TriSet& set, int ncomp, int csize, const
 
 void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double* r, double* y, double* z, int grid,
                       int sleep_ns, int cluster, double* pa, double* pb, const StreamSet* SL, const StreamSet* SU,
-                      cudaStream_t s) {
+                      cudaStream_t s, const PipeSet* PL, const PipeSet* PU) {
+    if (cluster == kPipeMode) {  // block-pipelined sweeps, one cluster per component
+        for (int c = 0; c < 3; ++c)  // r -> lower-sweep positions
+            gather_pos_kernel<<<592, 256, 0, s>>>(PL->t[c].order, PL->t[c].n_pos, c, 1, r, pa);
+        launch_tri_pipe(*PL, false, pa, pb, s);
+        for (int c = 0; c < 3; ++c)  // y: lower-sweep -> upper-sweep positions
+            permute_pos_kernel<<<592, 256, 0, s>>>(PU->t[c].to_lower, PU->t[c].n_pos, c, 1, pb, pa);
+        launch_tri_pipe(*PU, true, pa, pb, s);
+        for (int c = 0; c < 3; ++c)  // upper-sweep positions -> rows
+            scatter_pos_kernel<<<592, 256, 0, s>>>(PU->t[c].order, PU->t[c].n_pos, c, 1, pb, z);
+        return;
+    }
     if (cluster > 0) {  // level-synchronous position-space sweeps (default)
         const int per = ncomp == 1 ? 3 : 1;
         for (int c = 0; c < ncomp; ++c)  // r -> L positions

@@ -378,6 +378,148 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
     return true;
 }
 
+bool build_pipe(const ScalarCsr& lu, bool upper, int blocks, int ring, PipeSchedule& out, std::string* why) {
+    auto fail = [&](const char* m) {
+        if (why) *why = m;
+        return false;
+    };
+    const int n = lu.n;
+    if (n < blocks || ring <= 0 || (ring & (ring - 1))) return fail("pipe: bad size");
+    // dependencies of row i in the reference's order (linalg.cpp:302-316)
+    auto entries = [&](int i, std::vector<int>& c, std::vector<double>& v, double& d) {
+        c.clear();
+        v.clear();
+        d = 1.0;
+        if (!upper) {
+            for (int p = lu.rp[i]; p < lu.rp[i + 1] && lu.col[p] < i; ++p) {
+                c.push_back(lu.col[p]);
+                v.push_back(lu.val[p]);
+            }
+        } else {
+            d = 0.0;
+            for (int p = lu.rp[i + 1] - 1; p >= lu.rp[i] && lu.col[p] >= i; --p) {
+                if (lu.col[p] == i)
+                    d = lu.val[p];
+                else {
+                    c.push_back(lu.col[p]);
+                    v.push_back(lu.val[p]);
+                }
+            }
+        }
+    };
+    // sweep order k -> row, global dependency levels, blocks
+    auto row_at = [&](int k) { return upper ? n - 1 - k : k; };
+    std::vector<int> level(n, 0), blk(n);
+    std::vector<int> c;
+    std::vector<double> v;
+    double d;
+    for (int k = 0; k < n; ++k) {
+        const int i = row_at(k);
+        blk[i] = static_cast<int>(static_cast<long long>(k) * blocks / n);
+        entries(i, c, v, d);
+        if (c.size() > 8) return fail("pipe: more than 8 dependencies in a row");
+        int l = 0;
+        for (int j : c) {
+            l = std::max(l, level[j] + 1);
+            if (blk[j] != blk[i] && blk[j] != blk[i] - 1) return fail("pipe: dependency beyond the previous block");
+        }
+        level[i] = l;
+    }
+    // per block: rows by (level, sweep order); steps = distinct levels
+    out = PipeSchedule{};
+    out.blocks = blocks;
+    out.ring = ring;
+    std::vector<std::vector<int>> rows_of(blocks);
+    for (int k = 0; k < n; ++k) rows_of[blk[row_at(k)]].push_back(row_at(k));
+    std::vector<int> step(n, 0);
+    out.step_off.assign(blocks + 1, 0);
+    std::vector<int> block_start(blocks + 1, 0);
+    int npos = 0;
+    for (int b = 0; b < blocks; ++b) {
+        std::vector<int>& rs = rows_of[b];
+        std::stable_sort(rs.begin(), rs.end(), [&](int x, int y) { return level[x] < level[y]; });
+        block_start[b] = npos;
+        int nsteps = 0;
+        for (size_t x = 0; x < rs.size();) {
+            size_t y = x;
+            while (y < rs.size() && level[rs[y]] == level[rs[x]]) ++y;
+            out.step_ptr.push_back(npos);
+            for (size_t q = x; q < y; ++q) step[rs[q]] = nsteps;
+            const int cnt = static_cast<int>(y - x);
+            out.max_rows = std::max(out.max_rows, cnt);
+            for (size_t q = x; q < y; ++q) out.order.push_back(rs[q]);
+            const int padded = (cnt + 31) / 32 * 32;
+            for (int q = cnt; q < padded; ++q) out.order.push_back(-1);
+            npos += padded;
+            ++nsteps;
+            x = y;
+        }
+        out.step_ptr.push_back(npos);
+        out.step_off[b + 1] = out.step_off[b] + nsteps;
+    }
+    block_start[blocks] = npos;
+    out.n_pos = npos;
+    if (out.max_rows > ring / 2) return fail("pipe: ring smaller than two steps");
+    out.pos.assign(n, -1);
+    std::vector<int> pblk(npos), pstep(npos);
+    for (int b = 0; b < blocks; ++b)
+        for (int s = 0; s < out.step_off[b + 1] - out.step_off[b]; ++s) {
+            const int i0 = out.step_off[b] + b + s;
+            for (int p = out.step_ptr[i0]; p < out.step_ptr[i0 + 1]; ++p) {
+                pblk[p] = b;
+                pstep[p] = s;
+            }
+        }
+    for (int p = 0; p < npos; ++p)
+        if (out.order[p] >= 0) out.pos[out.order[p]] = p;
+    const int total = out.step_off[blocks];
+    out.need.assign(total, 0);
+    out.guard.assign(total, 0);
+    // last reader step (in block b + 1) of every position read remotely
+    std::vector<int> last_remote(npos, -1);
+    out.rec.assign(static_cast<size_t>(npos / 32) * kPipeChunkBytes, 0);
+    for (int p = 0; p < npos; ++p) {
+        unsigned char* ch = out.rec.data() + static_cast<size_t>(p / 32) * kPipeChunkBytes;
+        const int ln = p % 32;
+        const uint32_t none = 0xffffffffu;
+        for (int q = 0; q < 8; ++q) std::memcpy(ch + 2304 + (q * 32 + ln) * 4, &none, 4);
+        const int i = out.order[p];
+        if (i < 0) continue;
+        entries(i, c, v, d);
+        std::memcpy(ch + 2048 + ln * 8, &d, 8);
+        const int b = pblk[p], s = pstep[p];
+        for (size_t q = 0; q < c.size(); ++q) {
+            const int pj = out.pos[c[q]];
+            const int bj = pblk[pj];
+            const uint32_t slot = static_cast<uint32_t>(pj - block_start[bj]) & static_cast<uint32_t>(ring - 1);
+            // local reuse: the slot is rewritten by position pj + ring of block bj
+            const int over = pj + ring;
+            if (over < block_start[bj + 1] && bj == b && pstep[over] <= s) return fail("pipe: ring too small (local)");
+            const uint32_t dep = bj == b ? slot : (slot | 0x80000000u);
+            std::memcpy(ch + 2304 + (q * 32 + ln) * 4, &dep, 4);
+            std::memcpy(ch + (q * 32 + ln) * 8, &v[q], 8);
+            if (bj != b) {
+                out.need[out.step_off[b] + s] = std::max(out.need[out.step_off[b] + s], pstep[pj] + 1);
+                last_remote[pj] = std::max(last_remote[pj], s);
+            }
+        }
+    }
+    for (int b = 0; b + 1 < blocks; ++b)
+        for (int p = block_start[b]; p < block_start[b + 1]; ++p) {
+            if (last_remote[p] < 0) continue;
+            const int over = p + ring;  // rewritten by this position of block b
+            if (over >= block_start[b + 1]) continue;
+            int& g = out.guard[out.step_off[b] + pstep[over]];
+            g = std::max(g, last_remote[p] + 1);
+        }
+    for (int b = 0; b < blocks; ++b)
+        for (int s = out.step_off[b] + 1; s < out.step_off[b + 1]; ++s) {
+            out.need[s] = std::max(out.need[s], out.need[s - 1]);
+            out.guard[s] = std::max(out.guard[s], out.guard[s - 1]);
+        }
+    return true;
+}
+
 void pack_stream_chunks(const std::vector<StreamRecord>& recs, std::vector<unsigned char>& out) {
     const size_t nchunk = (recs.size() + 31) / 32;
     out.assign(nchunk * kChunkBytes, 0);

@@ -62,6 +62,30 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
 constexpr int kChunkBytes = 3072;
 void pack_stream_chunks(const std::vector<StreamRecord>& recs, std::vector<unsigned char>& out);
 
+// Block-pipelined sweep (precond_pipe.cu): the rows, in sweep order, are cut into `blocks`
+// contiguous blocks, one CTA each; CTA b walks only the dependency levels present in its
+// block ("steps"), in order.  Every dependency of a block-b row lies in block b or b-1
+// (checked; false otherwise).  Positions are block-major, step-major, each (block, step)
+// padded to 32.  Values live in a ring of `ring` doubles in each CTA's shared memory; a
+// dependency is its ring slot, bit 31 set when it is in block b-1's ring (read over DSMEM).
+//   need[b][s]:  steps block b-1 must have completed before block b runs step s (data);
+//   guard[b][s]: steps block b+1 must have completed before block b runs step s (its ring
+//                slots about to be rewritten have been read by all their remote readers).
+// Both are non-decreasing in s.  Records are chunk-SoA per 32 positions: val[8][32],
+// diag[32], dep[8][32] (u32); 3328 bytes.
+constexpr int kPipeChunkBytes = 3328;
+struct PipeSchedule {
+    int blocks = 0, ring = 0, n_pos = 0, max_rows = 0;
+    std::vector<int> order;       // position -> row (-1 padding)
+    std::vector<int> pos;         // row -> position
+    std::vector<int> step_off;    // [blocks + 1] first step of block b in the flat step tables
+    std::vector<int> step_ptr;    // [total steps + blocks] positions: step s of block b spans
+                                  // [step_ptr[step_off[b] + b + s], step_ptr[step_off[b] + b + s + 1])
+    std::vector<int> need, guard;  // [total steps]
+    std::vector<unsigned char> rec;  // n_pos / 32 chunks of kPipeChunkBytes
+};
+bool build_pipe(const ScalarCsr& lu, bool upper, int blocks, int ring, PipeSchedule& out, std::string* why);
+
 // Banded Cholesky of -A after reverse Cuthill-McKee (A symmetric negative definite);
 // returns "" or "lu: factorisation failed".  Band row i holds L(i, i-bw .. i).
 struct BandChol {

@@ -86,6 +86,7 @@ def lib():
         "sfv_precond_create": (C.c_int, [_vp, C.c_int]),
         "sfv_precond_apply": (C.c_int, [_vp, _vp, _vp]),
         "sfv_precond_info": (C.c_int, [_vp, _ip]),
+        "sfv_precond_sweep": (C.c_int, [_vp]),
         "sfv_gmres_jv": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_double, C.c_int, _ip, _ip, _dp]),
         "sfv_jfnk_solve": (C.c_int, [_vp, _vp, C.POINTER(SolverCfg), C.POINTER(SolveReport)]),
         "sfv_run_steps": (C.c_int, [_vp, _vp, C.POINTER(SolverCfg), C.c_int, C.POINTER(SolveReport), C.c_int,
@@ -281,7 +282,7 @@ class Preconditioner:
         i = np.zeros(5, dtype=np.int32)
         self.ev.L.sfv_precond_info(self.ev.h, iptr(i))
         return {"kind": int(i[0]), "levels_fwd": int(i[1]), "levels_bwd": int(i[2]), "nnz_L": int(i[3]),
-                "nnz_U": int(i[4])}
+                "nnz_U": int(i[4]), "sweep": int(self.ev.L.sfv_precond_sweep(self.ev.h))}
 
 
 def make_preconditioner(ev: ResidualEvaluator, kind: str = "auto") -> Preconditioner:

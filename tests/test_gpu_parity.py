@@ -141,6 +141,26 @@ def test_ilu_apply_bitwise(kind, level):
     assert info["levels_fwd"] > 1 and info["nnz_L"] > 0
 
 
+@pytest.mark.parametrize("mode", ["stream", "pipe", "cluster"])
+def test_ilu_sweep_modes_bitwise(mode, monkeypatch):
+    """Every device sweep (streamed default, block-pipelined opt-in, ELL cluster fallback)
+    reproduces IlukPrecond::solve bit for bit on a mesh with several blocks per level."""
+    sv = _sv()
+    if mode == "pipe":
+        monkeypatch.setenv("SFV_PIPE", "1")
+    if mode == "cluster":
+        monkeypatch.setenv("SFV_TRI_CLUSTER", "16")
+    case = cases.config("c2", n=24)
+    mesh = case.mesh()
+    ev, orc = _pair(mesh, case.physics)
+    pc = sv.make_preconditioner(ev, "ilu1")
+    assert pc.info()["sweep"] == {"stream": 200, "pipe": 300, "cluster": 16}[mode]
+    orc.precond_create(3)  # PRECOND_ILU1
+    for seed in (5, 6):
+        r = cases.uniform(seed, 3 * mesh.n_cells)
+        assert np.array_equal(pc.solve(r).cpu().numpy(), orc.precond_apply(r))
+
+
 def test_ilu_apply_transient_bitwise():
     sv = _sv()
     case = cases.config("c4", n=8)
