@@ -114,7 +114,7 @@ struct sfv_ctx {
     DevBuf<int> slot_face, slot_other, bnd_si;  // bnd_si: slot index of each boundary face
     DevBuf<double> slot_ls, gam, del, dmag, w, volume;
     // jv_pair.cu scratch + face records
-    DevBuf<double> pw, pG, face9, bres;
+    DevBuf<double> pwg, face9, bres;  // pwg = [w (3 nc) | G (9 nc)]
     PairScratch ps;
     // scratch
     DevBuf<double> grad, red, scal;  // scal: [0]=eps [1]=u_norm [2..] misc
@@ -224,8 +224,7 @@ std::string build_layout(sfv_ctx* c) {
     }
     if (!c->slot_face.upload(sf) || !c->slot_other.upload(so) || !c->slot_ls.upload(sl) || !c->gam.upload(gm) ||
         !c->del.upload(de) || !c->dmag.upload(dmg) || !c->w.upload(ww) || !c->bnd_si.upload(bsi) ||
-        !c->bres.alloc(6 * bsi.size()) || !c->face9.upload(f9) || !c->pw.alloc(3 * static_cast<size_t>(nc)) ||
-        !c->pG.alloc(9 * static_cast<size_t>(nc)))
+        !c->bres.alloc(6 * bsi.size()) || !c->face9.upload(f9) || !c->pwg.alloc(12 * static_cast<size_t>(nc)))
         return "cuda: out of device memory for the mesh layout";
     if (c->ph.transient && !c->volume.upload(g.volume)) return "cuda: out of device memory";
     DevMesh& d = c->dm;
@@ -241,8 +240,31 @@ std::string build_layout(sfv_ctx* c) {
     d.dmag = c->dmag.p;
     d.w = c->w.p;
     d.volume = c->volume.p;
-    c->ps.w = c->pw.p;
-    c->ps.G = c->pG.p;
+    c->ps.w = c->pwg.p;
+    c->ps.G = c->pwg.p + 3 * static_cast<size_t>(nc);
+    // [w | G] in a persisting L2 window: opt-in experiment (SFV_L2_PERSIST=1, or 2 for G
+    // alone); measured 2-4% slower at 1M cells, the passes are latency-bound
+    c->ps.win_bytes = 0;
+    const char* pe = std::getenv("SFV_L2_PERSIST");
+    if (pe && std::atoi(pe) != 0) {
+        int dev = 0, max_persist = 0, max_window = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        const size_t want = 12 * sizeof(double) * static_cast<size_t>(nc);
+        if (max_persist > 0 && max_window > 0) {
+            size_t limit = 0;
+            cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize);
+            const size_t set_aside = std::min<size_t>(static_cast<size_t>(max_persist), want);
+            if (limit < set_aside) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set_aside);
+            cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize);
+            const bool g_only = pe && std::atoi(pe) == 2;  // experiment: G alone
+            c->ps.win_base = g_only ? static_cast<void*>(c->ps.G) : static_cast<void*>(c->pwg.p);
+            c->ps.win_bytes = std::min<size_t>(g_only ? want * 3 / 4 : want, static_cast<size_t>(max_window));
+            c->ps.win_hit = static_cast<float>(std::min(1.0, static_cast<double>(limit) / c->ps.win_bytes));
+            cudaGetLastError();
+        }
+    }
     c->ps.face9 = c->face9.p;
     c->ps.bnd_si = c->bnd_si.p;
     c->ps.bres = c->bres.p;

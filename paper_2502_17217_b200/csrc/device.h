@@ -82,6 +82,11 @@ struct PairScratch {
     const int* bnd_si = nullptr;  // [nf-nint] slot index (s*nc + cell) of boundary face nint+fb
     double* bres = nullptr;       // [6*(nf-nint)] boundary-face flux + stabilisation
     cudaEvent_t* marks = nullptr;  // optional: recorded after the perturb, gradient, boundary passes
+    // L2 persisting window over [w | G] (contiguous): both are gathered by the next pass,
+    // and G is rewritten in place by the next J.v, so resident lines never reach HBM
+    void* win_base = nullptr;
+    size_t win_bytes = 0;
+    float win_hit = 0.f;
 };
 void launch_residual_pair(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist,
                           const double* u, const double* v, const double* jv_eps, const double* r_u, double* out,

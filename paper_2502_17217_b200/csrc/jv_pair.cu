@@ -64,13 +64,28 @@ __device__ __forceinline__ dm3 ldG(const double* __restrict__ G, int nc, int c) 
     return r;
 }
 
+// programmatic dependent launch (see launch_win)
+__device__ __forceinline__ void wait_predecessor() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifndef SFV_PDL_EARLY
+#define SFV_PDL_EARLY 0  // 1: trigger dependents at kernel entry, 0: after the CTA's stores (measured better)
+#endif
+__device__ __forceinline__ void release_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void release_early() {
+    if (SFV_PDL_EARLY) release_dependents();
+}
+__device__ __forceinline__ void release_late() {
+    if (!SFV_PDL_EARLY) release_dependents();
+}
+
 // ---------------------------------------------------------------- perturbed state
 // w = u + eps v, formed once per J.v exactly as the reference forms u_pert
 // (nonlinear.cpp:116-118); plain residual: w = u.
 template <bool PERT>
 __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __restrict__ u, const double* __restrict__ v,
                                                       const double* __restrict__ eps_p, double* __restrict__ w) {
+    release_early();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    wait_predecessor();  // eps, and the previous pass that read w
     if (c >= nc) return;
     double x = u[3 * c], y = u[3 * c + 1], z = u[3 * c + 2];
     if (PERT) {
@@ -83,6 +98,7 @@ __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __re
     st_keep(&w[c], x, pol);
     st_keep(&w[nc + c], y, pol);
     st_keep(&w[2 * nc + c], z, pol);
+    release_late();
 }
 
 // ---------------------------------------------------------------- gradients
@@ -93,9 +109,11 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
                                                         double* __restrict__ G) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= m.nc) return;
+    release_early();
     int o[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) o[s] = s < m.slots ? __ldcs(&m.slot_other[s * m.nc + c]) : -1;
+    wait_predecessor();  // w
     const d3 wc = ldw(w, m.nc, c);
     d3 wn[S];
 #pragma unroll
@@ -124,6 +142,7 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
     const unsigned long long pol = evict_last_policy();
 #pragma unroll
     for (int q = 0; q < 9; ++q) st_keep(&G[q * m.nc + c], g[q], pol);
+    release_late();
 }
 
 // ---------------------------------------------------------------- boundary faces
@@ -135,8 +154,10 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
                                                        const double* __restrict__ eps_p,
                                                        const double* __restrict__ G, double* __restrict__ bres,
                                                        ErrWords* __restrict__ err) {
+    release_early();
     const int nbf = m.nf - m.nint;
     const int fb = blockIdx.x * blockDim.x + threadIdx.x;
+    wait_predecessor();  // G
     if (fb >= nbf) return;
     if (eps_p && *eps_p == 0.0) return;
     const int si = bnd_si[fb];
@@ -183,6 +204,7 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
     bres[3 * static_cast<size_t>(nbf) + fb] = st.x;
     bres[4 * static_cast<size_t>(nbf) + fb] = st.y;
     bres[5 * static_cast<size_t>(nbf) + fb] = st.z;
+    release_late();
 }
 
 // ---------------------------------------------------------------- fluxes + epilogue
@@ -223,6 +245,7 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
     int fr_next, o_next;
     double ru_next;
     fetch(blockIdx.x, fr_next, o_next, ru_next);
+    wait_predecessor();  // bres (and through it G, w)
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         double(*res)[6][kCells] = res_buf[it & 1];
@@ -342,6 +365,37 @@ int flux_grid(int ntiles) {
     return ntiles < g ? ntiles : g;
 }
 
+// Every pass is launched as a programmatic dependent of the previous one (PDL): its CTAs
+// are scheduled while the predecessor drains, load what does not depend on it (slot
+// tables, least-squares vectors, r_u), and block in griddepcontrol.wait — which returns
+// once the predecessor grid has completed and its writes are visible — before the first
+// read of the predecessor's output.  Optionally the [w | G] L2 persisting window.
+
+template <typename... KArgs, typename... Args>
+void launch_win(void (*kern)(KArgs...), int grid, int block, cudaStream_t st, const PairScratch& ps, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+    if (ps.win_bytes) {
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = ps.win_base;
+        attr[na].val.accessPolicyWindow.num_bytes = ps.win_bytes;
+        attr[na].val.accessPolicyWindow.hitRatio = ps.win_hit;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <bool PERT, int S>
 void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist, const double* u,
               const double* v, const double* eps, const double* r_u, double* out, const PairScratch& ps,
@@ -349,23 +403,23 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     double* w = ps.w;
     double* G = ps.G;
     const int cb = (m.nc + 255) / 256;
-    perturb_kernel<PERT><<<cb, 256, 0, st>>>(m.nc, u, v, eps, w);
+    launch_win(perturb_kernel<PERT>, cb, 256, st, ps, m.nc, u, v, eps, w);
     if (ps.marks) cudaEventRecord(ps.marks[0], st);
-    grad_cell_kernel<S><<<cb, 256, 0, st>>>(m, pt, w, G);
+    launch_win(grad_cell_kernel<S>, cb, 256, st, ps, m, pt, w, G);
     if (ps.marks) cudaEventRecord(ps.marks[1], st);
     const int nbf = m.nf - m.nint;
     if (nbf > 0)
-        boundary_kernel<<<(nbf + 127) / 128, 128, 0, st>>>(m, ph, pt, ps.bnd_si, w, PERT ? eps : nullptr, G, ps.bres,
-                                                           err);
+        launch_win(boundary_kernel, (nbf + 127) / 128, 128, st, ps, m, ph, pt, ps.bnd_si, w,
+                   PERT ? eps : static_cast<const double*>(nullptr), G, ps.bres, err);
     if (ps.marks) cudaEventRecord(ps.marks[2], st);
     const int ntiles = (m.nc + kCells - 1) / kCells;
     const double* f9 = ps.face9;
     if (ph.law != SFV_LAW_HOOKE || ph.tl)
-        flux_pair_kernel<PERT, S, true>
-            <<<flux_grid<PERT, S, true>(ntiles), kCells * S, 0, st>>>(m, ph, pt, hist, w, eps, G, f9, ps.bres, r_u, out, err);
+        launch_win(flux_pair_kernel<PERT, S, true>, flux_grid<PERT, S, true>(ntiles), kCells * S, st, ps, m, ph, pt,
+                   hist, w, eps, G, f9, ps.bres, r_u, out, err);
     else
-        flux_pair_kernel<PERT, S, false>
-            <<<flux_grid<PERT, S, false>(ntiles), kCells * S, 0, st>>>(m, ph, pt, hist, w, eps, G, f9, ps.bres, r_u, out, err);
+        launch_win(flux_pair_kernel<PERT, S, false>, flux_grid<PERT, S, false>(ntiles), kCells * S, st, ps, m, ph,
+                   pt, hist, w, eps, G, f9, ps.bres, r_u, out, err);
 }
 
 }  // namespace
