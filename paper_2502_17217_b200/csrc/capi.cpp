@@ -1282,24 +1282,27 @@ int sfv_jv_stage_times(sfv_ctx* c, const double* u, const double* r_u, const dou
                        double* ms) {
     if (c->jv_path != 0 || reps <= 0 || !ms) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "jv_stage_times: default path only");
     if (c->singular_cell >= 0) return gradient_failure(c);
-    cudaEvent_t ev[6];
+    // all reps queued back to back (as in a throughput loop), one host sync at the end
+    std::vector<cudaEvent_t> ev(6 * static_cast<size_t>(reps));
     for (auto& e : ev) cudaEventCreate(&e);
-    double acc[5] = {0, 0, 0, 0, 0};
     for (int r = 0; r < reps; ++r) {
-        cudaEventRecord(ev[0], c->stream);
+        cudaEvent_t* e = ev.data() + 6 * r;
+        cudaEventRecord(e[0], c->stream);
         launch_jv_eps(u, v, c->n, c->red.p, c->counter.p, c->scal.p, c->scal.p + 1, false, c->stream);
-        cudaEventRecord(ev[1], c->stream);
-        c->ps.marks = ev + 2;
+        cudaEventRecord(e[1], c->stream);
+        c->ps.marks = e + 2;
         launch_residual_pair(c->dm, c->ph, c->pt, c->hist, u, v, c->scal.p, r_u, out, c->ps, c->err.p, c->stream);
         c->ps.marks = nullptr;
-        cudaEventRecord(ev[5], c->stream);
-        if (cudaEventSynchronize(ev[5]) != cudaSuccess) break;
+        cudaEventRecord(e[5], c->stream);
+    }
+    const cudaError_t se = cudaEventSynchronize(ev.back());
+    double acc[5] = {0, 0, 0, 0, 0};
+    for (int r = 0; r < reps && se == cudaSuccess; ++r)
         for (int k = 0; k < 5; ++k) {
             float t = 0.f;
-            cudaEventElapsedTime(&t, ev[k], ev[k + 1]);
+            cudaEventElapsedTime(&t, ev[6 * r + k], ev[6 * r + k + 1]);
             acc[k] += t;
         }
-    }
     for (auto& e : ev) cudaEventDestroy(e);
     for (int k = 0; k < 5; ++k) ms[k] = acc[k] / reps;
     c->launches += static_cast<long long>(reps) * (c->dm.nf > c->dm.nint ? 5 : 4);

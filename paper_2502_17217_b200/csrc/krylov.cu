@@ -50,7 +50,20 @@ __global__ void __launch_bounds__(kT) dot_kernel(const double* __restrict__ a, c
                                                  double* __restrict__ out, double* partial, unsigned* counter) {
     __shared__ double sh[kT];
     double acc = 0.0;
-    for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += gridDim.x * kT) acc += a[i] * b[i];
+    const int st = gridDim.x * kT;
+    int i = blockIdx.x * kT + threadIdx.x;
+    // the plain grid-stride order, 8 iterations' loads issued together (same sums)
+    for (; i + 7 * st < n; i += 8 * st) {
+        double x[8], y[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            x[k] = a[i + k * st];
+            y[k] = b[i + k * st];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += x[k] * y[k];
+    }
+    for (; i < n; i += st) acc += a[i] * b[i];
     const double part = block_sum(acc, sh);
     if (publish_partial(part, partial, counter)) finish_sum(partial, counter, out, sh);
 }
@@ -62,8 +75,25 @@ __global__ void __launch_bounds__(kT) axpy_dot_kernel(double* __restrict__ w, co
     __shared__ double sh[kT];
     const double hi = *h;
     double acc = 0.0;
-    for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += gridDim.x * kT) {
-        const double wn = w[i] + (-hi) * vi[i];  // axpy(-h_i, v_i, w): w += (-h_i) v_i
+    const int st = gridDim.x * kT;
+    int i = blockIdx.x * kT + threadIdx.x;
+    for (; i + 3 * st < n; i += 4 * st) {  // 4 iterations' loads together, same order
+        double x[4], y[4], z[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            x[k] = w[i + k * st];
+            y[k] = vi[i + k * st];
+            z[k] = vnext ? vnext[i + k * st] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double wn = x[k] + (-hi) * y[k];  // axpy(-h_i, v_i, w): w += (-h_i) v_i
+            w[i + k * st] = wn;
+            acc += vnext ? wn * z[k] : wn * wn;
+        }
+    }
+    for (; i < n; i += st) {
+        const double wn = w[i] + (-hi) * vi[i];
         w[i] = wn;
         acc += vnext ? wn * vnext[i] : wn * wn;
     }

@@ -15,7 +15,9 @@
 //
 // This translation unit is compiled with -fmad=false: the reference build has no FMA
 // (baseline x86-64), and contraction would change the rounding of every term.
+#include <algorithm>
 #include <cfloat>
+#include <cstdint>
 #include <climits>
 
 #include "device.h"
@@ -360,37 +362,102 @@ __global__ void __launch_bounds__(128) flux_kernel(DevMesh m, Physics ph, PatchT
     }
 }
 
-// |u|^2 and |v|^2 with a fixed-order two-level reduction, then eps (nonlinear.cpp:109-115)
-constexpr int kRedThreads = 256;
+// |u|^2 and |v|^2 with a fixed-order two-level reduction, then eps (nonlinear.cpp:109-115).
+// 16-byte loads, 8 of them in flight per thread, warp-shuffle block sums; the last block
+// to finish (one atomic per block) sums the block partials in block order.
+constexpr int kRedThreads = 512;
 
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    return x;
+}
+// fixed-order block sum of two values (lane 0 of warp 0 holds the result)
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh[2 * w] = a;
+        sh[2 * w + 1] = b;
+    }
+    __syncthreads();
+    if (w == 0) {
+        a = l < kRedThreads / 32 ? sh[2 * l] : 0.0;
+        b = l < kRedThreads / 32 ? sh[2 * l + 1] : 0.0;
+        a = warp_sum(a);
+        b = warp_sum(b);
+    }
+}
+
+// VEC: both vectors 16-byte aligned (a GMRES basis vector V + j n is not when n is odd)
+template <bool VEC>
 __global__ void __launch_bounds__(kRedThreads) jv_eps_kernel(const double* __restrict__ u, const double* __restrict__ v,
                                                             int n, double* __restrict__ partial,
                                                             unsigned* __restrict__ counter, double* __restrict__ eps_out,
                                                             double* __restrict__ u_norm, bool cached) {
-    __shared__ double su[kRedThreads], sv[kRedThreads];
+    __shared__ double sh[2 * kRedThreads / 32];
     __shared__ bool last;
     double au = 0.0, av = 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const double b = v[i];
-        av += b * b;
+    const int st = gridDim.x * blockDim.x;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (!VEC) {
+        for (; i + 7 * st < n; i += 8 * st) {  // 8 iterations' loads together
+            double x[8], y[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                y[k] = v[i + k * st];
+                x[k] = cached ? 0.0 : u[i + k * st];
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                av += y[k] * y[k];
+                if (!cached) au += x[k] * x[k];
+            }
+        }
+        for (; i < n; i += st) {
+            av += v[i] * v[i];
+            if (!cached) au += u[i] * u[i];
+        }
+    }
+    const int n2 = VEC ? n / 2 : 0;  // double2 elements
+    const double2* u2 = reinterpret_cast<const double2*>(u);
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+    for (; i + 3 * st < n2; i += 4 * st) {
+        double2 x[4], y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            y[k] = v2[i + k * st];
+            x[k] = cached ? make_double2(0.0, 0.0) : u2[i + k * st];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            av += y[k].x * y[k].x;
+            av += y[k].y * y[k].y;
+            if (!cached) {
+                au += x[k].x * x[k].x;
+                au += x[k].y * x[k].y;
+            }
+        }
+    }
+    for (; i < n2; i += st) {
+        const double2 y = v2[i];
+        av += y.x * y.x;
+        av += y.y * y.y;
         if (!cached) {
-            const double a = u[i];
-            au += a * a;
+            const double2 x = u2[i];
+            au += x.x * x.x;
+            au += x.y * x.y;
         }
     }
-    su[threadIdx.x] = au;
-    sv[threadIdx.x] = av;
-    __syncthreads();
-    for (int s = kRedThreads / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) {
-            su[threadIdx.x] += su[threadIdx.x + s];
-            sv[threadIdx.x] += sv[threadIdx.x + s];
-        }
-        __syncthreads();
+    if (VEC && blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {  // odd tail
+        av += v[n - 1] * v[n - 1];
+        if (!cached) au += u[n - 1] * u[n - 1];
     }
+    block_sum2(au, av, sh);
     if (threadIdx.x == 0) {
-        partial[2 * blockIdx.x] = su[0];
-        partial[2 * blockIdx.x + 1] = sv[0];
+        partial[2 * blockIdx.x] = au;
+        partial[2 * blockIdx.x + 1] = av;
         __threadfence();
         last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
@@ -402,19 +469,11 @@ __global__ void __launch_bounds__(kRedThreads) jv_eps_kernel(const double* __res
         tu += __ldcg(&partial[2 * b]);
         tv += __ldcg(&partial[2 * b + 1]);
     }
-    su[threadIdx.x] = tu;
-    sv[threadIdx.x] = tv;
     __syncthreads();
-    for (int s = kRedThreads / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) {
-            su[threadIdx.x] += su[threadIdx.x + s];
-            sv[threadIdx.x] += sv[threadIdx.x + s];
-        }
-        __syncthreads();
-    }
+    block_sum2(tu, tv, sh);
     if (threadIdx.x == 0) {
-        const double vn = sqrt(sv[0]);
-        const double un = cached ? *u_norm : sqrt(su[0]);
+        const double vn = sqrt(tv);
+        const double un = cached ? *u_norm : sqrt(tu);
         if (!cached) *u_norm = un;
         *eps_out = vn == 0.0 ? 0.0 : sqrt(DBL_EPSILON) * sqrt(1.0 + un) / vn;
         *counter = 0u;
@@ -455,8 +514,20 @@ void launch_gradients(const DevMesh& m, const PatchTable& pt, const double* u, d
 
 void launch_jv_eps(const double* u, const double* v, int n, double* scratch, unsigned* counter, double* eps_out,
                    double* u_norm_inout, bool u_norm_cached, cudaStream_t s) {
-    const int blocks = reduce_blocks(n);
-    jv_eps_kernel<<<blocks, kRedThreads, 0, s>>>(u, v, n, scratch, counter, eps_out, u_norm_inout, u_norm_cached);
+    static const int sms = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return std::max(1, std::min(v, 148 * 2));
+    }();
+    const int blocks = std::max(1, std::min(4 * sms, (n / 2 + kRedThreads - 1) / kRedThreads));
+    const bool vec = ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+    if (vec)
+        jv_eps_kernel<true><<<blocks, kRedThreads, 0, s>>>(u, v, n, scratch, counter, eps_out, u_norm_inout,
+                                                           u_norm_cached);
+    else
+        jv_eps_kernel<false><<<blocks, kRedThreads, 0, s>>>(u, v, n, scratch, counter, eps_out, u_norm_inout,
+                                                            u_norm_cached);
 }
 
 }  // namespace sfv
