@@ -537,6 +537,10 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
     double beta = r0;
     std::vector<std::vector<double>> H;
     std::vector<double> cs, sn, g, y;
+    static const bool no_fused_mgs = [] {
+        const char* e = std::getenv("SFV_FUSED_MGS");
+        return e && std::atoi(e) == 0;
+    }();
     while (total < max_iters) {
         const double cycle_start = beta;
         launch_scale_div_host(r, beta, V, n, c->stream);  // v0 = r / beta
@@ -551,15 +555,24 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
             double* vj = V + static_cast<size_t>(j) * n;
             op(vj, tmp);
             if (int e = precond_apply_async(c, tmp, w)) return e;
-            // modified Gram-Schmidt (linalg.cpp:469-473): h_0 = w.v_0, then
+            // modified Gram-Schmidt (linalg.cpp:469-473).  Fused: one cooperative launch with
+            // w in shared memory, also writing v_{j+1} = w / |w|.  Otherwise h_0 = w.v_0, then
             // w -= h_i v_i fused with h_{i+1} = w.v_{i+1}; the last pass yields w.w
-            launch_dot(w, V, n, c->hdev.p, c->red.p, c->counter.p, c->stream);
-            ++c->launches;
-            for (int i = 0; i <= j; ++i) {
-                const double* vnext = i < j ? V + static_cast<size_t>(i + 1) * n : nullptr;
-                launch_axpy_dot(w, V + static_cast<size_t>(i) * n, c->hdev.p + i, vnext, n, c->hdev.p + i + 1,
-                                c->red.p, c->counter.p, c->stream);
+            bool fused = !no_fused_mgs &&
+                         launch_arnoldi_fused(w, V, n, j, c->hdev.p, c->red.p,
+                                              j + 1 < restart + 1 ? V + static_cast<size_t>(j + 1) * n : nullptr,
+                                              c->stream);
+            if (fused) {
                 ++c->launches;
+            } else {
+                launch_dot(w, V, n, c->hdev.p, c->red.p, c->counter.p, c->stream);
+                ++c->launches;
+                for (int i = 0; i <= j; ++i) {
+                    const double* vnext = i < j ? V + static_cast<size_t>(i + 1) * n : nullptr;
+                    launch_axpy_dot(w, V + static_cast<size_t>(i) * n, c->hdev.p + i, vnext, n, c->hdev.p + i + 1,
+                                    c->red.p, c->counter.p, c->stream);
+                    ++c->launches;
+                }
             }
             if (int e = c->cuda_check("arnoldi")) return e;
             if (int e = fetch(c, j + 2)) return e;
@@ -590,7 +603,7 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
                 break;
             }
             if (std::abs(g[j]) <= target) break;
-            if (j < restart) {
+            if (j < restart && !fused) {  // (the fused step already wrote v_j = w / subdiag)
                 launch_scale_div_host(w, subdiag, V + static_cast<size_t>(j) * n, n, c->stream);
                 ++c->launches;
             }

@@ -139,6 +139,11 @@ void launch_dot(const double* a, const double* b, int n, double* out, double* sc
 // w -= (*h) * vi ; then *out = dot(w, vnext) (vnext == nullptr: *out = dot(w, w))
 void launch_axpy_dot(double* w, const double* vi, const double* h, const double* vnext, int n, double* out,
                      double* scratch, unsigned* counter, cudaStream_t s);
+// Fused Arnoldi step (cooperative, w held in shared memory): h[0..j] = MGS projections of
+// w on V[0..j], h[j+1] = w.w after them, vnext (if not null) = w / sqrt(h[j+1]).  partial:
+// 2 * SMs doubles.  Returns false (nothing launched) when w does not fit on chip.
+bool launch_arnoldi_fused(const double* w, const double* V, int n, int j, double* h, double* partial, double* vnext,
+                          cudaStream_t s);
 void launch_scale_div(const double* in, const double* divisor, double* out, int n, cudaStream_t s);
 void launch_scale_div_host(const double* in, double divisor, double* out, int n, cudaStream_t s);
 void launch_update(double* x, const double* V, const double* y, int j, int n, cudaStream_t s);

@@ -6,7 +6,11 @@
 // Newton/stepping vector updates of nonlinear.cpp.  Every reduction is a fixed-order
 // two-level tree (block partials, then one last block in block order), so results are
 // run-to-run deterministic; the scalar h_i never leaves the device between passes.
+#include <cooperative_groups.h>
+
 #include "device.h"
+
+namespace cg = cooperative_groups;
 
 namespace sfv {
 namespace {
@@ -161,6 +165,91 @@ __global__ void predict_kernel(double* __restrict__ u, const double* __restrict_
         u[i] = (uo[i] + vo[i] * dt) + ao[i] * h;
 }
 
+// ---------------------------------------------------------------- fused Arnoldi step
+// One cooperative launch per Arnoldi step: the SM-resident grid holds w in shared memory
+// (one contiguous chunk per CTA), so the modified Gram-Schmidt chain of linalg.cpp:469-473
+// — h_i = w.v_i ; w -= h_i v_i, i = 0..j — streams each basis vector once and never
+// writes w back; then h_{j+1} = w.w and v_{j+1} = w / sqrt(h_{j+1}) (linalg.cpp:500-501).
+// Each dot is a fixed-order reduction (thread, warp, block in order, then every block
+// sums the block partials in block order), so all CTAs agree on h_i bit for bit.
+constexpr int kAT = 1024;
+
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    return x;
+}
+__device__ __forceinline__ double block_sum_fixed(double v, double* sh) {  // result valid in thread 0
+    v = warp_sum_d(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = l < kAT / 32 ? sh[l] : 0.0;
+        r = warp_sum_d(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kAT, 1) arnoldi_kernel(const double* __restrict__ w_in, const double* __restrict__ V,
+                                                        int n, int j, int chunk, double* __restrict__ h,
+                                                        double* __restrict__ partial, double* __restrict__ vnext) {
+    extern __shared__ double wsh[];  // [chunk]
+    __shared__ double sh[kAT / 32];
+    __shared__ double bcast;
+    cg::grid_group grid = cg::this_grid();
+    const int lo = blockIdx.x * chunk;
+    const int cnt = max(0, min(chunk, n - lo));
+    for (int e = threadIdx.x; e < cnt; e += kAT) wsh[e] = w_in[lo + e];
+    __syncthreads();
+    const int G = gridDim.x;
+    for (int i = 0; i <= j + 1; ++i) {
+        const bool norm = i == j + 1;
+        const double* vi = V + static_cast<size_t>(i) * n + lo;
+        // partial dot: fixed order within the thread (ascending e), 4 loads in flight
+        double acc = 0.0;
+        int e = threadIdx.x;
+        for (; e + 3 * kAT < cnt; e += 4 * kAT) {
+            double x[4], y[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                x[k] = wsh[e + k * kAT];
+                y[k] = norm ? x[k] : vi[e + k * kAT];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc += x[k] * y[k];
+        }
+        for (; e < cnt; e += kAT) {
+            const double x = wsh[e];
+            acc += x * (norm ? x : vi[e]);
+        }
+        const double bs = block_sum_fixed(acc, sh);
+        double* part = partial + (i & 1) * G;  // alternate buffers: no block overwrites one still being read
+        if (threadIdx.x == 0) part[blockIdx.x] = bs;
+        grid.sync();
+        double t = 0.0;
+        for (int b = threadIdx.x; b < G; b += kAT) t += __ldcg(&part[b]);
+        const double hi = block_sum_fixed(t, sh);
+        if (threadIdx.x == 0) {
+            bcast = hi;
+            if (blockIdx.x == 0) h[i] = hi;
+        }
+        __syncthreads();
+        const double hv = bcast;
+        if (norm) {
+            if (vnext) {  // v_{j+1} = w / |w|
+                const double nr = sqrt(hv);
+                for (int q = threadIdx.x; q < cnt; q += kAT) vnext[lo + q] = wsh[q] / nr;
+            }
+            break;
+        }
+        for (int q = threadIdx.x; q < cnt; q += kAT) wsh[q] = wsh[q] + (-hv) * vi[q];  // w += (-h_i) v_i
+        __syncthreads();
+    }
+}
+
 int grid_for(int n) {
     const int b = (n + 255) / 256;
     return b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16;
@@ -181,6 +270,31 @@ void launch_dot(const double* a, const double* b, int n, double* out, double* sc
 void launch_axpy_dot(double* w, const double* vi, const double* h, const double* vnext, int n, double* out,
                      double* scratch, unsigned* counter, cudaStream_t s) {
     axpy_dot_kernel<<<reduce_blocks(n), kT, 0, s>>>(w, vi, h, vnext, n, out, scratch, counter);
+}
+
+int arnoldi_fused_grid(int n, int* chunk_out) {
+    static int sms = 0, max_smem = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncSetAttribute(arnoldi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
+    }
+    const long long chunk = (static_cast<long long>(n) + sms - 1) / sms;
+    if (chunk * 8 > max_smem - 1024) return 0;  // w does not fit in the grid's shared memory
+    *chunk_out = static_cast<int>(chunk);
+    return sms;
+}
+
+bool launch_arnoldi_fused(const double* w, const double* V, int n, int j, double* h, double* partial, double* vnext,
+                          cudaStream_t s) {
+    int chunk = 0;
+    const int grid = arnoldi_fused_grid(n, &chunk);
+    if (!grid) return false;
+    void* args[] = {&w, &V, &n, &j, &chunk, &h, &partial, &vnext};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_kernel), dim3(grid), dim3(kAT), args,
+                                       static_cast<size_t>(chunk) * 8, s) == cudaSuccess;
 }
 
 void launch_scale_div(const double* in, const double* divisor, double* out, int n, cudaStream_t s) {
