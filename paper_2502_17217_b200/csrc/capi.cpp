@@ -15,6 +15,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "device.h"
@@ -63,10 +64,12 @@ struct TriDev {
     DevTri view;
     int n_levels = 0;
     size_t nnz = 0;
-    bool upload(const TriSchedule& t, int n_rows) {
-        bool ok = order.upload(t.order) && rp.upload(t.rp) && col.upload(t.col) && val.upload(t.val) &&
-                  diag.upload(t.diag) && level_ptr.upload(t.level_ptr) && ell_col.upload(t.ell_col) &&
-                  ell_val.upload(t.ell_val) && ell_pcol.upload(t.ell_pcol);
+    // full = false: only the position map and level pointers (all the streamed sweep reads)
+    bool upload(const TriSchedule& t, int n_rows, bool full) {
+        bool ok = order.upload(t.order) && level_ptr.upload(t.level_ptr);
+        if (full)
+            ok = ok && rp.upload(t.rp) && col.upload(t.col) && val.upload(t.val) && diag.upload(t.diag) &&
+                 ell_col.upload(t.ell_col) && ell_val.upload(t.ell_val) && ell_pcol.upload(t.ell_pcol);
         view.ell_pcol = ell_pcol.p;
         view.level_ptr = level_ptr.p;
         view.maxd = t.maxd;
@@ -757,7 +760,20 @@ int jfnk(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep
     return SFV_OK;
 }
 
+// SFV_TIMING=1: host setup phases on stderr
+struct PhaseTimer {
+    bool on = std::getenv("SFV_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[sfv] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
 int precond_create(sfv_ctx* c, int kind) {
+    PhaseTimer pt;
     c->pc_kind = SFV_PRECOND_NONE;
     if (kind == SFV_PRECOND_AUTO) kind = 3 * c->nc <= 30000 ? SFV_PRECOND_LU : SFV_PRECOND_ILU1;  // nonlinear.cpp:355-356
     if (kind == SFV_PRECOND_NONE) return SFV_OK;
@@ -765,6 +781,7 @@ int precond_create(sfv_ctx* c, int kind) {
     const std::string msg = cell_jacobian(c->mesh, c->geom, c->ph.kbar, c->ph.transient != 0, c->ph.rho, c->ph.dt, comps);
     if (!msg.empty()) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, msg);
     c->pc_ncomp = static_cast<int>(comps.size());
+    pt.mark("cell_jacobian");
     if (kind == SFV_PRECOND_LU) {
         for (size_t a = 0; a < comps.size(); ++a) {
             BandChol bc;
@@ -807,73 +824,98 @@ int precond_create(sfv_ctx* c, int kind) {
             if (!m3.empty()) return c->fail(SFV_ERR_ILU_BREAKDOWN, -1, m3);
         }
     }
+    pt.mark("iluk_factor");
     int max_pos = 0;
     bool ring_ok_all = true, stream_ok_all = true;
-    std::vector<TriSchedule> scheds;  // L0, U0, L1, U1, ...
+    std::vector<TriSchedule> scheds(2 * lus.size());  // L0, U0, L1, U1, ...
+    {
+        std::vector<std::thread> th;  // the sweeps' schedules are independent
+        for (size_t x = 0; x < scheds.size(); ++x)
+            th.emplace_back([&, x] {
+                if (x % 2) schedule_upper(lus[x / 2], scheds[x]);
+                else schedule_lower(lus[x / 2], scheds[x]);
+            });
+        for (auto& t : th) t.join();
+    }
+    std::vector<std::vector<int>> u2ls(lus.size());
     for (size_t a = 0; a < lus.size(); ++a) {
-        TriSchedule tl, tu;
-        schedule_lower(lus[a], tl);
-        schedule_upper(lus[a], tu);
-        std::vector<int> u2l(tu.n_pos, -1);  // backward-sweep position -> forward-sweep position
+        const TriSchedule& tl = scheds[2 * a];
+        const TriSchedule& tu = scheds[2 * a + 1];
+        u2ls[a].assign(tu.n_pos, -1);  // backward-sweep position -> forward-sweep position
         for (int p = 0; p < tu.n_pos; ++p)
-            if (tu.order[p] >= 0) u2l[p] = tl.pos[tu.order[p]];
-        if (!c->L[a].upload(tl, c->nc) || !c->U[a].upload(tu, c->nc) || !c->U[a].u2l.upload(u2l))
+            if (tu.order[p] >= 0) u2ls[a][p] = tl.pos[tu.order[p]];
+        max_pos = std::max(max_pos, std::max(tl.n_pos, tu.n_pos));
+    }
+    pt.mark("schedules");
+    // streamed sweep (precond_stream.cu): rows per CTA-slice, the smallest safe value ring,
+    // and as many cp.async stages as the remaining shared memory holds
+    std::vector<std::vector<unsigned char>> packed(scheds.size());
+    int s_ring = 0, s_rows = 32, s_stages = 0;
+    {
+        for (const TriSchedule& ts : scheds)
+            for (int l = 0; l < ts.n_levels; ++l) {
+                const int nch = (ts.level_ptr[l + 1] - ts.level_ptr[l]) / 32;
+                s_rows = std::max(s_rows, (nch + kStreamCluster - 1) / kStreamCluster * 32);
+            }
+        if (s_rows <= kStreamMaxRows)
+            for (int cand : {1024, 2048, 3072, 4096}) {
+                std::vector<char> ok(scheds.size(), 0);
+                std::vector<std::thread> th;
+                for (size_t x = 0; x < scheds.size(); ++x)
+                    th.emplace_back([&, x] {
+                        std::vector<StreamRecord> recs;
+                        ok[x] = build_stream_records(scheds[x], kStreamCluster, cand, s_rows, recs);
+                        if (ok[x]) pack_stream_chunks(recs, packed[x]);
+                    });
+                for (auto& t : th) t.join();
+                if (std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; })) {
+                    s_ring = cand;
+                    break;
+                }
+            }
+        const int smem_cap = 232448;
+        s_stages = s_ring ? std::min(8, (smem_cap - stream_smem_bytes(s_ring, s_rows, 0)) / (s_rows * 120)) : 0;
+        stream_ok_all = s_ring > 0 && s_stages >= 3;
+    }
+    pt.mark("stream records");
+    // device copies: the streamed sweep needs only the position maps and level pointers;
+    // the CSR / ELL copies feed the fallback sweeps (uploaded when they may be selected)
+    const bool full = !stream_ok_all || std::getenv("SFV_TRI_CLUSTER") != nullptr;
+    for (size_t a = 0; a < lus.size(); ++a) {
+        const TriSchedule& tl = scheds[2 * a];
+        const TriSchedule& tu = scheds[2 * a + 1];
+        if (!c->L[a].upload(tl, c->nc, full) || !c->U[a].upload(tu, c->nc, full) || !c->U[a].u2l.upload(u2ls[a]))
             return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
         c->U[a].view.u2l = c->U[a].u2l.p;
-        max_pos = std::max(max_pos, std::max(tl.n_pos, tu.n_pos));
         for (const TriSchedule* ts : {&tl, &tu}) {  // DSMEM ring admissibility
+            if (!full) {
+                ring_ok_all = false;
+                break;
+            }
             int dist = 0, width = 0;
             for (int l = 0; l < ts->n_levels; ++l) width = std::max(width, ts->level_ptr[l + 1] - ts->level_ptr[l]);
             for (size_t q = 0; q < ts->ell_pcol.size(); ++q)
                 if (ts->ell_pcol[q] >= 0) dist = std::max(dist, static_cast<int>(q % ts->n_pos) - ts->ell_pcol[q]);
             if (dist + 2 * width + 64 > ilu_ring_window()) ring_ok_all = false;
         }
-        scheds.push_back(std::move(tl));
-        scheds.push_back(std::move(tu));
     }
-    // streamed sweep (precond_stream.cu): rows per CTA-slice, the smallest safe value ring,
-    // and as many cp.async stages as the remaining shared memory holds
-    {
-        int max_rows = 32;
-        for (const TriSchedule& ts : scheds)
-            for (int l = 0; l < ts.n_levels; ++l) {
-                const int nch = (ts.level_ptr[l + 1] - ts.level_ptr[l]) / 32;
-                max_rows = std::max(max_rows, (nch + kStreamCluster - 1) / kStreamCluster * 32);
-            }
-        std::vector<std::vector<StreamRecord>> recs(scheds.size());
-        int ring = 0;
-        if (max_rows <= kStreamMaxRows)
-            for (int cand : {1024, 2048, 3072, 4096}) {
-                bool ok = true;
-                for (size_t x = 0; x < scheds.size() && ok; ++x)
-                    ok = build_stream_records(scheds[x], kStreamCluster, cand, max_rows, recs[x]);
-                if (ok) {
-                    ring = cand;
-                    break;
-                }
-            }
-        const int smem_cap = 232448;
-        const int stages = ring ? std::min(8, (smem_cap - stream_smem_bytes(ring, max_rows, 0)) / (max_rows * 120)) : 0;
-        stream_ok_all = ring > 0 && stages >= 3;
-        if (stream_ok_all) {
-            for (size_t x = 0; x < scheds.size(); ++x) {
-                DevBuf<unsigned char>& b = c->srec[(x % 2) * 3 + x / 2];
-                std::vector<unsigned char> packed;
-                pack_stream_chunks(recs[x], packed);
-                if (!b.alloc(packed.size()) ||
-                    cudaMemcpy(b.p, packed.data(), b.bytes(), cudaMemcpyHostToDevice) != cudaSuccess)
-                    return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
-                const int a = static_cast<int>(x / 2);
-                DevStream ds{scheds[x].n_levels, x % 2 ? c->U[a].view.level_ptr : c->L[a].view.level_ptr, b.p};
-                (x % 2 ? c->sU : c->sL).t[a] = ds;
-            }
-            for (StreamSet* ss : {&c->sL, &c->sU}) {
-                ss->ring = ring;
-                ss->max_rows = max_rows;
-                ss->stages = stages;
-            }
+    if (stream_ok_all) {
+        for (size_t x = 0; x < scheds.size(); ++x) {
+            DevBuf<unsigned char>& b = c->srec[(x % 2) * 3 + x / 2];
+            if (!b.alloc(packed[x].size()) ||
+                cudaMemcpy(b.p, packed[x].data(), b.bytes(), cudaMemcpyHostToDevice) != cudaSuccess)
+                return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
+            const int a = static_cast<int>(x / 2);
+            DevStream ds{scheds[x].n_levels, x % 2 ? c->U[a].view.level_ptr : c->L[a].view.level_ptr, b.p};
+            (x % 2 ? c->sU : c->sL).t[a] = ds;
+        }
+        for (StreamSet* ss : {&c->sL, &c->sU}) {
+            ss->ring = s_ring;
+            ss->max_rows = s_rows;
+            ss->stages = s_stages;
         }
     }
+    pt.mark("uploads");
     c->ring_ok = ring_ok_all;
     c->stream_ok = stream_ok_all;
     if (!c->ily.alloc(c->n) || !c->ipa.alloc(3 * static_cast<size_t>(max_pos)) ||
@@ -965,6 +1007,7 @@ int precond_create(sfv_ctx* c, int kind) {
     for (int a = 0; a < c->pc_ncomp; ++a)  // the ELL cluster sweep holds rows of up to 32 entries
         if (c->tri_cluster != kPipeMode && (c->L[a].view.maxd > 32 || c->U[a].view.maxd > 32)) c->tri_cluster = 0;
     c->pc_kind = kind;
+    pt.mark("rest");
     return c->cuda_check("ilu setup");
 }
 
@@ -1039,6 +1082,7 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     if (md->dim != 3) return fail("sfv: only 3-D meshes are on the hot path");
     if (md->n_patches > kMaxPatches) return fail("sfv: too many patches");
     auto c = std::make_unique<sfv_ctx>();
+    PhaseTimer pt;
     HostMesh& m = c->mesh;
     m.points.resize(md->n_points);
     for (int i = 0; i < md->n_points; ++i)
@@ -1052,8 +1096,10 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     m.n_internal = md->n_internal;
     std::string e = m.finalise();
     if (!e.empty()) return fail(e);
+    pt.mark("mesh copy + finalise");
     e = compute_geometry(m, c->geom);
     if (!e.empty()) return fail(e);
+    pt.mark("compute_geometry");
     // ResidualEvaluator ctor checks (discretisation.cpp:64-67)
     if (!(ph->alpha > 0.0)) return fail("discretisation: alpha must be positive");
     if (ph->transient && !(ph->dt > 0.0)) return fail("discretisation: transient mode needs dt > 0");
@@ -1081,6 +1127,7 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     update_patch_values(c.get());
     e = build_layout(c.get());
     if (!e.empty()) return fail(e);
+    pt.mark("device layout + upload");
     if (const char* j = std::getenv("SFV_JV")) {  // kernel-path override (scripts/microbench.py)
         const std::string js(j);
         c->jv_path = js == "fused" ? 1 : js == "twopass" ? 2 : 0;

@@ -3,6 +3,8 @@
 #include "precond_host.h"
 
 #include <algorithm>
+#include <thread>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -78,8 +80,148 @@ std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar,
     return "";
 }
 
+namespace {
+
+// Spin barrier for the level-synchronous host factorisation (one wait per level).
+struct SpinBarrier {
+    explicit SpinBarrier(int n) : count(n) {}
+    void wait() {
+        const int g = gen.load(std::memory_order_acquire);
+        if (arrived.fetch_add(1, std::memory_order_acq_rel) == count - 1) {
+            arrived.store(0, std::memory_order_relaxed);
+            gen.fetch_add(1, std::memory_order_acq_rel);
+        } else {
+            while (gen.load(std::memory_order_acquire) == g) std::this_thread::yield();
+        }
+    }
+    const int count;
+    std::atomic<int> arrived{0}, gen{0};
+};
+
+// ILU(0) / ILU(1) with the reference's arithmetic, multi-threaded.  For level <= 1 the
+// pattern of row i depends only on the original pattern (a fill entry i,j arises from
+// level-0 entries i,k and k,j alone), so rows are built independently; the numeric IKJ
+// phase reads only final rows k < i of row i's lower pattern, so rows run level by level
+// (levels of the final lower pattern) with each row's operations in the sequential order:
+// the factor is bit-identical.  Returns false on a breakdown (the caller reruns the
+// sequential code for the reference's exact message).
+bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nthreads) {
+    const int n = a.n;
+    std::vector<std::vector<int>> rc(n);
+    std::vector<std::vector<int>> rl(n);
+    auto worker_sym = [&](int t) {
+        std::vector<int> mark(n, -1);
+        for (int i = t; i < n; i += nthreads) {
+            std::vector<int>& c = rc[i];
+            std::vector<int>& l = rl[i];
+            c.assign(a.col.begin() + a.rp[i], a.col.begin() + a.rp[i + 1]);
+            if (!std::binary_search(c.begin(), c.end(), i)) c.insert(std::lower_bound(c.begin(), c.end(), i), i);
+            for (int j : c) mark[j] = i;
+            const size_t orig = c.size();
+            if (level >= 1) {
+                for (size_t x = 0; x < orig && c[x] < i; ++x) {
+                    const int k = c[x];
+                    for (int q = a.rp[k]; q < a.rp[k + 1]; ++q) {
+                        const int j = a.col[q];
+                        if (j <= k || mark[j] == i) continue;
+                        mark[j] = i;
+                        c.push_back(j);
+                    }
+                }
+            }
+            l.assign(c.size(), 0);
+            if (c.size() > orig) {  // merge the fill (level 1) into the sorted original pattern
+                std::vector<std::pair<int, int>> e(c.size());
+                for (size_t x = 0; x < c.size(); ++x) e[x] = {c[x], x < orig ? 0 : 1};
+                std::sort(e.begin(), e.end());
+                for (size_t x = 0; x < e.size(); ++x) {
+                    c[x] = e[x].first;
+                    l[x] = e[x].second;
+                }
+            }
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int t = 0; t < nthreads; ++t) th.emplace_back(worker_sym, t);
+        for (auto& t : th) t.join();
+    }
+    out.n = n;
+    out.rp.assign(n + 1, 0);
+    for (int i = 0; i < n; ++i) out.rp[i + 1] = out.rp[i] + static_cast<int>(rc[i].size());
+    out.col.resize(out.rp[n]);
+    out.val.assign(out.rp[n], 0.0);
+    std::vector<int> diag(n, -1);
+    for (int i = 0; i < n; ++i) {
+        std::copy(rc[i].begin(), rc[i].end(), out.col.begin() + out.rp[i]);
+        diag[i] = out.rp[i] + static_cast<int>(std::lower_bound(rc[i].begin(), rc[i].end(), i) - rc[i].begin());
+        std::vector<int>().swap(rc[i]);
+        std::vector<int>().swap(rl[i]);
+    }
+    // levels of the final lower pattern
+    std::vector<int> lev(n, 0);
+    int nlev = 0;
+    for (int i = 0; i < n; ++i) {
+        int l = 0;
+        for (int p = out.rp[i]; p < out.rp[i + 1] && out.col[p] < i; ++p) l = std::max(l, lev[out.col[p]] + 1);
+        lev[i] = l;
+        nlev = std::max(nlev, l + 1);
+    }
+    std::vector<int> lptr(nlev + 1, 0), rows(n);
+    for (int i = 0; i < n; ++i) ++lptr[lev[i] + 1];
+    for (int l = 0; l < nlev; ++l) lptr[l + 1] += lptr[l];
+    {
+        std::vector<int> fill(lptr.begin(), lptr.end() - 1);
+        for (int i = 0; i < n; ++i) rows[fill[lev[i]]++] = i;
+    }
+    std::atomic<bool> broke{false};
+    SpinBarrier bar(nthreads);
+    auto worker_num = [&](int t) {
+        std::vector<int> pos(n, 0);
+        for (int L = 0; L < nlev; ++L) {
+            for (int x = lptr[L] + t; x < lptr[L + 1]; x += nthreads) {
+                const int i = rows[x];
+                // values of the original matrix at the pattern positions (fill = 0)
+                for (int q = out.rp[i]; q < out.rp[i + 1]; ++q) pos[out.col[q]] = q + 1;
+                for (int p = a.rp[i]; p < a.rp[i + 1]; ++p) out.val[pos[a.col[p]] - 1] = a.val[p];
+                // IKJ on the fixed pattern (linalg.cpp:283-299)
+                for (int p = out.rp[i]; p < out.rp[i + 1] && out.col[p] < i; ++p) {
+                    const int k = out.col[p];
+                    const double pivot = out.val[diag[k]];
+                    if (pivot == 0.0 || !std::isfinite(pivot)) {
+                        broke = true;
+                        break;
+                    }
+                    const double lik = (out.val[p] /= pivot);
+                    for (int q = out.rp[k]; q < out.rp[k + 1]; ++q) {
+                        if (out.col[q] <= k) continue;
+                        if (pos[out.col[q]]) out.val[pos[out.col[q]] - 1] -= lik * out.val[q];
+                    }
+                }
+                for (int q = out.rp[i]; q < out.rp[i + 1]; ++q) pos[out.col[q]] = 0;
+                const double d = out.val[diag[i]];
+                if (d == 0.0 || !std::isfinite(d)) broke = true;
+            }
+            bar.wait();
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int t = 0; t < nthreads; ++t) th.emplace_back(worker_num, t);
+        for (auto& t : th) t.join();
+    }
+    return !broke;
+}
+
+}  // namespace
+
 std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& out) {
     const int n = a.n;
+    const int hw = static_cast<int>(std::thread::hardware_concurrency());
+    const int nthreads = std::max(1, std::min(16, hw));
+    if (level <= 1 && n >= 65536 && nthreads > 1 && !std::getenv("SFV_ILU_SERIAL") &&
+        iluk_factor_parallel(a, level, out, nthreads))
+        return "";
     // symbolic phase: level-of-fill row merge in ascending column order (linalg.cpp:252-269)
     out.n = n;
     out.rp.assign(n + 1, 0);

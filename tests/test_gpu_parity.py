@@ -161,6 +161,23 @@ def test_ilu_sweep_modes_bitwise(mode, monkeypatch):
         assert np.array_equal(pc.solve(r).cpu().numpy(), orc.precond_apply(r))
 
 
+def test_ilu_parallel_factorisation_bitwise(monkeypatch):
+    """Above 65536 cells the host factors ILU(1) with threads (level-synchronous numeric
+    phase); the factor must equal the sequential one bit for bit (compared through the
+    device apply) and the reference's (through the oracle)."""
+    sv = _sv()
+    case = cases.config("c2", n=42)  # 74088 cells
+    mesh = case.mesh()
+    ev, orc = _pair(mesh, case.physics)
+    r = cases.uniform(8, 3 * mesh.n_cells)
+    z_par = sv.make_preconditioner(ev, "ilu1").solve(r).cpu().numpy()
+    monkeypatch.setenv("SFV_ILU_SERIAL", "1")
+    z_ser = sv.make_preconditioner(ev, "ilu1").solve(r).cpu().numpy()
+    assert np.array_equal(z_par, z_ser)
+    orc.precond_create(3)
+    assert np.array_equal(z_par, orc.precond_apply(r))
+
+
 def test_ilu_apply_transient_bitwise():
     sv = _sv()
     case = cases.config("c4", n=8)
