@@ -117,7 +117,7 @@ struct sfv_ctx {
     DevBuf<int> slot_face, slot_other, bnd_si;  // bnd_si: slot index of each boundary face
     DevBuf<double> slot_ls, gam, del, dmag, w, volume;
     // jv_pair.cu scratch + face records
-    DevBuf<double> pwg, face9, bres;  // pwg = [w (3 nc) | G (9 nc)]
+    DevBuf<double> pwg, face9, bres, psig;  // pwg = [w (3 nc) | G (9 nc)], psig: cell stress (6 nc)
     PairScratch ps;
     // scratch
     DevBuf<double> grad, red, scal;  // scal: [0]=eps [1]=u_norm [2..] misc
@@ -243,6 +243,9 @@ std::string build_layout(sfv_ctx* c) {
     d.dmag = c->dmag.p;
     d.w = c->w.p;
     d.volume = c->volume.p;
+    if ((c->ph.law != SFV_LAW_HOOKE || c->ph.tl) && !c->psig.alloc(6 * static_cast<size_t>(nc)))
+        return "cuda: out of device memory for the mesh layout";
+    c->ps.sig = c->psig.p;
     c->ps.w = c->pwg.p;
     c->ps.G = c->pwg.p + 3 * static_cast<size_t>(nc);
     // [w | G] in a persisting L2 window: opt-in experiment (SFV_L2_PERSIST=1, or 2 for G
@@ -540,6 +543,34 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
     double beta = r0;
     std::vector<std::vector<double>> H;
     std::vector<double> cs, sn, g, y;
+    // SFV_TIMING=1: per-iteration device time of J.v / preconditioner / Arnoldi, and the
+    // host wall time of the per-iteration fetch, summed over the solve (stderr)
+    struct IterTimer {
+        bool on = std::getenv("SFV_TIMING") != nullptr;
+        cudaEvent_t ev[4];
+        double ms[4] = {0, 0, 0, 0};
+        int iters = 0;
+        IterTimer() {
+            if (on)
+                for (auto& e : ev) cudaEventCreate(&e);
+        }
+        void add(double host_ms) {
+            float t = 0.f;
+            for (int k = 0; k < 3; ++k) {
+                cudaEventElapsedTime(&t, ev[k], ev[k + 1]);
+                ms[k] += t;
+            }
+            ms[3] += host_ms;
+            ++iters;
+        }
+        ~IterTimer() {
+            if (!on) return;
+            if (iters)
+                std::fprintf(stderr, "[sfv] gmres %d iters: jv %.3f  precond %.3f  arnoldi %.3f  fetch(host) %.3f ms/iter\n",
+                             iters, ms[0] / iters, ms[1] / iters, ms[2] / iters, ms[3] / iters);
+            for (auto& e : ev) cudaEventDestroy(e);
+        }
+    } tim;
     static const bool no_fused_mgs = [] {
         const char* e = std::getenv("SFV_FUSED_MGS");
         return e && std::atoi(e) == 0;
@@ -556,8 +587,11 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
         bool happy = false;
         while (j < restart && total < max_iters) {
             double* vj = V + static_cast<size_t>(j) * n;
+            if (tim.on) cudaEventRecord(tim.ev[0], c->stream);
             op(vj, tmp);
+            if (tim.on) cudaEventRecord(tim.ev[1], c->stream);
             if (int e = precond_apply_async(c, tmp, w)) return e;
+            if (tim.on) cudaEventRecord(tim.ev[2], c->stream);
             // modified Gram-Schmidt (linalg.cpp:469-473).  Fused: one cooperative launch with
             // w in shared memory, also writing v_{j+1} = w / |w|.  Otherwise h_0 = w.v_0, then
             // w -= h_i v_i fused with h_{i+1} = w.v_{i+1}; the last pass yields w.w
@@ -578,7 +612,10 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
                 }
             }
             if (int e = c->cuda_check("arnoldi")) return e;
+            if (tim.on) cudaEventRecord(tim.ev[3], c->stream);
+            const auto th0 = std::chrono::steady_clock::now();
             if (int e = fetch(c, j + 2)) return e;
+            if (tim.on) tim.add(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
             if (int e = decode_residual_errors(c, true)) return e;
             std::vector<double> hj(j + 2, 0.0);
             for (int i = 0; i <= j; ++i) hj[i] = c->st->h[i];

@@ -78,6 +78,7 @@ void launch_residual(const DevMesh& m, const Physics& ph, const PatchTable& pt, 
 struct PairScratch {
     double* w = nullptr;            // [3*nc] perturbed state u + eps v, SoA
     double* G = nullptr;            // [9*nc] cell gradients, row-major entries, SoA
+    double* sig = nullptr;          // [6*nc] cell stress (xx, xy, xz, yy, yz, zz), non-Hooke / TL only
     const double* face9 = nullptr;  // [9*nf] Gamma xyz, Delta xyz, |Delta|/|d|, |Gamma|, w; SoA
     const int* bnd_si = nullptr;  // [nf-nint] slot index (s*nc + cell) of boundary face nint+fb
     double* bres = nullptr;       // [6*(nf-nint)] boundary-face flux + stabilisation

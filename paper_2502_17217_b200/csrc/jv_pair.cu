@@ -77,6 +77,18 @@ __device__ __forceinline__ void release_late() {
     if (!SFV_PDL_EARLY) release_dependents();
 }
 
+// symmetric cell stress from its 6 stored entries (grad_cell_kernel<S, true>)
+__device__ __forceinline__ dm3 ld_sig(const double* __restrict__ sig, int nc, int c) {
+    dm3 r;
+    r.a[0][0] = sig[c];
+    r.a[0][1] = r.a[1][0] = sig[nc + c];
+    r.a[0][2] = r.a[2][0] = sig[2 * nc + c];
+    r.a[1][1] = sig[3 * nc + c];
+    r.a[1][2] = r.a[2][1] = sig[4 * nc + c];
+    r.a[2][2] = sig[5 * nc + c];
+    return r;
+}
+
 // ---------------------------------------------------------------- perturbed state
 // w = u + eps v, formed once per J.v exactly as the reference forms u_pert
 // (nonlinear.cpp:116-118); plain residual: w = u.
@@ -104,9 +116,15 @@ __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __re
 // ---------------------------------------------------------------- gradients
 // one thread per cell, slots unrolled so the neighbour loads are all in flight together
 // (discretisation.cpp:10-31: g += ls_f (x) (u_N - u_P), faces in cell order)
-template <int S>
-__global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt, const double* __restrict__ w,
-                                                        double* __restrict__ G) {
+// GEN (non-Hooke law or total Lagrangian): the cell's stress sigma(G_c) is evaluated here
+// once (laws.cpp; the stress loop of discretisation.cpp:116-119, which also reports an
+// inverted cell) and stored as its 6 independent entries, instead of twice per face in
+// the flux pass — same function on the same G, so the same bits (sigma is symmetric
+// bitwise: every entry pair is a product sum of the same factors).
+template <int S, bool GEN>
+__global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt, Physics ph,
+                                                        const double* __restrict__ w, double* __restrict__ G,
+                                                        double* __restrict__ sig, ErrWords* __restrict__ err) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= m.nc) return;
     release_early();
@@ -142,6 +160,20 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
     const unsigned long long pol = evict_last_policy();
 #pragma unroll
     for (int q = 0; q < 9; ++q) st_keep(&G[q * m.nc + c], g[q], pol);
+    if (GEN) {
+        dm3 gm;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) gm.a[q / 3][q % 3] = g[q];
+        bool ok;
+        const dm3 sc = stress(ph, gm, ok);
+        if (!ok) atomicMin(&err->inverted_cell, c);
+        st_keep(&sig[c], sc.a[0][0], pol);
+        st_keep(&sig[m.nc + c], sc.a[0][1], pol);
+        st_keep(&sig[2 * m.nc + c], sc.a[0][2], pol);
+        st_keep(&sig[3 * m.nc + c], sc.a[1][1], pol);
+        st_keep(&sig[4 * m.nc + c], sc.a[1][2], pol);
+        st_keep(&sig[5 * m.nc + c], sc.a[2][2], pol);
+    }
     release_late();
 }
 
@@ -214,7 +246,7 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
 template <bool PERT, int S, bool GEN>
 __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
     flux_pair_kernel(DevMesh m, Physics ph, PatchTable pt, History hist, const double* __restrict__ w,
-                     const double* __restrict__ eps_p, const double* __restrict__ G,
+                     const double* __restrict__ eps_p, const double* __restrict__ G, const double* __restrict__ sig,
                      const double* __restrict__ face9, const double* __restrict__ bres,
                      const double* __restrict__ r_u, double* __restrict__ out, ErrWords* __restrict__ err) {
     // double-buffered per-slot results: one barrier per tile; the sums of tile i (warps
@@ -273,8 +305,7 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
                     hooke_face(gp, gn, wf, ph.mu, ph.lam, gam, del, up, un, cfac, gmag, ph.alpha, ph.kbar, flux, st);
                 } else {
                     const dm3 gp = ldG(G, m.nc, ip), gn = ldG(G, m.nc, in);
-                    bool okp, okn;
-                    const dm3 sp = stress(ph, gp, okp), sn = stress(ph, gn, okn);
+                    const dm3 sp = ld_sig(sig, m.nc, ip), sn = ld_sig(sig, m.nc, in);
                     d3 gm = gam;
                     if (ph.tl) {
                         bool ok;
@@ -316,11 +347,6 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
             if (zero) {
                 out[ik] = 0.0;
             } else {
-                if (GEN && k == 0 && ph.law == SFV_LAW_NEO_HOOKEAN) {  // the stress loop visits every cell
-                    bool ok;
-                    (void)stress(ph, ldG(G, m.nc, c), ok);
-                    if (!ok) atomicMin(&err->inverted_cell, c);
-                }
                 double r = 0.0;
                 if (!ph.stab_only) {
 #pragma unroll
@@ -405,7 +431,9 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     const int cb = (m.nc + 255) / 256;
     launch_win(perturb_kernel<PERT>, cb, 256, st, ps, m.nc, u, v, eps, w);
     if (ps.marks) cudaEventRecord(ps.marks[0], st);
-    launch_win(grad_cell_kernel<S>, cb, 256, st, ps, m, pt, w, G);
+    const bool gen = ph.law != SFV_LAW_HOOKE || ph.tl;
+    if (gen) launch_win(grad_cell_kernel<S, true>, cb, 256, st, ps, m, pt, ph, w, G, ps.sig, err);
+    else launch_win(grad_cell_kernel<S, false>, cb, 256, st, ps, m, pt, ph, w, G, ps.sig, err);
     if (ps.marks) cudaEventRecord(ps.marks[1], st);
     const int nbf = m.nf - m.nint;
     if (nbf > 0)
@@ -414,12 +442,12 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     if (ps.marks) cudaEventRecord(ps.marks[2], st);
     const int ntiles = (m.nc + kCells - 1) / kCells;
     const double* f9 = ps.face9;
-    if (ph.law != SFV_LAW_HOOKE || ph.tl)
+    if (gen)
         launch_win(flux_pair_kernel<PERT, S, true>, flux_grid<PERT, S, true>(ntiles), kCells * S, st, ps, m, ph, pt,
-                   hist, w, eps, G, f9, ps.bres, r_u, out, err);
+                   hist, w, eps, G, static_cast<const double*>(ps.sig), f9, ps.bres, r_u, out, err);
     else
         launch_win(flux_pair_kernel<PERT, S, false>, flux_grid<PERT, S, false>(ntiles), kCells * S, st, ps, m, ph,
-                   pt, hist, w, eps, G, f9, ps.bres, r_u, out, err);
+                   pt, hist, w, eps, G, static_cast<const double*>(ps.sig), f9, ps.bres, r_u, out, err);
 }
 
 }  // namespace
