@@ -75,6 +75,7 @@ def lib():
         "sfv_set_history": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
         "sfv_residual": (C.c_int, [_vp, _vp, _vp, _ip]),
         "sfv_stabilisation": (C.c_int, [_vp, _vp, _vp, _ip]),
+        "sfv_gradients": (C.c_int, [_vp, _vp, _vp, _ip]),
         "sfv_jv": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _ip]),
         "sfv_jv_eps": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _vp, _ip]),
         "sfv_jv_async": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
@@ -228,6 +229,22 @@ class ResidualEvaluator:
         cell = C.c_int(-1)
         self._check(self.L.sfv_residual(self.h, _ptr(ud), _ptr(r), C.byref(cell)), cell.value)
         return r
+
+    def stabilisation(self, u):
+        """ResidualEvaluator::stabilisation (discretisation.cpp:210-214): the Rhie-Chow sum alone."""
+        ud = to_device(u)
+        r = self.empty()
+        cell = C.c_int(-1)
+        self._check(self.L.sfv_stabilisation(self.h, _ptr(ud), _ptr(r), C.byref(cell)), cell.value)
+        return r
+
+    def gradients(self, u):
+        """cell_gradients (discretisation.cpp:10-31) as an (n_cells, 3, 3) array, G[c, i, j] = du_j/dx_i."""
+        ud = to_device(u)
+        G = _torch().empty(9 * self.mesh.n_cells, dtype=_torch().float64, device="cuda")
+        cell = C.c_int(-1)
+        self._check(self.L.sfv_gradients(self.h, _ptr(ud), _ptr(G), C.byref(cell)), cell.value)
+        return G.reshape(9, self.mesh.n_cells).T.reshape(-1, 3, 3)
 
     def geometry(self) -> dict:
         m = self.mesh
