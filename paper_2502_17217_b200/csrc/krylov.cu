@@ -193,6 +193,8 @@ __device__ __forceinline__ double block_sum_fixed(double v, double* sh) {  // re
     return r;
 }
 
+constexpr int kAK = 24;  // elements of a basis vector per thread held in registers (n <= 148 * 1024 * 24)
+
 __global__ void __launch_bounds__(kAT, 1) arnoldi_kernel(const double* __restrict__ w_in, const double* __restrict__ V,
                                                         int n, int j, int chunk, double* __restrict__ h,
                                                         double* __restrict__ partial, double* __restrict__ vnext) {
@@ -208,22 +210,19 @@ __global__ void __launch_bounds__(kAT, 1) arnoldi_kernel(const double* __restric
     for (int i = 0; i <= j + 1; ++i) {
         const bool norm = i == j + 1;
         const double* vi = V + static_cast<size_t>(i) * n + lo;
-        // partial dot: fixed order within the thread (ascending e), 4 loads in flight
-        double acc = 0.0;
-        int e = threadIdx.x;
-        for (; e + 3 * kAT < cnt; e += 4 * kAT) {
-            double x[4], y[4];
+        // this thread's slice of v_i (elements threadIdx.x + k kAT) stays in registers for
+        // the update after the dot: each basis vector is read once
+        double vr[kAK];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                x[k] = wsh[e + k * kAT];
-                y[k] = norm ? x[k] : vi[e + k * kAT];
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc += x[k] * y[k];
+        for (int k = 0; k < kAK; ++k) {
+            const int e = threadIdx.x + k * kAT;
+            vr[k] = e < cnt ? (norm ? wsh[e] : vi[e]) : 0.0;
         }
-        for (; e < cnt; e += kAT) {
-            const double x = wsh[e];
-            acc += x * (norm ? x : vi[e]);
+        double acc = 0.0;  // fixed order within the thread (ascending e)
+#pragma unroll
+        for (int k = 0; k < kAK; ++k) {
+            const int e = threadIdx.x + k * kAT;
+            if (e < cnt) acc += wsh[e] * vr[k];
         }
         const double bs = block_sum_fixed(acc, sh);
         double* part = partial + (i & 1) * G;  // alternate buffers: no block overwrites one still being read
@@ -241,12 +240,20 @@ __global__ void __launch_bounds__(kAT, 1) arnoldi_kernel(const double* __restric
         if (norm) {
             if (vnext) {  // v_{j+1} = w / |w|
                 const double nr = sqrt(hv);
-                for (int q = threadIdx.x; q < cnt; q += kAT) vnext[lo + q] = wsh[q] / nr;
+#pragma unroll
+                for (int k = 0; k < kAK; ++k) {
+                    const int e = threadIdx.x + k * kAT;
+                    if (e < cnt) vnext[lo + e] = vr[k] / nr;
+                }
             }
             break;
         }
-        for (int q = threadIdx.x; q < cnt; q += kAT) wsh[q] = wsh[q] + (-hv) * vi[q];  // w += (-h_i) v_i
-        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kAK; ++k) {  // w += (-h_i) v_i
+            const int e = threadIdx.x + k * kAT;
+            if (e < cnt) wsh[e] = wsh[e] + (-hv) * vr[k];
+        }
+        // (each thread rewrites only its own w elements: no barrier needed before the next dot)
     }
 }
 
@@ -282,7 +289,7 @@ int arnoldi_fused_grid(int n, int* chunk_out) {
         cudaFuncSetAttribute(arnoldi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - 1024);
     }
     const long long chunk = (static_cast<long long>(n) + sms - 1) / sms;
-    if (chunk * 8 > max_smem - 1024) return 0;  // w does not fit in the grid's shared memory
+    if (chunk * 8 > max_smem - 1024 || chunk > static_cast<long long>(kAT) * kAK) return 0;  // w must fit on chip
     *chunk_out = static_cast<int>(chunk);
     return sms;
 }
