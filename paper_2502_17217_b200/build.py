@@ -39,21 +39,25 @@ def _run(cmd: list[str]) -> None:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
-    objs = []
+    objs, jobs = [], []
     for f in CU:
         src = os.path.join(CSRC, f)
         obj = os.path.join(OBJ, f + ".o")
         if _stale(obj, [src] + HEADERS):
-            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
-                  "-Xptxas", "-v" if verbose else "-O3", *INC, "-c", src, "-o", obj])
+            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+                         "-Xptxas", "-v" if verbose else "-O3", *INC, "-c", src, "-o", obj])
         objs.append(obj)
     for f in CPP:
         src = os.path.join(CSRC, f)
         obj = os.path.join(OBJ, f + ".o")
         if _stale(obj, [src] + HEADERS):
-            _run(["g++", "-O2", "-ffp-contract=off", "-fPIC", "-std=c++17", "-Wall", "-Wno-unused-function",
-                  *INC, "-I/usr/local/cuda/include", "-c", src, "-o", obj])
+            jobs.append(["g++", "-O2", "-ffp-contract=off", "-fPIC", "-std=c++17", "-Wall", "-Wno-unused-function",
+                         *INC, "-I/usr/local/cuda/include", "-c", src, "-o", obj])
         objs.append(obj)
+    if jobs:  # translation units compile independently
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            list(ex.map(_run, jobs))
     if _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
     return LIB
