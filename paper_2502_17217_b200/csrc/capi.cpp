@@ -428,6 +428,16 @@ void residual_async(sfv_ctx* c, const double* u, double* r) {
 
 // J.v (async).  u_norm_cached: *scal[1] already holds |u| for this u.
 void jv_async(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out, bool u_norm_cached) {
+    if (c->jv_path == 0) {  // norms as block partials; eps finished inside the perturb pass
+        c->ps.npart = launch_norm_partials(u, v, c->n, c->red.p, u_norm_cached, c->stream);
+        c->ps.partials = c->red.p;
+        c->ps.u_norm = c->scal.p + 1;
+        c->ps.u_norm_cached = u_norm_cached;
+        residual_pass(c, c->ph, u, v, c->scal.p, r_u, out);
+        c->ps.partials = nullptr;
+        c->launches += 1;
+        return;
+    }
     launch_jv_eps(u, v, c->n, c->red.p, c->counter.p, c->scal.p, c->scal.p + 1, u_norm_cached, c->stream);
     residual_pass(c, c->ph, u, v, c->scal.p, r_u, out);
     c->launches += 1;
@@ -1385,10 +1395,14 @@ int sfv_jv_stage_times(sfv_ctx* c, const double* u, const double* r_u, const dou
     for (int r = 0; r < reps; ++r) {
         cudaEvent_t* e = ev.data() + 6 * r;
         cudaEventRecord(e[0], c->stream);
-        launch_jv_eps(u, v, c->n, c->red.p, c->counter.p, c->scal.p, c->scal.p + 1, false, c->stream);
+        c->ps.npart = launch_norm_partials(u, v, c->n, c->red.p, false, c->stream);
         cudaEventRecord(e[1], c->stream);
         c->ps.marks = e + 2;
+        c->ps.partials = c->red.p;
+        c->ps.u_norm = c->scal.p + 1;
+        c->ps.u_norm_cached = false;
         launch_residual_pair(c->dm, c->ph, c->pt, c->hist, u, v, c->scal.p, r_u, out, c->ps, c->err.p, c->stream);
+        c->ps.partials = nullptr;
         c->ps.marks = nullptr;
         cudaEventRecord(e[5], c->stream);
     }

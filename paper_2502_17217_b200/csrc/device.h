@@ -83,6 +83,12 @@ struct PairScratch {
     const int* bnd_si = nullptr;  // [nf-nint] slot index (s*nc + cell) of boundary face nint+fb
     double* bres = nullptr;       // [6*(nf-nint)] boundary-face flux + stabilisation
     cudaEvent_t* marks = nullptr;  // optional: recorded after the perturb, gradient, boundary passes
+    // J.v: eps computed in the perturb pass from launch_norm_partials' block partials
+    // (nullptr: eps given in *jv_eps)
+    const double* partials = nullptr;
+    int npart = 0;
+    double* u_norm = nullptr;
+    bool u_norm_cached = false;
     // L2 persisting window over [w | G] (contiguous): both are gathered by the next pass,
     // and G is rewritten in place by the next J.v, so resident lines never reach HBM
     void* win_base = nullptr;
@@ -94,6 +100,9 @@ void launch_residual_pair(const DevMesh& m, const Physics& ph, const PatchTable&
                           const PairScratch& ps, ErrWords* err, cudaStream_t s);
 // cell_gradients only (discretisation.cpp:10-31), SoA [k*nc + c], k = 3i + j
 void launch_gradients(const DevMesh& m, const PatchTable& pt, const double* u, double* G, cudaStream_t s);
+// Block partials of |u|^2 and |v|^2 (2 per block, fixed order) for the jv_pair.cu path;
+// returns the number of blocks.
+int launch_norm_partials(const double* u, const double* v, int n, double* partial, bool u_norm_cached, cudaStream_t s);
 // eps = sqrt(DBL_EPSILON) sqrt(1 + |u|) / |v| into *eps (nonlinear.cpp:109-115), with
 // |u| taken from *u_norm when u_norm_cached is set.
 void launch_jv_eps(const double* u, const double* v, int n, double* scratch, unsigned* counter,

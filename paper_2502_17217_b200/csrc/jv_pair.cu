@@ -15,6 +15,7 @@
 // Internal faces are evaluated from both sides with the operands in (owner, neighbour)
 // order and the result negated on the neighbour side, which is bit-identical to the
 // reference's r[N] -= flux.  Compiled with -fmad=false (see residual.cu).
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 
@@ -92,24 +93,75 @@ __device__ __forceinline__ dm3 ld_sig(const double* __restrict__ sig, int nc, in
 // ---------------------------------------------------------------- perturbed state
 // w = u + eps v, formed once per J.v exactly as the reference forms u_pert
 // (nonlinear.cpp:116-118); plain residual: w = u.
+// ε from the block partials of ‖u‖², ‖v‖² (launch_norm_partials): every block sums them in
+// the same fixed order, so all blocks hold the same bits; block 0 publishes ε (and ‖u‖).
+// Replaces a last-block finalisation (atomics and a serial tail) on the J·v critical path.
+__device__ __forceinline__ double eps_from_partials(const double* __restrict__ part, int np, double* __restrict__ u_norm,
+                                                    bool cached, double* sh) {
+    double tu = 0.0, tv = 0.0;
+    for (int b = threadIdx.x; b < np; b += blockDim.x) {
+        tu += __ldcg(&part[2 * b]);
+        tv += __ldcg(&part[2 * b + 1]);
+    }
+    // fixed-order block sums (warp shuffles, then warps in order)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        tu += __shfl_down_sync(0xffffffffu, tu, o);
+        tv += __shfl_down_sync(0xffffffffu, tv, o);
+    }
+    const int wi = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (l == 0) {
+        sh[2 * wi] = tu;
+        sh[2 * wi + 1] = tv;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double su = 0.0, sv = 0.0;
+        for (int k = 0; k < nw; ++k) {
+            su += sh[2 * k];
+            sv += sh[2 * k + 1];
+        }
+        const double vn = sqrt(sv);
+        const double un = cached ? *u_norm : sqrt(su);
+        sh[2 * nw] = vn == 0.0 ? 0.0 : sqrt(DBL_EPSILON) * sqrt(1.0 + un) / vn;  // nonlinear.cpp:109-115
+        sh[2 * nw + 1] = un;
+    }
+    __syncthreads();
+    return sh[2 * nw];
+}
+
 template <bool PERT>
 __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __restrict__ u, const double* __restrict__ v,
-                                                      const double* __restrict__ eps_p, double* __restrict__ w) {
+                                                      double* __restrict__ eps_p, double* __restrict__ w,
+                                                      const double* __restrict__ part, int np,
+                                                      double* __restrict__ u_norm, bool cached) {
+    __shared__ double sh[2 * 8 + 2];
     release_early();
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    wait_predecessor();  // eps, and the previous pass that read w
-    if (c >= nc) return;
-    double x = u[3 * c], y = u[3 * c + 1], z = u[3 * c + 2];
+    wait_predecessor();  // ‖u‖² / ‖v‖² partials (or a given ε), and the previous pass that read w
+    double eps = 0.0;
     if (PERT) {
-        const double eps = *eps_p;
-        x = x + eps * v[3 * c];
-        y = y + eps * v[3 * c + 1];
-        z = z + eps * v[3 * c + 2];
+        if (part) {
+            eps = eps_from_partials(part, np, u_norm, cached, sh);
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                *eps_p = eps;
+                if (!cached) *u_norm = sh[2 * (blockDim.x >> 5) + 1];
+            }
+        } else {
+            eps = *eps_p;
+        }
     }
-    const unsigned long long pol = evict_last_policy();
-    st_keep(&w[c], x, pol);
-    st_keep(&w[nc + c], y, pol);
-    st_keep(&w[2 * nc + c], z, pol);
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+        double x = u[3 * c], y = u[3 * c + 1], z = u[3 * c + 2];
+        if (PERT) {
+            x = x + eps * v[3 * c];
+            y = y + eps * v[3 * c + 1];
+            z = z + eps * v[3 * c + 2];
+        }
+        const unsigned long long pol = evict_last_policy();
+        st_keep(&w[c], x, pol);
+        st_keep(&w[nc + c], y, pol);
+        st_keep(&w[2 * nc + c], z, pol);
+    }
     release_late();
 }
 
@@ -255,8 +307,6 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
     __shared__ double res_buf[2][S][6][kCells];
     __shared__ unsigned char kind_buf[2][S][kCells];
     const int lane = threadIdx.x % kCells, s = threadIdx.x / kCells;
-    const double eps = PERT ? *eps_p : 0.0;
-    const bool zero = PERT && eps == 0.0;  // |v| = 0 short-circuit (nonlinear.cpp:110)
     const int ntiles = (m.nc + kCells - 1) / kCells;
     // Persistent grid-stride loop over tiles of kCells cells.  The slot indices of a tile
     // and the epilogue operand r_u of (component s, cell) — threads s < 3 do the per-cell
@@ -277,7 +327,9 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
     int fr_next, o_next;
     double ru_next;
     fetch(blockIdx.x, fr_next, o_next, ru_next);
-    wait_predecessor();  // bres (and through it G, w)
+    wait_predecessor();  // bres (and through it G, w, eps)
+    const double eps = PERT ? *eps_p : 0.0;
+    const bool zero = PERT && eps == 0.0;  // |v| = 0 short-circuit (nonlinear.cpp:110)
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         double(*res)[6][kCells] = res_buf[it & 1];
@@ -429,7 +481,10 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     double* w = ps.w;
     double* G = ps.G;
     const int cb = (m.nc + 255) / 256;
-    launch_win(perturb_kernel<PERT>, cb, 256, st, ps, m.nc, u, v, eps, w);
+    // with the ε reduction folded in, a grid of a few waves keeps the per-block partial sums cheap
+    const int pgrid = ps.partials ? std::min(cb, 148 * 8) : cb;
+    launch_win(perturb_kernel<PERT>, pgrid, 256, st, ps, m.nc, u, v, const_cast<double*>(eps), w, ps.partials,
+               ps.npart, ps.u_norm, ps.u_norm_cached);
     if (ps.marks) cudaEventRecord(ps.marks[0], st);
     const bool gen = ph.law != SFV_LAW_HOOKE || ph.tl;
     if (gen) launch_win(grad_cell_kernel<S, true>, cb, 256, st, ps, m, pt, ph, w, G, ps.sig, err);

@@ -480,6 +480,75 @@ __global__ void __launch_bounds__(kRedThreads) jv_eps_kernel(const double* __res
     }
 }
 
+// |u|^2, |v|^2 block partials only (the jv_pair.cu perturb pass finishes the reduction)
+template <bool VEC>
+__global__ void __launch_bounds__(kRedThreads) norm_partials_kernel(const double* __restrict__ u,
+                                                                   const double* __restrict__ v, int n,
+                                                                   double* __restrict__ partial, bool cached) {
+    __shared__ double sh[2 * kRedThreads / 32];
+    double au = 0.0, av = 0.0;
+    const int st = gridDim.x * blockDim.x;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (!VEC) {
+        for (; i + 7 * st < n; i += 8 * st) {
+            double x[8], y[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                y[k] = v[i + k * st];
+                x[k] = cached ? 0.0 : u[i + k * st];
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                av += y[k] * y[k];
+                if (!cached) au += x[k] * x[k];
+            }
+        }
+        for (; i < n; i += st) {
+            av += v[i] * v[i];
+            if (!cached) au += u[i] * u[i];
+        }
+    }
+    const int n2 = VEC ? n / 2 : 0;
+    const double2* u2 = reinterpret_cast<const double2*>(u);
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+    for (; i + 3 * st < n2; i += 4 * st) {
+        double2 x[4], y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            y[k] = v2[i + k * st];
+            x[k] = cached ? make_double2(0.0, 0.0) : u2[i + k * st];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            av += y[k].x * y[k].x;
+            av += y[k].y * y[k].y;
+            if (!cached) {
+                au += x[k].x * x[k].x;
+                au += x[k].y * x[k].y;
+            }
+        }
+    }
+    for (; i < n2; i += st) {
+        const double2 y = v2[i];
+        av += y.x * y.x;
+        av += y.y * y.y;
+        if (!cached) {
+            const double2 x = u2[i];
+            au += x.x * x.x;
+            au += x.y * x.y;
+        }
+    }
+    if (VEC && blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
+        av += v[n - 1] * v[n - 1];
+        if (!cached) au += u[n - 1] * u[n - 1];
+    }
+    block_sum2(au, av, sh);
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = au;
+        partial[2 * blockIdx.x + 1] = av;
+    }
+}
+
 }  // namespace
 
 void launch_residual(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist, const double* u,
@@ -510,6 +579,21 @@ void launch_residual(const DevMesh& m, const Physics& ph, const PatchTable& pt, 
 
 void launch_gradients(const DevMesh& m, const PatchTable& pt, const double* u, double* G, cudaStream_t s) {
     grad_kernel<false><<<(m.nc + 255) / 256, 256, 0, s>>>(m, pt, u, nullptr, nullptr, G);
+}
+
+int launch_norm_partials(const double* u, const double* v, int n, double* partial, bool u_norm_cached,
+                         cudaStream_t s) {
+    static const int sms = [] {
+        int dev = 0, x = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&x, cudaDevAttrMultiProcessorCount, dev);
+        return std::max(1, std::min(x, 148 * 2));
+    }();
+    const int blocks = std::max(1, std::min(4 * sms, (n / 2 + kRedThreads - 1) / kRedThreads));
+    const bool vec = ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+    if (vec) norm_partials_kernel<true><<<blocks, kRedThreads, 0, s>>>(u, v, n, partial, u_norm_cached);
+    else norm_partials_kernel<false><<<blocks, kRedThreads, 0, s>>>(u, v, n, partial, u_norm_cached);
+    return blocks;
 }
 
 void launch_jv_eps(const double* u, const double* v, int n, double* scratch, unsigned* counter, double* eps_out,
