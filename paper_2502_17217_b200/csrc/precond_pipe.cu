@@ -23,9 +23,13 @@
 // Compiled with -fmad=false: bit-identical results.
 //
 // Status: opt-in (SFV_PIPE=1).  Measured at 1M cells it is slower than the streamed
-// level-synchronous sweep (2.3 vs 0.86 ms per apply): with ILU(1) fill a block trails its
-// predecessor by ~12 steps, so the pipelined critical path is still ~490 dependent steps
-// (vs 595 levels), and a step costs ~1600 cycles here against ~1100 per level there.
+// level-synchronous sweep (2.3 vs 0.86 ms per apply).  With ILU(1) fill a row's level is
+// ~2(i+j+k) on the box, so block b (planes 6.25b..6.25b+6) trails block b-1 by ~12 steps
+// and the pipelined critical path is 15 x 12 + ~412 ~ 590 steps: no shorter than the 595
+// levels it replaces.  It can only win on the cost of a step, and a step (wait for the
+// producer's clearance, rows, named barrier) measured ~2 us here against ~0.7 us per level
+// there; relaxing the publisher's cluster fence and the neighbours' acquire polls
+// (-DSFV_PIPE_PROBE=2|4) moved it by < 10%.
 #include <cooperative_groups.h>
 #include <cstdio>
 
@@ -60,7 +64,11 @@ __device__ __forceinline__ void st_release_cta(int* p, int v) {
 }
 __device__ __forceinline__ int ld_acquire_cluster(uint32_t cluster_addr) {
     int v;
+#if SFV_PIPE_PROBE & 4  // timing probe: relaxed poll
+    asm volatile("ld.relaxed.cluster.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(cluster_addr) : "memory");
+#else
     asm volatile("ld.acquire.cluster.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(cluster_addr) : "memory");
+#endif
     return v;
 }
 __device__ __forceinline__ void mbar_init(uint32_t a, int count) {
@@ -142,9 +150,9 @@ __global__ void __launch_bounds__(kPT + 64, 1) tri_pipe_kernel(PipeSet set, cons
                 en = ptr[s + 2];
                 if (tid < en - an) load_row(t.rec, src, an + tid, comp, nxt);  // in flight during step s
             }
-            if (SFV_PIPE_PROBE) t0 = clock64();
+            if (SFV_PIPE_PROBE & 1) t0 = clock64();
             mbar_wait(clear_base + 8u * (s % kClear), static_cast<uint32_t>((s / kClear) & 1));
-            if (SFV_PIPE_PROBE) {
+            if (SFV_PIPE_PROBE & 1) {
                 const long long t1 = clock64();
                 tw += t1 - t0;
                 t0 = t1;
@@ -179,19 +187,19 @@ __global__ void __launch_bounds__(kPT + 64, 1) tri_pipe_kernel(PipeSet set, cons
                 ring[(p - pbase) & (ring_n - 1)] = z;
                 dst[3 * static_cast<size_t>(p) + comp] = z;
             }
-            if (SFV_PIPE_PROBE) {
+            if (SFV_PIPE_PROBE & 1) {
                 const long long t1 = clock64();
                 tc += t1 - t0;
                 t0 = t1;
             }
             bar_consumers();
-            if (SFV_PIPE_PROBE) tb += clock64() - t0;
+            if (SFV_PIPE_PROBE & 1) tb += clock64() - t0;
             if (tid == 0) st_release_cta(done, s + 1);
             cur = nxt;
             a0 = an;
             e0 = en;
         }
-        if (SFV_PIPE_PROBE && tid == 0)
+        if ((SFV_PIPE_PROBE & 1) && tid == 0)
             printf("pipe U=%d comp %d block %d steps %d: consumer wait %lld compute %lld bar %lld cycles/step\n",
                    UPPER ? 1 : 0, comp, b, nsteps, tw / max(nsteps, 1), tc / max(nsteps, 1), tb / max(nsteps, 1));
     } else if (tid == kPT) {
@@ -212,22 +220,22 @@ __global__ void __launch_bounds__(kPT + 64, 1) tri_pipe_kernel(PipeSet set, cons
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(from), "r"(bytes) : "memory");
             }
             const int nd = t.need[base + s], gd = t.guard[base + s];
-            if (SFV_PIPE_PROBE) t0 = clock64();
+            if (SFV_PIPE_PROBE & 1) t0 = clock64();
             if (b > 0)
                 while (pv < nd) pv = ld_acquire_cluster(prev);
-            if (SFV_PIPE_PROBE) {
+            if (SFV_PIPE_PROBE & 1) {
                 const long long t1 = clock64();
                 tp += t1 - t0;
                 t0 = t1;
             }
             if (b + 1 < kPipeCluster)
                 while (nx < gd) nx = ld_acquire_cluster(next);
-            if (SFV_PIPE_PROBE) tn += clock64() - t0;
+            if (SFV_PIPE_PROBE & 1) tn += clock64() - t0;
             // the mbarrier slot of step s was last used by step s - kClear
             while (ld_acquire_cta(done) < s - kClear + 1) __nanosleep(32);
             mbar_arrive(clear_base + 8u * (s % kClear));
         }
-        if (SFV_PIPE_PROBE)
+        if (SFV_PIPE_PROBE & 1)
             printf("pipe U=%d comp %d block %d: producer wait prev %lld next %lld cycles total, start %lld\n",
                    UPPER ? 1 : 0, comp, b, tp, tn, 0LL);
     } else if (tid == kPT + 32) {
@@ -241,16 +249,20 @@ __global__ void __launch_bounds__(kPT + 64, 1) tri_pipe_kernel(PipeSet set, cons
                 __nanosleep(32);
                 continue;
             }
-            const long long t0 = SFV_PIPE_PROBE ? clock64() : 0;
+            const long long t0 = (SFV_PIPE_PROBE & 1) ? clock64() : 0;
+#if SFV_PIPE_PROBE & 2  // timing probe: CTA-scope fence instead of the cluster-scope release
+            asm volatile("fence.acq_rel.cta;" ::: "memory");
+#else
             asm volatile("fence.acq_rel.cluster;" ::: "memory");
-            if (SFV_PIPE_PROBE) {
+#endif
+            if (SFV_PIPE_PROBE & 1) {
                 tf += clock64() - t0;
                 ++npub;
             }
             asm volatile("st.relaxed.cluster.shared.b32 [%0], %1;" ::"r"(smem_u32(prog)), "r"(d) : "memory");
             pub = d;
         }
-        if (SFV_PIPE_PROBE)
+        if (SFV_PIPE_PROBE & 1)
             printf("pipe U=%d comp %d block %d: publisher %d publishes, fence %lld cycles each\n", UPPER ? 1 : 0,
                    comp, b, npub, tf / max(npub, 1));
     }
