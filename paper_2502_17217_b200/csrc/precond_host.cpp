@@ -493,7 +493,7 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
         }
     }
     out.assign(np, StreamRecord{});
-    long long n_dep = 0, n_local = 0;
+    long long n_dep = 0, n_local = 0, n_near = 0, n_near_remote = 0;
     for (int p = 0; p < np; ++p) {
         StreamRecord& rec = out[p];
         rec.own = static_cast<uint16_t>(ordinal[p] % ring);
@@ -512,11 +512,18 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
             rec.val[k] = t.ell_val[static_cast<size_t>(k) * np + p];
             ++n_dep;
             if (r == owner[p]) ++n_local;
+            if (level_of[q] == level_of[p] - 1) {
+                ++n_near;
+                if (r != owner[p]) ++n_near_remote;
+            }
         }
     }
     if (std::getenv("SFV_STREAM_STATS"))
-        std::fprintf(stderr, "stream records: %d positions, %d levels, %lld deps, %.1f%% in the reading CTA\n", np,
-                     t.n_levels, n_dep, 100.0 * n_local / std::max(1LL, n_dep));
+        std::fprintf(stderr,
+                     "stream records: %d positions, %d levels, %lld deps, %.1f%% in the reading CTA, %.1f%% from the "
+                     "previous level (%.1f%% of all deps: previous level and another CTA)\n",
+                     np, t.n_levels, n_dep, 100.0 * n_local / std::max(1LL, n_dep),
+                     100.0 * n_near / std::max(1LL, n_dep), 100.0 * n_near_remote / std::max(1LL, n_dep));
     return true;
 }
 

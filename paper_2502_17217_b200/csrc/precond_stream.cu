@@ -31,7 +31,8 @@ namespace cg = cooperative_groups;
 
 // timing probes (scripts/build_variant.py): -DSFV_TS_PROBE=m drops 1: the CTA fence,
 // 2: the result stores to HBM, 4: the record prefetch, 8: the dependency loads,
-// 16: the whole row loop (results are then wrong); 32: per-phase clock64 totals of
+// 16: the whole row loop, 64: every dependency read from the reading CTA (results are then
+// wrong); 32: per-phase clock64 totals of
 // CTA 0 / CTA 15 printed at exit (results stay right).
 #ifndef SFV_TS_PROBE
 #define SFV_TS_PROBE 0
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
 #pragma unroll
                     for (int k = 0; k < NRHS; ++k) dv[q][k] = 0.0;
                     if (d != 0xffffu && TSP(8)) {
-                        const uint32_t ad = mapa(ring_base + (d & 0xfffu) * 8u, static_cast<int>(d >> 12));
+                        const uint32_t ad = mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank);
 #pragma unroll
                         for (int k = 0; k < NRHS; ++k)
                             asm volatile("ld.shared::cluster.f64 %0, [%1];"
