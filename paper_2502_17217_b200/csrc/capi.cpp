@@ -156,6 +156,11 @@ struct sfv_ctx {
     int v_cap = 0;
     long long launches = 0;
     SfvError last{0, -1, ""};
+    ~sfv_ctx() {
+        if (ps.ev_w) cudaEventDestroy(ps.ev_w);
+        if (ps.ev_b) cudaEventDestroy(ps.ev_b);
+        if (ps.side) cudaStreamDestroy(ps.side);
+    }
 
     int fail(int code, int cell, const std::string& msg) {
         last = {code, cell, msg};
@@ -247,6 +252,14 @@ std::string build_layout(sfv_ctx* c) {
         return "cuda: out of device memory for the mesh layout";
     c->ps.sig = c->psig.p;
     c->ps.w = c->pwg.p;
+    // boundary pass on a side stream beside the gradient pass: opt-in (SFV_SIDE_STREAM=1);
+    // measured 3% slower at 1M cells (the stream events break the PDL chain)
+    if (const char* se = std::getenv("SFV_SIDE_STREAM"); se && std::atoi(se) != 0 && nf > m.n_internal) {
+        if (cudaStreamCreateWithFlags(&c->ps.side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ps.ev_w, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ps.ev_b, cudaEventDisableTiming) != cudaSuccess)
+            return "cuda: cannot create the side stream";
+    }
     c->ps.G = c->pwg.p + 3 * static_cast<size_t>(nc);
     // [w | G] in a persisting L2 window: opt-in experiment (SFV_L2_PERSIST=1, or 2 for G
     // alone); measured 2-4% slower at 1M cells, the passes are latency-bound

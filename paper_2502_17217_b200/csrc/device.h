@@ -85,6 +85,9 @@ struct PairScratch {
     cudaEvent_t* marks = nullptr;  // optional: recorded after the perturb, gradient, boundary passes
     // J.v: eps computed in the perturb pass from launch_norm_partials' block partials
     // (nullptr: eps given in *jv_eps)
+    // boundary pass on a side stream, beside the gradient pass (null: in line)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_w = nullptr, ev_b = nullptr;
     const double* partials = nullptr;
     int npart = 0;
     double* u_norm = nullptr;

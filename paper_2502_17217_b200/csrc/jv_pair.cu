@@ -229,6 +229,38 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
     release_late();
 }
 
+// One cell's gradient with exactly grad_cell_kernel's operations (slots in face order), for
+// the boundary pass, which then needs w only and can run beside the gradient pass.
+__device__ __forceinline__ dm3 cell_gradient_at(const DevMesh& m, const PatchTable& pt, const double* __restrict__ w,
+                                                int c) {
+    const d3 wc = ldw(w, m.nc, c);
+    double g[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) g[q] = 0.0;
+    for (int s = 0; s < m.slots; ++s) {
+        const int o = m.slot_other[s * m.nc + c];
+        d3 du;
+        if (o >= 0) {
+            du = sub(ldw(w, m.nc, o), wc);
+        } else if (o <= -2 && pt.kind[-o - 2] == SFV_PATCH_SYMMETRY) {
+            const dm3 R = reflection(ldsoa(m.gam, m.nf, m.slot_face[s * m.nc + c] & ~kSign));
+            du = sub(mv(R, wc), wc);
+        } else {
+            continue;
+        }
+        const d3 ls = {m.slot_ls[(3 * s) * m.nc + c], m.slot_ls[(3 * s + 1) * m.nc + c],
+                       m.slot_ls[(3 * s + 2) * m.nc + c]};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) g[3 * i + j] += cmp(ls, i) * cmp(du, j);
+    }
+    dm3 r;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) r.a[q / 3][q % 3] = g[q];
+    return r;
+}
+
 // ---------------------------------------------------------------- boundary faces
 // One thread per boundary face (face f = nint + fb, slot index bnd_si[fb] = s * nc + cell):
 // flux and stabilisation term into bres[q * nbf + fb] (discretisation.cpp:128-154, :186-205).
@@ -241,7 +273,7 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
     release_early();
     const int nbf = m.nf - m.nint;
     const int fb = blockIdx.x * blockDim.x + threadIdx.x;
-    wait_predecessor();  // G
+    wait_predecessor();  // w (and G when it is read)
     if (fb >= nbf) return;
     if (eps_p && *eps_p == 0.0) return;
     const int si = bnd_si[fb];
@@ -255,7 +287,7 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
     if (pk == SFV_PATCH_TRACTION) {  // nominal load |Gamma| T (discretisation.cpp:151-154)
         flux = scl(bc, nrm(gam));
     } else {
-        const dm3 gc = ldG(G, m.nc, c);
+        const dm3 gc = G ? ldG(G, m.nc, c) : cell_gradient_at(m, pt, w, c);
         const d3 uc = ldw(w, m.nc, c);
         const d3 del = ldsoa(m.del, m.nf, f);
         const double dmag = m.dmag[f];
@@ -486,14 +518,24 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     launch_win(perturb_kernel<PERT>, pgrid, 256, st, ps, m.nc, u, v, const_cast<double*>(eps), w, ps.partials,
                ps.npart, ps.u_norm, ps.u_norm_cached);
     if (ps.marks) cudaEventRecord(ps.marks[0], st);
+    const int nbf = m.nf - m.nint;
+    if (nbf > 0 && ps.side) cudaEventRecord(ps.ev_w, st);  // w ready: the boundary pass may start
     const bool gen = ph.law != SFV_LAW_HOOKE || ph.tl;
     if (gen) launch_win(grad_cell_kernel<S, true>, cb, 256, st, ps, m, pt, ph, w, G, ps.sig, err);
     else launch_win(grad_cell_kernel<S, false>, cb, 256, st, ps, m, pt, ph, w, G, ps.sig, err);
     if (ps.marks) cudaEventRecord(ps.marks[1], st);
-    const int nbf = m.nf - m.nint;
-    if (nbf > 0)
-        launch_win(boundary_kernel, (nbf + 127) / 128, 128, st, ps, m, ph, pt, ps.bnd_si, w,
-                   PERT ? eps : static_cast<const double*>(nullptr), G, ps.bres, err);
+    if (nbf > 0) {
+        if (ps.side) {  // beside the gradient pass: the boundary pass computes its own cells' gradients
+            cudaStreamWaitEvent(ps.side, ps.ev_w, 0);
+            boundary_kernel<<<(nbf + 127) / 128, 128, 0, ps.side>>>(
+                m, ph, pt, ps.bnd_si, w, PERT ? eps : static_cast<const double*>(nullptr), nullptr, ps.bres, err);
+            cudaEventRecord(ps.ev_b, ps.side);
+            cudaStreamWaitEvent(st, ps.ev_b, 0);
+        } else {
+            launch_win(boundary_kernel, (nbf + 127) / 128, 128, st, ps, m, ph, pt, ps.bnd_si, w,
+                       PERT ? eps : static_cast<const double*>(nullptr), G, ps.bres, err);
+        }
+    }
     if (ps.marks) cudaEventRecord(ps.marks[2], st);
     const int ntiles = (m.nc + kCells - 1) / kCells;
     const double* f9 = ps.face9;
