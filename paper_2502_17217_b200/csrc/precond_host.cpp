@@ -54,28 +54,38 @@ std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar,
         s.rp = rp;
         s.col = col;
         s.val.assign(col.size(), 0.0);
-        for (int f = 0; f < m.n_faces(); ++f) {
-            // alpha is unity in the matrix (discretisation.cpp:239-240)
-            const double coeff = kbar * g.delta_mag[f] / g.d_mag[f] * g.area_mag[f];
-            const int p = m.owner[f];
-            if (f < m.n_internal) {
-                const int n = m.neighbour[f];
-                s.val[find(p, n)] += coeff * 1.0;
-                s.val[find(n, p)] += coeff * 1.0;
-                s.val[find(p, p)] += -coeff * 1.0;
-                s.val[find(n, n)] += -coeff * 1.0;
-            } else {
-                const int kind = m.patches[m.face_patch[f]].kind;
-                if (kind == SFV_PATCH_DISPLACEMENT) {
-                    s.val[find(p, p)] += -coeff * 1.0;
-                } else if (kind == SFV_PATCH_SYMMETRY) {
-                    const double na = a == 0 ? g.normal[f].x : (a == 1 ? g.normal[f].y : g.normal[f].z);
-                    s.val[find(p, p)] += (na * na) * -coeff;
+        // The reference adds the face contributions face by face in ascending face order
+        // (discretisation.cpp:224-262).  Every entry of row i is touched only by faces of
+        // cell i, and cell_faces[i] is in ascending face order, so assembling row by row over
+        // cell_faces gives every entry the same sequence of additions: rows in parallel.
+        auto rows = [&](int i0, int i1) {
+            for (int i = i0; i < i1; ++i) {
+                for (int q = m.cf_off[i]; q < m.cf_off[i + 1]; ++q) {
+                    const int f = m.cf[q];
+                    // alpha is unity in the matrix (discretisation.cpp:239-240)
+                    const double coeff = kbar * g.delta_mag[f] / g.d_mag[f] * g.area_mag[f];
+                    if (f < m.n_internal) {
+                        const int o = m.owner[f] == i ? m.neighbour[f] : m.owner[f];
+                        s.val[find(i, o)] += coeff * 1.0;
+                        s.val[find(i, i)] += -coeff * 1.0;
+                    } else {
+                        const int kind = m.patches[m.face_patch[f]].kind;
+                        if (kind == SFV_PATCH_DISPLACEMENT) {
+                            s.val[find(i, i)] += -coeff * 1.0;
+                        } else if (kind == SFV_PATCH_SYMMETRY) {
+                            const double na = a == 0 ? g.normal[f].x : (a == 1 ? g.normal[f].y : g.normal[f].z);
+                            s.val[find(i, i)] += (na * na) * -coeff;
+                        }
+                    }
                 }
+                if (transient) s.val[find(i, i)] += (-2.25 * rho * g.volume[i] / (dt * dt)) * 1.0;
             }
-        }
-        if (transient)
-            for (int c = 0; c < nc; ++c) s.val[find(c, c)] += (-2.25 * rho * g.volume[c] / (dt * dt)) * 1.0;
+        };
+        const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+        std::vector<std::thread> th;
+        const int ch = (nc + nth - 1) / nth;
+        for (int k = 0; k < nth; ++k) th.emplace_back(rows, std::min(nc, k * ch), std::min(nc, (k + 1) * ch));
+        for (auto& x : th) x.join();
     }
     return "";
 }
@@ -318,23 +328,41 @@ void pack(const std::vector<int>& level, int n_levels, TriSchedule& t,
     std::vector<int> fill(start.begin(), start.end() - 1);
     for (int i = 0; i < n; ++i) t.order[fill[level[i]]++] = i;
     t.rp.assign(t.n_pos + 1, 0);
-    t.col.clear();
-    t.val.clear();
     t.diag.assign(t.n_pos, 1.0);
-    std::vector<int> c;
-    std::vector<double> v;
-    for (int p = 0; p < t.n_pos; ++p) {
-        const int i = t.order[p];
-        if (i >= 0) {
-            c.clear();
-            v.clear();
-            double d = 1.0;
-            row_entries(i, c, v, d);
-            t.col.insert(t.col.end(), c.begin(), c.end());
-            t.val.insert(t.val.end(), v.begin(), v.end());
-            t.diag[p] = d;
-        }
-        t.rp[p + 1] = static_cast<int>(t.col.size());
+    // rows gathered by position ranges in parallel, then concatenated in position order
+    const int nthr = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    const int pchunk = (t.n_pos + nthr - 1) / nthr;
+    std::vector<std::vector<int>> pc(nthr);
+    std::vector<std::vector<double>> pv(nthr);
+    {
+        std::vector<std::thread> th;
+        for (int k = 0; k < nthr; ++k)
+            th.emplace_back([&, k] {
+                std::vector<int> c;
+                std::vector<double> v;
+                for (int p = std::min(t.n_pos, k * pchunk); p < std::min(t.n_pos, (k + 1) * pchunk); ++p) {
+                    const int i = t.order[p];
+                    if (i >= 0) {
+                        c.clear();
+                        v.clear();
+                        double d = 1.0;
+                        row_entries(i, c, v, d);
+                        pc[k].insert(pc[k].end(), c.begin(), c.end());
+                        pv[k].insert(pv[k].end(), v.begin(), v.end());
+                        t.diag[p] = d;
+                        t.rp[p + 1] = static_cast<int>(c.size());
+                    }
+                }
+            });
+        for (auto& x : th) x.join();
+    }
+    for (int p = 0; p < t.n_pos; ++p) t.rp[p + 1] += t.rp[p];
+    t.col.resize(t.rp[t.n_pos]);
+    t.val.resize(t.rp[t.n_pos]);
+    for (int k = 0; k < nthr; ++k) {
+        const int p0 = std::min(t.n_pos, k * pchunk);
+        std::copy(pc[k].begin(), pc[k].end(), t.col.begin() + t.rp[p0]);
+        std::copy(pv[k].begin(), pv[k].end(), t.val.begin() + t.rp[p0]);
     }
     t.maxd = 0;
     for (int p = 0; p < t.n_pos; ++p) t.maxd = std::max(t.maxd, t.rp[p + 1] - t.rp[p]);
@@ -344,12 +372,21 @@ void pack(const std::vector<int>& level, int n_levels, TriSchedule& t,
     for (int p = 0; p < t.n_pos; ++p)
         if (t.order[p] >= 0) t.pos[t.order[p]] = p;
     t.ell_pcol.assign(static_cast<size_t>(t.maxd) * t.n_pos, -1);
-    for (int p = 0; p < t.n_pos; ++p)
-        for (int q = t.rp[p]; q < t.rp[p + 1]; ++q) {
-            t.ell_col[static_cast<size_t>(q - t.rp[p]) * t.n_pos + p] = t.col[q];
-            t.ell_val[static_cast<size_t>(q - t.rp[p]) * t.n_pos + p] = t.val[q];
-            t.ell_pcol[static_cast<size_t>(q - t.rp[p]) * t.n_pos + p] = t.pos[t.col[q]];
-        }
+    // ELL transposition: entry k of position p at k * n_pos + p; threads own position ranges
+    const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    auto ell = [&](int p0, int p1) {
+        for (int p = p0; p < p1; ++p)
+            for (int q = t.rp[p]; q < t.rp[p + 1]; ++q) {
+                const size_t x = static_cast<size_t>(q - t.rp[p]) * t.n_pos + p;
+                t.ell_col[x] = t.col[q];
+                t.ell_val[x] = t.val[q];
+                t.ell_pcol[x] = t.pos[t.col[q]];
+            }
+    };
+    std::vector<std::thread> th;
+    const int chunk = (t.n_pos + nth - 1) / nth;
+    for (int k = 0; k < nth; ++k) th.emplace_back(ell, std::min(t.n_pos, k * chunk), std::min(t.n_pos, (k + 1) * chunk));
+    for (auto& x : th) x.join();
 }
 
 }  // namespace
@@ -494,7 +531,12 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
     }
     out.assign(np, StreamRecord{});
     long long n_dep = 0, n_local = 0, n_near = 0, n_near_remote = 0;
-    for (int p = 0; p < np; ++p) {
+    // positions are independent: threads own position ranges; statistics only when asked
+    const bool stats = std::getenv("SFV_STREAM_STATS") != nullptr;
+    const int nthr = stats ? 1 : std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    std::atomic<bool> bad{false};
+    auto body = [&](int p0, int p1) {
+    for (int p = p0; p < p1 && !bad; ++p) {
         StreamRecord& rec = out[p];
         rec.own = static_cast<uint16_t>(ordinal[p] % ring);
         rec.diag = t.diag[p];
@@ -507,17 +549,30 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
             // the slot of q is rewritten by its owner's (ordinal + ring)-th position: that
             // position must lie in a strictly later level than the reader p
             const int r = owner[q], o = ordinal[q] + ring;
-            if (o < static_cast<int>(ord_level[r].size()) && ord_level[r][o] <= level_of[p]) return false;
+            if (o < static_cast<int>(ord_level[r].size()) && ord_level[r][o] <= level_of[p]) {
+                bad = true;
+                return;
+            }
             rec.dep[k] = static_cast<uint16_t>((r << 12) | (ordinal[q] % ring));
             rec.val[k] = t.ell_val[static_cast<size_t>(k) * np + p];
-            ++n_dep;
-            if (r == owner[p]) ++n_local;
-            if (level_of[q] == level_of[p] - 1) {
-                ++n_near;
-                if (r != owner[p]) ++n_near_remote;
+            if (stats) {
+                ++n_dep;
+                if (r == owner[p]) ++n_local;
+                if (level_of[q] == level_of[p] - 1) {
+                    ++n_near;
+                    if (r != owner[p]) ++n_near_remote;
+                }
             }
         }
     }
+    };
+    {
+        std::vector<std::thread> th;
+        const int ch = (np + nthr - 1) / nthr;
+        for (int k = 0; k < nthr; ++k) th.emplace_back(body, std::min(np, k * ch), std::min(np, (k + 1) * ch));
+        for (auto& x : th) x.join();
+    }
+    if (bad) return false;
     if (std::getenv("SFV_STREAM_STATS"))
         std::fprintf(stderr,
                      "stream records: %d positions, %d levels, %lld deps, %.1f%% in the reading CTA, %.1f%% from the "
@@ -672,23 +727,35 @@ bool build_pipe(const ScalarCsr& lu, bool upper, int blocks, int ring, PipeSched
 void pack_stream_chunks(const std::vector<StreamRecord>& recs, std::vector<unsigned char>& out) {
     const size_t nchunk = (recs.size() + 31) / 32;
     out.assign(nchunk * kChunkBytes, 0);
-    for (size_t p = 0; p < recs.size(); ++p) {
-        const StreamRecord& r = recs[p];
-        unsigned char* c = out.data() + (p / 32) * kChunkBytes;
-        const size_t l = p % 32;
-        for (int q = 0; q < 8; ++q) {
-            std::memcpy(c + (q * 32 + l) * 8, &r.val[q], 8);
-            std::memcpy(c + 2304 + (q * 32 + l) * 2, &r.dep[q], 2);
+    const int nthr = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    auto body = [&](size_t c0, size_t c1) {
+        for (size_t ch = c0; ch < c1; ++ch) {
+            unsigned char* c = out.data() + ch * kChunkBytes;
+            double* val = reinterpret_cast<double*>(c);
+            double* diag = reinterpret_cast<double*>(c + 2048);
+            uint16_t* dep = reinterpret_cast<uint16_t*>(c + 2304);
+            uint16_t* own = reinterpret_cast<uint16_t*>(c + 2816);
+            for (size_t l = 0; l < 32; ++l) {
+                const size_t p = ch * 32 + l;
+                if (p >= recs.size()) {  // padding rows: no dependencies
+                    for (int q = 0; q < 8; ++q) dep[q * 32 + l] = 0xffff;
+                    continue;
+                }
+                const StreamRecord& r = recs[p];
+                for (int q = 0; q < 8; ++q) {
+                    val[q * 32 + l] = r.val[q];
+                    dep[q * 32 + l] = r.dep[q];
+                }
+                diag[l] = r.diag;
+                own[l] = r.own;
+            }
         }
-        std::memcpy(c + 2048 + l * 8, &r.diag, 8);
-        std::memcpy(c + 2816 + l * 2, &r.own, 2);
-    }
-    for (size_t p = recs.size(); p < nchunk * 32; ++p) {  // padding rows: no dependencies
-        unsigned char* c = out.data() + (p / 32) * kChunkBytes;
-        const size_t l = p % 32;
-        const uint16_t none = 0xffff;
-        for (int q = 0; q < 8; ++q) std::memcpy(c + 2304 + (q * 32 + l) * 2, &none, 2);
-    }
+    };
+    std::vector<std::thread> th;
+    const size_t cpt = (nchunk + nthr - 1) / nthr;
+    for (int k = 0; k < nthr; ++k)
+        th.emplace_back(body, std::min(nchunk, k * cpt), std::min(nchunk, (k + 1) * cpt));
+    for (auto& x : th) x.join();
 }
 
 }  // namespace sfv
