@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <thread>
@@ -196,7 +197,15 @@ std::string build_layout(sfv_ctx* c) {
     std::vector<int> bsi(std::max(1, nf - m.n_internal), 0);
     if (static_cast<size_t>(slots) * nc > static_cast<size_t>(INT_MAX))
         return "mesh: too many cells for 32-bit slot indices";
-    for (int i = 0; i < nc; ++i) {
+    auto par = [](int n, const std::function<void(int, int)>& body) {  // independent ranges
+        const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+        std::vector<std::thread> th;
+        const int ch = (n + nth - 1) / nth;
+        for (int k = 0; k < nth; ++k) th.emplace_back(body, std::min(n, k * ch), std::min(n, (k + 1) * ch));
+        for (auto& t : th) t.join();
+    };
+    par(nc, [&](int i0, int i1) {
+    for (int i = i0; i < i1; ++i) {
         int s = 0;
         for (int q = m.cf_off[i]; q < m.cf_off[i + 1]; ++q, ++s) {
             const int f = m.cf[q];
@@ -210,9 +219,13 @@ std::string build_layout(sfv_ctx* c) {
             if (f >= m.n_internal) bsi[f - m.n_internal] = static_cast<int>(si);
         }
     }
-    std::vector<double> gm(3 * static_cast<size_t>(nf)), de(3 * static_cast<size_t>(nf)), dmg(nf), ww(nf);
+    });
+    const bool legacy = c->jv_path != 0;  // separate face arrays only for the alternative J.v kernels
+    const size_t nfl = legacy ? static_cast<size_t>(nf) : 0;
+    std::vector<double> gm(3 * nfl), de(3 * nfl), dmg(nfl), ww(nfl);
     std::vector<double> f9(9 * static_cast<size_t>(nf));
-    for (int f = 0; f < nf; ++f) {
+    par(nf, [&](int f0, int f1) {
+    for (int f = f0; f < f1; ++f) {
         // per-face constants of rhie_chow(): |Delta| / |d| and |Gamma| (discretisation.cpp:176-208),
         // same IEEE operations as the reference (sqrt of the left-to-right dot, then divide)
         const double* a = &g.area[f].x;
@@ -221,6 +234,7 @@ std::string build_layout(sfv_ctx* c) {
                                std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]) / g.d_mag[f],
                                std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]), g.w[f]};
         for (int q = 0; q < 9; ++q) f9[static_cast<size_t>(q) * nf + f] = rec[q];
+        if (!legacy) continue;
         gm[f] = g.area[f].x;
         gm[nf + f] = g.area[f].y;
         gm[2 * static_cast<size_t>(nf) + f] = g.area[f].z;
@@ -230,8 +244,12 @@ std::string build_layout(sfv_ctx* c) {
         dmg[f] = g.d_mag[f];
         ww[f] = g.w[f];
     }
-    if (!c->slot_face.upload(sf) || !c->slot_other.upload(so) || !c->slot_ls.upload(sl) || !c->gam.upload(gm) ||
-        !c->del.upload(de) || !c->dmag.upload(dmg) || !c->w.upload(ww) || !c->bnd_si.upload(bsi) ||
+    });
+    // the default path reads the face SoA rows of face9 (Gamma, Delta, w share its layout);
+    // the separate arrays (and |d|) are uploaded only for the alternative J.v kernels
+    if (!c->slot_face.upload(sf) || !c->slot_other.upload(so) || !c->slot_ls.upload(sl) ||
+        (legacy && (!c->gam.upload(gm) || !c->del.upload(de) || !c->dmag.upload(dmg) || !c->w.upload(ww))) ||
+        !c->bnd_si.upload(bsi) ||
         !c->bres.alloc(6 * bsi.size()) || !c->face9.upload(f9) || !c->pwg.alloc(12 * static_cast<size_t>(nc)))
         return "cuda: out of device memory for the mesh layout";
     if (c->ph.transient && !c->volume.upload(g.volume)) return "cuda: out of device memory";
@@ -243,10 +261,10 @@ std::string build_layout(sfv_ctx* c) {
     d.slot_face = c->slot_face.p;
     d.slot_other = c->slot_other.p;
     d.slot_ls = c->slot_ls.p;
-    d.gam = c->gam.p;
-    d.del = c->del.p;
-    d.dmag = c->dmag.p;
-    d.w = c->w.p;
+    d.gam = legacy ? c->gam.p : c->face9.p;
+    d.del = legacy ? c->del.p : c->face9.p + 3 * static_cast<size_t>(nf);
+    d.dmag = legacy ? c->dmag.p : nullptr;
+    d.w = legacy ? c->w.p : c->face9.p + 8 * static_cast<size_t>(nf);
     d.volume = c->volume.p;
     if ((c->ph.law != SFV_LAW_HOOKE || c->ph.tl) && !c->psig.alloc(6 * static_cast<size_t>(nc)))
         return "cuda: out of device memory for the mesh layout";
@@ -1185,13 +1203,13 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     c->bc_ramp.assign(ph->bc_ramp, ph->bc_ramp + md->n_patches);
     for (int q = 0; q < md->n_patches; ++q) c->pt.kind[q] = md->patch_kind[q];
     update_patch_values(c.get());
-    e = build_layout(c.get());
-    if (!e.empty()) return fail(e);
-    pt.mark("device layout + upload");
     if (const char* j = std::getenv("SFV_JV")) {  // kernel-path override (scripts/microbench.py)
         const std::string js(j);
         c->jv_path = js == "fused" ? 1 : js == "twopass" ? 2 : 0;
     }
+    e = build_layout(c.get());
+    if (!e.empty()) return fail(e);
+    pt.mark("device layout + upload");
     if (c->jv_path == 1 && build_fused_layout(c.get()).rfind("cuda", 0) == 0)
         return fail("cuda: out of device memory");
     const size_t n = static_cast<size_t>(c->n);

@@ -7,8 +7,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
 
 #include "sfv_case.h"
 
@@ -300,6 +304,41 @@ std::string distort(HostMesh& mesh, double factor, uint64_t seed) {  // mesh.cpp
     return "";
 }
 
+namespace {
+
+// Runs body(i) for i in [0, n) on up to 16 threads; body returns "" or an error.  Returns
+// the error of the smallest failing index, i.e. what the sequential loop would report.
+std::string parallel_for(int n, const std::function<std::string(int)>& body) {
+    const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    if (n < 4096 || nth == 1) {
+        for (int i = 0; i < n; ++i)
+            if (std::string e = body(i); !e.empty()) return e;
+        return "";
+    }
+    std::vector<int> first(nth, n);
+    std::vector<std::string> msg(nth);
+    std::vector<std::thread> th;
+    const int ch = (n + nth - 1) / nth;
+    for (int k = 0; k < nth; ++k)
+        th.emplace_back([&, k] {
+            for (int i = k * ch; i < std::min(n, (k + 1) * ch); ++i)
+                if (std::string e = body(i); !e.empty()) {
+                    first[k] = i;
+                    msg[k] = e;
+                    return;
+                }
+        });
+    for (auto& t : th) t.join();
+    for (int k = 0; k < nth; ++k)  // ranges are ascending: the first thread with an error has the smallest index
+        if (first[k] < n) return msg[k];
+    return "";
+}
+
+}  // namespace
+
+// Every pass is either per face, or per cell accumulating its faces in ascending face
+// order (cell_faces order) — the order in which the reference's face loops reach the cell —
+// so each pass runs in parallel with the sequential arithmetic of every entry.
 std::string compute_geometry(const HostMesh& m, HostGeometry& g) {  // mesh.cpp:347-510
     const int nf = m.n_faces(), nc = m.n_cells;
     g.face_centroid.assign(nf, V3{});
@@ -313,7 +352,7 @@ std::string compute_geometry(const HostMesh& m, HostGeometry& g) {  // mesh.cpp:
     g.delta_mag.assign(nf, 0.0);
     auto kind = [&](int f) { return m.patches[m.face_patch[f]].kind; };
     // pass 1: face centroid + area by fan decomposition about the vertex average
-    for (int f = 0; f < nf; ++f) {
+    std::string e = parallel_for(nf, [&](int f) -> std::string {
         const int b = m.face_off[f], n = m.face_off[f + 1] - b;
         V3 centre{};
         for (int i = 0; i < n; ++i) centre = add(centre, m.points[m.face_pts[b + i]]);
@@ -334,30 +373,28 @@ std::string compute_geometry(const HostMesh& m, HostGeometry& g) {  // mesh.cpp:
         g.area_mag[f] = norm(area);
         if (g.area_mag[f] <= 0.0) return "compute_geometry: zero-area face " + std::to_string(f);
         g.normal[f] = vdiv(area, g.area_mag[f]);
-    }
-    // pass 2: volumes and centroids by pyramids about the vertex average.  Per cell the
-    // contributions arrive in ascending face order, exactly as the reference's face loop.
+        return "";
+    });
+    if (!e.empty()) return e;
+    // pass 2: volumes and centroids by pyramids about the vertex average
     std::vector<V3> apex(nc);
-    {
-        std::vector<int> cnt(nc, 0);
-        for (int f = 0; f < nf; ++f)
-            for (int q = m.face_off[f]; q < m.face_off[f + 1]; ++q)
-                for (int side = 0; side < 2; ++side) {
-                    const int c = side == 0 ? m.owner[f] : m.neighbour[f];
-                    if (c < 0) continue;
-                    apex[c] = add(apex[c], m.points[m.face_pts[q]]);
-                    ++cnt[c];
-                }
-        for (int c = 0; c < nc; ++c) apex[c] = vdiv(apex[c], static_cast<double>(cnt[c]));
-    }
     g.volume.assign(nc, 0.0);
     g.centroid.assign(nc, V3{});
-    for (int f = 0; f < nf; ++f) {
-        const int b = m.face_off[f], n = m.face_off[f + 1] - b;
-        for (int side = 0; side < 2; ++side) {
-            const int c = side == 0 ? m.owner[f] : m.neighbour[f];
-            if (c < 0) continue;
-            const double sign = side == 0 ? 1.0 : -1.0;
+    e = parallel_for(nc, [&](int c) -> std::string {
+        V3 a{};
+        int cnt = 0;
+        for (int q = m.cf_off[c]; q < m.cf_off[c + 1]; ++q) {
+            const int f = m.cf[q];
+            for (int x = m.face_off[f]; x < m.face_off[f + 1]; ++x) {
+                a = add(a, m.points[m.face_pts[x]]);
+                ++cnt;
+            }
+        }
+        apex[c] = vdiv(a, static_cast<double>(cnt));
+        for (int q = m.cf_off[c]; q < m.cf_off[c + 1]; ++q) {
+            const int f = m.cf[q];
+            const int b = m.face_off[f], n = m.face_off[f + 1] - b;
+            const double sign = m.owner[f] == c ? 1.0 : -1.0;
             for (int i = 0; i < n; ++i) {
                 const V3 p0 = m.points[m.face_pts[b + i]];
                 const V3 p1 = m.points[m.face_pts[b + (i + 1) % n]];
@@ -367,13 +404,13 @@ std::string compute_geometry(const HostMesh& m, HostGeometry& g) {  // mesh.cpp:
                 g.centroid[c] = add(g.centroid[c], scale(add(add(add(apex[c], fc), p0), p1), v * 0.25));
             }
         }
-    }
-    for (int c = 0; c < nc; ++c) {
         if (!(g.volume[c] > 0.0)) return "compute_geometry: non-positive volume in cell " + std::to_string(c);
         g.centroid[c] = vdiv(g.centroid[c], g.volume[c]);
-    }
+        return "";
+    });
+    if (!e.empty()) return e;
     // pass 3: d, w, delta
-    for (int f = 0; f < nf; ++f) {
+    e = parallel_for(nf, [&](int f) -> std::string {
         const V3 n = g.normal[f];
         const V3 xp = g.centroid[m.owner[f]];
         if (f < m.n_internal) {
@@ -394,34 +431,31 @@ std::string compute_geometry(const HostMesh& m, HostGeometry& g) {  // mesh.cpp:
         if (!(dn > 0.0)) return "compute_geometry: degenerate centroid geometry at face " + std::to_string(f);
         g.delta[f] = vdiv(g.d[f], dn);
         g.delta_mag[f] = norm(g.delta[f]);
-    }
+        return "";
+    });
+    if (!e.empty()) return e;
     // pass 4: least-squares tensors and per-(cell, face) vectors
     g.g_inv.assign(9 * static_cast<std::size_t>(nc), 0.0);
     g.g_singular.assign(nc, 0);
-    std::vector<M3> gt(nc, mzero());
+    g.ls.assign(m.cf.size(), V3{});
     auto incl = [&](int f) { return f < m.n_internal || kind(f) == SFV_PATCH_SYMMETRY; };
-    for (int f = 0; f < nf; ++f) {
-        if (!incl(f)) continue;
-        const M3 dd = mscale(outer(g.d[f], g.d[f]), g.area_mag[f] / dot(g.d[f], g.d[f]));
-        madd_to(gt[m.owner[f]], mscale(dd, g.w[f]));
-        if (f < m.n_internal) madd_to(gt[m.neighbour[f]], mscale(dd, 1.0 - g.w[f]));
-    }
-    std::vector<M3> ginv(nc, mzero());
-    for (int c = 0; c < nc; ++c) {
-        const M3& G = gt[c];
+    parallel_for(nc, [&](int c) -> std::string {
+        M3 G = mzero();
+        for (int q = m.cf_off[c]; q < m.cf_off[c + 1]; ++q) {
+            const int f = m.cf[q];
+            if (!incl(f)) continue;
+            const M3 dd = mscale(outer(g.d[f], g.d[f]), g.area_mag[f] / dot(g.d[f], g.d[f]));
+            madd_to(G, mscale(dd, m.owner[f] == c ? g.w[f] : 1.0 - g.w[f]));
+        }
         double sc = 0.0;
         for (int i = 0; i < 3; ++i) sc = std::max(sc, std::abs(G.m[i][i]));
         if (sc <= 0.0 || std::abs(mdet(G)) < 1e-10 * sc * sc * sc) {
             g.g_singular[c] = 1;
-            continue;
+            return "";
         }
-        ginv[c] = minverse(G);
+        const M3 ginv = minverse(G);
         for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) g.g_inv[9 * static_cast<std::size_t>(c) + 3 * i + j] = ginv[c].m[i][j];
-    }
-    g.ls.assign(m.cf.size(), V3{});
-    for (int c = 0; c < nc; ++c) {
-        if (g.g_singular[c]) continue;
+            for (int j = 0; j < 3; ++j) g.g_inv[9 * static_cast<std::size_t>(c) + 3 * i + j] = ginv.m[i][j];
         for (int q = m.cf_off[c]; q < m.cf_off[c + 1]; ++q) {
             const int f = m.cf[q];
             if (!incl(f)) continue;
@@ -431,9 +465,10 @@ std::string compute_geometry(const HostMesh& m, HostGeometry& g) {  // mesh.cpp:
                 d = {-d.x, -d.y, -d.z};
                 w = 1.0 - w;
             }
-            g.ls[q] = scale(mv(ginv[c], d), w * g.area_mag[f] / dot(d, d));
+            g.ls[q] = scale(mv(ginv, d), w * g.area_mag[f] / dot(d, d));
         }
-    }
+        return "";
+    });
     return "";
 }
 

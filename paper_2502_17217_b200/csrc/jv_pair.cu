@@ -266,7 +266,8 @@ __device__ __forceinline__ dm3 cell_gradient_at(const DevMesh& m, const PatchTab
 // flux and stabilisation term into bres[q * nbf + fb] (discretisation.cpp:128-154, :186-205).
 // Kept out of the per-slot kernel so its register budget is set by the internal faces.
 __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, PatchTable pt,
-                                                       const int* __restrict__ bnd_si, const double* __restrict__ w,
+                                                       const int* __restrict__ bnd_si, const double* __restrict__ face9,
+                                                       const double* __restrict__ w,
                                                        const double* __restrict__ eps_p,
                                                        const double* __restrict__ G, double* __restrict__ bres,
                                                        ErrWords* __restrict__ err) {
@@ -282,15 +283,21 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
     const int patch = -m.slot_other[si] - 2;
     const int pk = pt.kind[patch];
     const d3 bc = {pt.value[patch][0], pt.value[patch][1], pt.value[patch][2]};
-    const d3 gam = ldsoa(m.gam, m.nf, f);
+    const d3 gam = ldsoa(face9, m.nf, f);
+    // rhie_chow()'s per-face constants |Delta| / |d| and |Gamma|, precomputed on the host with
+    // the reference's operations (see flux_pair_kernel)
+    const double cfac = face9[6 * static_cast<size_t>(m.nf) + f], gmag = face9[7 * static_cast<size_t>(m.nf) + f];
+    auto rc = [&](d3 up, d3 uo, const dm3& gf, d3 delta) {
+        const d3 compact = scl(sub(uo, up), cfac);
+        return scl(sub(compact, dot_left(delta, gf)), ph.alpha * ph.kbar * gmag);
+    };
     d3 flux, st{0.0, 0.0, 0.0};
     if (pk == SFV_PATCH_TRACTION) {  // nominal load |Gamma| T (discretisation.cpp:151-154)
-        flux = scl(bc, nrm(gam));
+        flux = scl(bc, gmag);
     } else {
         const dm3 gc = G ? ldG(G, m.nc, c) : cell_gradient_at(m, pt, w, c);
         const d3 uc = ldw(w, m.nc, c);
-        const d3 del = ldsoa(m.del, m.nf, f);
-        const double dmag = m.dmag[f];
+        const d3 del = ldsoa(face9 + 3 * static_cast<size_t>(m.nf), m.nf, f);
         bool okc;
         const dm3 sc = stress(ph, gc, okc);
         if (pk == SFV_PATCH_DISPLACEMENT) {
@@ -301,7 +308,7 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
                 if (!ok) atomicMin(&err->inverted_face, f);
             }
             flux = dot_left(gm, sc);
-            st = rhie_chow(uc, bc, gc, del, dmag, nrm(gam), ph.alpha, ph.kbar);
+            st = rc(uc, bc, gc, del);
         } else {  // symmetry plane (discretisation.cpp:138-150, :194-203)
             const dm3 R = reflection(gam);
             d3 gm = gam;
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
                 if (!ok) atomicMin(&err->inverted_face, f);
             }
             flux = dot_left(gm, mirror_avg(sc, R));
-            st = rhie_chow(uc, mv(R, uc), mirror_avg(gc, R), del, dmag, nrm(gam), ph.alpha, ph.kbar);
+            st = rc(uc, mv(R, uc), mirror_avg(gc, R), del);
         }
     }
     bres[fb] = flux.x;
@@ -528,11 +535,11 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
         if (ps.side) {  // beside the gradient pass: the boundary pass computes its own cells' gradients
             cudaStreamWaitEvent(ps.side, ps.ev_w, 0);
             boundary_kernel<<<(nbf + 127) / 128, 128, 0, ps.side>>>(
-                m, ph, pt, ps.bnd_si, w, PERT ? eps : static_cast<const double*>(nullptr), nullptr, ps.bres, err);
+                m, ph, pt, ps.bnd_si, ps.face9, w, PERT ? eps : static_cast<const double*>(nullptr), nullptr, ps.bres, err);
             cudaEventRecord(ps.ev_b, ps.side);
             cudaStreamWaitEvent(st, ps.ev_b, 0);
         } else {
-            launch_win(boundary_kernel, (nbf + 127) / 128, 128, st, ps, m, ph, pt, ps.bnd_si, w,
+            launch_win(boundary_kernel, (nbf + 127) / 128, 128, st, ps, m, ph, pt, ps.bnd_si, ps.face9, w,
                        PERT ? eps : static_cast<const double*>(nullptr), G, ps.bres, err);
         }
     }

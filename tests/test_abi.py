@@ -86,7 +86,7 @@ def _host_geometry(mesh):
     return g
 
 
-@pytest.mark.parametrize("name,n", [("c1", 6), ("c2", 8), ("c3", 12), ("c5", 4)])
+@pytest.mark.parametrize("name,n", [("c1", 6), ("c2", 8), ("c2", 24), ("c3", 12), ("c5", 4), ("c5", 12)])
 def test_product_geometry_matches_oracle(name, n):
     from oracle.bind import OracleCase
     case = cases.config(name, n=n)
