@@ -175,22 +175,29 @@ __device__ __forceinline__ void hooke_face(const double* gp, const double* gn, d
     const double tp = lam * ((gp[0] + gp[4]) + gp[8]);
     const double tn = lam * ((gn[0] + gn[4]) + gn[8]);
     const double wn = 1.0 - w;
-    double f[3], dg[3];
+    // interp(sigma_P, sigma_N, w) is symmetric bit for bit ((g_ij + g_ji) == (g_ji + g_ij) in
+    // IEEE arithmetic), so its 6 distinct entries are evaluated once each
+    double a[3][3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        double a[3], g[3];
+    for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
+        for (int j = i; j < 3; ++j) {
             double sp = (gp[3 * i + j] + gp[3 * j + i]) * mu;
             double sn = (gn[3 * i + j] + gn[3 * j + i]) * mu;
             if (i == j) {
                 sp += tp;
                 sn += tn;
             }
-            a[i] = sp * w + sn * wn;
-            g[i] = gp[3 * i + j] * w + gn[3 * i + j] * wn;
+            a[i][j] = sp * w + sn * wn;
+            a[j][i] = a[i][j];
         }
-        f[j] = gam.x * a[0] + gam.y * a[1] + gam.z * a[2];
+    double f[3], dg[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        double g[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) g[i] = gp[3 * i + j] * w + gn[3 * i + j] * wn;
+        f[j] = gam.x * a[0][j] + gam.y * a[1][j] + gam.z * a[2][j];
         dg[j] = del.x * g[0] + del.y * g[1] + del.z * g[2];
     }
     flux = {f[0], f[1], f[2]};
