@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     double* stage_src = reinterpret_cast<double*>(stage_rec + static_cast<size_t>(kStages) * kMaxRows * 96);  // [kStages][kMaxRows*3]
     int* lp = reinterpret_cast<int*>(stage_src + kStages * kMaxRows * 3);  // [kLvl + 2]
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(lp + kLvl + 2);  // [kStages], 8-aligned
+    double* zero_slot = reinterpret_cast<double*>(mbar + kStages);  // 0.0: read by absent dependencies
+    const uint32_t zero_addr = smem_u32(zero_slot);
     const uint32_t ring_base = smem_u32(ring);
     const uint32_t mbar_base = smem_u32(mbar);
     int lbase = 0;
@@ -129,6 +131,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
         }
     };
     if (threadIdx.x < kStages) mbar_init(mbar_base + 8u * threadIdx.x, 1);
+    if (threadIdx.x == 0) *zero_slot = 0.0;
     stage_levels(0);  // its __syncthreads also publishes the mbarrier init
     if (producer)
         for (int l = 0; l < kStages - 1; ++l) issue(l);
@@ -163,28 +166,30 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 double z[NRHS];
 #pragma unroll
                 for (int k = 0; k < NRHS; ++k) z[k] = stage_src[(s * kMaxRows + j) * 3 + comp + k];
+                // Branch-free: an absent dependency (0xffff) reads a zero slot with factor value
+                // 0, and z - 0*0 is z bit for bit (also for -0, inf, NaN), as the reference's
+                // skipping it.  Every dependency load is issued before the first use.
                 double dv[8][NRHS];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {  // all dependency loads in flight together
+                for (int q = 0; q < 8; ++q) {
                     const unsigned d = dep[q];
+                    const uint32_t ad = d != 0xffffu && TSP(8)
+                                            ? mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank)
+                                            : zero_addr;
 #pragma unroll
-                    for (int k = 0; k < NRHS; ++k) dv[q][k] = 0.0;
-                    if (d != 0xffffu && TSP(8)) {
-                        const uint32_t ad = mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank);
-#pragma unroll
-                        for (int k = 0; k < NRHS; ++k)
-                            asm volatile("ld.shared::cluster.f64 %0, [%1];"
-                                         : "=d"(dv[q][k])
-                                         : "r"(ad + static_cast<uint32_t>(k * ring_n * 8)));
-                    }
+                    for (int k = 0; k < NRHS; ++k)
+                        asm("ld.shared::cluster.f64 %0, [%1];"
+                            : "=d"(dv[q][k])
+                            : "r"(ad + (d != 0xffffu ? static_cast<uint32_t>(k * ring_n * 8) : 0u))
+                            : "memory");
                 }
+                double vq[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) vq[q] = rval[q * 32];
 #pragma unroll
                 for (int q = 0; q < 8; ++q)  // the reference's order of subtraction
-                    if (dep[q] != 0xffffu) {
-                        const double vq = rval[q * 32];
 #pragma unroll
-                        for (int k = 0; k < NRHS; ++k) z[k] -= vq * dv[q][k];
-                    }
+                    for (int k = 0; k < NRHS; ++k) z[k] -= vq[q] * dv[q][k];
                 if (UPPER) {
                     const double dg = reinterpret_cast<const double*>(ch + kOffDiag)[ln];
 #pragma unroll
@@ -260,7 +265,7 @@ cudaError_t launch_one(const StreamSet& set, int ncomp, const double* src, doubl
 }  // namespace
 
 int stream_smem_bytes(int ring, int max_rows, int stages) {
-    return ring * 24 + stages * max_rows * (96 + 24) + (kLvl + 2) * 4 + 8 * 8;
+    return ring * 24 + stages * max_rows * (96 + 24) + (kLvl + 2) * 4 + 8 * 8 + 16;
 }
 
 cudaError_t launch_tri_stream(const StreamSet& set, bool upper, int ncomp, const double* src, double* dst,
