@@ -115,10 +115,11 @@ struct sfv_ctx {
     double time = 0.0;
     cudaStream_t stream = nullptr;
     // owned layout buffers
-    DevBuf<int> slot_face, slot_other, bnd_si;  // bnd_si: slot index of each boundary face
-    DevBuf<double> slot_ls, gam, del, dmag, w, volume;
-    // jv_pair.cu scratch + face records
-    DevBuf<double> pwg, face9, bres, psig;  // pwg = [w (3 nc) | G (9 nc)], psig: cell stress (6 nc)
+    // bnd_si: per boundary face, slot index s * nc + cell (alternative paths) or cell * 8 + s (default)
+    DevBuf<int> slot_face, slot_other, bnd_si, tslot;
+    DevBuf<double> slot_ls, gam, del, dmag, w, volume, tls;
+    // jv_pair.cu scratch + tiled face records (device.h): pwg = tiled [w | G], psig: tiled cell stress
+    DevBuf<double> pwg, face9, bres, psig;
     PairScratch ps;
     // scratch
     DevBuf<double> grad, red, scal;  // scal: [0]=eps [1]=u_norm [2..] misc
@@ -192,10 +193,7 @@ std::string build_layout(sfv_ctx* c) {
     int slots = 0;
     for (int i = 0; i < nc; ++i) slots = std::max(slots, m.cf_off[i + 1] - m.cf_off[i]);
     if (slots > kMaxSlots) return "mesh: cells with more than 8 faces are not supported by the device layout";
-    std::vector<int> sf(static_cast<size_t>(slots) * nc, -1), so(static_cast<size_t>(slots) * nc, -1);
-    std::vector<double> sl(static_cast<size_t>(3) * slots * nc, 0.0);
-    std::vector<int> bsi(std::max(1, nf - m.n_internal), 0);
-    if (static_cast<size_t>(slots) * nc > static_cast<size_t>(INT_MAX))
+    if (static_cast<size_t>(slots) * nc > static_cast<size_t>(INT_MAX) || nc > (INT_MAX >> 3))
         return "mesh: too many cells for 32-bit slot indices";
     auto par = [](int n, const std::function<void(int, int)>& body) {  // independent ranges
         const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
@@ -204,28 +202,60 @@ std::string build_layout(sfv_ctx* c) {
         for (int k = 0; k < nth; ++k) th.emplace_back(body, std::min(n, k * ch), std::min(n, (k + 1) * ch));
         for (auto& t : th) t.join();
     };
+    const bool legacy = c->jv_path != 0;  // SoA slot / face arrays only for the alternative J.v kernels
+    // default path: tiled tables (device.h), slot stride padded to the kernels' template width
+    const int spad = slots <= 4 ? 4 : slots <= 6 ? 6 : 8;
+    const int ntc = (nc + 31) / 32, ntf = (nf + 31) / 32;
+    const size_t nsl = legacy ? static_cast<size_t>(slots) * nc : 0;
+    std::vector<int> sf(nsl, -1), so(nsl, -1);
+    std::vector<double> sl(3 * nsl, 0.0);
+    std::vector<int> tsl(legacy ? 0 : static_cast<size_t>(ntc) * 2 * spad * 32, -1);
+    std::vector<double> tls(legacy ? 0 : static_cast<size_t>(ntc) * 3 * spad * 32, 0.0);
+    std::vector<int> bsi(std::max(1, nf - m.n_internal), 0);
     par(nc, [&](int i0, int i1) {
     for (int i = i0; i < i1; ++i) {
         int s = 0;
         for (int q = m.cf_off[i]; q < m.cf_off[i + 1]; ++q, ++s) {
             const int f = m.cf[q];
-            const size_t si = static_cast<size_t>(s) * nc + i;
             const bool nb = f < m.n_internal && m.neighbour[f] == i;
-            sf[si] = f | (nb ? static_cast<int>(0x80000000u) : 0);
-            so[si] = f < m.n_internal ? (nb ? m.owner[f] : m.neighbour[f]) : -(2 + m.face_patch[f]);
-            sl[(3 * static_cast<size_t>(s)) * nc + i] = g.ls[q].x;
-            sl[(3 * static_cast<size_t>(s) + 1) * nc + i] = g.ls[q].y;
-            sl[(3 * static_cast<size_t>(s) + 2) * nc + i] = g.ls[q].z;
-            if (f >= m.n_internal) bsi[f - m.n_internal] = static_cast<int>(si);
+            const int code = f | (nb ? static_cast<int>(0x80000000u) : 0);
+            const int other = f < m.n_internal ? (nb ? m.owner[f] : m.neighbour[f]) : -(2 + m.face_patch[f]);
+            if (legacy) {
+                const size_t si = static_cast<size_t>(s) * nc + i;
+                sf[si] = code;
+                so[si] = other;
+                sl[(3 * static_cast<size_t>(s)) * nc + i] = g.ls[q].x;
+                sl[(3 * static_cast<size_t>(s) + 1) * nc + i] = g.ls[q].y;
+                sl[(3 * static_cast<size_t>(s) + 2) * nc + i] = g.ls[q].z;
+                if (f >= m.n_internal) bsi[f - m.n_internal] = static_cast<int>(si);
+            } else {
+                const size_t tb = tiled(i, 2 * spad), lb = tiled(i, 3 * spad);
+                tsl[tb + 32 * s] = code;
+                tsl[tb + 32 * (spad + s)] = other;
+                tls[lb + 32 * (3 * s)] = g.ls[q].x;
+                tls[lb + 32 * (3 * s + 1)] = g.ls[q].y;
+                tls[lb + 32 * (3 * s + 2)] = g.ls[q].z;
+                if (f >= m.n_internal) bsi[f - m.n_internal] = i * 8 + s;
+            }
         }
     }
     });
-    const bool legacy = c->jv_path != 0;  // separate face arrays only for the alternative J.v kernels
     const size_t nfl = legacy ? static_cast<size_t>(nf) : 0;
     std::vector<double> gm(3 * nfl), de(3 * nfl), dmg(nfl), ww(nfl);
-    std::vector<double> f9(9 * static_cast<size_t>(nf));
+    std::vector<double> f9(legacy ? 0 : static_cast<size_t>(ntf) * 9 * 32, 0.0);
     par(nf, [&](int f0, int f1) {
     for (int f = f0; f < f1; ++f) {
+        if (legacy) {
+            gm[f] = g.area[f].x;
+            gm[nf + f] = g.area[f].y;
+            gm[2 * static_cast<size_t>(nf) + f] = g.area[f].z;
+            de[f] = g.delta[f].x;
+            de[nf + f] = g.delta[f].y;
+            de[2 * static_cast<size_t>(nf) + f] = g.delta[f].z;
+            dmg[f] = g.d_mag[f];
+            ww[f] = g.w[f];
+            continue;
+        }
         // per-face constants of rhie_chow(): |Delta| / |d| and |Gamma| (discretisation.cpp:176-208),
         // same IEEE operations as the reference (sqrt of the left-to-right dot, then divide)
         const double* a = &g.area[f].x;
@@ -233,24 +263,15 @@ std::string build_layout(sfv_ctx* c) {
         const double rec[9] = {a[0], a[1], a[2], d[0], d[1], d[2],
                                std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]) / g.d_mag[f],
                                std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]), g.w[f]};
-        for (int q = 0; q < 9; ++q) f9[static_cast<size_t>(q) * nf + f] = rec[q];
-        if (!legacy) continue;
-        gm[f] = g.area[f].x;
-        gm[nf + f] = g.area[f].y;
-        gm[2 * static_cast<size_t>(nf) + f] = g.area[f].z;
-        de[f] = g.delta[f].x;
-        de[nf + f] = g.delta[f].y;
-        de[2 * static_cast<size_t>(nf) + f] = g.delta[f].z;
-        dmg[f] = g.d_mag[f];
-        ww[f] = g.w[f];
+        const size_t fb = tiled(f, 9);
+        for (int q = 0; q < 9; ++q) f9[fb + 32 * q] = rec[q];
     }
     });
-    // the default path reads the face SoA rows of face9 (Gamma, Delta, w share its layout);
-    // the separate arrays (and |d|) are uploaded only for the alternative J.v kernels
-    if (!c->slot_face.upload(sf) || !c->slot_other.upload(so) || !c->slot_ls.upload(sl) ||
-        (legacy && (!c->gam.upload(gm) || !c->del.upload(de) || !c->dmag.upload(dmg) || !c->w.upload(ww))) ||
-        !c->bnd_si.upload(bsi) ||
-        !c->bres.alloc(6 * bsi.size()) || !c->face9.upload(f9) || !c->pwg.alloc(12 * static_cast<size_t>(nc)))
+    if ((legacy && (!c->slot_face.upload(sf) || !c->slot_other.upload(so) || !c->slot_ls.upload(sl) ||
+                    !c->gam.upload(gm) || !c->del.upload(de) || !c->dmag.upload(dmg) || !c->w.upload(ww))) ||
+        (!legacy && (!c->tslot.upload(tsl) || !c->tls.upload(tls) || !c->face9.upload(f9) ||
+                     !c->pwg.alloc(static_cast<size_t>(ntc) * kWG * 32))) ||
+        !c->bnd_si.upload(bsi) || !c->bres.alloc(6 * bsi.size()))
         return "cuda: out of device memory for the mesh layout";
     if (c->ph.transient && !c->volume.upload(g.volume)) return "cuda: out of device memory";
     DevMesh& d = c->dm;
@@ -258,18 +279,22 @@ std::string build_layout(sfv_ctx* c) {
     d.nf = nf;
     d.nint = m.n_internal;
     d.slots = slots;
+    d.spad = spad;
     d.slot_face = c->slot_face.p;
     d.slot_other = c->slot_other.p;
     d.slot_ls = c->slot_ls.p;
-    d.gam = legacy ? c->gam.p : c->face9.p;
-    d.del = legacy ? c->del.p : c->face9.p + 3 * static_cast<size_t>(nf);
-    d.dmag = legacy ? c->dmag.p : nullptr;
-    d.w = legacy ? c->w.p : c->face9.p + 8 * static_cast<size_t>(nf);
+    d.gam = c->gam.p;
+    d.del = c->del.p;
+    d.dmag = c->dmag.p;
+    d.w = c->w.p;
+    d.tslot = c->tslot.p;
+    d.tls = c->tls.p;
+    d.tf9 = c->face9.p;
     d.volume = c->volume.p;
-    if ((c->ph.law != SFV_LAW_HOOKE || c->ph.tl) && !c->psig.alloc(6 * static_cast<size_t>(nc)))
+    if (!legacy && (c->ph.law != SFV_LAW_HOOKE || c->ph.tl) && !c->psig.alloc(static_cast<size_t>(ntc) * kSig * 32))
         return "cuda: out of device memory for the mesh layout";
     c->ps.sig = c->psig.p;
-    c->ps.w = c->pwg.p;
+    c->ps.wg = c->pwg.p;
     // boundary pass on a side stream beside the gradient pass: opt-in (SFV_SIDE_STREAM=1);
     // measured 3% slower at 1M cells (the stream events break the PDL chain)
     if (const char* se = std::getenv("SFV_SIDE_STREAM"); se && std::atoi(se) != 0 && nf > m.n_internal) {
@@ -278,9 +303,8 @@ std::string build_layout(sfv_ctx* c) {
             cudaEventCreateWithFlags(&c->ps.ev_b, cudaEventDisableTiming) != cudaSuccess)
             return "cuda: cannot create the side stream";
     }
-    c->ps.G = c->pwg.p + 3 * static_cast<size_t>(nc);
-    // [w | G] in a persisting L2 window: opt-in experiment (SFV_L2_PERSIST=1, or 2 for G
-    // alone); measured 2-4% slower at 1M cells, the passes are latency-bound
+    // [w | G] in a persisting L2 window: opt-in experiment (SFV_L2_PERSIST=1);
+    // measured 2-4% slower at 1M cells, the passes are latency-bound
     c->ps.win_bytes = 0;
     const char* pe = std::getenv("SFV_L2_PERSIST");
     if (pe && std::atoi(pe) != 0) {
@@ -288,22 +312,20 @@ std::string build_layout(sfv_ctx* c) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
         cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-        const size_t want = 12 * sizeof(double) * static_cast<size_t>(nc);
+        const size_t want = kWG * sizeof(double) * 32 * static_cast<size_t>(ntc);
         if (max_persist > 0 && max_window > 0) {
             size_t limit = 0;
             cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize);
             const size_t set_aside = std::min<size_t>(static_cast<size_t>(max_persist), want);
             if (limit < set_aside) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set_aside);
             cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize);
-            const bool g_only = pe && std::atoi(pe) == 2;  // experiment: G alone
-            c->ps.win_base = g_only ? static_cast<void*>(c->ps.G) : static_cast<void*>(c->pwg.p);
-            c->ps.win_bytes = std::min<size_t>(g_only ? want * 3 / 4 : want, static_cast<size_t>(max_window));
+            c->ps.win_base = static_cast<void*>(c->pwg.p);
+            c->ps.win_bytes = std::min<size_t>(want, static_cast<size_t>(max_window));
             c->ps.win_hit = static_cast<float>(std::min(1.0, static_cast<double>(limit) / c->ps.win_bytes));
             cudaGetLastError();
         }
     }
-    c->ps.face9 = c->face9.p;
-    c->ps.bnd_si = c->bnd_si.p;
+    c->ps.bnd_cs = c->bnd_si.p;
     c->ps.bres = c->bres.p;
     return "";
 }
@@ -1243,7 +1265,9 @@ long long sfv_launch_count(const sfv_ctx* c) { return c->launches; }
 
 size_t sfv_device_bytes(const sfv_ctx* c) {
     return c->slot_face.bytes() + c->slot_other.bytes() + c->slot_ls.bytes() + c->gam.bytes() + c->del.bytes() +
-           c->dmag.bytes() + c->w.bytes() + c->volume.bytes() + c->grad.bytes() + c->V.bytes() + c->dense_w[0].bytes() + c->dense_w[1].bytes() + c->dense_w[2].bytes();
+           c->dmag.bytes() + c->w.bytes() + c->volume.bytes() + c->grad.bytes() + c->V.bytes() + c->dense_w[0].bytes() +
+           c->dense_w[1].bytes() + c->dense_w[2].bytes() + c->tslot.bytes() + c->tls.bytes() + c->face9.bytes() +
+           c->pwg.bytes() + c->psig.bytes() + c->bres.bytes();
 }
 
 double sfv_jv_bytes(const sfv_ctx* c) {
@@ -1346,8 +1370,13 @@ int sfv_gradients(sfv_ctx* c, const double* u, double* G, int* cell) {
         if (cell) *cell = c->singular_cell;
         return gradient_failure(c);
     }
-    launch_gradients(c->dm, c->pt, u, G, c->stream);
-    c->launches += 1;
+    if (c->jv_path == 0) {
+        launch_gradients_pair(c->dm, c->pt, c->ph, u, G, c->ps, c->err.p, c->stream);
+        c->launches += 3;
+    } else {
+        launch_gradients(c->dm, c->pt, u, G, c->stream);
+        c->launches += 1;
+    }
     if (int e = c->cuda_check("gradients")) return e;
     return cudaStreamSynchronize(c->stream) == cudaSuccess ? SFV_OK : c->cuda_check("gradients");
 }

@@ -40,7 +40,22 @@ struct DevMesh {
     const double* dmag = nullptr;     // [nf]
     const double* w = nullptr;        // [nf]
     const double* volume = nullptr;   // [nc]
+    // Default path (jv_pair.cu): tiled ("AoSoA") tables, 32 cells or faces per tile, so that
+    // entry q of cell c sits at (c >> 5) * (nq * 32) + q * 32 + (c & 31).  A warp of 32
+    // consecutive cells still loads 32 consecutive values per instruction, and a gather of
+    // one cell's record needs one base address: the nq field offsets are immediates.
+    int spad = 0;                  // slot stride of the tiled slot tables (4, 6 or 8)
+    const int* tslot = nullptr;    // [(c>>5)][2 * spad][32]: face code (slot s), then other cell (spad + s)
+    const double* tls = nullptr;   // [(c>>5)][3 * spad][32]: least-squares vector of slot s, row 3 s + k
+    const double* tf9 = nullptr;   // [(f>>5)][9][32]: Gamma xyz, Delta xyz, |Delta|/|d|, |Gamma|, w
 };
+
+constexpr int kTileShift = 5;  // 32 cells (faces) per tile of the tiled tables
+__host__ __device__ __forceinline__ size_t tiled(int c, int nq) {
+    return static_cast<size_t>(c >> kTileShift) * (static_cast<size_t>(nq) << kTileShift) + (c & 31);
+}
+constexpr int kWG = 12;   // rows of the tiled [w | G] record: w xyz, then G row-major
+constexpr int kSig = 6;   // rows of the tiled cell-stress record
 
 struct Physics {
     int law;  // SFV_LAW_*
@@ -76,11 +91,9 @@ void launch_residual(const DevMesh& m, const Physics& ph, const PatchTable& pt, 
 // ---- jv_pair.cu: same contract as launch_residual; perturb + gradient + boundary-face +
 // per-(cell, face slot) flux kernels
 struct PairScratch {
-    double* w = nullptr;            // [3*nc] perturbed state u + eps v, SoA
-    double* G = nullptr;            // [9*nc] cell gradients, row-major entries, SoA
-    double* sig = nullptr;          // [6*nc] cell stress (xx, xy, xz, yy, yz, zz), non-Hooke / TL only
-    const double* face9 = nullptr;  // [9*nf] Gamma xyz, Delta xyz, |Delta|/|d|, |Gamma|, w; SoA
-    const int* bnd_si = nullptr;  // [nf-nint] slot index (s*nc + cell) of boundary face nint+fb
+    double* wg = nullptr;           // tiled [w | G] (kWG rows): perturbed state u + eps v, cell gradients
+    double* sig = nullptr;          // tiled cell stress (xx, xy, xz, yy, yz, zz), non-Hooke / TL only
+    const int* bnd_cs = nullptr;    // [nf-nint] cell * 8 + slot of boundary face nint+fb
     double* bres = nullptr;       // [6*(nf-nint)] boundary-face flux + stabilisation
     cudaEvent_t* marks = nullptr;  // optional: recorded after the perturb, gradient, boundary passes
     // J.v: eps computed in the perturb pass from launch_norm_partials' block partials
@@ -92,7 +105,7 @@ struct PairScratch {
     int npart = 0;
     double* u_norm = nullptr;
     bool u_norm_cached = false;
-    // L2 persisting window over [w | G] (contiguous): both are gathered by the next pass,
+    // L2 persisting window over [w | G]: both are gathered by the next pass,
     // and G is rewritten in place by the next J.v, so resident lines never reach HBM
     void* win_base = nullptr;
     size_t win_bytes = 0;
@@ -101,7 +114,11 @@ struct PairScratch {
 void launch_residual_pair(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist,
                           const double* u, const double* v, const double* jv_eps, const double* r_u, double* out,
                           const PairScratch& ps, ErrWords* err, cudaStream_t s);
-// cell_gradients only (discretisation.cpp:10-31), SoA [k*nc + c], k = 3i + j
+// cell_gradients only (discretisation.cpp:10-31), SoA [k*nc + c], k = 3i + j, through the
+// default path's kernels (scratch in ps)
+void launch_gradients_pair(const DevMesh& m, const PatchTable& pt, const Physics& ph, const double* u, double* G,
+                           const PairScratch& ps, ErrWords* err, cudaStream_t s);
+// the same through residual.cu (alternative paths)
 void launch_gradients(const DevMesh& m, const PatchTable& pt, const double* u, double* G, cudaStream_t s);
 // Block partials of |u|^2 and |v|^2 (2 per block, fixed order) for the jv_pair.cu path;
 // returns the number of blocks.

@@ -31,14 +31,16 @@ using namespace fm;
 constexpr int kCells = 32;  // cells per CTA (one warp-width); CTA = kCells x S threads
 constexpr int kSign = static_cast<int>(0x80000000u);
 
-__device__ __forceinline__ d3 ldsoa(const double* __restrict__ p, int n, int i) {
-    return {p[i], p[n + i], p[2 * static_cast<size_t>(n) + i]};
-}
+// Tiled tables (device.h): entry q of cell (face) c at tiled(c, nq) + 32 q.  One base
+// address per gathered record, the field offsets are immediates (no per-load IMADs).
+__device__ __forceinline__ d3 ld3(const double* __restrict__ p) { return {p[0], p[32], p[64]}; }
+// face record of face f: Gamma (rows 0-2), Delta (3-5), |Delta|/|d|, |Gamma|, w
+__device__ __forceinline__ const double* face_rec(const DevMesh& m, int f) { return m.tf9 + tiled(f, 9); }
 // Streams read once per pass (slot tables, least-squares vectors, r_u) are loaded with
 // evict-first (ld.global.cs) so that the gathered w and G (~96 MB at 1M cells) stay in L2.
-// All gathered arrays are SoA so that the 32 lanes of a warp (32 consecutive cells, one
-// face slot) load 32 consecutive doubles per instruction: the L1 wavefront queue, not DRAM,
-// limits a gather kernel whose loads each touch many 128-byte lines.
+// The 32 lanes of a warp (32 consecutive cells, one face slot) load 32 consecutive values
+// per instruction: the L1 wavefront queue, not DRAM, limits a gather kernel whose loads
+// each touch many 128-byte lines.
 // w and G are written with an L2 evict-last policy: their consumers gather them within
 // the next two kernels, after ~170 MB of streamed least-squares vectors and slot tables.
 __device__ __forceinline__ unsigned long long evict_last_policy() {
@@ -49,20 +51,17 @@ __device__ __forceinline__ unsigned long long evict_last_policy() {
 __device__ __forceinline__ void st_keep(double* a, double v, unsigned long long pol) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
-// perturbed state w[k * nc + c] = u + eps v
-__device__ __forceinline__ d3 ldw(const double* __restrict__ w, int nc, int c) {
-    return {w[c], w[nc + c], w[2 * nc + c]};
-}
-// cell gradient G[q * nc + c], q = 3 i + j (row-major)
-__device__ __forceinline__ void ldg9(const double* __restrict__ G, int nc, int c, double* g) {
+// [w | G] record of cell c: w xyz (rows 0-2), G row-major (rows 3-11, q = 3 i + j)
+__device__ __forceinline__ const double* wg_rec(const double* __restrict__ wg, int c) { return wg + tiled(c, kWG); }
+__device__ __forceinline__ void ldg9(const double* __restrict__ r, double* g) {
 #pragma unroll
-    for (int q = 0; q < 9; ++q) g[q] = G[q * nc + c];
+    for (int q = 0; q < 9; ++q) g[q] = r[32 * (3 + q)];
 }
-__device__ __forceinline__ dm3 ldG(const double* __restrict__ G, int nc, int c) {
-    dm3 r;
+__device__ __forceinline__ dm3 ldG(const double* __restrict__ r) {
+    dm3 a;
 #pragma unroll
-    for (int q = 0; q < 9; ++q) r.a[q / 3][q % 3] = G[q * nc + c];
-    return r;
+    for (int q = 0; q < 9; ++q) a.a[q / 3][q % 3] = r[32 * (3 + q)];
+    return a;
 }
 
 // programmatic dependent launch (see launch_win)
@@ -78,16 +77,16 @@ __device__ __forceinline__ void release_late() {
     if (!SFV_PDL_EARLY) release_dependents();
 }
 
-// symmetric cell stress from its 6 stored entries (grad_cell_kernel<S, true>)
-__device__ __forceinline__ dm3 ld_sig(const double* __restrict__ sig, int nc, int c) {
-    dm3 r;
-    r.a[0][0] = sig[c];
-    r.a[0][1] = r.a[1][0] = sig[nc + c];
-    r.a[0][2] = r.a[2][0] = sig[2 * nc + c];
-    r.a[1][1] = sig[3 * nc + c];
-    r.a[1][2] = r.a[2][1] = sig[4 * nc + c];
-    r.a[2][2] = sig[5 * nc + c];
-    return r;
+// symmetric cell stress from its 6 stored entries (grad_cell_kernel<S, true>), tiled record
+__device__ __forceinline__ dm3 ld_sig(const double* __restrict__ r) {
+    dm3 a;
+    a.a[0][0] = r[0];
+    a.a[0][1] = a.a[1][0] = r[32];
+    a.a[0][2] = a.a[2][0] = r[64];
+    a.a[1][1] = r[96];
+    a.a[1][2] = a.a[2][1] = r[128];
+    a.a[2][2] = r[160];
+    return a;
 }
 
 // ---------------------------------------------------------------- perturbed state
@@ -132,7 +131,7 @@ __device__ __forceinline__ double eps_from_partials(const double* __restrict__ p
 
 template <bool PERT>
 __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __restrict__ u, const double* __restrict__ v,
-                                                      double* __restrict__ eps_p, double* __restrict__ w,
+                                                      double* __restrict__ eps_p, double* __restrict__ wg,
                                                       const double* __restrict__ part, int np,
                                                       double* __restrict__ u_norm, bool cached) {
     __shared__ double sh[2 * 8 + 2];
@@ -158,9 +157,10 @@ __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __re
             z = z + eps * v[3 * c + 2];
         }
         const unsigned long long pol = evict_last_policy();
-        st_keep(&w[c], x, pol);
-        st_keep(&w[nc + c], y, pol);
-        st_keep(&w[2 * nc + c], z, pol);
+        double* r = wg + tiled(c, kWG);
+        st_keep(r, x, pol);
+        st_keep(r + 32, y, pol);
+        st_keep(r + 64, z, pol);
     }
     release_late();
 }
@@ -174,20 +174,22 @@ __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __re
 // the flux pass — same function on the same G, so the same bits (sigma is symmetric
 // bitwise: every entry pair is a product sum of the same factors).
 template <int S, bool GEN>
-__global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt, Physics ph,
-                                                        const double* __restrict__ w, double* __restrict__ G,
+__global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt, Physics ph, double* __restrict__ wg,
                                                         double* __restrict__ sig, ErrWords* __restrict__ err) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= m.nc) return;
     release_early();
+    const int* ts = m.tslot + tiled(c, 2 * S);
+    const double* tl = m.tls + tiled(c, 3 * S);
     int o[S];
 #pragma unroll
-    for (int s = 0; s < S; ++s) o[s] = s < m.slots ? __ldcs(&m.slot_other[s * m.nc + c]) : -1;
+    for (int s = 0; s < S; ++s) o[s] = __ldcs(ts + 32 * (S + s));  // padding slots hold -1
     wait_predecessor();  // w
-    const d3 wc = ldw(w, m.nc, c);
+    double* rc = wg + tiled(c, kWG);
+    const d3 wc = ld3(rc);
     d3 wn[S];
 #pragma unroll
-    for (int s = 0; s < S; ++s) wn[s] = o[s] >= 0 ? ldw(w, m.nc, o[s]) : d3{0.0, 0.0, 0.0};
+    for (int s = 0; s < S; ++s) wn[s] = o[s] >= 0 ? ld3(wg_rec(wg, o[s])) : d3{0.0, 0.0, 0.0};
     double g[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) g[q] = 0.0;
@@ -197,13 +199,12 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
         if (o[s] >= 0) {
             du = sub(wn[s], wc);
         } else if (o[s] <= -2 && pt.kind[-o[s] - 2] == SFV_PATCH_SYMMETRY) {
-            const dm3 R = reflection(ldsoa(m.gam, m.nf, m.slot_face[s * m.nc + c] & ~kSign));
+            const dm3 R = reflection(ld3(face_rec(m, ts[32 * s] & ~kSign)));
             du = sub(mv(R, wc), wc);
         } else {
             continue;  // traction / displacement faces are not in the stencil; padding
         }
-        const d3 ls = {__ldcs(&m.slot_ls[(3 * s) * m.nc + c]), __ldcs(&m.slot_ls[(3 * s + 1) * m.nc + c]),
-                       __ldcs(&m.slot_ls[(3 * s + 2) * m.nc + c])};
+        const d3 ls = {__ldcs(tl + 32 * (3 * s)), __ldcs(tl + 32 * (3 * s + 1)), __ldcs(tl + 32 * (3 * s + 2))};
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
     }
     const unsigned long long pol = evict_last_policy();
 #pragma unroll
-    for (int q = 0; q < 9; ++q) st_keep(&G[q * m.nc + c], g[q], pol);
+    for (int q = 0; q < 9; ++q) st_keep(rc + 32 * (3 + q), g[q], pol);
     if (GEN) {
         dm3 gm;
 #pragma unroll
@@ -219,37 +220,39 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
         bool ok;
         const dm3 sc = stress(ph, gm, ok);
         if (!ok) atomicMin(&err->inverted_cell, c);
-        st_keep(&sig[c], sc.a[0][0], pol);
-        st_keep(&sig[m.nc + c], sc.a[0][1], pol);
-        st_keep(&sig[2 * m.nc + c], sc.a[0][2], pol);
-        st_keep(&sig[3 * m.nc + c], sc.a[1][1], pol);
-        st_keep(&sig[4 * m.nc + c], sc.a[1][2], pol);
-        st_keep(&sig[5 * m.nc + c], sc.a[2][2], pol);
+        double* rs = sig + tiled(c, kSig);
+        st_keep(rs, sc.a[0][0], pol);
+        st_keep(rs + 32, sc.a[0][1], pol);
+        st_keep(rs + 64, sc.a[0][2], pol);
+        st_keep(rs + 96, sc.a[1][1], pol);
+        st_keep(rs + 128, sc.a[1][2], pol);
+        st_keep(rs + 160, sc.a[2][2], pol);
     }
     release_late();
 }
 
 // One cell's gradient with exactly grad_cell_kernel's operations (slots in face order), for
 // the boundary pass, which then needs w only and can run beside the gradient pass.
-__device__ __forceinline__ dm3 cell_gradient_at(const DevMesh& m, const PatchTable& pt, const double* __restrict__ w,
+__device__ __forceinline__ dm3 cell_gradient_at(const DevMesh& m, const PatchTable& pt, const double* __restrict__ wg,
                                                 int c) {
-    const d3 wc = ldw(w, m.nc, c);
+    const int* ts = m.tslot + tiled(c, 2 * m.spad);
+    const double* tl = m.tls + tiled(c, 3 * m.spad);
+    const d3 wc = ld3(wg_rec(wg, c));
     double g[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) g[q] = 0.0;
     for (int s = 0; s < m.slots; ++s) {
-        const int o = m.slot_other[s * m.nc + c];
+        const int o = ts[32 * (m.spad + s)];
         d3 du;
         if (o >= 0) {
-            du = sub(ldw(w, m.nc, o), wc);
+            du = sub(ld3(wg_rec(wg, o)), wc);
         } else if (o <= -2 && pt.kind[-o - 2] == SFV_PATCH_SYMMETRY) {
-            const dm3 R = reflection(ldsoa(m.gam, m.nf, m.slot_face[s * m.nc + c] & ~kSign));
+            const dm3 R = reflection(ld3(face_rec(m, ts[32 * s] & ~kSign)));
             du = sub(mv(R, wc), wc);
         } else {
             continue;
         }
-        const d3 ls = {m.slot_ls[(3 * s) * m.nc + c], m.slot_ls[(3 * s + 1) * m.nc + c],
-                       m.slot_ls[(3 * s + 2) * m.nc + c]};
+        const d3 ls = {tl[32 * (3 * s)], tl[32 * (3 * s + 1)], tl[32 * (3 * s + 2)]};
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -262,31 +265,31 @@ __device__ __forceinline__ dm3 cell_gradient_at(const DevMesh& m, const PatchTab
 }
 
 // ---------------------------------------------------------------- boundary faces
-// One thread per boundary face (face f = nint + fb, slot index bnd_si[fb] = s * nc + cell):
+// One thread per boundary face (face f = nint + fb, bnd_cs[fb] = cell * 8 + slot):
 // flux and stabilisation term into bres[q * nbf + fb] (discretisation.cpp:128-154, :186-205).
 // Kept out of the per-slot kernel so its register budget is set by the internal faces.
+// with_g: G is read from wg (else each cell's gradient is recomputed from w).
 __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, PatchTable pt,
-                                                       const int* __restrict__ bnd_si, const double* __restrict__ face9,
-                                                       const double* __restrict__ w,
-                                                       const double* __restrict__ eps_p,
-                                                       const double* __restrict__ G, double* __restrict__ bres,
-                                                       ErrWords* __restrict__ err) {
+                                                       const int* __restrict__ bnd_cs, const double* __restrict__ wg,
+                                                       const double* __restrict__ eps_p, bool with_g,
+                                                       double* __restrict__ bres, ErrWords* __restrict__ err) {
     release_early();
     const int nbf = m.nf - m.nint;
     const int fb = blockIdx.x * blockDim.x + threadIdx.x;
     wait_predecessor();  // w (and G when it is read)
     if (fb >= nbf) return;
     if (eps_p && *eps_p == 0.0) return;
-    const int si = bnd_si[fb];
-    const int c = si % m.nc;
+    const int cs = bnd_cs[fb];
+    const int c = cs >> 3, s = cs & 7;
     const int f = m.nint + fb;
-    const int patch = -m.slot_other[si] - 2;
+    const int patch = -m.tslot[tiled(c, 2 * m.spad) + 32 * (m.spad + s)] - 2;
     const int pk = pt.kind[patch];
     const d3 bc = {pt.value[patch][0], pt.value[patch][1], pt.value[patch][2]};
-    const d3 gam = ldsoa(face9, m.nf, f);
+    const double* fr = face_rec(m, f);
+    const d3 gam = ld3(fr);
     // rhie_chow()'s per-face constants |Delta| / |d| and |Gamma|, precomputed on the host with
     // the reference's operations (see flux_pair_kernel)
-    const double cfac = face9[6 * static_cast<size_t>(m.nf) + f], gmag = face9[7 * static_cast<size_t>(m.nf) + f];
+    const double cfac = fr[32 * 6], gmag = fr[32 * 7];
     auto rc = [&](d3 up, d3 uo, const dm3& gf, d3 delta) {
         const d3 compact = scl(sub(uo, up), cfac);
         return scl(sub(compact, dot_left(delta, gf)), ph.alpha * ph.kbar * gmag);
@@ -295,9 +298,10 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
     if (pk == SFV_PATCH_TRACTION) {  // nominal load |Gamma| T (discretisation.cpp:151-154)
         flux = scl(bc, gmag);
     } else {
-        const dm3 gc = G ? ldG(G, m.nc, c) : cell_gradient_at(m, pt, w, c);
-        const d3 uc = ldw(w, m.nc, c);
-        const d3 del = ldsoa(face9 + 3 * static_cast<size_t>(m.nf), m.nf, f);
+        const double* rcell = wg_rec(wg, c);
+        const dm3 gc = with_g ? ldG(rcell) : cell_gradient_at(m, pt, wg, c);
+        const d3 uc = ld3(rcell);
+        const d3 del = ld3(fr + 32 * 3);
         bool okc;
         const dm3 sc = stress(ph, gc, okc);
         if (pk == SFV_PATCH_DISPLACEMENT) {
@@ -331,15 +335,15 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
 }
 
 // ---------------------------------------------------------------- fluxes + epilogue
-// face9[q * nf + f], q = Gamma xyz, Delta xyz, |Delta| / |d|, |Gamma|, w (the two ratios are
+// Face records (m.tf9): Gamma xyz, Delta xyz, |Delta| / |d|, |Gamma|, w (the two ratios are
 // the per-face constants of rhie_chow(), precomputed with the same IEEE operations).
 // kind of a slot's contribution: 0 none (padding), 1 flux only (traction), 2 flux + stabilisation
 template <bool PERT, int S, bool GEN>
 __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
-    flux_pair_kernel(DevMesh m, Physics ph, PatchTable pt, History hist, const double* __restrict__ w,
-                     const double* __restrict__ eps_p, const double* __restrict__ G, const double* __restrict__ sig,
-                     const double* __restrict__ face9, const double* __restrict__ bres,
-                     const double* __restrict__ r_u, double* __restrict__ out, ErrWords* __restrict__ err) {
+    flux_pair_kernel(DevMesh m, Physics ph, PatchTable pt, History hist, const double* __restrict__ wg,
+                     const double* __restrict__ eps_p, const double* __restrict__ sig,
+                     const double* __restrict__ bres, const double* __restrict__ r_u, double* __restrict__ out,
+                     ErrWords* __restrict__ err) {
     // double-buffered per-slot results: one barrier per tile; the sums of tile i (warps
     // s < 3) overlap the face work of tile i + 1, and the barrier of tile i + 1 orders
     // them before buffer i & 1 is rewritten by tile i + 2
@@ -347,20 +351,20 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
     __shared__ unsigned char kind_buf[2][S][kCells];
     const int lane = threadIdx.x % kCells, s = threadIdx.x / kCells;
     const int ntiles = (m.nc + kCells - 1) / kCells;
-    // Persistent grid-stride loop over tiles of kCells cells.  The slot indices of a tile
-    // and the epilogue operand r_u of (component s, cell) — threads s < 3 do the per-cell
-    // sums — are loaded one iteration ahead, so a tile's dependent chain is one gather.
+    // Persistent grid-stride loop over tiles of kCells cells (= the tiles of the tables).
+    // The slot indices of a tile and the epilogue operand r_u of (component s, cell) —
+    // threads s < 3 do the per-cell sums — are loaded one iteration ahead, so a tile's
+    // dependent chain is one gather.
     auto fetch = [&](int t, int& fr, int& o, double& ru) {
         const int cc = t * kCells + lane;
         fr = -1;
         o = -1;
         ru = 0.0;
-        if (t < ntiles && cc < m.nc) {
-            if (s < m.slots) {
-                fr = __ldcs(&m.slot_face[s * m.nc + cc]);
-                o = __ldcs(&m.slot_other[s * m.nc + cc]);
-            }
-            if (PERT && s < 3) ru = __ldcs(&r_u[3 * cc + s]);
+        if (t < ntiles) {  // padding cells of the last tile hold fr = o = -1
+            const int* ts = m.tslot + static_cast<size_t>(t) * (2 * S * kCells) + lane;
+            fr = __ldcs(ts + kCells * s);
+            o = __ldcs(ts + kCells * (S + s));
+            if (PERT && s < 3 && cc < m.nc) ru = __ldcs(&r_u[3 * cc + s]);
         }
     };
     int fr_next, o_next;
@@ -384,19 +388,20 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
             if (o >= 0) {
                 const bool nb = (fr & kSign) != 0;
                 const int ip = nb ? o : c, in = nb ? c : o;  // reference owner / neighbour
-                const int nf = m.nf;
-                const d3 gam = {face9[f], face9[nf + f], face9[2 * nf + f]};
-                const d3 del = {face9[3 * nf + f], face9[4 * nf + f], face9[5 * nf + f]};
-                const double cfac = face9[6 * nf + f], gmag = face9[7 * nf + f], wf = face9[8 * nf + f];
-                const d3 up = ldw(w, m.nc, ip), un = ldw(w, m.nc, in);
+                const double* rf = face_rec(m, f);
+                const double* rp = wg_rec(wg, ip);
+                const double* rn = wg_rec(wg, in);
+                const d3 gam = ld3(rf), del = ld3(rf + 96);
+                const double cfac = rf[192], gmag = rf[224], wf = rf[256];
+                const d3 up = ld3(rp), un = ld3(rn);
                 if (!GEN) {
                     double gp[9], gn[9];
-                    ldg9(G, m.nc, ip, gp);
-                    ldg9(G, m.nc, in, gn);
+                    ldg9(rp, gp);
+                    ldg9(rn, gn);
                     hooke_face(gp, gn, wf, ph.mu, ph.lam, gam, del, up, un, cfac, gmag, ph.alpha, ph.kbar, flux, st);
                 } else {
-                    const dm3 gp = ldG(G, m.nc, ip), gn = ldG(G, m.nc, in);
-                    const dm3 sp = ld_sig(sig, m.nc, ip), sn = ld_sig(sig, m.nc, in);
+                    const dm3 gp = ldG(rp), gn = ldG(rn);
+                    const dm3 sp = ld_sig(sig + tiled(ip, kSig)), sn = ld_sig(sig + tiled(in, kSig));
                     d3 gm = gam;
                     if (ph.tl) {
                         bool ok;
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
                 for (int t = 0; t < S; ++t)
                     if (kind[t][lane] == 2) r += res[t][3 + k][lane];
                 if (ph.transient && !ph.stab_only) {  // BDF2 inertia (discretisation.cpp:48-57, :163-169)
-                    const double uc = w[k * m.nc + c];
+                    const double uc = wg[tiled(c, kWG) + 32 * k];
                     const double idt = 1.0 / (2.0 * ph.dt);
                     const double vn = ((uc * 3.0 - hist.u_old[ik] * 4.0) + hist.u_old_old[ik]) * idt;
                     const double ac = ((vn * 3.0 - hist.v_old[ik] * 4.0) + hist.v_old_old[ik]) * idt;
@@ -465,6 +470,14 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
             }
         }
     }
+}
+
+// G (tiled rows 3-11 of wg) -> SoA [q * nc + c] (sfv_gradients)
+__global__ void untile_grad_kernel(int nc, const double* __restrict__ wg, double* __restrict__ G) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) G[static_cast<size_t>(q) * nc + c] = wg[tiled(c, kWG) + 32 * (3 + q)];
 }
 
 template <bool PERT, int S, bool GEN>
@@ -513,45 +526,55 @@ void launch_win(void (*kern)(KArgs...), int grid, int block, cudaStream_t st, co
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+template <int S>
+void launch_grad(const DevMesh& m, const Physics& ph, const PatchTable& pt, const PairScratch& ps, ErrWords* err,
+                 cudaStream_t st) {
+    const int cb = (m.nc + 255) / 256;
+    const bool gen = ph.law != SFV_LAW_HOOKE || ph.tl;
+    if (gen) launch_win(grad_cell_kernel<S, true>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, err);
+    else launch_win(grad_cell_kernel<S, false>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, err);
+}
+
 template <bool PERT, int S>
 void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const History& hist, const double* u,
               const double* v, const double* eps, const double* r_u, double* out, const PairScratch& ps,
               ErrWords* err, cudaStream_t st) {
-    double* w = ps.w;
-    double* G = ps.G;
+    double* wg = ps.wg;
     const int cb = (m.nc + 255) / 256;
     // with the ε reduction folded in, a grid of a few waves keeps the per-block partial sums cheap
     const int pgrid = ps.partials ? std::min(cb, 148 * 8) : cb;
-    launch_win(perturb_kernel<PERT>, pgrid, 256, st, ps, m.nc, u, v, const_cast<double*>(eps), w, ps.partials,
+    launch_win(perturb_kernel<PERT>, pgrid, 256, st, ps, m.nc, u, v, const_cast<double*>(eps), wg, ps.partials,
                ps.npart, ps.u_norm, ps.u_norm_cached);
     if (ps.marks) cudaEventRecord(ps.marks[0], st);
     const int nbf = m.nf - m.nint;
     if (nbf > 0 && ps.side) cudaEventRecord(ps.ev_w, st);  // w ready: the boundary pass may start
     const bool gen = ph.law != SFV_LAW_HOOKE || ph.tl;
-    if (gen) launch_win(grad_cell_kernel<S, true>, cb, 256, st, ps, m, pt, ph, w, G, ps.sig, err);
-    else launch_win(grad_cell_kernel<S, false>, cb, 256, st, ps, m, pt, ph, w, G, ps.sig, err);
+    launch_grad<S>(m, ph, pt, ps, err, st);
     if (ps.marks) cudaEventRecord(ps.marks[1], st);
+    const double* no_eps = nullptr;
     if (nbf > 0) {
         if (ps.side) {  // beside the gradient pass: the boundary pass computes its own cells' gradients
             cudaStreamWaitEvent(ps.side, ps.ev_w, 0);
-            boundary_kernel<<<(nbf + 127) / 128, 128, 0, ps.side>>>(
-                m, ph, pt, ps.bnd_si, ps.face9, w, PERT ? eps : static_cast<const double*>(nullptr), nullptr, ps.bres, err);
+            boundary_kernel<<<(nbf + 127) / 128, 128, 0, ps.side>>>(m, ph, pt, ps.bnd_cs, wg, PERT ? eps : no_eps,
+                                                                   false, ps.bres, err);
             cudaEventRecord(ps.ev_b, ps.side);
             cudaStreamWaitEvent(st, ps.ev_b, 0);
         } else {
-            launch_win(boundary_kernel, (nbf + 127) / 128, 128, st, ps, m, ph, pt, ps.bnd_si, ps.face9, w,
-                       PERT ? eps : static_cast<const double*>(nullptr), G, ps.bres, err);
+            launch_win(boundary_kernel, (nbf + 127) / 128, 128, st, ps, m, ph, pt, ps.bnd_cs, wg, PERT ? eps : no_eps,
+                       true, ps.bres, err);
         }
     }
     if (ps.marks) cudaEventRecord(ps.marks[2], st);
     const int ntiles = (m.nc + kCells - 1) / kCells;
-    const double* f9 = ps.face9;
+    const double* cwg = wg;
     if (gen)
         launch_win(flux_pair_kernel<PERT, S, true>, flux_grid<PERT, S, true>(ntiles), kCells * S, st, ps, m, ph, pt,
-                   hist, w, eps, G, static_cast<const double*>(ps.sig), f9, ps.bres, r_u, out, err);
+                   hist, cwg, eps, static_cast<const double*>(ps.sig), static_cast<const double*>(ps.bres), r_u, out,
+                   err);
     else
         launch_win(flux_pair_kernel<PERT, S, false>, flux_grid<PERT, S, false>(ntiles), kCells * S, st, ps, m, ph,
-                   pt, hist, w, eps, G, static_cast<const double*>(ps.sig), f9, ps.bres, r_u, out, err);
+                   pt, hist, cwg, eps, static_cast<const double*>(ps.sig), static_cast<const double*>(ps.bres), r_u,
+                   out, err);
 }
 
 }  // namespace
@@ -560,16 +583,30 @@ void launch_residual_pair(const DevMesh& m, const Physics& ph, const PatchTable&
                           const double* u, const double* v, const double* jv_eps, const double* r_u, double* out,
                           const PairScratch& ps, ErrWords* err, cudaStream_t s) {
     const bool pert = jv_eps != nullptr;
-    if (m.slots <= 4) {
+    if (m.spad == 4) {
         if (pert) launch_s<true, 4>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
         else launch_s<false, 4>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
-    } else if (m.slots <= 6) {
+    } else if (m.spad == 6) {
         if (pert) launch_s<true, 6>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
         else launch_s<false, 6>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
     } else {
         if (pert) launch_s<true, 8>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
         else launch_s<false, 8>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
     }
+}
+
+void launch_gradients_pair(const DevMesh& m, const PatchTable& pt, const Physics& ph, const double* u, double* G,
+                           const PairScratch& ps, ErrWords* err, cudaStream_t s) {
+    Physics hp = ph;  // gradients only: no stress evaluation
+    hp.law = SFV_LAW_HOOKE;
+    hp.tl = 0;
+    const int cb = (m.nc + 255) / 256;
+    launch_win(perturb_kernel<false>, cb, 256, s, ps, m.nc, u, u, static_cast<double*>(nullptr), ps.wg,
+               static_cast<const double*>(nullptr), 0, static_cast<double*>(nullptr), false);
+    if (m.spad == 4) launch_grad<4>(m, hp, pt, ps, err, s);
+    else if (m.spad == 6) launch_grad<6>(m, hp, pt, ps, err, s);
+    else launch_grad<8>(m, hp, pt, ps, err, s);
+    untile_grad_kernel<<<cb, 256, 0, s>>>(m.nc, ps.wg, G);
 }
 
 }  // namespace sfv
