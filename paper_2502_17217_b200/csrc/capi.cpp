@@ -124,6 +124,7 @@ struct sfv_ctx {
     // scratch
     DevBuf<double> grad, red, scal;  // scal: [0]=eps [1]=u_norm [2..] misc
     DevBuf<unsigned> counter;
+    DevBuf<unsigned long long> epsbar;  // grid-barrier counter of eps_perturb_kernel
     DevBuf<ErrWords> err;
     Status* st = nullptr;  // pinned
     History hist{};
@@ -482,13 +483,15 @@ void residual_async(sfv_ctx* c, const double* u, double* r) {
 // J.v (async).  u_norm_cached: *scal[1] already holds |u| for this u.
 void jv_async(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out, bool u_norm_cached) {
     if (c->jv_path == 0) {  // norms as block partials; eps finished inside the perturb pass
-        c->ps.npart = launch_norm_partials(u, v, c->n, c->red.p, u_norm_cached, c->stream);
+        if (!c->ps.bar) {
+            c->ps.npart = launch_norm_partials(u, v, c->n, c->red.p, u_norm_cached, c->stream);
+            c->launches += 1;
+        }
         c->ps.partials = c->red.p;
         c->ps.u_norm = c->scal.p + 1;
         c->ps.u_norm_cached = u_norm_cached;
         residual_pass(c, c->ph, u, v, c->scal.p, r_u, out);
         c->ps.partials = nullptr;
-        c->launches += 1;
         return;
     }
     launch_jv_eps(u, v, c->n, c->red.p, c->counter.p, c->scal.p, c->scal.p + 1, u_norm_cached, c->stream);
@@ -1239,6 +1242,13 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
         !c->counter.alloc(1) || !c->err.alloc(1) || !c->hdev.alloc(72) || !c->dzero.alloc(n))
         return fail("cuda: out of device memory");
     cudaMemset(c->counter.p, 0, sizeof(unsigned));
+    // ε reduction fused into the perturb pass (default; SFV_EPS_FUSED=0: separate partials pass)
+    const char* ef = std::getenv("SFV_EPS_FUSED");
+    if (c->jv_path == 0 && !(ef && std::atoi(ef) == 0) && eps_perturb_grid_for(c->nc) > 0) {
+        if (!c->epsbar.alloc(1)) return fail("cuda: out of device memory");
+        cudaMemset(c->epsbar.p, 0, sizeof(unsigned long long));
+        c->ps.bar = c->epsbar.p;
+    }
     cudaMemset(c->dzero.p, 0, sizeof(double) * n);
     if (c->ph.transient) {
         c->hist.u_old = c->hist.u_old_old = c->hist.v_old = c->hist.v_old_old = c->dzero.p;
@@ -1289,7 +1299,7 @@ void sfv_jv_stage_bytes(const sfv_ctx* c, double* b) {
     // N_c cells, S face slots per cell, N_f faces, N_b boundary faces
     const double nc = c->nc, S = c->dm.slots, nf = c->dm.nf, nb = c->dm.nf - c->dm.nint;
     const double tr = c->ph.transient ? 104.0 * nc : 0.0;  // volume + 4 history vectors
-    b[0] = 48.0 * nc;                                       // u, v
+    b[0] = c->ps.bar ? 0.0 : 48.0 * nc;                     // u, v (fused into the next pass by default)
     b[1] = 72.0 * nc;                                       // u, v -> w
     b[2] = (4.0 * S + 24.0 * S + 24.0 + 72.0) * nc;         // slot_other, ls, w, G
     b[3] = 208.0 * nb;                                      // slot, geometry, G, w -> 6 results
@@ -1455,7 +1465,8 @@ int sfv_jv_stage_times(sfv_ctx* c, const double* u, const double* r_u, const dou
     for (int r = 0; r < reps; ++r) {
         cudaEvent_t* e = ev.data() + 6 * r;
         cudaEventRecord(e[0], c->stream);
-        c->ps.npart = launch_norm_partials(u, v, c->n, c->red.p, false, c->stream);
+        // fused ε: stage 0 is empty and stage 1 (the perturb pass) includes the reduction
+        if (!c->ps.bar) c->ps.npart = launch_norm_partials(u, v, c->n, c->red.p, false, c->stream);
         cudaEventRecord(e[1], c->stream);
         c->ps.marks = e + 2;
         c->ps.partials = c->red.p;
@@ -1476,7 +1487,7 @@ int sfv_jv_stage_times(sfv_ctx* c, const double* u, const double* r_u, const dou
         }
     for (auto& e : ev) cudaEventDestroy(e);
     for (int k = 0; k < 5; ++k) ms[k] = acc[k] / reps;
-    c->launches += static_cast<long long>(reps) * (c->dm.nf > c->dm.nint ? 5 : 4);
+    c->launches += static_cast<long long>(reps) * ((c->dm.nf > c->dm.nint ? 4 : 3) + (c->ps.bar ? 0 : 1));
     return c->cuda_check("jv_stage_times");
 }
 

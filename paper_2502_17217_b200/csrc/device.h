@@ -101,8 +101,11 @@ struct PairScratch {
     // boundary pass on a side stream, beside the gradient pass (null: in line)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_w = nullptr, ev_b = nullptr;
-    const double* partials = nullptr;
+    const double* partials = nullptr;  // block partials (or, with bar, the fused pass's scratch)
     int npart = 0;
+    // set: eps_perturb_kernel reduces the norms itself (grid barrier on this counter) and
+    // partials is only its scratch (>= 2 * eps_perturb grid doubles)
+    unsigned long long* bar = nullptr;
     double* u_norm = nullptr;
     bool u_norm_cached = false;
     // L2 persisting window over [w | G]: both are gathered by the next pass,
@@ -118,6 +121,8 @@ void launch_residual_pair(const DevMesh& m, const Physics& ph, const PatchTable&
 // default path's kernels (scratch in ps)
 void launch_gradients_pair(const DevMesh& m, const PatchTable& pt, const Physics& ph, const double* u, double* G,
                            const PairScratch& ps, ErrWords* err, cudaStream_t s);
+// grid of the fused ε + perturb pass for nc cells, 0 when it cannot run (not co-resident)
+int eps_perturb_grid_for(int nc);
 // the same through residual.cu (alternative paths)
 void launch_gradients(const DevMesh& m, const PatchTable& pt, const double* u, double* G, cudaStream_t s);
 // Block partials of |u|^2 and |v|^2 (2 per block, fixed order) for the jv_pair.cu path;

@@ -96,9 +96,11 @@ __device__ __forceinline__ dm3 ld_sig(const double* __restrict__ r) {
 // the same fixed order, so all blocks hold the same bits; block 0 publishes ε (and ‖u‖).
 // Replaces a last-block finalisation (atomics and a serial tail) on the J·v critical path.
 __device__ __forceinline__ double eps_from_partials(const double* __restrict__ part, int np, double* __restrict__ u_norm,
-                                                    bool cached, double* sh) {
+                                                    bool cached, double* sh, int nthr = 0) {
     double tu = 0.0, tv = 0.0;
-    for (int b = threadIdx.x; b < np; b += blockDim.x) {
+    const int nt = nthr ? nthr : blockDim.x;
+    if (threadIdx.x < nt)
+    for (int b = threadIdx.x; b < np; b += nt) {
         tu += __ldcg(&part[2 * b]);
         tv += __ldcg(&part[2 * b + 1]);
     }
@@ -163,6 +165,141 @@ __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __re
         st_keep(r + 64, z, pol);
     }
     release_late();
+}
+
+// ε and w = u + εv in one launch: the grid (all CTAs resident) reduces ‖u‖², ‖v‖² to fixed-order
+// block partials, meets at a grid barrier, and every block finishes ε from the partials in
+// the same order (so all hold the same bits) and forms w.  u and v are read from HBM once;
+// the second read hits L2 (48 MB at 1M cells).  Replaces launch_norm_partials + perturb.
+// bar: monotonically increasing arrival counter, 64-bit (never wraps), same grid every call.
+// The reduction is the one of launch_norm_partials + perturb_kernel operation for operation
+// (same grid, per-thread strides, block trees and final partial sum), so ε — and with it
+// every Krylov and Newton decision — is bitwise what the two-launch path computes.
+constexpr int kEpT = 512;
+template <bool VEC>  // VEC: u and v 16-byte aligned (double2 loads)
+__global__ void __launch_bounds__(kEpT, 4) eps_perturb_kernel(int nc, const double* __restrict__ u,
+                                                          const double* __restrict__ v, double* __restrict__ eps_p,
+                                                          double* __restrict__ wg, double* __restrict__ part,
+                                                          double* __restrict__ u_norm, bool cached,
+                                                          unsigned long long* __restrict__ bar) {
+    __shared__ double sh[2 * (kEpT / 32) + 2];
+    release_early();
+    wait_predecessor();  // u, v, and the previous pass that read w
+    const int n2 = VEC ? 3 * nc / 2 : 0;  // double2 elements of u and v (3 nc is even, or the tail below)
+    const double2* u2 = reinterpret_cast<const double2*>(u);
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+    const int st = gridDim.x * blockDim.x;
+    double au = 0.0, av = 0.0;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (!VEC) {
+        for (; i < 3 * nc; i += st) {
+            av += v[i] * v[i];
+            if (!cached) au += u[i] * u[i];
+        }
+    }
+    for (; i + 3 * st < n2; i += 4 * st) {
+        double2 x[4], y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            y[k] = v2[i + k * st];
+            x[k] = cached ? make_double2(0.0, 0.0) : u2[i + k * st];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            av += y[k].x * y[k].x;
+            av += y[k].y * y[k].y;
+            if (!cached) {
+                au += x[k].x * x[k].x;
+                au += x[k].y * x[k].y;
+            }
+        }
+    }
+    for (; i < n2; i += st) {
+        const double2 y = v2[i];
+        av += y.x * y.x;
+        av += y.y * y.y;
+        if (!cached) {
+            const double2 x = u2[i];
+            au += x.x * x.x;
+            au += x.y * x.y;
+        }
+    }
+    if (VEC && (3 * nc) % 2 != 0 && blockIdx.x == 0 && threadIdx.x == 0) {  // odd length: last entry
+        const double y = v[3 * nc - 1];
+        av += y * y;
+        if (!cached) au += u[3 * nc - 1] * u[3 * nc - 1];
+    }
+    // block tree of norm_partials_kernel (residual.cu block_sum2): warp shuffles, then warp 0
+    // shuffles the 16 warp sums
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        au += __shfl_down_sync(0xffffffffu, au, o);
+        av += __shfl_down_sync(0xffffffffu, av, o);
+    }
+    const int wi = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh[2 * wi] = au;
+        sh[2 * wi + 1] = av;
+    }
+    __syncthreads();
+    if (wi == 0) {
+        au = l < kEpT / 32 ? sh[2 * l] : 0.0;
+        av = l < kEpT / 32 ? sh[2 * l + 1] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            au += __shfl_down_sync(0xffffffffu, au, o);
+            av += __shfl_down_sync(0xffffffffu, av, o);
+        }
+    }
+    __syncthreads();  // sh is reused below
+    if (threadIdx.x == 0) {
+        __stcg(&part[2 * blockIdx.x], au);
+        __stcg(&part[2 * blockIdx.x + 1], av);
+        // grid barrier (all CTAs are resident: the grid is sized to the occupancy)
+        __threadfence();
+        const unsigned long long old = atomicAdd(bar, 1ull);
+        const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
+        unsigned long long seen;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(bar) : "memory");
+        } while (seen < target);
+        __threadfence();
+    }
+    __syncthreads();
+    // perturb_kernel's final sum ran on 256-thread blocks: threads >= 256 contribute +0.0
+    // after the 8 warp sums, which leaves every value unchanged
+    const double eps = eps_from_partials(part, gridDim.x, u_norm, cached, sh, 256);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *eps_p = eps;
+        if (!cached) *u_norm = sh[2 * (kEpT >> 5) + 1];
+    }
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += st) {
+        const double x = u[3 * c] + eps * v[3 * c];
+        const double y = u[3 * c + 1] + eps * v[3 * c + 1];
+        const double z = u[3 * c + 2] + eps * v[3 * c + 2];
+        const unsigned long long pol = evict_last_policy();
+        double* r = wg + tiled(c, kWG);
+        st_keep(r, x, pol);
+        st_keep(r + 32, y, pol);
+        st_keep(r + 64, z, pol);
+    }
+    release_late();
+}
+
+// launch_norm_partials' grid, or 0 when it cannot be co-resident (then the two-launch path runs)
+int eps_perturb_grid(int nc) {
+    static int sms = -1, resident = 0;
+    if (sms < 0) {
+        int dev = 0, a = 0, b = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, eps_perturb_kernel<true>, kEpT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, eps_perturb_kernel<false>, kEpT, 0);
+        resident = std::min(a, b) * sms;
+    }
+    const int n = 3 * nc;
+    const int want = std::max(1, std::min(4 * std::max(1, std::min(sms, 148 * 2)), (n / 2 + kEpT - 1) / kEpT));
+    return want <= resident ? want : 0;
 }
 
 // ---------------------------------------------------------------- gradients
@@ -541,10 +678,18 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
               ErrWords* err, cudaStream_t st) {
     double* wg = ps.wg;
     const int cb = (m.nc + 255) / 256;
-    // with the ε reduction folded in, a grid of a few waves keeps the per-block partial sums cheap
-    const int pgrid = ps.partials ? std::min(cb, 148 * 8) : cb;
-    launch_win(perturb_kernel<PERT>, pgrid, 256, st, ps, m.nc, u, v, const_cast<double*>(eps), wg, ps.partials,
-               ps.npart, ps.u_norm, ps.u_norm_cached);
+    const int epg = PERT && ps.partials && ps.bar ? eps_perturb_grid(m.nc) : 0;
+    if (epg > 0) {  // ε reduction and w in one launch
+        const bool vec = ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+        launch_win(vec ? eps_perturb_kernel<true> : eps_perturb_kernel<false>, epg, kEpT, st, ps,
+                   m.nc, u, v, const_cast<double*>(eps), wg, const_cast<double*>(ps.partials), ps.u_norm,
+                   ps.u_norm_cached, ps.bar);
+    } else {
+        // with the ε reduction folded in, a grid of a few waves keeps the per-block partial sums cheap
+        const int pgrid = ps.partials ? std::min(cb, 148 * 8) : cb;
+        launch_win(perturb_kernel<PERT>, pgrid, 256, st, ps, m.nc, u, v, const_cast<double*>(eps), wg, ps.partials,
+                   ps.npart, ps.u_norm, ps.u_norm_cached);
+    }
     if (ps.marks) cudaEventRecord(ps.marks[0], st);
     const int nbf = m.nf - m.nint;
     if (nbf > 0 && ps.side) cudaEventRecord(ps.ev_w, st);  // w ready: the boundary pass may start
@@ -594,6 +739,8 @@ void launch_residual_pair(const DevMesh& m, const Physics& ph, const PatchTable&
         else launch_s<false, 8>(m, ph, pt, hist, u, v, jv_eps, r_u, out, ps, err, s);
     }
 }
+
+int eps_perturb_grid_for(int nc) { return eps_perturb_grid(nc); }
 
 void launch_gradients_pair(const DevMesh& m, const PatchTable& pt, const Physics& ph, const double* u, double* G,
                            const PairScratch& ps, ErrWords* err, cudaStream_t s) {

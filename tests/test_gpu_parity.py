@@ -266,3 +266,31 @@ def test_nan_and_inverted_errors():
     with pytest.raises(Exception) as e5:
         orc2.residual(u2)
     assert e4.value.kind == "InvertedElement" and e4.value.cell == e5.value.cell
+
+
+@pytest.mark.parametrize("n,odd", [(24, False), (13, True), (60, False)])
+def test_fused_eps_bitwise(n, odd, monkeypatch):
+    """The fused eps + perturb pass (default) reproduces the two-launch path (norm
+    partials, then perturb) bit for bit: eps, and with it J.v, every Krylov and Newton
+    decision.  Unaligned vectors (an odd offset into a buffer) take the scalar loads."""
+    sv = _sv()
+    import torch
+    case = cases.config("c2", n=n)
+    mesh = case.mesh()
+    u, v = cases.jv_inputs(mesh)
+    out = {}
+    for fused in ("0", "1"):
+        monkeypatch.setenv("SFV_EPS_FUSED", fused)
+        ev = sv.ResidualEvaluator(mesh, case.physics)
+        ev.set_time(1.0)
+        r_u = ev.residual(u)
+        if odd:  # vectors at an 8-byte (not 16-byte) aligned address
+            buf = torch.zeros(3 * 3 * mesh.n_cells + 3, dtype=torch.float64, device="cuda")
+            ud = buf[1:1 + 3 * mesh.n_cells]
+            ud.copy_(torch.as_tensor(u).cuda())
+            vd = buf[2 + 3 * mesh.n_cells:2 + 6 * mesh.n_cells]
+            vd.copy_(torch.as_tensor(v).cuda())
+            out[fused] = sv.jacobian_vector_product(ev, ud, r_u, vd).cpu().numpy()
+        else:
+            out[fused] = sv.jacobian_vector_product(ev, u, r_u, v).cpu().numpy()
+    assert np.array_equal(out["0"], out["1"])
