@@ -100,7 +100,9 @@ int sfv_check_errors(sfv_ctx* ctx, int* cell);
 /* Measurement only (bench.py): average device time in ms of each stage of `reps`
  * J.v calls, timed with CUDA events on the context stream: ms[0] |u|,|v| block partials
  * (0 when the reduction is fused into the next pass, the default), ms[1] eps + perturbed
- * state, ms[2] gradients, ms[3] boundary faces, ms[4] face fluxes + per-cell sums.  Returns SFV_ERR_INVALID_ARGUMENT unless the default (jv_pair.cu) path is active. */
+ * state, ms[2] gradients, ms[3] boundary faces (0 when the flux pass evaluates them: Hooke,
+ * small strain, no symmetry patch), ms[4] face fluxes + per-cell sums.  Returns
+ * SFV_ERR_INVALID_ARGUMENT unless the default (jv_pair.cu) path is active. */
 int sfv_jv_stage_times(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* v_dev,
                        double* out_dev, int reps, double* ms);
 /* The bytes each of those five stages moves at least once (its algorithmic traffic). */

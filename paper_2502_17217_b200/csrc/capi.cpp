@@ -327,6 +327,7 @@ std::string build_layout(sfv_ctx* c) {
         }
     }
     c->ps.bnd_cs = c->bnd_si.p;
+    for (int q = 0; q < c->pt.n; ++q) c->ps.sym = c->ps.sym || c->pt.kind[q] == SFV_PATCH_SYMMETRY;
     c->ps.bres = c->bres.p;
     return "";
 }
@@ -427,6 +428,11 @@ void launch_fused_pass(sfv_ctx* c, const Physics& ph, const double* u, const dou
     c->launches += 1;
 }
 
+// the default path runs boundary_kernel (else the flux pass evaluates the boundary faces)
+bool boundary_pass(const sfv_ctx* c) {
+    return c->dm.nf > c->dm.nint && (c->ph.law != SFV_LAW_HOOKE || c->ph.tl || c->ps.sym || c->ps.side);
+}
+
 void reset_err(sfv_ctx* c) { cudaMemsetAsync(c->err.p, 0x7f, sizeof(ErrWords), c->stream); }
 
 // read the error words (and optionally k doubles from hdev) in one D2H + sync
@@ -469,7 +475,7 @@ void residual_pass(sfv_ctx* c, const Physics& ph, const double* u, const double*
     }
     if (c->jv_path == 0) {
         launch_residual_pair(c->dm, ph, c->pt, c->hist, u, v, eps, r_u, out, c->ps, c->err.p, c->stream);
-        c->launches += c->dm.nf > c->dm.nint ? 4 : 3;
+        c->launches += boundary_pass(c) ? 4 : 3;
         return;
     }
     launch_residual(c->dm, ph, c->pt, c->hist, u, v, eps, r_u, out, c->grad.p, c->err.p, c->stream);
@@ -1302,8 +1308,9 @@ void sfv_jv_stage_bytes(const sfv_ctx* c, double* b) {
     b[0] = c->ps.bar ? 0.0 : 48.0 * nc;                     // u, v (fused into the next pass by default)
     b[1] = 72.0 * nc;                                       // u, v -> w
     b[2] = (4.0 * S + 24.0 * S + 24.0 + 72.0) * nc;         // slot_other, ls, w, G
-    b[3] = 208.0 * nb;                                      // slot, geometry, G, w -> 6 results
-    b[4] = (8.0 * S + 72.0 + 24.0 + 24.0 + 24.0) * nc + 72.0 * nf + 48.0 * nb + tr;  // slots, G, w, r_u, out, faces
+    const bool bp = boundary_pass(c);                       // else boundary faces are read by the flux pass
+    b[3] = bp ? 208.0 * nb : 0.0;                           // slot, geometry, G, w -> 6 results
+    b[4] = (8.0 * S + 72.0 + 24.0 + 24.0 + 24.0) * nc + 72.0 * nf + (bp ? 48.0 * nb : 0.0) + tr;  // slots, G, w, r_u, out, faces
 }
 
 int sfv_geometry(const sfv_ctx* c, double* volume, double* centroid, double* face_centroid, double* area, double* d,
@@ -1487,7 +1494,7 @@ int sfv_jv_stage_times(sfv_ctx* c, const double* u, const double* r_u, const dou
         }
     for (auto& e : ev) cudaEventDestroy(e);
     for (int k = 0; k < 5; ++k) ms[k] = acc[k] / reps;
-    c->launches += static_cast<long long>(reps) * ((c->dm.nf > c->dm.nint ? 4 : 3) + (c->ps.bar ? 0 : 1));
+    c->launches += static_cast<long long>(reps) * ((boundary_pass(c) ? 4 : 3) + (c->ps.bar ? 0 : 1));
     return c->cuda_check("jv_stage_times");
 }
 

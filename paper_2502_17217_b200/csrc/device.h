@@ -106,6 +106,7 @@ struct PairScratch {
     // set: eps_perturb_kernel reduces the norms itself (grid barrier on this counter) and
     // partials is only its scratch (>= 2 * eps_perturb grid doubles)
     unsigned long long* bar = nullptr;
+    bool sym = false;  // the mesh has a symmetry patch (boundary faces then need boundary_kernel)
     double* u_norm = nullptr;
     bool u_norm_cached = false;
     // L2 persisting window over [w | G]: both are gathered by the next pass,

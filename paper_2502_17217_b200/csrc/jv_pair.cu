@@ -475,7 +475,9 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
 // Face records (m.tf9): Gamma xyz, Delta xyz, |Delta| / |d|, |Gamma|, w (the two ratios are
 // the per-face constants of rhie_chow(), precomputed with the same IEEE operations).
 // kind of a slot's contribution: 0 none (padding), 1 flux only (traction), 2 flux + stabilisation
-template <bool PERT, int S, bool GEN>
+// INLB (Hooke, small strain, no symmetry patch): boundary faces are evaluated here, from the
+// cell's own gradient, instead of by boundary_kernel.
+template <bool PERT, int S, bool GEN, bool INLB>
 __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
     flux_pair_kernel(DevMesh m, Physics ph, PatchTable pt, History hist, const double* __restrict__ wg,
                      const double* __restrict__ eps_p, const double* __restrict__ sig,
@@ -555,6 +557,27 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
                     st = neg(st);
                 }
                 kd = 2;
+            } else if (INLB) {
+                // boundary face (boundary_kernel's operations): traction |Gamma| T
+                // (discretisation.cpp:151-154, no stabilisation term, :204-205), displacement
+                // Gamma . sigma_P and the Rhie-Chow term towards the prescribed value (:136-140, :189-193)
+                const int patch = -o - 2;
+                const d3 bc = {pt.value[patch][0], pt.value[patch][1], pt.value[patch][2]};
+                const double* rf = face_rec(m, f);
+                const double gmag = rf[224];
+                if (pt.kind[patch] == SFV_PATCH_TRACTION) {
+                    flux = scl(bc, gmag);
+                    st = {0.0, 0.0, 0.0};
+                    kd = 1;
+                } else {
+                    const double* rc = wg_rec(wg, c);
+                    const dm3 gc = ldG(rc);
+                    const d3 uc = ld3(rc);
+                    flux = dot_left(ld3(rf), hooke(gc, ph.mu, ph.lam));
+                    const d3 compact = scl(sub(bc, uc), rf[192]);
+                    st = scl(sub(compact, dot_left(ld3(rf + 96), gc)), ph.alpha * ph.kbar * gmag);
+                    kd = 2;
+                }
             } else {
                 // boundary face: evaluated by boundary_kernel; traction faces carry no
                 // stabilisation term (discretisation.cpp:204-205)
@@ -617,7 +640,7 @@ __global__ void untile_grad_kernel(int nc, const double* __restrict__ wg, double
     for (int q = 0; q < 9; ++q) G[static_cast<size_t>(q) * nc + c] = wg[tiled(c, kWG) + 32 * (3 + q)];
 }
 
-template <bool PERT, int S, bool GEN>
+template <bool PERT, int S, bool GEN, bool INLB>
 int flux_grid(int ntiles) {
     static int per_sm = -1;
     static int sms = 0;
@@ -625,7 +648,7 @@ int flux_grid(int ntiles) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flux_pair_kernel<PERT, S, GEN>, kCells * S, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flux_pair_kernel<PERT, S, GEN, INLB>, kCells * S, 0);
         per_sm = per_sm < 1 ? 1 : per_sm;
     }
     const int g = per_sm * sms;
@@ -697,7 +720,8 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     launch_grad<S>(m, ph, pt, ps, err, st);
     if (ps.marks) cudaEventRecord(ps.marks[1], st);
     const double* no_eps = nullptr;
-    if (nbf > 0) {
+    const bool inlb = !gen && !ps.sym && !ps.side;  // boundary faces inside the flux pass
+    if (nbf > 0 && !inlb) {
         if (ps.side) {  // beside the gradient pass: the boundary pass computes its own cells' gradients
             cudaStreamWaitEvent(ps.side, ps.ev_w, 0);
             boundary_kernel<<<(nbf + 127) / 128, 128, 0, ps.side>>>(m, ph, pt, ps.bnd_cs, wg, PERT ? eps : no_eps,
@@ -712,14 +736,17 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     if (ps.marks) cudaEventRecord(ps.marks[2], st);
     const int ntiles = (m.nc + kCells - 1) / kCells;
     const double* cwg = wg;
+    const double* sg = ps.sig;
+    const double* br = ps.bres;
     if (gen)
-        launch_win(flux_pair_kernel<PERT, S, true>, flux_grid<PERT, S, true>(ntiles), kCells * S, st, ps, m, ph, pt,
-                   hist, cwg, eps, static_cast<const double*>(ps.sig), static_cast<const double*>(ps.bres), r_u, out,
-                   err);
+        launch_win(flux_pair_kernel<PERT, S, true, false>, flux_grid<PERT, S, true, false>(ntiles), kCells * S, st,
+                   ps, m, ph, pt, hist, cwg, eps, sg, br, r_u, out, err);
+    else if (inlb)
+        launch_win(flux_pair_kernel<PERT, S, false, true>, flux_grid<PERT, S, false, true>(ntiles), kCells * S, st,
+                   ps, m, ph, pt, hist, cwg, eps, sg, br, r_u, out, err);
     else
-        launch_win(flux_pair_kernel<PERT, S, false>, flux_grid<PERT, S, false>(ntiles), kCells * S, st, ps, m, ph,
-                   pt, hist, cwg, eps, static_cast<const double*>(ps.sig), static_cast<const double*>(ps.bres), r_u,
-                   out, err);
+        launch_win(flux_pair_kernel<PERT, S, false, false>, flux_grid<PERT, S, false, false>(ntiles), kCells * S, st,
+                   ps, m, ph, pt, hist, cwg, eps, sg, br, r_u, out, err);
 }
 
 }  // namespace
