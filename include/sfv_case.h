@@ -26,7 +26,7 @@ extern "C" {
 enum { SFV_PATCH_DISPLACEMENT = 0, SFV_PATCH_TRACTION = 1, SFV_PATCH_SYMMETRY = 2 };
 
 /* constitutive laws on the hot path (laws.hpp:95, :117) */
-enum { SFV_LAW_HOOKE = 0, SFV_LAW_NEO_HOOKEAN = 1 };
+enum { SFV_LAW_HOOKE = 0, SFV_LAW_NEO_HOOKEAN = 1, SFV_LAW_STVK = 2, SFV_LAW_GUCCIONE = 3 };
 
 /* PreconditionerKind (nonlinear.hpp:18) */
 enum {
@@ -89,6 +89,8 @@ typedef struct sfv_physics {
     double rho;
     const double* bc_value; /* 3 * n_patches; unused for symmetry patches */
     const int* bc_ramp;     /* n_patches; value * t when nonzero */
+    /* SFV_LAW_GUCCIONE (GuccioneParams, laws.hpp:38-43): C, c_f, c_t, c_fs, kappa, f0 xyz */
+    double guccione[8];
 } sfv_physics;
 
 typedef struct sfv_solver_cfg {

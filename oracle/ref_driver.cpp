@@ -228,10 +228,17 @@ void* ref_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, int 
         rc->mesh = mesh_from_desc(md);
         rc->geom = compute_geometry(rc->mesh);
         std::shared_ptr<MechanicalLaw> law;
-        if (ph->law == SFV_LAW_NEO_HOOKEAN)
+        if (ph->law == SFV_LAW_NEO_HOOKEAN) {
             law = std::make_shared<NeoHookeanLaw>(ph->mu, ph->lambda);
-        else
+        } else if (ph->law == SFV_LAW_STVK) {
+            law = std::make_shared<StVenantKirchhoffLaw>(ph->mu, ph->lambda);
+        } else if (ph->law == SFV_LAW_GUCCIONE) {
+            const double* q = ph->guccione;
+            GuccioneParams gp{q[0], q[1], q[2], q[3], q[4], Vec3{q[5], q[6], q[7]}};
+            law = std::make_shared<GuccioneLaw>(gp);
+        } else {
             law = std::make_shared<HookeLaw>(ph->mu, ph->lambda);
+        }
         BoundaryConditions bcs;
         for (int p = 0; p < md->n_patches; ++p) {
             const Vec3 v{ph->bc_value[3 * p], ph->bc_value[3 * p + 1], ph->bc_value[3 * p + 2]};

@@ -169,6 +169,7 @@ struct orc_case {
     /* physics */
     int law;
     double mu, lam;
+    double gc[8]; /* Guccione: C, c_f, c_t, c_fs, kappa, f0 */
     double alpha;
     int tl, transient;
     double dt, rho;
@@ -420,6 +421,7 @@ orc_case* orc_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* errbu
         return NULL;
     }
     h->law = ph->law;
+    for (int k = 0; k < 8; ++k) h->gc[k] = ph->guccione[k];
     h->mu = ph->mu;
     h->lam = ph->lambda;
     h->alpha = ph->alpha;
@@ -563,6 +565,53 @@ static int neo_hookean(m3 g, double mu, double kappa, m3* out) {
     return 1;
 }
 
+/* kinematics E (laws.cpp:15): 0.5 * (G + G^T + G G^T) */
+static m3 green_strain(m3 g) { return mscale(madd(madd(g, mtrans(g)), mmul(g, mtrans(g))), 0.5); }
+static double mddot(m3 a, m3 b) { /* types.hpp:158-164 */
+    double s = 0.0;
+    for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) s += a.m[i][j] * b.m[i][j];
+    return s;
+}
+
+/* stvk_stress (laws.cpp:29-37); returns 0 on det F <= 0 */
+static int stvk(m3 g, double mu, double lam, m3* out) {
+    const m3 F = madd(mident(), mtrans(g));
+    const double J = mdet(F);
+    if (!(J > 0.0)) return 0;
+    const m3 E = green_strain(g);
+    m3 S = mscale(E, 2.0 * mu);
+    const double t = lam * mtrace(E);
+    S.m[0][0] += t; S.m[1][1] += t; S.m[2][2] += t;
+    *out = mscale(mmul(mmul(F, S), mtrans(F)), 1.0 / J);
+    return 1;
+}
+
+/* guccione_stress with guccione_Q / guccione_dQ_dE (laws.cpp:49-77); gc = C, c_f, c_t, c_fs,
+ * kappa, f0 xyz.  Returns 1 ok, 0 det F <= 0 (InvertedElement), -1 exponent overflow
+ * (LawOverflow: Q > 500 or not finite). */
+static int guccione(m3 g, const double* gc, m3* out) {
+    const m3 F = madd(mident(), mtrans(g));
+    const double J = mdet(F);
+    if (!(J > 0.0)) return 0;
+    const m3 E = green_strain(g);
+    const double C = gc[0], cf = gc[1], ct = gc[2], cfs = gc[3], kappa = gc[4];
+    const v3 f0 = {gc[5], gc[6], gc[7]};
+    const m3 ff = outer(f0, f0);
+    const double i1 = mtrace(E);
+    const double i2 = 0.5 * (i1 * i1 - mtrace(mmul(E, E)));
+    const double i4 = mddot(E, ff);
+    const double i5 = mddot(mmul(E, E), ff);
+    const double Q = ct * i1 * i1 - 2.0 * ct * i2 + (cf - 2.0 * cfs + ct) * i4 * i4 + 2.0 * (cfs - ct) * i5;
+    if (Q > 500.0 || !isfinite(Q)) return -1;
+    const m3 dq = madd(madd(mscale(E, 2.0 * ct), mscale(ff, 2.0 * (cf - 2.0 * cfs + ct) * i4)),
+                       mscale(madd(mmul(E, ff), mmul(ff, E)), 2.0 * (cfs - ct)));
+    m3 S = mscale(dq, 0.5 * C * exp(Q));
+    const double pen = 0.5 * kappa * (J * J - 1.0) / J;
+    S.m[0][0] += pen; S.m[1][1] += pen; S.m[2][2] += pen;
+    *out = mscale(mmul(mmul(F, S), mtrans(F)), 1.0 / J);
+    return 1;
+}
+
 /* rhie_chow_face (discretisation.cpp:33-37) */
 static v3 rhie_chow(v3 up, v3 uo, m3 gf, v3 delta, double d_mag, double area_mag, double alpha,
                     double kbar) {
@@ -578,8 +627,10 @@ static int transform_area(v3 gamma, m3 ff, v3* out) {
     return 1;
 }
 
-static double kbar_of(const orc_case* h) { /* laws.hpp:100, :122 */
-    return h->law == SFV_LAW_NEO_HOOKEAN ? 4.0 / 3.0 * h->mu + h->lam : 2.0 * h->mu + h->lam;
+static double kbar_of(const orc_case* h) { /* laws.hpp:100, :111, :122, :133 */
+    if (h->law == SFV_LAW_NEO_HOOKEAN) return 4.0 / 3.0 * h->mu + h->lam;
+    if (h->law == SFV_LAW_GUCCIONE) return 4.0 / 3.0 * (h->gc[0] * h->gc[2]) + h->gc[4];
+    return 2.0 * h->mu + h->lam;
 }
 
 /* add_stabilisation (discretisation.cpp:176-208) */
@@ -626,6 +677,13 @@ static int residual(orc_case* h, const v3* u, v3* r) {
         if (h->law == SFV_LAW_NEO_HOOKEAN) {
             if (!neo_hookean(h->grad[c], h->mu, h->lam, &h->sigma[c]))
                 return fail(&h->err, SFV_ERR_INVERTED_ELEMENT, c, "kinematics: det F <= 0");
+        } else if (h->law == SFV_LAW_STVK) {
+            if (!stvk(h->grad[c], h->mu, h->lam, &h->sigma[c]))
+                return fail(&h->err, SFV_ERR_INVERTED_ELEMENT, c, "kinematics: det F <= 0");
+        } else if (h->law == SFV_LAW_GUCCIONE) {
+            const int k = guccione(h->grad[c], h->gc, &h->sigma[c]);
+            if (k == 0) return fail(&h->err, SFV_ERR_INVERTED_ELEMENT, c, "kinematics: det F <= 0");
+            if (k < 0) return fail(&h->err, SFV_ERR_LAW_OVERFLOW, c, "guccione_stress: exponent overflow");
         } else {
             h->sigma[c] = hooke(h->grad[c], h->mu, h->lam);
         }

@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 PATCH_DISPLACEMENT, PATCH_TRACTION, PATCH_SYMMETRY = 0, 1, 2
-LAW_HOOKE, LAW_NEO_HOOKEAN = 0, 1
+LAW_HOOKE, LAW_NEO_HOOKEAN, LAW_STVK, LAW_GUCCIONE = 0, 1, 2, 3
 PRECOND = {"auto": 0, "none": 1, "ilu0": 2, "ilu1": 3, "ilu2": 4, "lu": 5}
 CONVERGED, DIVERGED, MAX_ITERS = 0, 1, 2
 STATUS_NAME = {CONVERGED: "converged", DIVERGED: "diverged", MAX_ITERS: "max-iters"}
@@ -70,6 +70,7 @@ class PhysicsDesc(C.Structure):
         ("rho", C.c_double),
         ("bc_value", _dp),
         ("bc_ramp", _ip),
+        ("guccione", C.c_double * 8),
     ]
 
 
@@ -202,6 +203,8 @@ class Physics:
     rho: float = 0.0
     bc_value: np.ndarray = None  # (n_patches, 3)
     bc_ramp: np.ndarray = None  # (n_patches,)
+    # GuccioneParams (laws.hpp:38-43): C, c_f, c_t, c_fs, kappa, f0 (3)
+    guccione: tuple = (0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0)
     _keep: list = field(default_factory=list, repr=False)
 
     def desc(self) -> PhysicsDesc:
@@ -219,13 +222,18 @@ class Physics:
         p.rho = float(self.rho)
         p.bc_value = dptr(bv)
         p.bc_ramp = iptr(br)
+        for k, x in enumerate(self.guccione):
+            p.guccione[k] = float(x)
         return p
 
     @property
     def kbar(self) -> float:
-        """law.stabilisation_modulus() (laws.hpp:100, :122)."""
+        """law.stabilisation_modulus() (laws.hpp:100, :111, :122, :133)."""
         if self.law == LAW_NEO_HOOKEAN:
             return 4.0 / 3.0 * self.mu + self.lam
+        if self.law == LAW_GUCCIONE:
+            g = self.guccione
+            return 4.0 / 3.0 * (g[0] * g[2]) + g[4]
         return 2.0 * self.mu + self.lam
 
 

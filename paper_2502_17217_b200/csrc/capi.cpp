@@ -448,6 +448,10 @@ int fetch(sfv_ctx* c, int k) {
 // would raise them (stress loop, then face loop, then the NaN scan).
 int decode_residual_errors(sfv_ctx* c, bool jv) {
     const ErrWords& e = c->st->err;
+    // the stress loop throws at the first failing cell: LawOverflow there if it comes first
+    if (e.overflow_cell != kNone && e.overflow_cell < e.inverted_cell)
+        return jv ? c->fail(SFV_ERR_JVP_NAN, -1, "jvp: guccione_stress: exponent overflow")
+                  : c->fail(SFV_ERR_LAW_OVERFLOW, e.overflow_cell, "guccione_stress: exponent overflow");
     if (e.inverted_cell != kNone)
         return jv ? c->fail(SFV_ERR_JVP_NAN, -1, "jvp: kinematics: det F <= 0")
                   : c->fail(SFV_ERR_INVERTED_ELEMENT, e.inverted_cell, "kinematics: det F <= 0");
@@ -1226,7 +1230,12 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     p.mu = ph->mu;
     p.lam = ph->lambda;
     p.alpha = ph->alpha;
-    p.kbar = ph->law == SFV_LAW_NEO_HOOKEAN ? 4.0 / 3.0 * ph->mu + ph->lambda : 2.0 * ph->mu + ph->lambda;
+    if (ph->law < SFV_LAW_HOOKE || ph->law > SFV_LAW_GUCCIONE) return fail("law: unknown constitutive law");
+    for (int k = 0; k < 8; ++k) p.gc[k] = ph->guccione[k];
+    // MechanicalLaw::stabilisation_modulus (laws.hpp:100, :111, :122, :133)
+    p.kbar = ph->law == SFV_LAW_NEO_HOOKEAN ? 4.0 / 3.0 * ph->mu + ph->lambda
+             : ph->law == SFV_LAW_GUCCIONE  ? 4.0 / 3.0 * (ph->guccione[0] * ph->guccione[2]) + ph->guccione[4]
+                                            : 2.0 * ph->mu + ph->lambda;
     p.rho = ph->rho;
     p.dt = ph->dt;
     c->pt.n = md->n_patches;
@@ -1238,6 +1247,8 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
         const std::string js(j);
         c->jv_path = js == "fused" ? 1 : js == "twopass" ? 2 : 0;
     }
+    if (ph->law >= SFV_LAW_STVK && c->jv_path != 0)
+        return fail("law: St. Venant-Kirchhoff and Guccione run on the default J.v path only");
     e = build_layout(c.get());
     if (!e.empty()) return fail(e);
     pt.mark("device layout + upload");

@@ -55,7 +55,7 @@ __host__ __device__ __forceinline__ size_t tiled(int c, int nq) {
     return static_cast<size_t>(c >> kTileShift) * (static_cast<size_t>(nq) << kTileShift) + (c & 31);
 }
 constexpr int kWG = 12;   // rows of the tiled [w | G] record: w xyz, then G row-major
-constexpr int kSig = 6;   // rows of the tiled cell-stress record
+constexpr int kSig = 9;   // rows of the tiled cell-stress record (row-major, nothing mirrored)
 
 struct Physics {
     int law;  // SFV_LAW_*
@@ -64,6 +64,7 @@ struct Physics {
     double mu, lam, alpha, kbar;
     double rho, dt;
     int stab_only;  // ResidualEvaluator::stabilisation (discretisation.cpp:210-214)
+    double gc[8];   // Guccione: C, c_f, c_t, c_fs, kappa, f0 xyz (GuccioneParams, laws.hpp:38-43)
 };
 
 // Error words written by kernels (atomicMin of the first offending index; INT_MAX = none).
@@ -72,6 +73,7 @@ struct ErrWords {
     int inverted_face;  // transform_area: det F_f <= 0 (discretisation.cpp:102)
     int nan_cell;       // residual: non-finite entry (discretisation.cpp:171-172)
     int nan_jv;         // J.v: non-finite difference quotient (nonlinear.cpp:135)
+    int overflow_cell;  // law stress: Guccione exponent overflow (laws.cpp:69-70)
 };
 
 // History for the BDF2 inertia term (interleaved [3c+k]).
@@ -92,7 +94,7 @@ void launch_residual(const DevMesh& m, const Physics& ph, const PatchTable& pt, 
 // per-(cell, face slot) flux kernels
 struct PairScratch {
     double* wg = nullptr;           // tiled [w | G] (kWG rows): perturbed state u + eps v, cell gradients
-    double* sig = nullptr;          // tiled cell stress (xx, xy, xz, yy, yz, zz), non-Hooke / TL only
+    double* sig = nullptr;          // tiled cell stress (9 entries, row-major), non-Hooke / TL only
     const int* bnd_cs = nullptr;    // [nf-nint] cell * 8 + slot of boundary face nint+fb
     double* bres = nullptr;       // [6*(nf-nint)] boundary-face flux + stabilisation
     cudaEvent_t* marks = nullptr;  // optional: recorded after the perturb, gradient, boundary passes

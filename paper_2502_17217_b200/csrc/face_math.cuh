@@ -146,10 +146,82 @@ __device__ __forceinline__ dm3 neo_hookean(const dm3& g, double mu, double kappa
     s.a[2][2] += p;
     return s;
 }
+// Green-Lagrange strain of kinematics() (laws.cpp:9-18): 0.5 ((G + G^T) + G G^T)
+__device__ __forceinline__ dm3 green_strain(const dm3& g) { return mscl(madd(madd(g, mtr(g)), mmul(g, mtr(g))), 0.5); }
+__device__ __forceinline__ double trc(const dm3& a) { return (a.a[0][0] + a.a[1][1]) + a.a[2][2]; }
+// A : B, row by row (types.hpp ddot)
+__device__ __forceinline__ double ddot(const dm3& a, const dm3& b) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s += a.a[i][j] * b.a[i][j];
+    return s;
+}
+// St. Venant-Kirchhoff, Cauchy stress (laws.cpp:29-37): (1/J) F S F^T, S = 2 mu E + lambda tr(E) I
+__device__ __forceinline__ dm3 stvk(const dm3& g, double mu, double lam, bool& ok) {
+    const dm3 F = defgrad(g);
+    const double J = det(F);
+    ok = J > 0.0;
+    const dm3 E = green_strain(g);
+    dm3 S = mscl(E, 2.0 * mu);
+    const double t = lam * trc(E);
+    S.a[0][0] += t;
+    S.a[1][1] += t;
+    S.a[2][2] += t;
+    return mscl(mmul(mmul(F, S), mtr(F)), 1.0 / J);
+}
+// Guccione (laws.cpp:49-77); gc = C, c_f, c_t, c_fs, kappa, f0 xyz.  code: 0 ok, 1 det F <= 0,
+// 2 exponent overflow (Q > 500 or not finite, LawOverflow)
+__device__ __forceinline__ dm3 guccione(const dm3& g, const double* gc, int& code) {
+    const dm3 F = defgrad(g);
+    const double J = det(F);
+    code = J > 0.0 ? 0 : 1;
+    const dm3 E = green_strain(g);
+    const double C = gc[0], cf = gc[1], ct = gc[2], cfs = gc[3], kappa = gc[4];
+    const double f0[3] = {gc[5], gc[6], gc[7]};
+    dm3 ff;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) ff.a[i][j] = f0[i] * f0[j];
+    const dm3 EE = mmul(E, E);
+    const double i1 = trc(E);
+    const double i2 = 0.5 * (i1 * i1 - trc(EE));
+    const double i4 = ddot(E, ff);
+    const double i5 = ddot(EE, ff);
+    const double cq = (cf - 2.0 * cfs) + ct;
+    const double Q = (((ct * i1) * i1 - (2.0 * ct) * i2) + (cq * i4) * i4) + (2.0 * (cfs - ct)) * i5;
+    if (code == 0 && (Q > 500.0 || !isfinite(Q))) code = 2;
+    // guccione_dQ_dE: 2 c_t E + (2 cq i4) ff + 2 (c_fs - c_t) (E ff + ff E)
+    const dm3 dq = madd(madd(mscl(E, 2.0 * ct), mscl(ff, (2.0 * cq) * i4)),
+                        mscl(madd(mmul(E, ff), mmul(ff, E)), 2.0 * (cfs - ct)));
+    dm3 S = mscl(dq, (0.5 * C) * exp(Q));
+    const double pen = ((0.5 * kappa) * (J * J - 1.0)) / J;
+    S.a[0][0] += pen;
+    S.a[1][1] += pen;
+    S.a[2][2] += pen;
+    return mscl(mmul(mmul(F, S), mtr(F)), 1.0 / J);
+}
+// the law's Cauchy stress; code 0 ok, 1 inverted (det F <= 0), 2 exponent overflow
+__device__ __forceinline__ dm3 stress_code(const Physics& ph, const dm3& g, int& code) {
+    bool ok = true;
+    dm3 s;
+    code = 0;
+    switch (ph.law) {
+        case SFV_LAW_NEO_HOOKEAN: s = neo_hookean(g, ph.mu, ph.lam, ok); break;
+        case SFV_LAW_STVK: s = stvk(g, ph.mu, ph.lam, ok); break;
+        case SFV_LAW_GUCCIONE: return guccione(g, ph.gc, code);
+        default: return hooke(g, ph.mu, ph.lam);
+    }
+    code = ok ? 0 : 1;
+    return s;
+}
 __device__ __forceinline__ dm3 stress(const Physics& ph, const dm3& g, bool& ok) {
-    if (ph.law == SFV_LAW_NEO_HOOKEAN) return neo_hookean(g, ph.mu, ph.lam, ok);
-    ok = true;
-    return hooke(g, ph.mu, ph.lam);
+    int code;
+    const dm3 s = stress_code(ph, g, code);
+    ok = code == 0;
+    return s;
 }
 // Rhie-Chow term (discretisation.cpp:176-208)
 __device__ __forceinline__ d3 rhie_chow(d3 up, d3 uo, const dm3& gf, d3 delta, double d_mag, double area_mag,

@@ -77,15 +77,12 @@ __device__ __forceinline__ void release_late() {
     if (!SFV_PDL_EARLY) release_dependents();
 }
 
-// symmetric cell stress from its 6 stored entries (grad_cell_kernel<S, true>), tiled record
+// cell stress, all 9 entries (grad_cell_kernel<S, true>), tiled record: F S F^T of St.
+// Venant-Kirchhoff / Guccione is symmetric only up to rounding, so nothing is mirrored
 __device__ __forceinline__ dm3 ld_sig(const double* __restrict__ r) {
     dm3 a;
-    a.a[0][0] = r[0];
-    a.a[0][1] = a.a[1][0] = r[32];
-    a.a[0][2] = a.a[2][0] = r[64];
-    a.a[1][1] = r[96];
-    a.a[1][2] = a.a[2][1] = r[128];
-    a.a[2][2] = r[160];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) a.a[q / 3][q % 3] = r[32 * q];
     return a;
 }
 
@@ -307,9 +304,8 @@ int eps_perturb_grid(int nc) {
 // (discretisation.cpp:10-31: g += ls_f (x) (u_N - u_P), faces in cell order)
 // GEN (non-Hooke law or total Lagrangian): the cell's stress sigma(G_c) is evaluated here
 // once (laws.cpp; the stress loop of discretisation.cpp:116-119, which also reports an
-// inverted cell) and stored as its 6 independent entries, instead of twice per face in
-// the flux pass — same function on the same G, so the same bits (sigma is symmetric
-// bitwise: every entry pair is a product sum of the same factors).
+// inverted cell, or the Guccione exponent overflow) and stored, instead of twice per face
+// in the flux pass — same function on the same G, so the same bits.
 template <int S, bool GEN>
 __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt, Physics ph, double* __restrict__ wg,
                                                         double* __restrict__ sig, ErrWords* __restrict__ err) {
@@ -354,16 +350,13 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
         dm3 gm;
 #pragma unroll
         for (int q = 0; q < 9; ++q) gm.a[q / 3][q % 3] = g[q];
-        bool ok;
-        const dm3 sc = stress(ph, gm, ok);
-        if (!ok) atomicMin(&err->inverted_cell, c);
+        int code;
+        const dm3 sc = stress_code(ph, gm, code);
+        if (code == 1) atomicMin(&err->inverted_cell, c);
+        if (code == 2) atomicMin(&err->overflow_cell, c);
         double* rs = sig + tiled(c, kSig);
-        st_keep(rs, sc.a[0][0], pol);
-        st_keep(rs + 32, sc.a[0][1], pol);
-        st_keep(rs + 64, sc.a[0][2], pol);
-        st_keep(rs + 96, sc.a[1][1], pol);
-        st_keep(rs + 128, sc.a[1][2], pol);
-        st_keep(rs + 160, sc.a[2][2], pol);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) st_keep(rs + 32 * q, sc.a[q / 3][q % 3], pol);
     }
     release_late();
 }

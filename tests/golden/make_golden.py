@@ -20,8 +20,9 @@ sys.path.insert(0, ROOT)
 
 from oracle.bind import RefCase, ref_box_mesh  # noqa: E402
 from paper_2502_17217_b200 import cases  # noqa: E402
-from paper_2502_17217_b200.abi import (LAW_HOOKE, LAW_NEO_HOOKEAN, PATCH_DISPLACEMENT as D, PATCH_SYMMETRY as S,  # noqa: E402
-                                       PATCH_TRACTION as T, Mesh, Physics, solver_cfg)
+from paper_2502_17217_b200.abi import (LAW_GUCCIONE, LAW_HOOKE, LAW_NEO_HOOKEAN, LAW_STVK,  # noqa: E402
+                                       PATCH_DISPLACEMENT as D, PATCH_SYMMETRY as S, PATCH_TRACTION as T, Mesh,
+                                       Physics, solver_cfg)
 
 CASES = {
     "hex_hooke": dict(mesh=((1.0, 1.2, 0.8), (6, 5, 4), [D, T, T, T, T, T], 0.15, 42), law=LAW_HOOKE),
@@ -31,7 +32,14 @@ CASES = {
     "hex_transient": dict(mesh=((1.0, 1.0, 1.0), (5, 5, 5), [D, T, T, T, T, T], 0.15, 42), law=LAW_HOOKE,
                           transient=True),
     "tets": dict(tets=4, law=LAW_HOOKE),
+    # the remaining hyperelastic laws on the same residual
+    "hex_stvk": dict(mesh=((4.0, 1.0, 1.0), (12, 4, 4), [D, D, T, T, T, T], 0.05, 42), law=LAW_STVK, disp=0.3),
+    "hex_guccione_tl": dict(mesh=((4.0, 1.0, 1.0), (12, 4, 4), [D, D, T, T, T, T], 0.05, 42), law=LAW_GUCCIONE,
+                            tl=True, disp=0.02),
 }
+# GuccioneParams of the reference's own law test (test_laws.cpp:170-175): f0 = Vec3{1, 2, 2} / 3,
+# which types.hpp evaluates as a multiplication by (1.0 / 3.0)
+GUCCIONE = (10e3, 8.0, 2.0, 4.0, 50e3, 1.0 * (1.0 / 3.0), 2.0 * (1.0 / 3.0), 2.0 * (1.0 / 3.0))
 
 
 def physics(spec, npatch):
@@ -42,10 +50,10 @@ def physics(spec, npatch):
         mu, lam = cases.mu_from(200e9, 0.3), cases.lambda_from(200e9, 0.3)
     else:
         mu, lam = 0.4e6, 2e6
-        bv[1] = (0.3, 0.0, 0.0)  # prescribed displacement on xmax (C3 style)
+        bv[1] = (spec.get("disp", 0.3), 0.0, 0.0)  # prescribed displacement on xmax (C3 style)
     return Physics(spec["law"], mu, lam, total_lagrangian=spec.get("tl", False),
                    transient=spec.get("transient", False), dt=1e-5, rho=7800.0, bc_value=bv,
-                   bc_ramp=np.ones(npatch, dtype=np.int32))
+                   bc_ramp=np.ones(npatch, dtype=np.int32), guccione=GUCCIONE)
 
 
 def mesh_for(spec) -> Mesh:
@@ -56,13 +64,16 @@ def mesh_for(spec) -> Mesh:
 
 
 def main():
+    only = set(sys.argv[1:])
     for name, spec in CASES.items():
+        if only and name not in only:
+            continue
         m = mesh_for(spec)
         ph = physics(spec, len(m.patch_kind))
         ref = RefCase(m, ph)
         ref.set_time(0.7)
         u, v = cases.jv_inputs(m, seed=13)
-        if spec["law"] == LAW_NEO_HOOKEAN:
+        if spec["law"] != LAW_HOOKE:
             u = u * 1e4
         rng = np.random.default_rng(7)
         hist = np.zeros((4, 3 * m.n_cells))
@@ -76,7 +87,7 @@ def main():
                    neighbour=m.neighbour, n_cells=m.n_cells, n_internal=m.n_internal, patch_kind=m.patch_kind,
                    patch_start=m.patch_start, patch_count=m.patch_count, law=ph.law, mu=ph.mu, lam=ph.lam,
                    tl=int(ph.total_lagrangian), transient=int(ph.transient), dt=ph.dt, rho=ph.rho,
-                   bc_value=ph.bc_value, bc_ramp=ph.bc_ramp, time=0.7, u=u, v=v, hist=hist, residual=r, jv=jv,
+                   bc_value=ph.bc_value, bc_ramp=ph.bc_ramp, guccione=np.array(ph.guccione), time=0.7, u=u, v=v, hist=hist, residual=r, jv=jv,
                    stabilisation=stab)
         zin = cases.uniform(21, 3 * m.n_cells)
         if not (m.patch_kind == S).any():
@@ -98,6 +109,7 @@ def main():
         out["steps_krylov"] = np.array([sum(r.summary()["krylov_per_newton"]) for r in reps])
         out["steps_newton"] = np.array([r.outer_iters for r in reps])
         out["steps_status"] = np.array([r.status for r in reps])
+        out["steps_n"] = steps
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
         print(name, m.n_cells, "cells", "newton", out["steps_newton"], "krylov", out["steps_krylov"])
 

@@ -20,6 +20,8 @@ def load(path):
     ph = Physics(int(z["law"]), float(z["mu"]), float(z["lam"]), total_lagrangian=bool(z["tl"]),
                  transient=bool(z["transient"]), dt=float(z["dt"]), rho=float(z["rho"]), bc_value=z["bc_value"],
                  bc_ramp=z["bc_ramp"])
+    if "guccione" in z:
+        ph.guccione = tuple(float(x) for x in z["guccione"])
     return z, m, ph
 
 
@@ -46,7 +48,8 @@ def test_oracle_matches_reference_golden(path):
     lu = o.precond_apply(z["lu_in"])
     assert np.linalg.norm(lu - z["lu_out"]) <= 1e-12 * np.linalg.norm(z["lu_out"])
     o2 = OracleCase(m, ph)
-    f, reps, _ = o2.run_steps(z["steps_field0"], solver_cfg(r_tol=1e-8), len(z["steps_newton"]))
+    nsteps = int(z["steps_n"]) if "steps_n" in z else len(z["steps_newton"])
+    f, reps, _ = o2.run_steps(z["steps_field0"], solver_cfg(r_tol=1e-8), nsteps)
     assert [r.outer_iters for r in reps] == list(z["steps_newton"])
     assert [sum(r.summary()["krylov_per_newton"]) for r in reps] == list(z["steps_krylov"])
     assert np.abs(f - z["steps_field"]).max() <= 1e-12 * max(np.abs(z["steps_field"]).max(), 1e-300)
@@ -63,7 +66,9 @@ def test_gpu_matches_reference_golden(path):
         ev.set_history(*z["hist"])
     u, v = z["u"], z["v"]
     r = ev.residual(u).cpu().numpy()
-    tol = 0.0 if ph.law == 0 else 1e-12  # neo-Hookean: pow() is not correctly rounded
+    # neo-Hookean: pow(), Guccione: exp() are not correctly rounded on either side; Hooke and
+    # St. Venant-Kirchhoff are +, -, *, / only and bit-identical
+    tol = 0.0 if ph.law in (0, 2) else 1e-12
     assert np.abs(r - z["residual"]).max() <= tol * np.abs(z["residual"]).max()
     jv = sv.jacobian_vector_product(ev, u, z["residual"], v).cpu().numpy()
     assert np.linalg.norm(jv - z["jv"]) <= 1e-6 * np.linalg.norm(z["jv"])
@@ -79,7 +84,8 @@ def test_gpu_matches_reference_golden(path):
     lu = pc.solve(z["lu_in"]).cpu().numpy()
     assert np.linalg.norm(lu - z["lu_out"]) <= 1e-10 * np.linalg.norm(z["lu_out"])
     ev2 = sv.ResidualEvaluator(m, ph)
-    f, reps, _ = sv.run_steps(ev2, z["steps_field0"], solver_cfg(r_tol=1e-8), len(z["steps_newton"]))
+    nsteps = int(z["steps_n"]) if "steps_n" in z else len(z["steps_newton"])
+    f, reps, _ = sv.run_steps(ev2, z["steps_field0"], solver_cfg(r_tol=1e-8), nsteps)
     assert [r.outer_iters for r in reps] == list(z["steps_newton"])
     for rep, b in zip(reps, z["steps_krylov"]):
         a = sum(rep.summary()["krylov_per_newton"])

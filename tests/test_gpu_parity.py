@@ -7,8 +7,8 @@ import pytest
 
 from oracle.bind import OracleCase
 from paper_2502_17217_b200 import cases
-from paper_2502_17217_b200.abi import (LAW_HOOKE, LAW_NEO_HOOKEAN, PATCH_DISPLACEMENT as D, PATCH_SYMMETRY as S,
-                                       PATCH_TRACTION as T, Physics, solver_cfg)
+from paper_2502_17217_b200.abi import (LAW_GUCCIONE, LAW_HOOKE, LAW_NEO_HOOKEAN, LAW_STVK, PATCH_DISPLACEMENT as D,
+                                       PATCH_SYMMETRY as S, PATCH_TRACTION as T, Physics, solver_cfg)
 
 pytestmark = pytest.mark.gpu
 
@@ -36,7 +36,14 @@ def _phys(law=LAW_HOOKE, tl=False, transient=False, npatch=6, **kw):
     else:
         mu, lam = 0.4e6, 2e6
     return Physics(law, mu, lam, total_lagrangian=tl, transient=transient, dt=1e-5, rho=7800.0, bc_value=bv,
-                   bc_ramp=np.ones(npatch, dtype=np.int32), **kw)
+                   bc_ramp=np.ones(npatch, dtype=np.int32), guccione=GUCCIONE, **kw)
+
+
+# GuccioneParams of the reference's law test (test_laws.cpp:170-175), f0 = Vec3{1, 2, 2} / 3
+GUCCIONE = (10e3, 8.0, 2.0, 4.0, 50e3, 1.0 * (1.0 / 3.0), 2.0 * (1.0 / 3.0), 2.0 * (1.0 / 3.0))
+# laws whose stress calls a transcendental that is not correctly rounded on either side
+# (neo-Hookean pow, Guccione exp): R within 1e-12 relative instead of bit-identical
+NOT_BITWISE = (LAW_NEO_HOOKEAN, LAW_GUCCIONE)
 
 
 BOX_CASES = {
@@ -50,6 +57,14 @@ BOX_CASES = {
                   dict(transient=True)),
     "alpha": (dict(extents=(1.0, 1.0, 1.0), divisions=(6, 6, 6), kinds=[D, T, T, T, T, T], distort=0.2, seed=5),
               dict(alpha=0.8)),
+    "stvk": (dict(extents=(4.0, 1.0, 1.0), divisions=(16, 5, 5), kinds=[D, D, T, T, T, T], distort=0.05, seed=42),
+             dict(law=LAW_STVK)),
+    "stvk_tl_symmetry": (dict(extents=(1.0, 1.0, 1.0), divisions=(8, 6, 5), kinds=[D, T, S, T, S, T], distort=0.1,
+                              seed=3), dict(law=LAW_STVK, tl=True)),
+    "guccione_tl": (dict(extents=(4.0, 1.0, 1.0), divisions=(16, 5, 5), kinds=[D, D, T, T, T, T], distort=0.05,
+                         seed=42), dict(law=LAW_GUCCIONE, tl=True)),
+    "guccione": (dict(extents=(1.0, 1.0, 1.0), divisions=(7, 6, 5), kinds=[D, T, T, T, T, T], distort=0.15, seed=7),
+                 dict(law=LAW_GUCCIONE)),
 }
 
 
@@ -61,7 +76,7 @@ def test_residual_bitwise(name):
     phys = _phys(**pargs)
     ev, orc = _pair(mesh, phys)
     u, v = cases.jv_inputs(mesh, seed=11)
-    if pargs.get("law") == LAW_NEO_HOOKEAN:
+    if pargs.get("law", LAW_HOOKE) != LAW_HOOKE:
         u = u * 1e4  # O(1e-2) strains: genuinely nonlinear
     if pargs.get("transient"):
         rng = np.random.default_rng(1)
@@ -72,7 +87,7 @@ def test_residual_bitwise(name):
     r_orc = orc.residual(u)
     err = np.abs(r_gpu - r_orc).max() / np.abs(r_orc).max()
     assert err <= 1e-12
-    if pargs.get("law") != LAW_NEO_HOOKEAN:  # pow() is not correctly rounded on either side
+    if pargs.get("law") not in NOT_BITWISE:
         assert np.array_equal(r_gpu, r_orc)
 
 
@@ -84,13 +99,13 @@ def test_jv_fixed_eps_and_fd(name):
     phys = _phys(**pargs)
     ev, orc = _pair(mesh, phys)
     u, v = cases.jv_inputs(mesh, seed=5)
-    if pargs.get("law") == LAW_NEO_HOOKEAN:
+    if pargs.get("law", LAW_HOOKE) != LAW_HOOKE:
         u = u * 1e4
     r_u = orc.residual(u)
     eps = 3e-8
     jv_gpu = sv.jacobian_vector_product(ev, u, r_u, v, eps=eps).cpu().numpy()
     jv_orc = (orc.residual(u + eps * v) - r_u) / eps
-    if pargs.get("law") != LAW_NEO_HOOKEAN:
+    if pargs.get("law") not in NOT_BITWISE:
         assert np.array_equal(jv_gpu, jv_orc)
     else:
         assert np.linalg.norm(jv_gpu - jv_orc) / np.linalg.norm(jv_orc) < 1e-6
@@ -294,3 +309,24 @@ def test_fused_eps_bitwise(n, odd, monkeypatch):
         else:
             out[fused] = sv.jacobian_vector_product(ev, u, r_u, v).cpu().numpy()
     assert np.array_equal(out["0"], out["1"])
+
+
+def test_guccione_overflow_reported():
+    """guccione_stress throws LawOverflow when the exponent Q exceeds 500 (laws.cpp:69-70); the
+    residual reports the first such cell (the stress loop order), J.v maps it to JvpNan
+    (nonlinear.cpp:128-129)."""
+    sv = _sv()
+    mesh = sv.box_mesh((1.0, 1.0, 1.0), (5, 4, 4), [D, T, T, T, T, T])
+    phys = _phys(law=LAW_GUCCIONE)
+    ev, orc = _pair(mesh, phys)
+    x = cases.cell_centres(mesh)
+    u = np.zeros(3 * mesh.n_cells)
+    u[0::3] = 30.0 * x[:, 0] * x[:, 0] * (x[:, 2] > 0.6)  # large stretch in the top layer only
+    with pytest.raises(sv.SolidfvError) as e:
+        ev.residual(u)
+    with pytest.raises(Exception) as e2:
+        orc.residual(u)
+    assert e.value.kind == "LawOverflow" and e.value.cell == e2.value.cell
+    with pytest.raises(sv.SolidfvError) as e3:
+        sv.jacobian_vector_product(ev, u, np.zeros_like(u), np.ones_like(u))
+    assert e3.value.kind == "JvpNan"
