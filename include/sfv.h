@@ -85,6 +85,14 @@ int sfv_set_history(sfv_ctx* ctx, const double* u_old_dev, const double* u_old_o
 
 int sfv_residual(sfv_ctx* ctx, const double* u_dev, double* r_dev, int* cell);
 int sfv_stabilisation(sfv_ctx* ctx, const double* u_dev, double* r_dev, int* cell);
+/* ResidualEvaluator::commit (discretisation.hpp:60; discretisation.cpp:91-95): the law's trial
+ * state at u becomes its committed state.  Only SFV_LAW_J2 carries state (J2PlasticLaw::commit,
+ * laws.cpp:214); for the other laws it is a no-op.  Called by sfv_run_steps after every
+ * converged step, as run_steps does (nonlinear.cpp:426). */
+int sfv_commit(sfv_ctx* ctx, const double* u_dev);
+/* Committed J2 state, host buffer of 19 doubles per cell: b_bar (row-major), eps_p, F
+ * (PlasticCell, laws.hpp:66-70).  SFV_ERR_INVALID_ARGUMENT for the other laws. */
+int sfv_law_state(sfv_ctx* ctx, double* state);
 /* cell_gradients (discretisation.hpp:29-30): G_dev is 9*n_cells, SoA [(3i+j)*n_cells + c] */
 int sfv_gradients(sfv_ctx* ctx, const double* u_dev, double* G_dev, int* cell);
 int sfv_jv(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* v_dev, double* out_dev,

@@ -26,7 +26,7 @@ extern "C" {
 enum { SFV_PATCH_DISPLACEMENT = 0, SFV_PATCH_TRACTION = 1, SFV_PATCH_SYMMETRY = 2 };
 
 /* constitutive laws on the hot path (laws.hpp:95, :117) */
-enum { SFV_LAW_HOOKE = 0, SFV_LAW_NEO_HOOKEAN = 1, SFV_LAW_STVK = 2, SFV_LAW_GUCCIONE = 3 };
+enum { SFV_LAW_HOOKE = 0, SFV_LAW_NEO_HOOKEAN = 1, SFV_LAW_STVK = 2, SFV_LAW_GUCCIONE = 3, SFV_LAW_J2 = 4 };
 
 /* PreconditionerKind (nonlinear.hpp:18) */
 enum {
@@ -55,7 +55,8 @@ enum {
     SFV_ERR_ILU_BREAKDOWN = 8,
     SFV_ERR_LU_SINGULAR = 9,
     SFV_ERR_CUDA = 10,
-    SFV_ERR_INTERNAL = 11
+    SFV_ERR_INTERNAL = 11,
+    SFV_ERR_RETURN_MAP = 12
 };
 
 /* Face-addressed mesh (mesh.hpp:30-49).  Internal faces first, boundary faces in
@@ -91,6 +92,12 @@ typedef struct sfv_physics {
     const int* bc_ramp;     /* n_patches; value * t when nonzero */
     /* SFV_LAW_GUCCIONE (GuccioneParams, laws.hpp:38-43): C, c_f, c_t, c_fs, kappa, f0 xyz */
     double guccione[8];
+    /* SFV_LAW_J2 (J2PlasticLaw, mu and kappa = lambda): HardeningCurve saturation
+     * a + b e + (c - a)(1 - exp(-d e)) when j2_n_table == 0, else j2_n_table (<= 16)
+     * (eps_p, sigma_y) pairs, strictly increasing eps_p (laws.hpp:52-64) */
+    double j2_curve[4];
+    int j2_n_table;
+    const double* j2_table;
 } sfv_physics;
 
 typedef struct sfv_solver_cfg {

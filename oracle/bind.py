@@ -51,6 +51,11 @@ def _load(path: str, prefix: str):
     getattr(lib, p + "set_history").argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
     for name in ("residual", "stabilisation"):
         getattr(lib, p + name).argtypes = [C.c_void_p, _dp, _dp, _ip]
+    if prefix == "ref_":
+        lib.ref_commit.argtypes = [C.c_void_p, _dp, _ip]
+    else:
+        lib.orc_commit.argtypes = [C.c_void_p, _dp]
+        lib.orc_law_state.argtypes = [C.c_void_p, _dp]
     getattr(lib, p + "jv").argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _ip]
     getattr(lib, p + "precond_create").argtypes = [C.c_void_p, C.c_int]
     getattr(lib, p + "precond_apply").argtypes = [C.c_void_p, _dp, _dp]
@@ -123,6 +128,22 @@ class _CpuCase:
         rc = self._f("residual")(self.h, dptr(u), dptr(r), C.byref(cell))
         self._check(rc, cell.value)
         return r
+
+    def commit(self, u):
+        """ResidualEvaluator::commit (discretisation.cpp:91-95): J2's trial state becomes committed."""
+        u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
+        cell = C.c_int(-1)
+        if self.PREFIX == "ref_":
+            rc = self.lib.ref_commit(self.h, dptr(u), C.byref(cell))
+        else:
+            rc = self.lib.orc_commit(self.h, dptr(u))
+        self._check(rc, cell.value)
+
+    def law_state(self):
+        """Committed J2 state (oracle only): (n_cells, 19) = b_bar, eps_p, F."""
+        out = np.zeros(19 * self.n_cells)
+        self._check(self.lib.orc_law_state(self.h, dptr(out)))
+        return out.reshape(-1, 19)
 
     def stabilisation(self, u):
         u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)

@@ -103,6 +103,10 @@ int guarded(RefCase* rc, int* cell, F&& body) {
         if (cell) *cell = e.cell;
         rc->last_error = e.what();
         return SFV_ERR_LAW_OVERFLOW;
+    } catch (const ReturnMapFailure& e) {
+        if (cell) *cell = e.cell;
+        rc->last_error = e.what();
+        return SFV_ERR_RETURN_MAP;
     } catch (const ResidualNan& e) {
         if (cell) *cell = e.cell;
         rc->last_error = e.what();
@@ -232,6 +236,12 @@ void* ref_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, int 
             law = std::make_shared<NeoHookeanLaw>(ph->mu, ph->lambda);
         } else if (ph->law == SFV_LAW_STVK) {
             law = std::make_shared<StVenantKirchhoffLaw>(ph->mu, ph->lambda);
+        } else if (ph->law == SFV_LAW_J2) {
+            HardeningCurve curve = HardeningCurve::saturation(ph->j2_curve[0], ph->j2_curve[1], ph->j2_curve[2],
+                                                              ph->j2_curve[3]);
+            for (int k = 0; k < ph->j2_n_table; ++k)
+                curve.table.emplace_back(ph->j2_table[2 * k], ph->j2_table[2 * k + 1]);
+            law = std::make_shared<J2PlasticLaw>(ph->mu, ph->lambda, curve);
         } else if (ph->law == SFV_LAW_GUCCIONE) {
             const double* q = ph->guccione;
             GuccioneParams gp{q[0], q[1], q[2], q[3], q[4], Vec3{q[5], q[6], q[7]}};
@@ -319,6 +329,12 @@ void ref_set_history(void* h, const double* u_old, const double* u_old_old, cons
 int ref_residual(void* h, const double* u, double* r, int* cell) {
     RefCase* rc = static_cast<RefCase*>(h);
     return guarded(rc, cell, [&] { store(rc->eval->residual(cells_of(u, rc->mesh.n_cells)), r); });
+}
+
+// ResidualEvaluator::commit (discretisation.cpp:91-95)
+int ref_commit(void* h, const double* u, int* cell) {
+    RefCase* rc = static_cast<RefCase*>(h);
+    return guarded(rc, cell, [&] { rc->eval->commit(cells_of(u, rc->mesh.n_cells)); });
 }
 
 int ref_stabilisation(void* h, const double* u, double* r, int* cell) {

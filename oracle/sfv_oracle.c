@@ -170,6 +170,11 @@ struct orc_case {
     int law;
     double mu, lam;
     double gc[8]; /* Guccione: C, c_f, c_t, c_fs, kappa, f0 */
+    /* J2: HardeningCurve (saturation a, b, c, d, or jn table pairs) and committed PlasticCell */
+    double ja, jb, jc, jd, jt[32];
+    int jn;
+    m3 *j2_bbar, *j2_F;
+    double* j2_eps;
     double alpha;
     int tl, transient;
     double dt, rho;
@@ -442,6 +447,18 @@ orc_case* orc_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* errbu
     h->grad = xcalloc(h->nc, sizeof(m3));
     h->sigma = xcalloc(h->nc, sizeof(m3));
     h->fdef = xcalloc(h->nc, sizeof(m3));
+    h->ja = ph->j2_curve[0];
+    h->jb = ph->j2_curve[1];
+    h->jc = ph->j2_curve[2];
+    h->jd = ph->j2_curve[3];
+    h->jn = ph->law == SFV_LAW_J2 ? ph->j2_n_table : 0;
+    for (int k = 0; k < 2 * h->jn && k < 32; ++k) h->jt[k] = ph->j2_table[k];
+    if (ph->law == SFV_LAW_J2) { /* J2PlasticLaw::resize (laws.cpp:196-199): PlasticCell{} */
+        h->j2_bbar = xcalloc(h->nc, sizeof(m3));
+        h->j2_F = xcalloc(h->nc, sizeof(m3));
+        h->j2_eps = xcalloc(h->nc, sizeof(double));
+        for (int c = 0; c < h->nc; ++c) h->j2_bbar[c] = h->j2_F[c] = mident();
+    }
     return h;
 }
 
@@ -454,7 +471,7 @@ void orc_destroy(orc_case* h) {
                     h->centroid, h->g_inv, h->g_singular, h->face_centroid, h->area, h->area_mag,
                     h->normal, h->d, h->d_mag, h->w, h->delta, h->delta_mag, h->reflect, h->ls,
                     h->bc_value, h->bc_ramp, h->u_old, h->u_old_old, h->v_old, h->v_old_old,
-                    h->grad, h->sigma, h->fdef};
+                    h->grad, h->sigma, h->fdef, h->j2_bbar, h->j2_F, h->j2_eps};
     for (size_t i = 0; i < sizeof ptrs / sizeof ptrs[0]; ++i) free(ptrs[i]);
     csr_free(&h->ilu);
     lu_free(h->lu);
@@ -612,6 +629,89 @@ static int guccione(m3 g, const double* gc, m3* out) {
     return 1;
 }
 
+/* HardeningCurve::value / slope (laws.cpp:79-102) */
+static double hard_value(const orc_case* h, double e) {
+    if (h->jn > 0) {
+        if (e <= h->jt[0]) return h->jt[1];
+        for (int i = 1; i < h->jn; ++i)
+            if (e <= h->jt[2 * i]) {
+                const double e0 = h->jt[2 * i - 2], s0 = h->jt[2 * i - 1], e1 = h->jt[2 * i], s1 = h->jt[2 * i + 1];
+                return s0 + (s1 - s0) * (e - e0) / (e1 - e0);
+            }
+        return h->jt[2 * h->jn - 1];
+    }
+    return h->ja + h->jb * e + (h->jc - h->ja) * (1.0 - exp(-h->jd * e));
+}
+static double hard_slope(const orc_case* h, double e) {
+    if (h->jn > 0) {
+        if (e <= h->jt[0] || e >= h->jt[2 * h->jn - 2]) return 0.0;
+        for (int i = 1; i < h->jn; ++i)
+            if (e <= h->jt[2 * i]) return (h->jt[2 * i + 1] - h->jt[2 * i - 1]) / (h->jt[2 * i] - h->jt[2 * i - 2]);
+        return 0.0;
+    }
+    return h->jb + (h->jc - h->ja) * h->jd * exp(-h->jd * e);
+}
+static double mfrob(m3 a) { /* types.hpp:150-155 */
+    double s = 0.0;
+    for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) s += a.m[i][j] * a.m[i][j];
+    return sqrt(s);
+}
+
+/* j2_radial_return (laws.cpp:104-168) on cell c's committed state; trial state into the out
+ * pointers.  Returns 1 ok, 0 det F <= 0 / inverted increment (InvertedElement), -2 hardening
+ * Newton did not converge (ReturnMapFailure). */
+static int j2_return(const orc_case* h, int c, m3 g, m3* sigma, m3* bbar_out, double* eps_out, m3* F_out) {
+    const double mu = h->mu, kappa = h->lam;
+    const m3 F_new = madd(mident(), mtrans(g));
+    const double J = mdet(F_new);
+    if (!(J > 0.0)) return 0;
+    const m3 f_rel = mmul(F_new, minverse(h->j2_F[c]));
+    const double det_f = mdet(f_rel);
+    if (!(det_f > 0.0)) return 0;
+    const m3 f_bar = mscale(f_rel, pow(det_f, -1.0 / 3.0));
+    const m3 bt0 = mmul(mmul(f_bar, h->j2_bbar[c]), mtrans(f_bar));
+    const m3 b_trial = mscale(madd(bt0, mtrans(bt0)), 0.5);
+    const m3 s_trial = mscale(mdev(b_trial), mu / J);
+    const double s_norm = mfrob(s_trial);
+    const double sq23 = sqrt(2.0 / 3.0);
+    const double epc = h->j2_eps[c];
+    const double f_yield = s_norm - sq23 * hard_value(h, epc);
+    m3 s = s_trial;
+    m3 bnew = b_trial;
+    double epn = epc;
+    if (!(f_yield <= 0.0)) {
+        const double mu_bar = mu * mtrace(b_trial) / (3.0 * J);
+        double dg = 0.0;
+        int done = 0;
+        const double tol = 1e-12 * fmax(s_norm, hard_value(h, 0.0));
+        for (int it = 0; it < 50; ++it) {
+            const double eps = epc + sq23 * dg;
+            const double gg = s_norm - 2.0 * mu_bar * dg - sq23 * hard_value(h, eps);
+            if (fabs(gg) <= tol) {
+                done = 1;
+                break;
+            }
+            const double gp = -2.0 * mu_bar - (2.0 / 3.0) * hard_slope(h, eps);
+            const double next = dg - gg / gp;
+            dg = next > 0.0 ? next : 0.5 * dg;
+        }
+        if (!done) return -2;
+        const m3 n_dir = mscale(s_trial, 1.0 / s_norm);
+        s = msub(s_trial, mscale(n_dir, 2.0 * mu_bar * dg));
+        epn = epc + sq23 * dg;
+        bnew = mscale(s, J / mu);
+        const double iso = mtrace(b_trial) / 3.0;
+        bnew.m[0][0] += iso; bnew.m[1][1] += iso; bnew.m[2][2] += iso;
+    }
+    if (bbar_out) *bbar_out = bnew;
+    if (eps_out) *eps_out = epn;
+    if (F_out) *F_out = F_new;
+    const double p = 0.5 * kappa * (J * J - 1.0) / J;
+    s.m[0][0] += p; s.m[1][1] += p; s.m[2][2] += p;
+    *sigma = s;
+    return 1;
+}
+
 /* rhie_chow_face (discretisation.cpp:33-37) */
 static v3 rhie_chow(v3 up, v3 uo, m3 gf, v3 delta, double d_mag, double area_mag, double alpha,
                     double kbar) {
@@ -627,8 +727,8 @@ static int transform_area(v3 gamma, m3 ff, v3* out) {
     return 1;
 }
 
-static double kbar_of(const orc_case* h) { /* laws.hpp:100, :111, :122, :133 */
-    if (h->law == SFV_LAW_NEO_HOOKEAN) return 4.0 / 3.0 * h->mu + h->lam;
+static double kbar_of(const orc_case* h) { /* laws.hpp:100, :111, :122, :133, :147 */
+    if (h->law == SFV_LAW_NEO_HOOKEAN || h->law == SFV_LAW_J2) return 4.0 / 3.0 * h->mu + h->lam;
     if (h->law == SFV_LAW_GUCCIONE) return 4.0 / 3.0 * (h->gc[0] * h->gc[2]) + h->gc[4];
     return 2.0 * h->mu + h->lam;
 }
@@ -680,6 +780,10 @@ static int residual(orc_case* h, const v3* u, v3* r) {
         } else if (h->law == SFV_LAW_STVK) {
             if (!stvk(h->grad[c], h->mu, h->lam, &h->sigma[c]))
                 return fail(&h->err, SFV_ERR_INVERTED_ELEMENT, c, "kinematics: det F <= 0");
+        } else if (h->law == SFV_LAW_J2) {
+            const int k = j2_return(h, c, h->grad[c], &h->sigma[c], NULL, NULL, NULL);
+            if (k == 0) return fail(&h->err, SFV_ERR_INVERTED_ELEMENT, c, "j2_radial_return: det F <= 0");
+            if (k < 0) return fail(&h->err, SFV_ERR_RETURN_MAP, c, "j2_radial_return: hardening Newton did not converge");
         } else if (h->law == SFV_LAW_GUCCIONE) {
             const int k = guccione(h->grad[c], h->gc, &h->sigma[c]);
             if (k == 0) return fail(&h->err, SFV_ERR_INVERTED_ELEMENT, c, "kinematics: det F <= 0");
@@ -747,6 +851,55 @@ int orc_residual(orc_case* h, const double* uf, double* rf, int* cell) {
     free(u);
     free(r);
     return rc;
+}
+
+/* ResidualEvaluator::commit (discretisation.cpp:91-95) with J2PlasticLaw::commit (laws.cpp:214):
+ * the stress at u in every cell (in cell order: the first failure aborts, nothing committed),
+ * then every trial state becomes the committed one */
+static int commit_state(orc_case* h, const v3* u) {
+    if (h->law != SFV_LAW_J2) return SFV_OK;
+    int rc = cell_gradients(h, u, h->grad);
+    if (rc) return rc;
+    m3* nb = xcalloc(h->nc, sizeof(m3));
+    m3* nf = xcalloc(h->nc, sizeof(m3));
+    double* ne = xcalloc(h->nc, sizeof(double));
+    for (int c = 0; c < h->nc && !rc; ++c) {
+        m3 sig;
+        const int k = j2_return(h, c, h->grad[c], &sig, &nb[c], &ne[c], &nf[c]);
+        if (k == 0) rc = fail(&h->err, SFV_ERR_INVERTED_ELEMENT, c, "j2_radial_return: det F <= 0");
+        if (k < 0) rc = fail(&h->err, SFV_ERR_RETURN_MAP, c, "j2_radial_return: hardening Newton did not converge");
+    }
+    if (!rc) {
+        memcpy(h->j2_bbar, nb, sizeof(m3) * h->nc);
+        memcpy(h->j2_F, nf, sizeof(m3) * h->nc);
+        memcpy(h->j2_eps, ne, sizeof(double) * h->nc);
+    }
+    free(nb);
+    free(nf);
+    free(ne);
+    return rc;
+}
+
+int orc_commit(orc_case* h, const double* uf) {
+    v3* u = xcalloc(h->nc, sizeof(v3));
+    load_cells(u, uf, h->nc);
+    h->err.code = 0;
+    h->err.cell = -1;
+    const int rc = commit_state(h, u);
+    free(u);
+    return rc;
+}
+
+int orc_law_state(orc_case* h, double* out) {
+    if (h->law != SFV_LAW_J2) return fail(&h->err, SFV_ERR_INVALID_ARGUMENT, -1, "law_state: J2 only");
+    for (int c = 0; c < h->nc; ++c) {
+        for (int q = 0; q < 9; ++q) {
+            out[19 * (size_t)c + q] = h->j2_bbar[c].m[q / 3][q % 3];
+            out[19 * (size_t)c + 10 + q] = h->j2_F[c].m[q / 3][q % 3];
+        }
+        out[19 * (size_t)c + 9] = h->j2_eps[c];
+    }
+    return SFV_OK;
 }
 
 int orc_stabilisation(orc_case* h, const double* uf, double* rf, int* cell) {
@@ -1602,6 +1755,7 @@ int orc_run_steps(orc_case* h, double* field, const sfv_solver_cfg* cfg, int n_s
         if (*n_reports < cap) reports[*n_reports] = rep;
         ++*n_reports;
         if (rep.status != SFV_CONVERGED) break;
+        if ((rc = commit_state(h, u)) != SFV_OK) break; /* eval.commit(u) (nonlinear.cpp:426) */
         if (h->transient) {
             for (int c = 0; c < nc; ++c) {
                 const v3 vn = bdf2_vel(u[c], fuo[c], fuoo[c], dt);
@@ -1626,5 +1780,5 @@ int orc_run_steps(orc_case* h, double* field, const sfv_solver_cfg* cfg, int n_s
     store_cells(field + 15 * nc, fao, nc);
     free(fu); free(fuo); free(fuoo); free(fvo); free(fvoo); free(fao); free(u);
     *wall = now_s() - t0;
-    return SFV_OK;
+    return rc;
 }

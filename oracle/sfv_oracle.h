@@ -41,6 +41,10 @@ void orc_set_history(orc_case* h, const double* u_old, const double* u_old_old,
 
 int orc_residual(orc_case* h, const double* u, double* r, int* cell);
 int orc_stabilisation(orc_case* h, const double* u, double* r, int* cell);
+/* ResidualEvaluator::commit (discretisation.cpp:91-95); J2 only carries state */
+int orc_commit(orc_case* h, const double* u);
+/* committed J2 state, 19 doubles per cell: b_bar, eps_p, F */
+int orc_law_state(orc_case* h, double* out);
 int orc_jv(orc_case* h, const double* u, const double* r_u, const double* v, double* out,
            int* cell);
 

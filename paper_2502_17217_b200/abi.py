@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 PATCH_DISPLACEMENT, PATCH_TRACTION, PATCH_SYMMETRY = 0, 1, 2
-LAW_HOOKE, LAW_NEO_HOOKEAN, LAW_STVK, LAW_GUCCIONE = 0, 1, 2, 3
+LAW_HOOKE, LAW_NEO_HOOKEAN, LAW_STVK, LAW_GUCCIONE, LAW_J2 = 0, 1, 2, 3, 4
 PRECOND = {"auto": 0, "none": 1, "ilu0": 2, "ilu1": 3, "ilu2": 4, "lu": 5}
 CONVERGED, DIVERGED, MAX_ITERS = 0, 1, 2
 STATUS_NAME = {CONVERGED: "converged", DIVERGED: "diverged", MAX_ITERS: "max-iters"}
@@ -27,6 +27,7 @@ ERR = {
     3: "GradientFailure",
     4: "InvertedElement",
     5: "LawOverflow",
+    12: "ReturnMapFailure",
     6: "ResidualNan",
     7: "JvpNan",
     8: "IluBreakdown",
@@ -71,6 +72,9 @@ class PhysicsDesc(C.Structure):
         ("bc_value", _dp),
         ("bc_ramp", _ip),
         ("guccione", C.c_double * 8),
+        ("j2_curve", C.c_double * 4),
+        ("j2_n_table", C.c_int),
+        ("j2_table", _dp),
     ]
 
 
@@ -205,12 +209,17 @@ class Physics:
     bc_ramp: np.ndarray = None  # (n_patches,)
     # GuccioneParams (laws.hpp:38-43): C, c_f, c_t, c_fs, kappa, f0 (3)
     guccione: tuple = (0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0)
+    # J2 HardeningCurve (laws.hpp:52-64): saturation (a, b, c, d), or a table of (eps_p, sigma_y)
+    j2_curve: tuple = (0.0, 0.0, 0.0, 1.0)
+    j2_table: np.ndarray = None
     _keep: list = field(default_factory=list, repr=False)
 
     def desc(self) -> PhysicsDesc:
         bv = np.ascontiguousarray(self.bc_value, dtype=np.float64).reshape(-1)
         br = np.ascontiguousarray(self.bc_ramp, dtype=np.int32)
-        self._keep = [bv, br]
+        tab = np.ascontiguousarray(self.j2_table if self.j2_table is not None else np.zeros((0, 2)),
+                                   dtype=np.float64).reshape(-1)
+        self._keep = [bv, br, tab]
         p = PhysicsDesc()
         p.law = int(self.law)
         p.mu = float(self.mu)
@@ -224,12 +233,16 @@ class Physics:
         p.bc_ramp = iptr(br)
         for k, x in enumerate(self.guccione):
             p.guccione[k] = float(x)
+        for k, x in enumerate(self.j2_curve):
+            p.j2_curve[k] = float(x)
+        p.j2_n_table = len(tab) // 2
+        p.j2_table = dptr(tab) if len(tab) else None
         return p
 
     @property
     def kbar(self) -> float:
         """law.stabilisation_modulus() (laws.hpp:100, :111, :122, :133)."""
-        if self.law == LAW_NEO_HOOKEAN:
+        if self.law in (LAW_NEO_HOOKEAN, LAW_J2):
             return 4.0 / 3.0 * self.mu + self.lam
         if self.law == LAW_GUCCIONE:
             g = self.guccione

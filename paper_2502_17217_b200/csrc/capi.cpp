@@ -119,7 +119,7 @@ struct sfv_ctx {
     DevBuf<int> slot_face, slot_other, bnd_si, tslot;
     DevBuf<double> slot_ls, gam, del, dmag, w, volume, tls;
     // jv_pair.cu scratch + tiled face records (device.h): pwg = tiled [w | G], psig: tiled cell stress
-    DevBuf<double> pwg, face9, bres, psig;
+    DevBuf<double> pwg, face9, bres, psig, lawst;
     PairScratch ps;
     // scratch
     DevBuf<double> grad, red, scal;  // scal: [0]=eps [1]=u_norm [2..] misc
@@ -294,11 +294,19 @@ std::string build_layout(sfv_ctx* c) {
     d.volume = c->volume.p;
     if (!legacy && (c->ph.law != SFV_LAW_HOOKE || c->ph.tl) && !c->psig.alloc(static_cast<size_t>(ntc) * kSig * 32))
         return "cuda: out of device memory for the mesh layout";
+    if (c->ph.law == SFV_LAW_J2) {  // PlasticCell{} per cell (laws.hpp:66-70): b_bar = I, eps_p = 0, F = I
+        std::vector<double> st(static_cast<size_t>(ntc) * kJ2 * 32, 0.0);
+        for (int i = 0; i < ntc * 32; ++i)
+            for (int q : {0, 4, 8, 10, 14, 18}) st[tiled(i, kJ2) + 32 * q] = 1.0;
+        if (!c->lawst.upload(st)) return "cuda: out of device memory for the law state";
+    }
+    c->ps.lawst = c->lawst.p;
     c->ps.sig = c->psig.p;
     c->ps.wg = c->pwg.p;
     // boundary pass on a side stream beside the gradient pass: opt-in (SFV_SIDE_STREAM=1);
     // measured 3% slower at 1M cells (the stream events break the PDL chain)
-    if (const char* se = std::getenv("SFV_SIDE_STREAM"); se && std::atoi(se) != 0 && nf > m.n_internal) {
+    if (const char* se = std::getenv("SFV_SIDE_STREAM");
+        se && std::atoi(se) != 0 && nf > m.n_internal && c->ph.law != SFV_LAW_J2) {
         if (cudaStreamCreateWithFlags(&c->ps.side, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ps.ev_w, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->ps.ev_b, cudaEventDisableTiming) != cudaSuccess)
@@ -448,7 +456,11 @@ int fetch(sfv_ctx* c, int k) {
 // would raise them (stress loop, then face loop, then the NaN scan).
 int decode_residual_errors(sfv_ctx* c, bool jv) {
     const ErrWords& e = c->st->err;
-    // the stress loop throws at the first failing cell: LawOverflow there if it comes first
+    // the stress loop throws at the first failing cell: LawOverflow / ReturnMapFailure there if
+    // it comes first (a J.v maps LawOverflow to JvpNan and lets ReturnMapFailure through,
+    // nonlinear.cpp:122-131)
+    if (e.retmap_cell != kNone && e.retmap_cell < e.inverted_cell && e.retmap_cell < e.overflow_cell)
+        return c->fail(SFV_ERR_RETURN_MAP, e.retmap_cell, "j2_radial_return: hardening Newton did not converge");
     if (e.overflow_cell != kNone && e.overflow_cell < e.inverted_cell)
         return jv ? c->fail(SFV_ERR_JVP_NAN, -1, "jvp: guccione_stress: exponent overflow")
                   : c->fail(SFV_ERR_LAW_OVERFLOW, e.overflow_cell, "guccione_stress: exponent overflow");
@@ -1230,12 +1242,23 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     p.mu = ph->mu;
     p.lam = ph->lambda;
     p.alpha = ph->alpha;
-    if (ph->law < SFV_LAW_HOOKE || ph->law > SFV_LAW_GUCCIONE) return fail("law: unknown constitutive law");
+    if (ph->law < SFV_LAW_HOOKE || ph->law > SFV_LAW_J2) return fail("law: unknown constitutive law");
     for (int k = 0; k < 8; ++k) p.gc[k] = ph->guccione[k];
-    // MechanicalLaw::stabilisation_modulus (laws.hpp:100, :111, :122, :133)
-    p.kbar = ph->law == SFV_LAW_NEO_HOOKEAN ? 4.0 / 3.0 * ph->mu + ph->lambda
-             : ph->law == SFV_LAW_GUCCIONE  ? 4.0 / 3.0 * (ph->guccione[0] * ph->guccione[2]) + ph->guccione[4]
-                                            : 2.0 * ph->mu + ph->lambda;
+    p.ja = ph->j2_curve[0];
+    p.jb = ph->j2_curve[1];
+    p.jc = ph->j2_curve[2];
+    p.jd = ph->j2_curve[3];
+    p.jn = ph->law == SFV_LAW_J2 ? ph->j2_n_table : 0;
+    if (p.jn < 0 || p.jn > kMaxHardening || (p.jn > 0 && !ph->j2_table))
+        return fail("law: the J2 hardening table holds at most 16 points");
+    for (int k = 0; k < 2 * p.jn; ++k) p.jt[k] = ph->j2_table[k];
+    for (int k = 1; k < p.jn; ++k)
+        if (!(p.jt[2 * k] > p.jt[2 * k - 2])) return fail("law: hardening table eps_p must increase strictly");
+    p.commit = 0;
+    // MechanicalLaw::stabilisation_modulus (laws.hpp:100, :111, :122, :133, :147)
+    p.kbar = ph->law == SFV_LAW_NEO_HOOKEAN || ph->law == SFV_LAW_J2 ? 4.0 / 3.0 * ph->mu + ph->lambda
+             : ph->law == SFV_LAW_GUCCIONE ? 4.0 / 3.0 * (ph->guccione[0] * ph->guccione[2]) + ph->guccione[4]
+                                           : 2.0 * ph->mu + ph->lambda;
     p.rho = ph->rho;
     p.dt = ph->dt;
     c->pt.n = md->n_patches;
@@ -1390,6 +1413,31 @@ int sfv_stabilisation(sfv_ctx* c, const double* u, double* r, int* cell) {
     residual_pass(c, ph, u, nullptr, nullptr, nullptr, r);
     if (int e = c->cuda_check("stabilisation")) return e;
     return fetch(c, 0);
+}
+
+int sfv_commit(sfv_ctx* c, const double* u) {
+    // ResidualEvaluator::commit (discretisation.cpp:91-95): the law's stress at u in every cell,
+    // then trial -> committed.  Only J2 carries state; the hyperelastic laws' commit is empty.
+    if (c->ph.law != SFV_LAW_J2) return SFV_OK;
+    if (c->singular_cell >= 0) return gradient_failure(c);
+    reset_err(c);
+    Physics ph = c->ph;
+    ph.commit = 1;
+    launch_gradients_pair(c->dm, c->pt, ph, u, nullptr, c->ps, c->err.p, c->stream);
+    c->launches += 2;
+    if (int e = c->cuda_check("commit")) return e;
+    if (int e = fetch(c, 0)) return e;
+    return decode_residual_errors(c, false);
+}
+
+int sfv_law_state(sfv_ctx* c, double* state) {
+    if (c->ph.law != SFV_LAW_J2) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "law_state: J2 only");
+    std::vector<double> t(c->lawst.n);
+    if (cudaMemcpy(t.data(), c->lawst.p, c->lawst.bytes(), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return c->cuda_check("law_state");
+    for (int i = 0; i < c->nc; ++i)
+        for (int q = 0; q < kJ2; ++q) state[static_cast<size_t>(i) * kJ2 + q] = t[tiled(i, kJ2) + 32 * q];
+    return SFV_OK;
 }
 
 int sfv_gradients(sfv_ctx* c, const double* u, double* G, int* cell) {
@@ -1612,6 +1660,7 @@ int sfv_run_steps(sfv_ctx* c, double* field, const sfv_solver_cfg* cfg, int n_st
         if (*n_reports < cap) reports[*n_reports] = rep;
         ++*n_reports;
         if (rep.status != SFV_CONVERGED) break;
+        if (int ec = sfv_commit(c, u)) return ec;  // eval.commit(u) (nonlinear.cpp:426)
         if (transient) {
             launch_bdf2_rotate(fuo, fuoo, fvo, fvoo, fao, u, dt, n, c->stream);
             ++c->launches;

@@ -65,7 +65,15 @@ struct Physics {
     double rho, dt;
     int stab_only;  // ResidualEvaluator::stabilisation (discretisation.cpp:210-214)
     double gc[8];   // Guccione: C, c_f, c_t, c_fs, kappa, f0 xyz (GuccioneParams, laws.hpp:38-43)
+    // J2 plasticity (J2PlasticLaw, laws.hpp:139-155): mu, kappa = mu, lam; HardeningCurve
+    // (laws.hpp:52-64): saturation a, b, c, d, or a table of jn (eps_p, sigma_y) pairs
+    double ja, jb, jc, jd;
+    int jn;
+    double jt[2 * 16];
+    int commit;  // gradient pass of ResidualEvaluator::commit: write the trial state as committed
 };
+constexpr int kMaxHardening = 16;
+constexpr int kJ2 = 19;  // rows of the tiled J2 state record: b_bar (9), eps_p, F (9)  (PlasticCell)
 
 // Error words written by kernels (atomicMin of the first offending index; INT_MAX = none).
 struct ErrWords {
@@ -74,6 +82,7 @@ struct ErrWords {
     int nan_cell;       // residual: non-finite entry (discretisation.cpp:171-172)
     int nan_jv;         // J.v: non-finite difference quotient (nonlinear.cpp:135)
     int overflow_cell;  // law stress: Guccione exponent overflow (laws.cpp:69-70)
+    int retmap_cell;    // law stress: J2 hardening Newton did not converge (laws.cpp:145-146)
 };
 
 // History for the BDF2 inertia term (interleaved [3c+k]).
@@ -95,6 +104,7 @@ void launch_residual(const DevMesh& m, const Physics& ph, const PatchTable& pt, 
 struct PairScratch {
     double* wg = nullptr;           // tiled [w | G] (kWG rows): perturbed state u + eps v, cell gradients
     double* sig = nullptr;          // tiled cell stress (9 entries, row-major), non-Hooke / TL only
+    double* lawst = nullptr;        // tiled committed J2 state (kJ2 rows), J2 only
     const int* bnd_cs = nullptr;    // [nf-nint] cell * 8 + slot of boundary face nint+fb
     double* bres = nullptr;       // [6*(nf-nint)] boundary-face flux + stabilisation
     cudaEvent_t* marks = nullptr;  // optional: recorded after the perturb, gradient, boundary passes

@@ -203,6 +203,121 @@ __device__ __forceinline__ dm3 guccione(const dm3& g, const double* gc, int& cod
     S.a[2][2] += pen;
     return mscl(mmul(mmul(F, S), mtr(F)), 1.0 / J);
 }
+// HardeningCurve::value / slope (laws.cpp:79-102): table (piecewise linear) or saturation
+__device__ __forceinline__ double hard_value(const Physics& ph, double e) {
+    if (ph.jn > 0) {
+        if (e <= ph.jt[0]) return ph.jt[1];
+        for (int i = 1; i < ph.jn; ++i)
+            if (e <= ph.jt[2 * i]) {
+                const double e0 = ph.jt[2 * i - 2], s0 = ph.jt[2 * i - 1], e1 = ph.jt[2 * i], s1 = ph.jt[2 * i + 1];
+                return s0 + (s1 - s0) * (e - e0) / (e1 - e0);
+            }
+        return ph.jt[2 * ph.jn - 1];
+    }
+    return ph.ja + ph.jb * e + (ph.jc - ph.ja) * (1.0 - exp(-ph.jd * e));
+}
+__device__ __forceinline__ double hard_slope(const Physics& ph, double e) {
+    if (ph.jn > 0) {
+        if (e <= ph.jt[0] || e >= ph.jt[2 * ph.jn - 2]) return 0.0;
+        for (int i = 1; i < ph.jn; ++i)
+            if (e <= ph.jt[2 * i]) return (ph.jt[2 * i + 1] - ph.jt[2 * i - 1]) / (ph.jt[2 * i] - ph.jt[2 * i - 2]);
+        return 0.0;
+    }
+    return ph.jb + (ph.jc - ph.ja) * ph.jd * exp(-ph.jd * e);
+}
+__device__ __forceinline__ double frob(const dm3& a) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s += a.a[i][j] * a.a[i][j];
+    return sqrt(s);
+}
+// j2_radial_return (laws.cpp:104-168) on the committed state st = b_bar (9), eps_p, F (9);
+// the trial state goes to nst.  code: 0 ok, 1 det F <= 0 or inverted increment
+// (InvertedElement), 3 hardening Newton did not converge (ReturnMapFailure).
+__device__ __forceinline__ dm3 j2_return(const dm3& g, const double* st, const Physics& ph, int& code, double* nst) {
+    const double mu = ph.mu, kappa = ph.lam;
+    const dm3 Fn = defgrad(g);
+    const double J = det(Fn);
+    code = 0;
+    dm3 bc, Fc;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        bc.a[q / 3][q % 3] = st[q];
+        Fc.a[q / 3][q % 3] = st[10 + q];
+    }
+    const double epc = st[9];
+    if (!(J > 0.0)) {
+        code = 1;
+        return Fn;
+    }
+    const dm3 frel = mmul(Fn, inverse(Fc));
+    const double detf = det(frel);
+    if (!(detf > 0.0)) {
+        code = 1;
+        return Fn;
+    }
+    const dm3 fbar = mscl(frel, pow(detf, -1.0 / 3.0));
+    const dm3 bt0 = mmul(mmul(fbar, bc), mtr(fbar));
+    const dm3 btr = mscl(madd(bt0, mtr(bt0)), 0.5);  // sym()
+    const double t = ((btr.a[0][0] + btr.a[1][1]) + btr.a[2][2]) / 3.0;
+    dm3 dv = btr;
+    dv.a[0][0] -= t;
+    dv.a[1][1] -= t;
+    dv.a[2][2] -= t;
+    const dm3 strial = mscl(dv, mu / J);
+    const double snorm = frob(strial);
+    const double sq23 = sqrt(2.0 / 3.0);
+    const double fy = snorm - sq23 * hard_value(ph, epc);
+    dm3 s = strial;
+    dm3 bnew = btr;
+    double epn = epc;
+    if (!(fy <= 0.0)) {  // plastic (laws.cpp:128: elastic iff f_yield <= 0)
+        const double trb = (btr.a[0][0] + btr.a[1][1]) + btr.a[2][2];
+        const double mub = mu * trb / (3.0 * J);
+        double dg = 0.0;
+        bool done = false;
+        const double tol = 1e-12 * fmax(snorm, hard_value(ph, 0.0));
+        for (int it = 0; it < 50; ++it) {
+            const double eps = epc + sq23 * dg;
+            const double gg = snorm - 2.0 * mub * dg - sq23 * hard_value(ph, eps);
+            if (fabs(gg) <= tol) {
+                done = true;
+                break;
+            }
+            const double gp = -2.0 * mub - (2.0 / 3.0) * hard_slope(ph, eps);
+            const double next = dg - gg / gp;
+            dg = next > 0.0 ? next : 0.5 * dg;
+        }
+        if (!done) code = 3;
+        const dm3 ndir = mscl(strial, 1.0 / snorm);
+        const double k = 2.0 * mub * dg;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) s.a[i][j] = strial.a[i][j] - ndir.a[i][j] * k;
+        epn = epc + sq23 * dg;
+        bnew = mscl(s, J / mu);
+        const double iso = trb / 3.0;
+        bnew.a[0][0] += iso;
+        bnew.a[1][1] += iso;
+        bnew.a[2][2] += iso;
+    }
+    if (nst) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            nst[q] = bnew.a[q / 3][q % 3];
+            nst[10 + q] = Fn.a[q / 3][q % 3];
+        }
+        nst[9] = epn;
+    }
+    const double p = 0.5 * kappa * (J * J - 1.0) / J;
+    s.a[0][0] += p;
+    s.a[1][1] += p;
+    s.a[2][2] += p;
+    return s;
+}
 // the law's Cauchy stress; code 0 ok, 1 inverted (det F <= 0), 2 exponent overflow
 __device__ __forceinline__ dm3 stress_code(const Physics& ph, const dm3& g, int& code) {
     bool ok = true;

@@ -306,9 +306,13 @@ int eps_perturb_grid(int nc) {
 // once (laws.cpp; the stress loop of discretisation.cpp:116-119, which also reports an
 // inverted cell, or the Guccione exponent overflow) and stored, instead of twice per face
 // in the flux pass — same function on the same G, so the same bits.
-template <int S, bool GEN>
+// J2: the stress is the radial return from the cell's committed state (J2PlasticLaw::stress,
+// laws.cpp:201-212); with ph.commit set the trial state replaces it (ResidualEvaluator::commit,
+// discretisation.cpp:91-95 — each cell reads and writes only its own record).
+template <int S, bool GEN, bool J2 = false>
 __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt, Physics ph, double* __restrict__ wg,
-                                                        double* __restrict__ sig, ErrWords* __restrict__ err) {
+                                                        double* __restrict__ sig, double* __restrict__ lawst,
+                                                        ErrWords* __restrict__ err) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= m.nc) return;
     release_early();
@@ -351,9 +355,22 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
 #pragma unroll
         for (int q = 0; q < 9; ++q) gm.a[q / 3][q % 3] = g[q];
         int code;
-        const dm3 sc = stress_code(ph, gm, code);
+        dm3 sc;
+        if constexpr (J2) {
+            double* rst = lawst + tiled(c, kJ2);
+            double st[kJ2], nst[kJ2];
+#pragma unroll
+            for (int q = 0; q < kJ2; ++q) st[q] = rst[32 * q];
+            sc = j2_return(gm, st, ph, code, nst);
+            if (ph.commit && code == 0)
+#pragma unroll
+                for (int q = 0; q < kJ2; ++q) rst[32 * q] = nst[q];
+        } else {
+            sc = stress_code(ph, gm, code);
+        }
         if (code == 1) atomicMin(&err->inverted_cell, c);
         if (code == 2) atomicMin(&err->overflow_cell, c);
+        if (code == 3) atomicMin(&err->retmap_cell, c);
         double* rs = sig + tiled(c, kSig);
 #pragma unroll
         for (int q = 0; q < 9; ++q) st_keep(rs + 32 * q, sc.a[q / 3][q % 3], pol);
@@ -402,7 +419,8 @@ __device__ __forceinline__ dm3 cell_gradient_at(const DevMesh& m, const PatchTab
 __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, PatchTable pt,
                                                        const int* __restrict__ bnd_cs, const double* __restrict__ wg,
                                                        const double* __restrict__ eps_p, bool with_g,
-                                                       double* __restrict__ bres, ErrWords* __restrict__ err) {
+                                                       const double* __restrict__ sig, double* __restrict__ bres,
+                                                       ErrWords* __restrict__ err) {
     release_early();
     const int nbf = m.nf - m.nint;
     const int fb = blockIdx.x * blockDim.x + threadIdx.x;
@@ -432,8 +450,9 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
         const dm3 gc = with_g ? ldG(rcell) : cell_gradient_at(m, pt, wg, c);
         const d3 uc = ld3(rcell);
         const d3 del = ld3(fr + 32 * 3);
+        // the cell stress of the gradient pass (J2 needs its committed state), else the law
         bool okc;
-        const dm3 sc = stress(ph, gc, okc);
+        const dm3 sc = with_g && sig ? ld_sig(sig + tiled(c, kSig)) : stress(ph, gc, okc);
         if (pk == SFV_PATCH_DISPLACEMENT) {
             d3 gm = gam;
             if (ph.tl) {
@@ -684,8 +703,10 @@ void launch_grad(const DevMesh& m, const Physics& ph, const PatchTable& pt, cons
                  cudaStream_t st) {
     const int cb = (m.nc + 255) / 256;
     const bool gen = ph.law != SFV_LAW_HOOKE || ph.tl;
-    if (gen) launch_win(grad_cell_kernel<S, true>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, err);
-    else launch_win(grad_cell_kernel<S, false>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, err);
+    if (ph.law == SFV_LAW_J2)
+        launch_win(grad_cell_kernel<S, true, true>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, ps.lawst, err);
+    else if (gen) launch_win(grad_cell_kernel<S, true>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, ps.lawst, err);
+    else launch_win(grad_cell_kernel<S, false>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, ps.lawst, err);
 }
 
 template <bool PERT, int S>
@@ -718,12 +739,12 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
         if (ps.side) {  // beside the gradient pass: the boundary pass computes its own cells' gradients
             cudaStreamWaitEvent(ps.side, ps.ev_w, 0);
             boundary_kernel<<<(nbf + 127) / 128, 128, 0, ps.side>>>(m, ph, pt, ps.bnd_cs, wg, PERT ? eps : no_eps,
-                                                                   false, ps.bres, err);
+                                                                   false, no_eps, ps.bres, err);
             cudaEventRecord(ps.ev_b, ps.side);
             cudaStreamWaitEvent(st, ps.ev_b, 0);
         } else {
             launch_win(boundary_kernel, (nbf + 127) / 128, 128, st, ps, m, ph, pt, ps.bnd_cs, wg, PERT ? eps : no_eps,
-                       true, ps.bres, err);
+                       true, static_cast<const double*>(ps.sig), ps.bres, err);
         }
     }
     if (ps.marks) cudaEventRecord(ps.marks[2], st);
@@ -764,16 +785,18 @@ int eps_perturb_grid_for(int nc) { return eps_perturb_grid(nc); }
 
 void launch_gradients_pair(const DevMesh& m, const PatchTable& pt, const Physics& ph, const double* u, double* G,
                            const PairScratch& ps, ErrWords* err, cudaStream_t s) {
-    Physics hp = ph;  // gradients only: no stress evaluation
-    hp.law = SFV_LAW_HOOKE;
-    hp.tl = 0;
+    Physics hp = ph;  // gradients only: no stress evaluation (except a J2 commit pass)
+    if (!ph.commit) {
+        hp.law = SFV_LAW_HOOKE;
+        hp.tl = 0;
+    }
     const int cb = (m.nc + 255) / 256;
     launch_win(perturb_kernel<false>, cb, 256, s, ps, m.nc, u, u, static_cast<double*>(nullptr), ps.wg,
                static_cast<const double*>(nullptr), 0, static_cast<double*>(nullptr), false);
     if (m.spad == 4) launch_grad<4>(m, hp, pt, ps, err, s);
     else if (m.spad == 6) launch_grad<6>(m, hp, pt, ps, err, s);
     else launch_grad<8>(m, hp, pt, ps, err, s);
-    untile_grad_kernel<<<cb, 256, 0, s>>>(m.nc, ps.wg, G);
+    if (G) untile_grad_kernel<<<cb, 256, 0, s>>>(m.nc, ps.wg, G);
 }
 
 }  // namespace sfv

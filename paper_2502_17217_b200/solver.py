@@ -76,6 +76,8 @@ def lib():
         "sfv_residual": (C.c_int, [_vp, _vp, _vp, _ip]),
         "sfv_stabilisation": (C.c_int, [_vp, _vp, _vp, _ip]),
         "sfv_gradients": (C.c_int, [_vp, _vp, _vp, _ip]),
+        "sfv_commit": (C.c_int, [_vp, _vp]),
+        "sfv_law_state": (C.c_int, [_vp, _vp]),
         "sfv_jv": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _ip]),
         "sfv_jv_eps": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _vp, _ip]),
         "sfv_jv_async": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
@@ -238,6 +240,18 @@ class ResidualEvaluator:
         self._check(self.L.sfv_stabilisation(self.h, _ptr(ud), _ptr(r), C.byref(cell)), cell.value)
         return r
 
+    def commit(self, u):
+        """ResidualEvaluator::commit (discretisation.cpp:91-95): J2's trial state at u becomes the
+        committed state (a no-op for the hyperelastic laws)."""
+        ud = to_device(u)
+        self._check(self.L.sfv_commit(self.h, _ptr(ud)))
+
+    def law_state(self):
+        """Committed J2 state, (n_cells, 19): b_bar (row-major), eps_p, F (PlasticCell)."""
+        out = np.zeros(19 * self.mesh.n_cells)
+        self._check(self.L.sfv_law_state(self.h, out.ctypes.data))
+        return out.reshape(-1, 19)
+
     def gradients(self, u):
         """cell_gradients (discretisation.cpp:10-31) as an (n_cells, 3, 3) array, G[c, i, j] = du_j/dx_i."""
         ud = to_device(u)
@@ -262,10 +276,6 @@ class ResidualEvaluator:
                             sing.ctypes.data_as(C.POINTER(C.c_byte)), iptr(cfo), iptr(cff), dptr(ls))
         g.update(g_singular=sing, cf_offsets=cfo, cf_faces=cff, ls_vec=ls)
         return g
-
-    def commit(self, u):
-        """Re-evaluates stress at u (stateless laws: nothing to promote)."""
-        self.residual(u)
 
 
 def jacobian_vector_product(ev: ResidualEvaluator, u, r_u, v, eps: float | None = None):

@@ -22,6 +22,8 @@ def load(path):
                  bc_ramp=z["bc_ramp"])
     if "guccione" in z:
         ph.guccione = tuple(float(x) for x in z["guccione"])
+    if "j2_curve" in z:
+        ph.j2_curve = tuple(float(x) for x in z["j2_curve"])
     return z, m, ph
 
 
@@ -50,6 +52,11 @@ def test_oracle_matches_reference_golden(path):
     o2 = OracleCase(m, ph)
     nsteps = int(z["steps_n"]) if "steps_n" in z else len(z["steps_newton"])
     f, reps, _ = o2.run_steps(z["steps_field0"], solver_cfg(r_tol=1e-8), nsteps)
+    if "residual_after_commit" in z:
+        o3 = OracleCase(m, ph)
+        o3.set_time(float(z["time"]))
+        o3.commit(u)
+        assert np.array_equal(o3.residual(0.5 * u), z["residual_after_commit"])
     assert [r.outer_iters for r in reps] == list(z["steps_newton"])
     assert [sum(r.summary()["krylov_per_newton"]) for r in reps] == list(z["steps_krylov"])
     assert np.abs(f - z["steps_field"]).max() <= 1e-12 * max(np.abs(z["steps_field"]).max(), 1e-300)
@@ -68,7 +75,7 @@ def test_gpu_matches_reference_golden(path):
     r = ev.residual(u).cpu().numpy()
     # neo-Hookean: pow(), Guccione: exp() are not correctly rounded on either side; Hooke and
     # St. Venant-Kirchhoff are +, -, *, / only and bit-identical
-    tol = 0.0 if ph.law in (0, 2) else 1e-12
+    tol = 0.0 if ph.law in (0, 2) else 1e-12  # J2: pow, exp in the return map
     assert np.abs(r - z["residual"]).max() <= tol * np.abs(z["residual"]).max()
     jv = sv.jacobian_vector_product(ev, u, z["residual"], v).cpu().numpy()
     assert np.linalg.norm(jv - z["jv"]) <= 1e-6 * np.linalg.norm(z["jv"])
@@ -86,6 +93,12 @@ def test_gpu_matches_reference_golden(path):
     ev2 = sv.ResidualEvaluator(m, ph)
     nsteps = int(z["steps_n"]) if "steps_n" in z else len(z["steps_newton"])
     f, reps, _ = sv.run_steps(ev2, z["steps_field0"], solver_cfg(r_tol=1e-8), nsteps)
+    if "residual_after_commit" in z:
+        ev3 = sv.ResidualEvaluator(m, ph)
+        ev3.set_time(float(z["time"]))
+        ev3.commit(u)
+        r3 = ev3.residual(0.5 * u).cpu().numpy()
+        assert np.abs(r3 - z["residual_after_commit"]).max() <= 1e-12 * np.abs(z["residual_after_commit"]).max()
     assert [r.outer_iters for r in reps] == list(z["steps_newton"])
     for rep, b in zip(reps, z["steps_krylov"]):
         a = sum(rep.summary()["krylov_per_newton"])

@@ -330,3 +330,38 @@ def test_guccione_overflow_reported():
     with pytest.raises(sv.SolidfvError) as e3:
         sv.jacobian_vector_product(ev, u, np.zeros_like(u), np.ones_like(u))
     assert e3.value.kind == "JvpNan"
+
+
+@pytest.mark.parametrize("table", [False, True])
+def test_j2_commit_and_state(table):
+    """J2 plasticity (J2PlasticLaw, laws.cpp:104-214): the stress is the radial return from the
+    committed state, commit() promotes the trial state at u.  Residuals before and after a
+    commit and the committed state itself (b_bar, eps_p, F) against the oracle; saturation and
+    piecewise-linear hardening (HardeningCurve::value / slope)."""
+    from paper_2502_17217_b200.abi import LAW_J2
+    sv = _sv()
+    mesh = sv.box_mesh((2.0, 1.0, 1.0), (10, 5, 5), [D, D, T, T, T, T], distort=0.08, seed=9)
+    phys = _phys(law=LAW_J2)
+    phys.mu, phys.lam = 200e9 / 2.6, 200e9 / 1.2
+    phys.bc_value[1] = (0.01, 0.0, 0.0)
+    if table:
+        phys.j2_table = np.array([[0.0, 250e6], [0.002, 300e6], [0.01, 340e6], [0.05, 380e6]])
+    else:
+        phys.j2_curve = (250e6, 1e9, 400e6, 20.0)
+    ev, orc = _pair(mesh, phys)
+    u, v = cases.jv_inputs(mesh, seed=4)
+    u = u * 1e3
+    tol = 1e-12  # pow / exp in the return map are not correctly rounded on either side
+    r0 = ev.residual(u).cpu().numpy()
+    assert np.abs(r0 - orc.residual(u)).max() <= tol * np.abs(r0).max()
+    ev.commit(u)
+    orc.commit(u)
+    s_gpu, s_orc = ev.law_state(), orc.law_state()
+    assert (s_orc[:, 9] > 0).sum() > mesh.n_cells // 2  # most cells yielded
+    assert np.abs(s_gpu - s_orc).max() <= 1e-12 * np.abs(s_orc).max()
+    r1 = ev.residual(0.6 * u).cpu().numpy()
+    r1o = orc.residual(0.6 * u)
+    assert np.abs(r1 - r1o).max() <= tol * np.abs(r1o).max()
+    jv = sv.jacobian_vector_product(ev, 0.6 * u, r1o, v).cpu().numpy()
+    ref = orc.jv(0.6 * u, r1o, v)
+    assert np.linalg.norm(jv - ref) / np.linalg.norm(ref) < 1e-6
