@@ -19,6 +19,7 @@
 #include <thread>
 #include <vector>
 
+#include "host_threads.h"
 #include "device.h"
 #include "host_mesh.h"
 #include "precond_host.h"
@@ -197,7 +198,7 @@ std::string build_layout(sfv_ctx* c) {
     if (static_cast<size_t>(slots) * nc > static_cast<size_t>(INT_MAX) || nc > (INT_MAX >> 3))
         return "mesh: too many cells for 32-bit slot indices";
     auto par = [](int n, const std::function<void(int, int)>& body) {  // independent ranges
-        const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+        const int nth = host_threads();
         std::vector<std::thread> th;
         const int ch = (n + nth - 1) / nth;
         for (int k = 0; k < nth; ++k) th.emplace_back(body, std::min(n, k * ch), std::min(n, (k + 1) * ch));

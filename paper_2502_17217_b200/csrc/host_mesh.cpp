@@ -2,6 +2,7 @@
 //
 // Restates /root/reference/proj/src/mesh.cpp arithmetic exactly (see host_mesh.h);
 // every V3 helper below mirrors the operator of include/solidfv/types.hpp it stands for.
+#include "host_threads.h"
 #include "host_mesh.h"
 
 #include <algorithm>
@@ -309,7 +310,7 @@ namespace {
 // Runs body(i) for i in [0, n) on up to 16 threads; body returns "" or an error.  Returns
 // the error of the smallest failing index, i.e. what the sequential loop would report.
 std::string parallel_for(int n, const std::function<std::string(int)>& body) {
-    const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    const int nth = host_threads();
     if (n < 4096 || nth == 1) {
         for (int i = 0; i < n; ++i)
             if (std::string e = body(i); !e.empty()) return e;

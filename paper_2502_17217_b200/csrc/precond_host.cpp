@@ -1,5 +1,6 @@
 // precond_host.cpp — preconditioner setup on the host (once per run, as in the reference:
 // run_steps factors once and reuses the factor for every step, nonlinear.cpp:390-400).
+#include "host_threads.h"
 #include "precond_host.h"
 
 #include <algorithm>
@@ -81,7 +82,7 @@ std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar,
                 if (transient) s.val[find(i, i)] += (-2.25 * rho * g.volume[i] / (dt * dt)) * 1.0;
             }
         };
-        const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+        const int nth = host_threads();
         std::vector<std::thread> th;
         const int ch = (nc + nth - 1) / nth;
         for (int k = 0; k < nth; ++k) th.emplace_back(rows, std::min(nc, k * ch), std::min(nc, (k + 1) * ch));
@@ -227,8 +228,7 @@ bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nth
 
 std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& out) {
     const int n = a.n;
-    const int hw = static_cast<int>(std::thread::hardware_concurrency());
-    const int nthreads = std::max(1, std::min(16, hw));
+    const int nthreads = host_threads();
     if (level <= 1 && n >= 65536 && nthreads > 1 && !std::getenv("SFV_ILU_SERIAL") &&
         iluk_factor_parallel(a, level, out, nthreads))
         return "";
@@ -330,7 +330,7 @@ void pack(const std::vector<int>& level, int n_levels, TriSchedule& t,
     t.rp.assign(t.n_pos + 1, 0);
     t.diag.assign(t.n_pos, 1.0);
     // rows gathered by position ranges in parallel, then concatenated in position order
-    const int nthr = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    const int nthr = host_threads();
     const int pchunk = (t.n_pos + nthr - 1) / nthr;
     std::vector<std::vector<int>> pc(nthr);
     std::vector<std::vector<double>> pv(nthr);
@@ -373,7 +373,7 @@ void pack(const std::vector<int>& level, int n_levels, TriSchedule& t,
         if (t.order[p] >= 0) t.pos[t.order[p]] = p;
     t.ell_pcol.assign(static_cast<size_t>(t.maxd) * t.n_pos, -1);
     // ELL transposition: entry k of position p at k * n_pos + p; threads own position ranges
-    const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    const int nth = host_threads();
     auto ell = [&](int p0, int p1) {
         for (int p = p0; p < p1; ++p)
             for (int q = t.rp[p]; q < t.rp[p + 1]; ++q) {
@@ -533,7 +533,7 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
     long long n_dep = 0, n_local = 0, n_near = 0, n_near_remote = 0;
     // positions are independent: threads own position ranges; statistics only when asked
     const bool stats = std::getenv("SFV_STREAM_STATS") != nullptr;
-    const int nthr = stats ? 1 : std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    const int nthr = stats ? 1 : host_threads();
     std::atomic<bool> bad{false};
     auto body = [&](int p0, int p1) {
     for (int p = p0; p < p1 && !bad; ++p) {
@@ -727,7 +727,7 @@ bool build_pipe(const ScalarCsr& lu, bool upper, int blocks, int ring, PipeSched
 void pack_stream_chunks(const std::vector<StreamRecord>& recs, std::vector<unsigned char>& out) {
     const size_t nchunk = (recs.size() + 31) / 32;
     out.assign(nchunk * kChunkBytes, 0);
-    const int nthr = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+    const int nthr = host_threads();
     auto body = [&](size_t c0, size_t c1) {
         for (size_t ch = c0; ch < c1; ++ch) {
             unsigned char* c = out.data() + ch * kChunkBytes;

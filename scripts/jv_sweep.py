@@ -19,7 +19,7 @@ import torch  # noqa: E402
 from paper_2502_17217_b200 import cases  # noqa: E402
 from paper_2502_17217_b200 import solver as sv  # noqa: E402
 
-NAMES = ["jv_eps_kernel", "perturb_kernel", "grad_cell_kernel", "boundary_kernel", "flux_pair_kernel"]
+NAMES = ["norm_partials_kernel", "eps_perturb_kernel", "grad_cell_kernel", "boundary_kernel", "flux_pair_kernel"]
 
 
 def peak():
