@@ -499,7 +499,8 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
     // s < 3) overlap the face work of tile i + 1, and the barrier of tile i + 1 orders
     // them before buffer i & 1 is rewritten by tile i + 2
     __shared__ double res_buf[2][S][6][kCells];
-    __shared__ unsigned char kind_buf[2][S][kCells];
+    // slot kinds lane-major, 8 bytes per cell: the summing thread reads them in one 64-bit load
+    __shared__ __align__(8) unsigned char kind_buf[2][kCells][8];
     const int lane = threadIdx.x % kCells, s = threadIdx.x / kCells;
     const int ntiles = (m.nc + kCells - 1) / kCells;
     // Persistent grid-stride loop over tiles of kCells cells (= the tiles of the tables).
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         double(*res)[6][kCells] = res_buf[it & 1];
-        unsigned char(*kind)[kCells] = kind_buf[it & 1];
+        unsigned char(*kind)[8] = kind_buf[it & 1];
         const int fr = fr_next, o = o_next;
         const double ru = ru_next;
         fetch(tile + gridDim.x, fr_next, o_next, ru_next);
@@ -606,7 +607,7 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
             res[s][4][lane] = st.y;
             res[s][5][lane] = st.z;
         }
-        kind[s][lane] = kd;
+        kind[lane][s] = kd;
         __syncthreads();
         // (component k = s, cell c): the reference's per-cell summation order
         if (s < 3 && c < m.nc) {
@@ -616,14 +617,15 @@ __global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
                 out[ik] = 0.0;
             } else {
                 double r = 0.0;
+                const unsigned long long kw = *reinterpret_cast<const unsigned long long*>(kind[lane]);
                 if (!ph.stab_only) {
 #pragma unroll
                     for (int t = 0; t < S; ++t)
-                        if (kind[t][lane] != 0) r += res[t][k][lane];
+                        if ((kw >> (8 * t)) & 0xff) r += res[t][k][lane];
                 }
 #pragma unroll
                 for (int t = 0; t < S; ++t)
-                    if (kind[t][lane] == 2) r += res[t][3 + k][lane];
+                    if (((kw >> (8 * t)) & 0xff) == 2) r += res[t][3 + k][lane];
                 if (ph.transient && !ph.stab_only) {  // BDF2 inertia (discretisation.cpp:48-57, :163-169)
                     const double uc = wg[tiled(c, kWG) + 32 * k];
                     const double idt = 1.0 / (2.0 * ph.dt);
