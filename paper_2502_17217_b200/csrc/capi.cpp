@@ -1223,7 +1223,8 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     std::string e = m.finalise();
     if (!e.empty()) return fail(e);
     pt.mark("mesh copy + finalise");
-    e = compute_geometry(m, c->geom);
+    // geometry on the device by default (bit-identical; SFV_HOST_GEOMETRY=1: the host passes)
+    e = std::getenv("SFV_HOST_GEOMETRY") ? compute_geometry(m, c->geom) : device_geometry(m, c->geom);
     if (!e.empty()) return fail(e);
     pt.mark("compute_geometry");
     // ResidualEvaluator ctor checks (discretisation.cpp:64-67)

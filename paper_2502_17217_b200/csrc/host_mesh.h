@@ -61,5 +61,7 @@ HostMesh kuhn_tets(const double ext[3], int n, const int kinds[6], uint64_t perm
                    bool rcm);
 // compute_geometry (mesh.cpp:347-510).
 std::string compute_geometry(const HostMesh& m, HostGeometry& g);
+// The same on the device (geometry.cu): bit-identical results and error texts.
+std::string device_geometry(const HostMesh& m, HostGeometry& g);
 
 }  // namespace sfv

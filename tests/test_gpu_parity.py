@@ -365,3 +365,25 @@ def test_j2_commit_and_state(table):
     jv = sv.jacobian_vector_product(ev, 0.6 * u, r1o, v).cpu().numpy()
     ref = orc.jv(0.6 * u, r1o, v)
     assert np.linalg.norm(jv - ref) / np.linalg.norm(ref) < 1e-6
+
+
+@pytest.mark.parametrize("mesh_kind", ["hex_symmetry", "tets"])
+def test_device_geometry_bitwise(mesh_kind, monkeypatch):
+    """compute_geometry on the device (geometry.cu, default) equals the host passes and the
+    oracle bit for bit: face centroids, areas, d, w, Delta, volumes, centroids, G^-1, the
+    least-squares vectors and the singular flags; geometry errors carry the same text."""
+    sv = _sv()
+    if mesh_kind == "tets":
+        mesh = sv.kuhn_tet_mesh((1.0, 1.0, 1.0), 8, [D, T, T, T, T, T], 7, True, True)
+        phys = _phys()
+    else:
+        mesh = sv.box_mesh((1.0, 1.0, 1.0), (9, 7, 6), [D, T, S, T, S, T], distort=0.2, seed=11)
+        phys = _phys()
+    g_dev = sv.ResidualEvaluator(mesh, phys).geometry()
+    monkeypatch.setenv("SFV_HOST_GEOMETRY", "1")
+    g_host = sv.ResidualEvaluator(mesh, phys).geometry()
+    g_orc = OracleCase(mesh, phys).geometry()
+    for k in g_dev:
+        assert np.array_equal(g_dev[k], g_host[k]), k
+        if k in g_orc:
+            assert np.array_equal(g_dev[k], g_orc[k]), k
