@@ -121,6 +121,7 @@ struct sfv_ctx {
     DevBuf<double> slot_ls, gam, del, dmag, w, volume, tls;
     // jv_pair.cu scratch + tiled face records (device.h): pwg = tiled [w | G], psig: tiled cell stress
     DevBuf<double> pwg, face9, bres, psig, lawst;
+    DeviceGeometry* dgeo = nullptr;  // device-resident geometry (the host copy is partial until host_geometry())
     PairScratch ps;
     // scratch
     DevBuf<double> grad, red, scal;  // scal: [0]=eps [1]=u_norm [2..] misc
@@ -161,6 +162,7 @@ struct sfv_ctx {
     long long launches = 0;
     SfvError last{0, -1, ""};
     ~sfv_ctx() {
+        free_device_geometry(dgeo);
         if (ps.ev_w) cudaEventDestroy(ps.ev_w);
         if (ps.ev_b) cudaEventDestroy(ps.ev_b);
         if (ps.side) cudaStreamDestroy(ps.side);
@@ -190,6 +192,9 @@ void update_patch_values(sfv_ctx* c) {
 
 std::string build_layout(sfv_ctx* c) {
     const HostMesh& m = c->mesh;
+    // the alternative J.v kernels build their tables on the host from the full geometry
+    if (c->jv_path != 0)
+        if (std::string e = download_geometry(c->dgeo, c->geom); !e.empty()) return e;
     const HostGeometry& g = c->geom;
     const int nc = m.n_cells, nf = m.n_faces();
     int slots = 0;
@@ -211,9 +216,12 @@ std::string build_layout(sfv_ctx* c) {
     const size_t nsl = legacy ? static_cast<size_t>(slots) * nc : 0;
     std::vector<int> sf(nsl, -1), so(nsl, -1);
     std::vector<double> sl(3 * nsl, 0.0);
-    std::vector<int> tsl(legacy ? 0 : static_cast<size_t>(ntc) * 2 * spad * 32, -1);
-    std::vector<double> tls(legacy ? 0 : static_cast<size_t>(ntc) * 3 * spad * 32, 0.0);
-    std::vector<int> bsi(std::max(1, nf - m.n_internal), 0);
+    // default path with the geometry on the device: the tables are built there (geometry.cu)
+    const bool on_dev = !legacy && c->dgeo;
+    std::vector<int> tsl(legacy || on_dev ? 0 : static_cast<size_t>(ntc) * 2 * spad * 32, -1);
+    std::vector<double> tls(legacy || on_dev ? 0 : static_cast<size_t>(ntc) * 3 * spad * 32, 0.0);
+    std::vector<int> bsi(on_dev ? 0 : std::max(1, nf - m.n_internal), 0);
+    if (!on_dev)
     par(nc, [&](int i0, int i1) {
     for (int i = i0; i < i1; ++i) {
         int s = 0;
@@ -244,7 +252,8 @@ std::string build_layout(sfv_ctx* c) {
     });
     const size_t nfl = legacy ? static_cast<size_t>(nf) : 0;
     std::vector<double> gm(3 * nfl), de(3 * nfl), dmg(nfl), ww(nfl);
-    std::vector<double> f9(legacy ? 0 : static_cast<size_t>(ntf) * 9 * 32, 0.0);
+    std::vector<double> f9(legacy || on_dev ? 0 : static_cast<size_t>(ntf) * 9 * 32, 0.0);
+    if (!on_dev)
     par(nf, [&](int f0, int f1) {
     for (int f = f0; f < f1; ++f) {
         if (legacy) {
@@ -269,12 +278,20 @@ std::string build_layout(sfv_ctx* c) {
         for (int q = 0; q < 9; ++q) f9[fb + 32 * q] = rec[q];
     }
     });
+    const size_t nbs = std::max(1, nf - m.n_internal);
     if ((legacy && (!c->slot_face.upload(sf) || !c->slot_other.upload(so) || !c->slot_ls.upload(sl) ||
                     !c->gam.upload(gm) || !c->del.upload(de) || !c->dmag.upload(dmg) || !c->w.upload(ww))) ||
-        (!legacy && (!c->tslot.upload(tsl) || !c->tls.upload(tls) || !c->face9.upload(f9) ||
-                     !c->pwg.alloc(static_cast<size_t>(ntc) * kWG * 32))) ||
-        !c->bnd_si.upload(bsi) || !c->bres.alloc(6 * bsi.size()))
+        (!legacy && !on_dev && (!c->tslot.upload(tsl) || !c->tls.upload(tls) || !c->face9.upload(f9))) ||
+        (on_dev && (!c->tslot.alloc(static_cast<size_t>(ntc) * 2 * spad * 32) ||
+                    !c->tls.alloc(static_cast<size_t>(ntc) * 3 * spad * 32) ||
+                    !c->face9.alloc(static_cast<size_t>(ntf) * 9 * 32) || !c->bnd_si.alloc(nbs))) ||
+        (!legacy && !c->pwg.alloc(static_cast<size_t>(ntc) * kWG * 32)) ||
+        (!on_dev && !c->bnd_si.upload(bsi)) || !c->bres.alloc(6 * nbs))
         return "cuda: out of device memory for the mesh layout";
+    if (on_dev) {
+        const std::string le = device_layout(c->dgeo, spad, c->tslot.p, c->tls.p, c->face9.p, c->bnd_si.p);
+        if (!le.empty()) return le;
+    }
     if (c->ph.transient && !c->volume.upload(g.volume)) return "cuda: out of device memory";
     DevMesh& d = c->dm;
     d.nc = nc;
@@ -1224,7 +1241,7 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
     if (!e.empty()) return fail(e);
     pt.mark("mesh copy + finalise");
     // geometry on the device by default (bit-identical; SFV_HOST_GEOMETRY=1: the host passes)
-    e = std::getenv("SFV_HOST_GEOMETRY") ? compute_geometry(m, c->geom) : device_geometry(m, c->geom);
+    e = std::getenv("SFV_HOST_GEOMETRY") ? compute_geometry(m, c->geom) : device_geometry(m, c->geom, &c->dgeo);
     if (!e.empty()) return fail(e);
     pt.mark("compute_geometry");
     // ResidualEvaluator ctor checks (discretisation.cpp:64-67)
@@ -1353,6 +1370,7 @@ int sfv_geometry(const sfv_ctx* c, double* volume, double* centroid, double* fac
                  double* d_mag, double* w, double* delta, double* g_inv, signed char* g_singular, int* cf_offsets,
                  int* cf_faces, double* ls_vec) {
     const HostMesh& m = c->mesh;
+    if (std::string e = download_geometry(c->dgeo, const_cast<sfv_ctx*>(c)->geom); !e.empty()) return SFV_ERR_CUDA;
     const HostGeometry& g = c->geom;
     for (int i = 0; i < m.n_cells; ++i) {
         volume[i] = g.volume[i];

@@ -222,6 +222,8 @@ __global__ void cell_ls_kernel(Topo t, Geo g) {
     }
 }
 
+}  // namespace
+
 template <typename T>
 struct Buf {
     T* p = nullptr;
@@ -233,19 +235,121 @@ struct Buf {
     bool down(T* h, size_t n) const { return !n || cudaMemcpy(h, p, sizeof(T) * n, cudaMemcpyDeviceToHost) == cudaSuccess; }
 };
 
+namespace {
+
+// Layout of the default J.v path from the device-resident geometry (capi.cpp build_layout,
+// host twin): per cell, its face slots in cell_faces order — face | neighbour bit, other cell
+// or -(2 + patch), least-squares vector — into the tiled tables; per boundary face its
+// cell * 8 + slot.
+__global__ void slot_layout_kernel(Topo t, const int* __restrict__ face_patch, const double* __restrict__ ls,
+                                   int spad, int* __restrict__ tsl, double* __restrict__ tls,
+                                   int* __restrict__ bnd) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= t.nc) return;
+    const size_t tb = static_cast<size_t>(i >> 5) * (2 * spad * 32) + (i & 31);
+    const size_t lb = static_cast<size_t>(i >> 5) * (3 * spad * 32) + (i & 31);
+    int s = 0;
+    for (int q = t.cf_off[i]; q < t.cf_off[i + 1]; ++q, ++s) {
+        const int f = t.cf[q];
+        const bool nb = f < t.nint && t.neigh[f] == i;
+        tsl[tb + 32 * s] = f | (nb ? static_cast<int>(0x80000000u) : 0);
+        tsl[tb + 32 * (spad + s)] = f < t.nint ? (nb ? t.owner[f] : t.neigh[f]) : -(2 + face_patch[f]);
+        tls[lb + 32 * (3 * s)] = ls[3 * static_cast<size_t>(q)];
+        tls[lb + 32 * (3 * s + 1)] = ls[3 * static_cast<size_t>(q) + 1];
+        tls[lb + 32 * (3 * s + 2)] = ls[3 * static_cast<size_t>(q) + 2];
+        if (f >= t.nint) bnd[f - t.nint] = i * 8 + s;
+    }
+}
+// face records: Gamma, Delta, |Delta| / |d|, |Gamma|, w (the host's rec[] of build_layout:
+// sqrt of the left-to-right dot, then one divide — the per-face constants of rhie_chow)
+__global__ void face_record_kernel(int nf, const double* __restrict__ area, const double* __restrict__ delta,
+                                   const double* __restrict__ dmag, const double* __restrict__ w,
+                                   double* __restrict__ f9) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    const double a0 = area[3 * f], a1 = area[3 * f + 1], a2 = area[3 * f + 2];
+    const double d0 = delta[3 * f], d1 = delta[3 * f + 1], d2 = delta[3 * f + 2];
+    const double rec[9] = {a0, a1, a2, d0, d1, d2, sqrt(d0 * d0 + d1 * d1 + d2 * d2) / dmag[f],
+                           sqrt(a0 * a0 + a1 * a1 + a2 * a2), w[f]};
+    const size_t b = static_cast<size_t>(f >> 5) * (9 * 32) + (f & 31);
+    for (int q = 0; q < 9; ++q) f9[b + 32 * q] = rec[q];
+}
+
 }  // namespace
+
+// device buffers kept from device_geometry for device_layout
+struct DeviceGeometry {
+    Buf<double> pts, fc, area, amag, normal, d, dmag, w, delta, delmag, vol, cen, ginv, ls;
+    Buf<int> foff, fpts, own, nei, cfo, cfq, fkd, fpatch, err;
+    Buf<signed char> sing;
+    Topo t{};
+};
+
+void free_device_geometry(DeviceGeometry* g) { delete g; }
+
+std::string device_layout(const DeviceGeometry* dg, int spad, int* tsl, double* tls, double* f9, int* bnd) {
+    const Topo& t = dg->t;
+    const int ntc = (t.nc + 31) / 32;
+    cudaMemset(tsl, 0xff, sizeof(int) * static_cast<size_t>(ntc) * 2 * spad * 32);
+    cudaMemset(tls, 0, sizeof(double) * static_cast<size_t>(ntc) * 3 * spad * 32);
+    cudaMemset(f9, 0, sizeof(double) * static_cast<size_t>((t.nf + 31) / 32) * 9 * 32);
+    slot_layout_kernel<<<(t.nc + 255) / 256, 256>>>(t, dg->fpatch.p, dg->ls.p, spad, tsl, tls, bnd);
+    face_record_kernel<<<(t.nf + 255) / 256, 256>>>(t.nf, dg->area.p, dg->delta.p, dg->dmag.p, dg->w.p, f9);
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess) return "cuda: device layout failed";
+    return "";
+}
+
+// the device-resident geometry fields download_geometry has not copied yet
+std::string download_geometry(const DeviceGeometry* dg, HostGeometry& g) {
+    if (!g.ls.empty() || !dg) return "";
+    const Topo& t = dg->t;
+    const int nf = t.nf, nc = t.nc;
+    size_t ncf = 0;
+    {
+        int last = 0;
+        if (cudaMemcpy(&last, dg->cfo.p + nc, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return "cuda: geometry download failed";
+        ncf = static_cast<size_t>(last);
+    }
+    g.face_centroid.resize(nf);
+    g.area.resize(nf);
+    g.d.resize(nf);
+    g.w.resize(nf);
+    g.delta.resize(nf);
+    g.centroid.resize(nc);
+    g.g_inv.resize(9 * static_cast<size_t>(nc));
+    g.ls.resize(ncf);
+    const bool dn = dg->fc.down(&g.face_centroid[0].x, 3 * nf) && dg->area.down(&g.area[0].x, 3 * nf) &&
+                    dg->d.down(&g.d[0].x, 3 * nf) && dg->w.down(g.w.data(), nf) &&
+                    dg->delta.down(&g.delta[0].x, 3 * nf) && dg->cen.down(&g.centroid[0].x, 3 * nc) &&
+                    dg->ginv.down(g.g_inv.data(), 9 * static_cast<size_t>(nc)) && dg->ls.down(&g.ls[0].x, 3 * ncf);
+    return dn ? "" : "cuda: geometry download failed";
+}
 
 // compute_geometry on the device; fills g exactly as compute_geometry (host_mesh.cpp) does.
 // Returns "" or the reference's error text (the first failing face / cell of the first
 // failing pass), "cuda: ..." on a device failure.
-std::string device_geometry(const HostMesh& m, HostGeometry& g) {
+std::string device_geometry(const HostMesh& m, HostGeometry& g, DeviceGeometry** keep) {
     const int nf = m.n_faces(), nc = m.n_cells;
     const size_t np = m.points.size(), ncf = m.cf.size();
     std::vector<int> fk(nf, -1);
     for (int f = m.n_internal; f < nf; ++f) fk[f] = m.patches[m.face_patch[f]].kind;
-    Buf<double> pts, fc, area, amag, normal, d, dmag, w, delta, delmag, vol, cen, ginv, ls;
-    Buf<int> foff, fpts, own, nei, cfo, cfq, fkd, err;
-    Buf<signed char> sing;
+    DeviceGeometry* dg = new DeviceGeometry;
+    struct Own {
+        DeviceGeometry*& p;
+        DeviceGeometry** keep;
+        ~Own() {
+            if (keep && p) *keep = p;
+            else delete p;
+        }
+    } own_dg{dg, keep};
+    Buf<double>&pts = dg->pts, &fc = dg->fc, &area = dg->area, &amag = dg->amag, &normal = dg->normal, &d = dg->d,
+                &dmag = dg->dmag, &w = dg->w, &delta = dg->delta, &delmag = dg->delmag, &vol = dg->vol,
+                &cen = dg->cen, &ginv = dg->ginv, &ls = dg->ls;
+    Buf<int>&foff = dg->foff, &fpts = dg->fpts, &own = dg->own, &nei = dg->nei, &cfo = dg->cfo, &cfq = dg->cfq,
+             &fkd = dg->fkd, &err = dg->err;
+    Buf<signed char>& sing = dg->sing;
+    if (keep && !dg->fpatch.up(m.face_patch.data(), m.face_patch.size())) return "cuda: out of device memory";
     const bool ok = pts.up(&m.points[0].x, 3 * np) && foff.up(m.face_off.data(), m.face_off.size()) &&
                     fpts.up(m.face_pts.data(), m.face_pts.size()) && own.up(m.owner.data(), nf) &&
                     nei.up(m.neighbour.data(), nf) && cfo.up(m.cf_off.data(), m.cf_off.size()) &&
@@ -259,6 +363,7 @@ std::string device_geometry(const HostMesh& m, HostGeometry& g) {
     cudaMemset(delta.p, 0, 3 * sizeof(double) * nf);
     cudaMemset(delmag.p, 0, sizeof(double) * nf);
     const Topo t{nf, nc, m.n_internal, pts.p, foff.p, fpts.p, own.p, nei.p, cfo.p, cfq.p, fkd.p};
+    dg->t = t;
     const Geo gg{fc.p, area.p, amag.p, normal.p, d.p, dmag.p, w.p, delta.p, delmag.p, vol.p, cen.p, ginv.p, ls.p,
                  sing.p, err.p};
     const int bf = (nf + 255) / 256, bc = (nc + 255) / 256;
@@ -279,27 +384,19 @@ std::string device_geometry(const HostMesh& m, HostGeometry& g) {
                           : "compute_geometry: face " + std::to_string(f) + " area vector does not leave the owner";
     }
     cell_ls_kernel<<<bc, 256>>>(t, gg);
-    g.face_centroid.resize(nf);
-    g.area.resize(nf);
+    // what the host reads later (J~ assembly: |Gamma|, |d|, |Delta|, n, volume; the singular
+    // flags) now; the rest stays on the device until download_geometry (lazy: only the
+    // geometry API and the alternative J.v layouts read it)
     g.area_mag.resize(nf);
     g.normal.resize(nf);
-    g.d.resize(nf);
     g.d_mag.resize(nf);
-    g.w.resize(nf);
-    g.delta.resize(nf);
     g.delta_mag.resize(nf);
     g.volume.resize(nc);
-    g.centroid.resize(nc);
-    g.g_inv.resize(9 * static_cast<size_t>(nc));
     g.g_singular.resize(nc);
-    g.ls.resize(ncf);
-    const bool dn = fc.down(&g.face_centroid[0].x, 3 * nf) && area.down(&g.area[0].x, 3 * nf) &&
-                    amag.down(g.area_mag.data(), nf) && normal.down(&g.normal[0].x, 3 * nf) &&
-                    d.down(&g.d[0].x, 3 * nf) && dmag.down(g.d_mag.data(), nf) && w.down(g.w.data(), nf) &&
-                    delta.down(&g.delta[0].x, 3 * nf) && delmag.down(g.delta_mag.data(), nf) &&
-                    vol.down(g.volume.data(), nc) && cen.down(&g.centroid[0].x, 3 * nc) &&
-                    ginv.down(g.g_inv.data(), 9 * static_cast<size_t>(nc)) &&
-                    sing.down(g.g_singular.data(), nc) && ls.down(&g.ls[0].x, 3 * ncf);
+    bool dn = amag.down(g.area_mag.data(), nf) && normal.down(&g.normal[0].x, 3 * nf) &&
+              dmag.down(g.d_mag.data(), nf) && delmag.down(g.delta_mag.data(), nf) && vol.down(g.volume.data(), nc) &&
+              sing.down(g.g_singular.data(), nc);
+    if (dn && !keep) dn = download_geometry(dg, g).empty();
     if (!dn || cudaGetLastError() != cudaSuccess) return "cuda: compute_geometry failed";
     return "";
 }

@@ -61,7 +61,18 @@ HostMesh kuhn_tets(const double ext[3], int n, const int kinds[6], uint64_t perm
                    bool rcm);
 // compute_geometry (mesh.cpp:347-510).
 std::string compute_geometry(const HostMesh& m, HostGeometry& g);
-// The same on the device (geometry.cu): bit-identical results and error texts.
-std::string device_geometry(const HostMesh& m, HostGeometry& g);
+// The same on the device (geometry.cu): bit-identical results and error texts.  With keep,
+// the device-resident topology and geometry stay alive for device_layout (free with
+// free_device_geometry).
+struct DeviceGeometry;
+std::string device_geometry(const HostMesh& m, HostGeometry& g, DeviceGeometry** keep = nullptr);
+void free_device_geometry(DeviceGeometry* g);
+// With keep, device_geometry copies only |Gamma|, n, |d|, |Delta|, volumes and the singular
+// flags to the host; this copies the rest (no-op once done).
+std::string download_geometry(const DeviceGeometry* dg, HostGeometry& g);
+// Tiled slot tables (face code, other cell), least-squares vectors, face records and the
+// boundary-face slot indices of the default J.v path (device.h), built on the device into
+// preallocated arrays.
+std::string device_layout(const DeviceGeometry* g, int spad, int* tslot, double* tls, double* face9, int* bnd);
 
 }  // namespace sfv

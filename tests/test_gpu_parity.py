@@ -379,11 +379,17 @@ def test_device_geometry_bitwise(mesh_kind, monkeypatch):
     else:
         mesh = sv.box_mesh((1.0, 1.0, 1.0), (9, 7, 6), [D, T, S, T, S, T], distort=0.2, seed=11)
         phys = _phys()
-    g_dev = sv.ResidualEvaluator(mesh, phys).geometry()
+    ev_dev = sv.ResidualEvaluator(mesh, phys)
+    g_dev = ev_dev.geometry()
     monkeypatch.setenv("SFV_HOST_GEOMETRY", "1")
-    g_host = sv.ResidualEvaluator(mesh, phys).geometry()
+    ev_host = sv.ResidualEvaluator(mesh, phys)
+    g_host = ev_host.geometry()
     g_orc = OracleCase(mesh, phys).geometry()
     for k in g_dev:
         assert np.array_equal(g_dev[k], g_host[k]), k
         if k in g_orc:
             assert np.array_equal(g_dev[k], g_orc[k]), k
+    # the J.v tables built on the device from it (slots, least-squares vectors, face records)
+    # give the same residual bits as the host-built ones
+    u, _ = cases.jv_inputs(mesh, seed=3)
+    assert np.array_equal(ev_dev.residual(u).cpu().numpy(), ev_host.residual(u).cpu().numpy())
