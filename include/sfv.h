@@ -22,6 +22,7 @@
  *   sfv_precond_apply       <- Preconditioner::solve             linalg.hpp:55-59
  *   sfv_gmres_jv            <- gmres_solve(op = J.v at u)        linalg.hpp:94-97
  *   sfv_jfnk_solve          <- jfnk_solve                        nonlinear.hpp:96-97
+ *   sfv_segregated_solve    <- segregated_solve                  nonlinear.hpp:101-103
  *   sfv_run_steps           <- run_steps                         nonlinear.hpp:117-118
  *
  * Errors: every call returns SFV_OK or one SFV_ERR_* code (include/sfv_case.h), one
@@ -132,6 +133,11 @@ int sfv_precond_sweep(const sfv_ctx* ctx);
 int sfv_gmres_jv(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* b_dev, double* x_dev,
                  int restart, double rel_reduction, int max_iters, int* iters, int* status, double* rel_residual);
 int sfv_jfnk_solve(sfv_ctx* ctx, double* u_dev, const sfv_solver_cfg* cfg, sfv_solve_report* report);
+/* segregated_solve (nonlinear.hpp:101-103; nonlinear.cpp:268-351): per outer iteration, each
+ * displacement component by IC(0)-preconditioned CG on A = -J~ (Jacobi when IC(0) breaks
+ * down), then u += relaxation (u_next - u).  cfg->algorithm is ignored here; sfv_run_steps
+ * dispatches on it (SFV_ALG_SEGREGATED) as run_steps does. */
+int sfv_segregated_solve(sfv_ctx* ctx, double* u_dev, const sfv_solver_cfg* cfg, sfv_solve_report* report);
 /* field_dev: 6 consecutive device arrays of 3*n_cells doubles:
  * u, u_old, u_old_old, v_old, v_old_old, a_old (VectorField, fields.hpp:29-42) */
 int sfv_run_steps(sfv_ctx* ctx, double* field_dev, const sfv_solver_cfg* cfg, int n_steps,

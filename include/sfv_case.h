@@ -110,7 +110,11 @@ typedef struct sfv_solver_cfg {
     int max_krylov;         /* 300, per linear solve */
     int preconditioner;     /* SFV_PRECOND_* */
     int line_search;        /* 1 */
+    int algorithm;          /* SFV_ALG_JFNK (default) or SFV_ALG_SEGREGATED (Algorithm, nonlinear.hpp:17) */
+    double relaxation;      /* segregated update under-relaxation in (0, 1]; 0 => 1 */
 } sfv_solver_cfg;
+
+enum { SFV_ALG_JFNK = 0, SFV_ALG_SEGREGATED = 1 };
 
 typedef struct sfv_iteration_record {
     int step;
@@ -132,6 +136,7 @@ typedef struct sfv_solve_report {
     int n_records; /* number of valid entries in records (<= capacity) */
     sfv_iteration_record records[64];
     char detail[SFV_DETAIL_LEN];
+    int cg_diag_fallback; /* segregated: an IC(0) breakdown fell back to Jacobi (SolveReport) */
 } sfv_solve_report;
 
 #ifdef __cplusplus

@@ -144,6 +144,8 @@ SolverConfig solver_of(const sfv_solver_cfg* c) {
         PreconditionerKind::ilu1,      PreconditionerKind::ilu2, PreconditionerKind::lu};
     s.preconditioner = kinds[c->preconditioner];
     s.line_search = c->line_search != 0;
+    s.algorithm = c->algorithm == SFV_ALG_SEGREGATED ? Algorithm::segregated : Algorithm::jfnk;
+    s.relaxation = c->relaxation > 0.0 ? c->relaxation : 1.0;
     return s;
 }
 
@@ -165,6 +167,7 @@ void report_of(const SolveReport& r, sfv_solve_report* out) {
                            r.iterations[i].krylov_iters, r.iterations[i].s};
     }
     std::snprintf(out->detail, SFV_DETAIL_LEN, "%s", r.detail.c_str());
+    out->cg_diag_fallback = r.cg_diag_fallback ? 1 : 0;
 }
 
 }  // namespace

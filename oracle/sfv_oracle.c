@@ -21,6 +21,11 @@ typedef struct { double x, y, z; } v3;
 typedef struct { double m[3][3]; } m3;
 
 static inline double vget(v3 a, int i) { return i == 0 ? a.x : (i == 1 ? a.y : a.z); }
+static inline void vset(v3* a, int i, double v) {
+    if (i == 0) a->x = v;
+    else if (i == 1) a->y = v;
+    else a->z = v;
+}
 static inline v3 vadd(v3 a, v3 b) { return (v3){a.x + b.x, a.y + b.y, a.z + b.z}; }
 static inline v3 vsub(v3 a, v3 b) { return (v3){a.x - b.x, a.y - b.y, a.z - b.z}; }
 static inline v3 vscale(v3 a, double s) { return (v3){a.x * s, a.y * s, a.z * s}; } /* s*a, a*s */
@@ -986,7 +991,7 @@ double orc_time_jv(orc_case* h, const double* u, const double* r_u, const double
 /* assemble_approximate_jacobian (discretisation.cpp:216-262) followed by
  * BlockSparseMatrix::expand_scalar (linalg.cpp:135-158): the 3n x 3n scalar CSR with
  * every block entry kept, explicit zeros included. */
-static csr expanded_jacobian(const orc_case* h) {
+static m3* block_jacobian(const orc_case* h, int** rp_out, int** col_out) {
     const int nc = h->nc;
     int* rp = xcalloc(nc + 1, sizeof(int));
     for (int c = 0; c < nc; ++c) rp[c + 1] = 1;
@@ -1044,6 +1049,16 @@ static csr expanded_jacobian(const orc_case* h) {
             for (q = rp[c]; col[q] != c; ++q) {}
             blocks[q] = madd(blocks[q], mscale(mident(), -2.25 * h->rho * h->volume[c] / (h->dt * h->dt)));
         }
+    free(fill);
+    *rp_out = rp;
+    *col_out = col;
+    return blocks;
+}
+
+static csr expanded_jacobian(const orc_case* h) {
+    const int nc = h->nc;
+    int *rp, *col;
+    m3* blocks = block_jacobian(h, &rp, &col);
     csr m;
     m.n = 3 * nc;
     m.row_ptr = xcalloc(m.n + 1, sizeof(int));
@@ -1064,9 +1079,39 @@ static csr expanded_jacobian(const orc_case* h) {
         }
     free(rp);
     free(col);
-    free(fill);
     free(blocks);
     return m;
+}
+
+/* BlockSparseMatrix::scalar_component (linalg.cpp:114-133) for c = 0..2, negated (A = -J~,
+ * nonlinear.cpp:278-281); 0, or -1 when a block is not diagonal (InvalidArgument) */
+static int negated_components(const orc_case* h, csr comps[3]) {
+    const int nc = h->nc;
+    int *rp, *col;
+    m3* blocks = block_jacobian(h, &rp, &col);
+    double scale = 0.0;
+    for (int p = 0; p < rp[nc]; ++p)
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) scale = fmax(scale, fabs(blocks[p].m[a][b]));
+    int rc = 0;
+    for (int p = 0; p < rp[nc] && !rc; ++p)
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b)
+                if (a != b && fabs(blocks[p].m[a][b]) > 1e-12 * scale) rc = -1;
+    for (int c = 0; c < 3; ++c) {
+        comps[c].n = nc;
+        comps[c].nnz = rp[nc];
+        comps[c].row_ptr = xcalloc(nc + 1, sizeof(int));
+        memcpy(comps[c].row_ptr, rp, sizeof(int) * (nc + 1));
+        comps[c].col = xcalloc(rp[nc] > 0 ? rp[nc] : 1, sizeof(int));
+        memcpy(comps[c].col, col, sizeof(int) * rp[nc]);
+        comps[c].val = xcalloc(rp[nc] > 0 ? rp[nc] : 1, sizeof(double));
+        for (int p = 0; p < rp[nc]; ++p) comps[c].val[p] = -blocks[p].m[c][c];
+    }
+    free(rp);
+    free(col);
+    free(blocks);
+    return rc;
 }
 
 /* ------------------------------------------------------------------ ILU(k) */
@@ -1699,6 +1744,214 @@ out:
     return err;
 }
 
+/* ------------------------------------------------------------------ segregated solver */
+
+/* Ic0Precond (linalg.cpp:174-221): L on the lower pattern of A, row-oriented; 0 or -1 on a
+ * breakdown (missing diagonal / non-positive pivot, IluBreakdown) */
+static int ic0_factor(const csr* a, csr* L) {
+    const int n = a->n;
+    L->n = n;
+    L->row_ptr = xcalloc(n + 1, sizeof(int));
+    int nnz = 0;
+    for (int i = 0; i < n; ++i)
+        for (int p = a->row_ptr[i]; p < a->row_ptr[i + 1]; ++p)
+            if (a->col[p] <= i) ++nnz;
+    L->nnz = nnz;
+    L->col = xcalloc(nnz > 0 ? nnz : 1, sizeof(int));
+    L->val = xcalloc(nnz > 0 ? nnz : 1, sizeof(double));
+    int q = 0;
+    for (int i = 0; i < n; ++i) {
+        for (int p = a->row_ptr[i]; p < a->row_ptr[i + 1]; ++p)
+            if (a->col[p] <= i) {
+                L->col[q] = a->col[p];
+                L->val[q++] = a->val[p];
+            }
+        L->row_ptr[i + 1] = q;
+    }
+    const int* rp = L->row_ptr;
+    const int* col = L->col;
+    double* val = L->val;
+    for (int i = 0; i < n; ++i) {
+        const int diag_p = rp[i + 1] - 1;
+        if (diag_p < rp[i] || col[diag_p] != i) return -1;
+        for (int p = rp[i]; p < diag_p; ++p) {
+            const int j = col[p];
+            double s = val[p];
+            int pi = rp[i], pj = rp[j];
+            while (pi < p && pj < rp[j + 1] - 1) {
+                if (col[pi] == col[pj]) s -= val[pi++] * val[pj++];
+                else if (col[pi] < col[pj]) ++pi;
+                else ++pj;
+            }
+            val[p] = s / val[rp[j + 1] - 1];
+        }
+        double s = val[diag_p];
+        for (int p = rp[i]; p < diag_p; ++p) s -= val[p] * val[p];
+        if (!(s > 0.0)) return -1;
+        val[diag_p] = sqrt(s);
+    }
+    return 0;
+}
+
+/* Ic0Precond::solve: forward L y = r, then backward L^T z = y in saxpy form */
+static void ic0_solve(const csr* L, const double* r, double* z) {
+    const int n = L->n;
+    memcpy(z, r, sizeof(double) * n);
+    for (int i = 0; i < n; ++i) {
+        for (int p = L->row_ptr[i]; p < L->row_ptr[i + 1] - 1; ++p) z[i] -= L->val[p] * z[L->col[p]];
+        z[i] /= L->val[L->row_ptr[i + 1] - 1];
+    }
+    for (int j = n - 1; j >= 0; --j) {
+        z[j] /= L->val[L->row_ptr[j + 1] - 1];
+        for (int p = L->row_ptr[j]; p < L->row_ptr[j + 1] - 1; ++p) z[L->col[p]] -= L->val[p] * z[j];
+    }
+}
+
+static void csr_apply(const csr* a, const double* x, double* y) { /* ScalarCsrMatrix::apply */
+    for (int i = 0; i < a->n; ++i) {
+        double s = 0.0;
+        for (int p = a->row_ptr[i]; p < a->row_ptr[i + 1]; ++p) s += a->val[p] * x[a->col[p]];
+        y[i] = s;
+    }
+}
+
+/* cg_solve (linalg.cpp:380-421): IC(0)-preconditioned CG, Jacobi on an IC(0) breakdown;
+ * x holds x0 on entry.  Returns the iteration count; *fallback set on the Jacobi fallback. */
+static int cg_solve(const csr* a, const double* b, double* x, double rel, int max_iters, int* fallback) {
+    const int n = a->n;
+    csr L;
+    memset(&L, 0, sizeof L);
+    double* inv_diag = NULL;
+    if (ic0_factor(a, &L) != 0) {
+        csr_free(&L);
+        *fallback = 1;
+        inv_diag = xcalloc(n, sizeof(double));
+        for (int i = 0; i < n; ++i) {
+            inv_diag[i] = 1.0;
+            for (int p = a->row_ptr[i]; p < a->row_ptr[i + 1]; ++p)
+                if (a->col[p] == i && a->val[p] != 0.0) inv_diag[i] = 1.0 / a->val[p];
+        }
+    }
+    double* r = xcalloc(n, sizeof(double));
+    double* z = xcalloc(n, sizeof(double));
+    double* p = xcalloc(n, sizeof(double));
+    double* ap = xcalloc(n, sizeof(double));
+    int iters = 0;
+    csr_apply(a, x, r);
+    for (int i = 0; i < n; ++i) r[i] = b[i] - r[i];
+    const double r0 = dnorm(r, n);
+    if (r0 != 0.0) {
+#define PRECOND(in, out)                                               \
+    do {                                                               \
+        if (inv_diag)                                                  \
+            for (int i_ = 0; i_ < n; ++i_) out[i_] = inv_diag[i_] * in[i_]; \
+        else                                                           \
+            ic0_solve(&L, in, out);                                    \
+    } while (0)
+        PRECOND(r, z);
+        memcpy(p, z, sizeof(double) * n);
+        double rz = ddot(r, z, n);
+        for (int it = 0; it < max_iters; ++it) {
+            csr_apply(a, p, ap);
+            const double pap = ddot(p, ap, n);
+            if (!(pap > 0.0)) break;
+            const double alpha = rz / pap;
+            daxpy(alpha, p, x, n);
+            daxpy(-alpha, ap, r, n);
+            iters = it + 1;
+            if (dnorm(r, n) <= rel * r0) break;
+            PRECOND(r, z);
+            const double rz_new = ddot(r, z, n);
+            const double beta = rz_new / rz;
+            rz = rz_new;
+            for (int i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+        }
+#undef PRECOND
+    }
+    free(r); free(z); free(p); free(ap); free(inv_diag);
+    if (!inv_diag) csr_free(&L);
+    return iters;
+}
+
+static int check_conv(double r_norm, double r0, double du_norm, double u_norm, const sfv_solver_cfg* cfg) {
+    if (r_norm <= cfg->a_tol) return 1; /* nonlinear.cpp:97-103 */
+    if (r_norm <= cfg->r_tol * r0) return 1;
+    if (cfg->s_tol > 0.0 && du_norm <= cfg->s_tol * u_norm) return 1;
+    return 0;
+}
+
+/* segregated_solve (nonlinear.cpp:268-351): per component, A u_next = A u + R_c(u) by CG */
+static int segregated(orc_case* h, v3* u, const sfv_solver_cfg* cfg, const csr comps[3], sfv_solve_report* rep) {
+    const double t0 = now_s();
+    const int nc = h->nc;
+    const int max_outer = cfg->max_outer > 0 ? cfg->max_outer : 2000;
+    const double inner = cfg->inner_reduction > 0.0 ? cfg->inner_reduction : 0.9;
+    const double relax = cfg->relaxation > 0.0 ? cfg->relaxation : 1.0;
+    memset(rep, 0, sizeof *rep);
+    rep->status = SFV_MAX_ITERS;
+    v3* r = xcalloc(nc, sizeof(v3));
+    v3* un = xcalloc(nc, sizeof(v3));
+    double *uc = xcalloc(nc, sizeof(double)), *rc_ = xcalloc(nc, sizeof(double)), *b = xcalloc(nc, sizeof(double));
+    int rc = residual(h, u, r);
+    if (rc) goto out;
+    double r_norm = field_norm(r, nc);
+    const double r0 = r_norm;
+    rep->initial_residual = r0;
+    rep->final_residual = r_norm;
+    push_record(rep, 0, r_norm, 0, 0.0);
+    if (check_conv(r_norm, r0, 0.0, 0.0, cfg)) {
+        rep->status = SFV_CONVERGED;
+        goto out;
+    }
+    for (int k = 0; k < max_outer; ++k) {
+        int krylov = 0;
+        for (int c = 0; c < 3; ++c) {
+            for (int i = 0; i < nc; ++i) {
+                uc[i] = vget(u[i], c);
+                rc_[i] = vget(r[i], c);
+            }
+            csr_apply(&comps[c], uc, b);
+            for (int i = 0; i < nc; ++i) b[i] += rc_[i];
+            krylov += cg_solve(&comps[c], b, uc, inner, nc > 50 ? nc : 50, &rep->cg_diag_fallback);
+            for (int i = 0; i < nc; ++i) vset(&un[i], c, uc[i]);
+        }
+        rep->krylov_iters += krylov;
+        double du_norm = 0.0;
+        for (int i = 0; i < nc; ++i) {
+            const v3 du = vscale(vsub(un[i], u[i]), relax);
+            du_norm += du.x * du.x;
+            du_norm += du.y * du.y;
+            du_norm += du.z * du.z;
+            u[i] = vadd(u[i], du);
+        }
+        du_norm = sqrt(du_norm);
+        if (residual(h, u, r)) {
+            rep->status = SFV_DIVERGED;
+            snprintf(rep->detail, SFV_DETAIL_LEN, "%s", h->err.msg);
+            rep->outer_iters = k + 1;
+            break;
+        }
+        r_norm = field_norm(r, nc);
+        rep->outer_iters = k + 1;
+        push_record(rep, k + 1, r_norm, krylov, 1.0);
+        rep->final_residual = r_norm;
+        if (!isfinite(r_norm)) {
+            rep->status = SFV_DIVERGED;
+            snprintf(rep->detail, SFV_DETAIL_LEN, "residual norm overflow");
+            break;
+        }
+        if (check_conv(r_norm, r0, du_norm, field_norm(u, nc), cfg)) {
+            rep->status = SFV_CONVERGED;
+            break;
+        }
+    }
+    if (rep->status == SFV_MAX_ITERS) snprintf(rep->detail, SFV_DETAIL_LEN, "outer iteration limit reached");
+out:
+    rep->wall_seconds = now_s() - t0;
+    free(r); free(un); free(uc); free(rc_); free(b);
+    return rc;
+}
+
 int orc_jfnk_solve(orc_case* h, double* uf, const sfv_solver_cfg* cfg, sfv_solve_report* rep) {
     v3* u = xcalloc(h->nc, sizeof(v3));
     load_cells(u, uf, h->nc);
@@ -1715,8 +1968,19 @@ int orc_run_steps(orc_case* h, double* field, const sfv_solver_cfg* cfg, int n_s
     const int nc = h->nc;
     if (n_steps < 1) return fail(&h->err, SFV_ERR_INVALID_ARGUMENT, -1, "run_steps: need at least one step");
     *n_reports = 0;
-    int rc = orc_precond_create(h, cfg->preconditioner);
-    if (rc) return rc;
+    const int seg = cfg->algorithm == SFV_ALG_SEGREGATED;
+    csr comps[3];
+    memset(comps, 0, sizeof comps);
+    int rc = 0;
+    if (seg) { /* scalar_component_matrices instead of a preconditioner (nonlinear.cpp:397-400) */
+        if (negated_components(h, comps) != 0) {
+            for (int c = 0; c < 3; ++c) csr_free(&comps[c]);
+            return fail(&h->err, SFV_ERR_INVALID_ARGUMENT, -1, "scalar_component: blocks are not diagonal");
+        }
+    } else {
+        rc = orc_precond_create(h, cfg->preconditioner);
+        if (rc) return rc;
+    }
     v3* fu = xcalloc(nc, sizeof(v3));
     v3* fuo = xcalloc(nc, sizeof(v3));
     v3* fuoo = xcalloc(nc, sizeof(v3));
@@ -1744,7 +2008,7 @@ int orc_run_steps(orc_case* h, double* field, const sfv_solver_cfg* cfg, int n_s
             memcpy(u, fu, sizeof(v3) * nc);
         }
         sfv_solve_report rep;
-        const int e = jfnk(h, u, cfg, &rep);
+        const int e = seg ? segregated(h, u, cfg, comps, &rep) : jfnk(h, u, cfg, &rep);
         if (e) {
             memset(&rep, 0, sizeof rep);
             rep.status = SFV_DIVERGED;
@@ -1779,6 +2043,7 @@ int orc_run_steps(orc_case* h, double* field, const sfv_solver_cfg* cfg, int n_s
     store_cells(field + 12 * nc, fvoo, nc);
     store_cells(field + 15 * nc, fao, nc);
     free(fu); free(fuo); free(fuoo); free(fvo); free(fvoo); free(fao); free(u);
+    for (int c = 0; c < 3; ++c) csr_free(&comps[c]);
     *wall = now_s() - t0;
     return rc;
 }

@@ -89,6 +89,8 @@ class SolverCfg(C.Structure):
         ("max_krylov", C.c_int),
         ("preconditioner", C.c_int),
         ("line_search", C.c_int),
+        ("algorithm", C.c_int),
+        ("relaxation", C.c_double),
     ]
 
 
@@ -114,6 +116,7 @@ class SolveReport(C.Structure):
         ("n_records", C.c_int),
         ("records", IterationRecord * 64),
         ("detail", C.c_char * 160),
+        ("cg_diag_fallback", C.c_int),
     ]
 
     def summary(self) -> dict:
@@ -129,6 +132,7 @@ class SolveReport(C.Structure):
             "krylov_per_newton": [self.records[i].krylov_iters for i in range(1, n)],
             "r_norms": [self.records[i].r_norm for i in range(n)],
             "s": [self.records[i].s for i in range(1, n)],
+            "cg_diag_fallback": bool(self.cg_diag_fallback),
             "detail": self.detail.decode(errors="replace"),
         }
 
@@ -251,9 +255,12 @@ class Physics:
 
 
 def solver_cfg(r_tol=1e-6, a_tol=1e-50, s_tol=0.0, max_outer=0, inner_reduction=0.0, restart=30,
-               max_krylov=300, preconditioner="auto", line_search=True) -> SolverCfg:
-    """SolverConfig defaults (nonlinear.hpp:27-44)."""
+               max_krylov=300, preconditioner="auto", line_search=True, algorithm="jfnk",
+               relaxation=1.0) -> SolverCfg:
+    """SolverConfig defaults (nonlinear.hpp:27-44); algorithm "jfnk" or "segregated"."""
     c = SolverCfg()
+    c.algorithm = {"jfnk": 0, "segregated": 1}[algorithm] if isinstance(algorithm, str) else int(algorithm)
+    c.relaxation = float(relaxation)
     c.a_tol, c.r_tol, c.s_tol = a_tol, r_tol, s_tol
     c.max_outer, c.inner_reduction = max_outer, inner_reduction
     c.restart, c.max_krylov = restart, max_krylov

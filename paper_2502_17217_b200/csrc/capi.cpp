@@ -122,6 +122,17 @@ struct sfv_ctx {
     // jv_pair.cu scratch + tiled face records (device.h): pwg = tiled [w | G], psig: tiled cell stress
     DevBuf<double> pwg, face9, bres, psig, lawst;
     DeviceGeometry* dgeo = nullptr;  // device-resident geometry (the host copy is partial until host_geometry())
+    // segregated solver (per component: A = -J~, IC(0) sweeps or the Jacobi fallback)
+    struct SegComp {
+        DevBuf<int> rp, col, f_order, f_rp, f_col, b_order, b_rp, b_col;
+        DevBuf<double> val, f_val, f_diag, b_val, b_diag, inv_diag;
+        SegCsr a;
+        SegSweep fwd, bwd;
+        bool jacobi = false;
+    };
+    SegComp seg[3];
+    int seg_ncomp = 0;
+    DevBuf<double> sg_b, sg_x, sg_r, sg_z, sg_p, sg_ap, sg_y, sg_un, sg_du;
     PairScratch ps;
     // scratch
     DevBuf<double> grad, red, scal;  // scal: [0]=eps [1]=u_norm [2..] misc
@@ -791,6 +802,188 @@ void push_record(sfv_solve_report* rep, int iter, double r_norm, int kry, double
 
 // jfnk_solve (nonlinear.cpp:173-266) with line_search (:140-163) and check_convergence
 // (:97-103).  Returns an error only where the reference lets an exception escape.
+// A = -J~ per component (scalar_component_matrices, linalg.cpp:160-165; nonlinear.cpp:278-281)
+// and its IC(0) factor (Ic0Precond, factored once: cg_solve re-factors the same matrix on
+// every call, linalg.cpp:384-390) or the Jacobi fallback (DiagPrecond) on a breakdown.
+int seg_create(sfv_ctx* c) {
+    if (c->seg_ncomp) return SFV_OK;
+    std::vector<ScalarCsr> comps;
+    const std::string msg = cell_jacobian(c->mesh, c->geom, c->ph.kbar, c->ph.transient != 0, c->ph.rho, c->ph.dt, comps);
+    if (!msg.empty()) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "scalar_component: blocks are not diagonal");
+    const int n = c->nc;
+    for (size_t a = 0; a < comps.size(); ++a) {
+        ScalarCsr& A = comps[a];
+        for (double& v : A.val) v = -v;
+        sfv_ctx::SegComp& sc = c->seg[a];
+        ScalarCsr L;
+        sc.jacobi = !ic0_factor(A, L);
+        bool ok = sc.rp.upload(A.rp) && sc.col.upload(A.col) && sc.val.upload(A.val);
+        if (sc.jacobi) {
+            std::vector<double> inv(n, 1.0);
+            for (int i = 0; i < n; ++i)
+                for (int p = A.rp[i]; p < A.rp[i + 1]; ++p)
+                    if (A.col[p] == i && A.val[p] != 0.0) inv[i] = 1.0 / A.val[p];
+            ok = ok && sc.inv_diag.upload(inv);
+        } else {
+            TriSchedule f, b;
+            schedule_ic0(L, f, b);
+            ok = ok && sc.f_order.upload(f.order) && sc.f_rp.upload(f.rp) && sc.f_col.upload(f.col) &&
+                 sc.f_val.upload(f.val) && sc.f_diag.upload(f.diag) && sc.b_order.upload(b.order) &&
+                 sc.b_rp.upload(b.rp) && sc.b_col.upload(b.col) && sc.b_val.upload(b.val) && sc.b_diag.upload(b.diag);
+            sc.fwd = {f.n_pos, sc.f_order.p, sc.f_rp.p, sc.f_col.p, sc.f_val.p, sc.f_diag.p};
+            sc.bwd = {b.n_pos, sc.b_order.p, sc.b_rp.p, sc.b_col.p, sc.b_val.p, sc.b_diag.p};
+        }
+        if (!ok) return c->fail(SFV_ERR_CUDA, -1, "segregated: out of device memory");
+        sc.a = {n, sc.rp.p, sc.col.p, sc.val.p};
+    }
+    const size_t nn = static_cast<size_t>(n);
+    if (!c->sg_b.alloc(nn) || !c->sg_x.alloc(nn) || !c->sg_r.alloc(nn) || !c->sg_z.alloc(nn) || !c->sg_p.alloc(nn) ||
+        !c->sg_ap.alloc(nn) || !c->sg_y.alloc(nn) || !c->sg_un.alloc(3 * nn) || !c->sg_du.alloc(3 * nn))
+        return c->fail(SFV_ERR_CUDA, -1, "segregated: out of device memory");
+    c->seg_ncomp = static_cast<int>(comps.size());
+    return SFV_OK;
+}
+
+// dot product of two device vectors of length n, on the host (fixed-order reduction, one sync)
+int dot_host(sfv_ctx* c, const double* a, const double* b, int n, double* out) {
+    launch_dot(a, b, n, c->hdev.p, c->red.p, c->counter.p, c->stream);
+    c->launches += 1;
+    if (int e = fetch(c, 1)) return e;
+    *out = c->st->h[0];
+    return SFV_OK;
+}
+
+// cg_solve (linalg.cpp:380-421) on component comp: x (holding x0) <- A^{-1} b approximately
+int seg_cg(sfv_ctx* c, const sfv_ctx::SegComp& sc, const double* b, double* x, double rel, int max_iters,
+           int* iters) {
+    const int n = c->nc;
+    double *r = c->sg_r.p, *z = c->sg_z.p, *p = c->sg_p.p, *ap = c->sg_ap.p;
+    cudaStream_t s = c->stream;
+    auto precond = [&](const double* in, double* out) {
+        if (sc.jacobi) seg_jacobi(n, sc.inv_diag.p, in, out, s);
+        else seg_ic0_apply(sc.fwd, sc.bwd, in, c->sg_y.p, out, n, seg_sweep_grid(), s);
+        c->launches += sc.jacobi ? 1 : 4;
+    };
+    *iters = 0;
+    seg_spmv(sc.a, x, r, s);
+    seg_rsub(n, b, r, s);
+    c->launches += 2;
+    double r0;
+    if (int e = dot_host(c, r, r, n, &r0)) return e;
+    r0 = std::sqrt(r0);
+    if (r0 == 0.0) return SFV_OK;
+    precond(r, z);
+    cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+    double rz;
+    if (int e = dot_host(c, r, z, n, &rz)) return e;
+    for (int it = 0; it < max_iters; ++it) {
+        seg_spmv(sc.a, p, ap, s);
+        ++c->launches;
+        double pap;
+        if (int e = dot_host(c, p, ap, n, &pap)) return e;
+        if (!(pap > 0.0)) break;  // loss of positive definiteness
+        const double alpha = rz / pap;
+        launch_axpy_host(x, alpha, p, n, s);
+        launch_axpy_host(r, -alpha, ap, n, s);
+        c->launches += 2;
+        *iters = it + 1;
+        double rn;
+        if (int e = dot_host(c, r, r, n, &rn)) return e;
+        if (std::sqrt(rn) <= rel * r0) return SFV_OK;
+        precond(r, z);
+        double rz_new;
+        if (int e = dot_host(c, r, z, n, &rz_new)) return e;
+        const double beta = rz_new / rz;
+        rz = rz_new;
+        seg_xpby(n, z, beta, p, s);
+        ++c->launches;
+    }
+    return SFV_OK;
+}
+
+// segregated_solve (nonlinear.cpp:268-351): per outer iteration, for each component
+// A u_next = A u + R_c(u) by IC(0)-CG, then u += relaxation (u_next - u)
+int segregated(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int n = c->n, nc = c->nc;
+    const int max_outer = cfg->max_outer > 0 ? cfg->max_outer : 2000;
+    const double inner = cfg->inner_reduction > 0.0 ? cfg->inner_reduction : 0.9;
+    const double relax = cfg->relaxation > 0.0 ? cfg->relaxation : 1.0;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->status = SFV_MAX_ITERS;
+    auto wall = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    if (!ensure_krylov(c, std::max(cfg->restart, 1))) return c->fail(SFV_ERR_CUDA, -1, "segregated: out of device memory");
+    if (int e = seg_create(c)) return e;
+    double* r = c->rscratch.p;
+    int e = residual_sync(c, u, r);
+    if (e) {
+        rep->wall_seconds = wall();
+        return e;
+    }
+    double r_norm;
+    if ((e = norm_host(c, r, &r_norm))) return e;
+    const double r0 = r_norm;
+    rep->initial_residual = r0;
+    rep->final_residual = r_norm;
+    push_record(rep, 0, r_norm, 0, 0.0);
+    auto converged = [&](double rn, double du, double un) {  // check_convergence (nonlinear.cpp:97-103)
+        return rn <= cfg->a_tol || rn <= cfg->r_tol * r0 || (cfg->s_tol > 0.0 && du <= cfg->s_tol * un);
+    };
+    if (converged(r_norm, 0.0, 0.0)) {
+        rep->status = SFV_CONVERGED;
+        rep->wall_seconds = wall();
+        return SFV_OK;
+    }
+    cudaStream_t s = c->stream;
+    for (int k = 0; k < max_outer; ++k) {
+        int krylov = 0;
+        for (int comp = 0; comp < 3; ++comp) {
+            const sfv_ctx::SegComp& sc = c->seg[c->seg_ncomp == 1 ? 0 : comp];
+            seg_component(nc, u, comp, c->sg_x.p, s);
+            seg_spmv(sc.a, c->sg_x.p, c->sg_b.p, s);
+            seg_add_component(nc, r, comp, c->sg_b.p, s);
+            c->launches += 3;
+            int it = 0;
+            if ((e = seg_cg(c, sc, c->sg_b.p, c->sg_x.p, inner, std::max(nc, 50), &it))) return e;
+            krylov += it;
+            rep->cg_diag_fallback |= sc.jacobi ? 1 : 0;
+            seg_set_component(nc, c->sg_x.p, comp, c->sg_un.p, s);
+            ++c->launches;
+        }
+        rep->krylov_iters += krylov;
+        seg_relax(n, c->sg_un.p, relax, u, c->sg_du.p, s);
+        ++c->launches;
+        double du_norm, u_norm;
+        if ((e = dot_host(c, c->sg_du.p, c->sg_du.p, n, &du_norm))) return e;
+        du_norm = std::sqrt(du_norm);
+        e = residual_sync(c, u, r);
+        if (e) {  // eval.residual threw (nonlinear.cpp:326-333)
+            rep->status = SFV_DIVERGED;
+            std::snprintf(rep->detail, SFV_DETAIL_LEN, "%s", c->last.msg.c_str());
+            rep->outer_iters = k + 1;
+            break;
+        }
+        if ((e = norm_host(c, r, &r_norm))) return e;
+        rep->outer_iters = k + 1;
+        push_record(rep, k + 1, r_norm, krylov, 1.0);
+        rep->final_residual = r_norm;
+        if (!std::isfinite(r_norm)) {
+            rep->status = SFV_DIVERGED;
+            std::snprintf(rep->detail, SFV_DETAIL_LEN, "residual norm overflow");
+            break;
+        }
+        if ((e = norm_host(c, u, &u_norm))) return e;
+        if (converged(r_norm, du_norm, u_norm)) {
+            rep->status = SFV_CONVERGED;
+            break;
+        }
+    }
+    if (rep->status == SFV_MAX_ITERS) std::snprintf(rep->detail, SFV_DETAIL_LEN, "outer iteration limit reached");
+    cudaStreamSynchronize(c->stream);
+    rep->wall_seconds = wall();
+    return SFV_OK;
+}
+
 int jfnk(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep) {
     const auto t0 = std::chrono::steady_clock::now();
     const int n = c->n;
@@ -1641,6 +1834,10 @@ int sfv_jfnk_solve(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_r
     return jfnk(c, u, cfg, rep);
 }
 
+int sfv_segregated_solve(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep) {
+    return segregated(c, u, cfg, rep);
+}
+
 // run_steps (nonlinear.cpp:382-446)
 int sfv_run_steps(sfv_ctx* c, double* field, const sfv_solver_cfg* cfg, int n_steps, sfv_solve_report* reports,
                   int cap, int* n_reports, double* wall_seconds) {
@@ -1648,7 +1845,12 @@ int sfv_run_steps(sfv_ctx* c, double* field, const sfv_solver_cfg* cfg, int n_st
     if (n_steps < 1) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "run_steps: need at least one step");
     const int n = c->n;
     *n_reports = 0;
-    if (int e = precond_create(c, cfg->preconditioner)) return e;
+    const bool seg = cfg->algorithm == SFV_ALG_SEGREGATED;
+    if (seg) {  // scalar_component_matrices instead of a preconditioner (nonlinear.cpp:397-400)
+        if (int e = seg_create(c)) return e;
+    } else if (int e = precond_create(c, cfg->preconditioner)) {
+        return e;
+    }
     if (!ensure_krylov(c, std::max(cfg->restart, 1))) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
     double* fu = field;
     double* fuo = field + n;
@@ -1669,7 +1871,7 @@ int sfv_run_steps(sfv_ctx* c, double* field, const sfv_solver_cfg* cfg, int n_st
             cudaMemcpyAsync(u, fu, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
         }
         sfv_solve_report rep;
-        const int e = jfnk(c, u, cfg, &rep);
+        const int e = seg ? segregated(c, u, cfg, &rep) : jfnk(c, u, cfg, &rep);
         if (e) {
             std::memset(&rep, 0, sizeof(rep));
             rep.status = SFV_DIVERGED;

@@ -180,6 +180,34 @@ struct FusedArgs {
 int fused_resident_ctas(bool general);  // resident CTAs of the persistent grid
 void launch_fused(const FusedArgs& a, int grid, cudaStream_t s);
 
+// ---- segregated.cu: the segregated solver's device kernels (nonlinear.cpp:268-351)
+struct SegCsr {  // one component of A = -J~ (ScalarCsrMatrix)
+    int n = 0;
+    const int* rp = nullptr;
+    const int* col = nullptr;
+    const double* val = nullptr;
+};
+struct SegSweep {  // one IC(0) sweep in dependency-level order (TriSchedule on the device)
+    int n_pos = 0;
+    const int* order = nullptr;
+    const int* rp = nullptr;
+    const int* col = nullptr;  // row indices
+    const double* val = nullptr;
+    const double* diag = nullptr;
+};
+// z = (L L^T)^{-1} r with y as the forward-sweep scratch (vectors of n)
+void seg_ic0_apply(const SegSweep& f, const SegSweep& b, const double* r, double* y, double* z, int n, int grid,
+                   cudaStream_t s);
+void seg_spmv(const SegCsr& a, const double* x, double* y, cudaStream_t s);
+void seg_component(int n, const double* u, int c, double* out, cudaStream_t s);      // out = u[:, c]
+void seg_set_component(int n, const double* x, int c, double* u, cudaStream_t s);    // u[:, c] = x
+void seg_add_component(int n, const double* r, int c, double* b, cudaStream_t s);    // b += r[:, c]
+void seg_rsub(int n, const double* b, double* r, cudaStream_t s);                    // r = b - r
+void seg_xpby(int n, const double* z, double beta, double* p, cudaStream_t s);       // p = z + beta p
+void seg_jacobi(int n, const double* inv, const double* r, double* z, cudaStream_t s);
+void seg_relax(int n3, const double* un, double relax, double* u, double* du, cudaStream_t s);
+int seg_sweep_grid();
+
 // ---- krylov.cu (deterministic fixed-order reductions)
 int reduce_blocks(int n);
 void launch_dot(const double* a, const double* b, int n, double* out, double* scratch, unsigned* counter,

@@ -410,6 +410,97 @@ void schedule_lower(const ScalarCsr& lu, TriSchedule& t) {
     });
 }
 
+bool ic0_factor(const ScalarCsr& a, ScalarCsr& L) {
+    const int n = a.n;
+    L.n = n;
+    L.rp.assign(n + 1, 0);
+    L.col.clear();
+    L.val.clear();
+    for (int i = 0; i < n; ++i) {
+        for (int p = a.rp[i]; p < a.rp[i + 1]; ++p)
+            if (a.col[p] <= i) {
+                L.col.push_back(a.col[p]);
+                L.val.push_back(a.val[p]);
+            }
+        L.rp[i + 1] = static_cast<int>(L.col.size());
+    }
+    const std::vector<int>& rp = L.rp;
+    const std::vector<int>& col = L.col;
+    std::vector<double>& val = L.val;
+    for (int i = 0; i < n; ++i) {
+        const int diag_p = rp[i + 1] - 1;
+        if (diag_p < rp[i] || col[diag_p] != i) return false;
+        for (int p = rp[i]; p < diag_p; ++p) {
+            const int j = col[p];
+            double s = val[p];
+            int pi = rp[i], pj = rp[j];
+            while (pi < p && pj < rp[j + 1] - 1) {
+                if (col[pi] == col[pj]) s -= val[pi++] * val[pj++];
+                else if (col[pi] < col[pj]) ++pi;
+                else ++pj;
+            }
+            val[p] = s / val[rp[j + 1] - 1];
+        }
+        double s = val[diag_p];
+        for (int p = rp[i]; p < diag_p; ++p) s -= val[p] * val[p];
+        if (!(s > 0.0)) return false;
+        val[diag_p] = std::sqrt(s);
+    }
+    return true;
+}
+
+void schedule_ic0(const ScalarCsr& L, TriSchedule& fwd, TriSchedule& bwd) {
+    const int n = L.n;
+    // forward: level of row i from its columns j < i
+    std::vector<int> level(n, 0);
+    int nl = 0;
+    for (int i = 0; i < n; ++i) {
+        int l = 0;
+        for (int p = L.rp[i]; p < L.rp[i + 1] - 1; ++p) l = std::max(l, level[L.col[p]] + 1);
+        level[i] = l;
+        nl = std::max(nl, l + 1);
+    }
+    pack(level, nl, fwd, [&](int i, std::vector<int>& c, std::vector<double>& v, double& d) {
+        for (int p = L.rp[i]; p < L.rp[i + 1] - 1; ++p) {
+            c.push_back(L.col[p]);
+            v.push_back(L.val[p]);
+        }
+        d = L.val[L.rp[i + 1] - 1];
+    });
+    // backward: row i of L^T holds L_ji for j > i; the saxpy loop subtracts them from z_i in
+    // descending j, then divides by L_ii (linalg.cpp:213-216)
+    std::vector<int> tp(n + 1, 0);
+    for (int j = 0; j < n; ++j)
+        for (int p = L.rp[j]; p < L.rp[j + 1] - 1; ++p) ++tp[L.col[p] + 1];
+    for (int i = 0; i < n; ++i) tp[i + 1] += tp[i];
+    std::vector<int> tcol(tp[n]);
+    std::vector<double> tval(tp[n]);
+    {
+        std::vector<int> fill(tp.begin(), tp.end() - 1);
+        for (int j = n - 1; j >= 0; --j)  // descending j within each row of L^T
+            for (int p = L.rp[j]; p < L.rp[j + 1] - 1; ++p) {
+                const int i = L.col[p];
+                tcol[fill[i]] = j;
+                tval[fill[i]++] = L.val[p];
+            }
+    }
+    std::vector<int> lev2(n, 0);
+    int nl2 = 0;
+    for (int i = n - 1; i >= 0; --i) {
+        int l = 0;
+        for (int q = tp[i]; q < tp[i + 1]; ++q) l = std::max(l, lev2[tcol[q]] + 1);
+        lev2[i] = l;
+        nl2 = std::max(nl2, l + 1);
+    }
+    pack(lev2, nl2, bwd, [&](int i, std::vector<int>& c, std::vector<double>& v, double& d) {
+        for (int q = tp[i]; q < tp[i + 1]; ++q) {
+            c.push_back(tcol[q]);
+            v.push_back(tval[q]);
+        }
+        d = L.val[L.rp[i + 1] - 1];
+    });
+}
+
 void schedule_upper(const ScalarCsr& lu, TriSchedule& t) {
     const int n = lu.n;
     std::vector<int> level(n, 0);

@@ -40,6 +40,14 @@ struct TriSchedule {
 void schedule_lower(const ScalarCsr& lu, TriSchedule& t);
 void schedule_upper(const ScalarCsr& lu, TriSchedule& t);
 
+// Ic0Precond (linalg.cpp:174-221): L on the lower pattern of A with the reference's
+// row-oriented arithmetic; false on a breakdown (missing diagonal / non-positive pivot).
+bool ic0_factor(const ScalarCsr& a, ScalarCsr& L);
+// Its two sweeps (Ic0Precond::solve, linalg.cpp:208-218) as schedules: forward, rows of L in
+// ascending column order then / L_ii; backward, the saxpy loop restated per row of L^T —
+// z_i loses L_ji z_j for j descending, then / L_ii — both in dependency-level order.
+void schedule_ic0(const ScalarCsr& L, TriSchedule& fwd, TriSchedule& bwd);
+
 // Streamed-sweep records (precond.cu, tri_stream_kernel): one 96-byte record per position,
 // position order.  Level l's positions are split into `cs` contiguous chunk-aligned slices
 // (CTA r of the cluster owns slice r); each CTA stores its positions' values in a ring of

@@ -38,6 +38,9 @@ CASES = {
                             tl=True, disp=0.02),
     # J2 plasticity with saturation hardening; the stepped solve commits the plastic state
     # after every increment (nonlinear.cpp:426), so steps 2-3 start from a yielded state
+    # the segregated solver (nonlinear.cpp:268-351, IC(0)-CG per component, linalg.cpp:174-421)
+    "hex_segregated": dict(mesh=((1.0, 1.0, 1.0), (6, 5, 4), [D, T, T, T, T, T], 0.1, 5), law=LAW_HOOKE,
+                           alg="segregated", steps=1),
     "hex_j2": dict(mesh=((4.0, 1.0, 1.0), (12, 4, 4), [D, D, T, T, T, T], 0.05, 42), law=LAW_J2, disp=0.03, steps=3),
 }
 # steel-like J2: E = 200 GPa, nu = 0.3 (mu, kappa); HardeningCurve::saturation(a, b, c, d)
@@ -111,7 +114,7 @@ def main():
         if spec.get("transient"):
             f0[3] = f0[4] = cases.sinusoid_field(cases.cell_centres(m), 1234, 1.0)
         ref2 = RefCase(m, ph)
-        cfg = solver_cfg(r_tol=1e-8)
+        cfg = solver_cfg(r_tol=1e-8 if spec.get("alg", "jfnk") == "jfnk" else 1e-6, algorithm=spec.get("alg", "jfnk"))
         steps = spec.get("steps", 2)
         f, reps, _ = ref2.run_steps(f0, cfg, steps)
         out["steps_field0"] = f0
@@ -120,6 +123,8 @@ def main():
         out["steps_newton"] = np.array([r.outer_iters for r in reps])
         out["steps_status"] = np.array([r.status for r in reps])
         out["steps_n"] = steps
+        out["steps_alg"] = 1 if spec.get("alg") == "segregated" else 0
+        out["steps_rtol"] = cfg.r_tol
         if spec["law"] == LAW_J2:  # R after a commit: the residual reads the committed state
             ref3 = RefCase(m, ph)
             ref3.set_time(0.7)
