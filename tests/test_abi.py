@@ -129,3 +129,24 @@ def test_gpu_path_fails_loudly_without_device(monkeypatch):
     case = cases.config("c1", n=4)
     with pytest.raises(RuntimeError):
         sv.ResidualEvaluator(case.mesh(), case.physics)
+
+
+def test_report_csv_writers(tmp_path):
+    """metrics.csv / iterations.csv in the reference's format (io.cpp:458-488)."""
+    from paper_2502_17217_b200.abi import SolveReport
+    from paper_2502_17217_b200.reports import write_iterations_csv, write_metrics_csv
+    r = SolveReport()
+    r.status, r.step, r.outer_iters, r.krylov_iters = 0, 1, 2, 17
+    r.initial_residual, r.final_residual, r.wall_seconds = 1234.5, 1.0 / 3.0, 0.25
+    r.n_records = 2
+    r.records[0].step, r.records[0].iter, r.records[0].r_norm = 1, 0, 1234.5
+    r.records[1].step, r.records[1].iter, r.records[1].r_norm = 1, 1, 2.0 / 3.0
+    r.records[1].krylov_iters, r.records[1].s = 17, 0.5
+    write_metrics_csv([r], str(tmp_path / "m.csv"))
+    write_iterations_csv([r], str(tmp_path / "i.csv"))
+    m = (tmp_path / "m.csv").read_text().splitlines()
+    assert m[0] == "step,status,outer_iters,krylov_iters,initial_residual,final_residual,wall_seconds,detail"
+    assert m[1] == "1,converged,2,17,1234.5,0.333333333333,0.25,"
+    assert m[2] == "total,,2,17,,,0.25,"
+    i = (tmp_path / "i.csv").read_text().splitlines()
+    assert i == ["step,iter,r_norm,krylov_iters,s", "1,0,1234.5,0,0", "1,1,0.666666666667,17,0.5"]
