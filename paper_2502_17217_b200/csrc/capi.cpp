@@ -48,7 +48,8 @@ struct DevBuf {
         if (count == 0) return true;
         return cudaMalloc(&p, sizeof(T) * count) == cudaSuccess;
     }
-    bool upload(const std::vector<T>& h) {
+    template <class A>
+    bool upload(const std::vector<T, A>& h) {
         if (!alloc(h.size())) return false;
         return h.empty() || cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     }
@@ -1185,7 +1186,7 @@ int precond_create(sfv_ctx* c, int kind) {
     pt.mark("schedules");
     // streamed sweep (precond_stream.cu): rows per CTA-slice, the smallest safe value ring,
     // and as many cp.async stages as the remaining shared memory holds
-    std::vector<std::vector<unsigned char>> packed(scheds.size());
+    std::vector<rawvec<unsigned char>> packed(scheds.size());
     int s_ring = 0, s_rows = 32, s_stages = 0;
     {
         for (const TriSchedule& ts : scheds)
@@ -1199,9 +1200,7 @@ int precond_create(sfv_ctx* c, int kind) {
                 std::vector<std::thread> th;
                 for (size_t x = 0; x < scheds.size(); ++x)
                     th.emplace_back([&, x] {
-                        std::vector<StreamRecord> recs;
-                        ok[x] = build_stream_records(scheds[x], kStreamCluster, cand, s_rows, recs);
-                        if (ok[x]) pack_stream_chunks(recs, packed[x]);
+                        ok[x] = build_stream_records(scheds[x], kStreamCluster, cand, s_rows, packed[x]);
                     });
                 for (auto& t : th) t.join();
                 if (std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; })) {

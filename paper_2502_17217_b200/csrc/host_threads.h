@@ -4,6 +4,8 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <thread>
 
@@ -17,5 +19,17 @@ inline int host_threads() {
     }();
     return n;
 }
+
+// SFV_TIMING=1: a phase's wall time on stderr (setup profiling)
+struct StageClock {
+    bool on = std::getenv("SFV_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[sfv]   %-26s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
 
 }  // namespace sfv

@@ -35,7 +35,17 @@ std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar,
         col[fill[m.owner[f]]++] = m.neighbour[f];
         col[fill[m.neighbour[f]]++] = m.owner[f];
     }
-    for (int c = 0; c < nc; ++c) std::sort(col.begin() + rp[c], col.begin() + rp[c + 1]);
+    {  // rows sort independently
+        const int nth = host_threads();
+        std::vector<std::thread> th;
+        const int ch = (nc + nth - 1) / nth;
+        for (int k = 0; k < nth; ++k)
+            th.emplace_back([&, k] {
+                for (int c = k * ch; c < std::min(nc, (k + 1) * ch); ++c)
+                    std::sort(col.begin() + rp[c], col.begin() + rp[c + 1]);
+            });
+        for (auto& x : th) x.join();
+    }
     bool sym = false;
     for (int f = m.n_internal; f < m.n_faces(); ++f)
         if (m.patches[m.face_patch[f]].kind == SFV_PATCH_SYMMETRY) {
@@ -117,14 +127,18 @@ struct SpinBarrier {
 // the factor is bit-identical.  Returns false on a breakdown (the caller reruns the
 // sequential code for the reference's exact message).
 bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nthreads) {
+    StageClock sc;
     const int n = a.n;
-    std::vector<std::vector<int>> rc(n);
-    std::vector<std::vector<int>> rl(n);
+    // symbolic phase: each thread builds a contiguous block of rows into one flat buffer
+    std::vector<int> rlen(n, 0);
+    std::vector<std::vector<int>> flat(nthreads);
+    const int rch = (n + nthreads - 1) / nthreads;
     auto worker_sym = [&](int t) {
         std::vector<int> mark(n, -1);
-        for (int i = t; i < n; i += nthreads) {
-            std::vector<int>& c = rc[i];
-            std::vector<int>& l = rl[i];
+        std::vector<int> c;
+        std::vector<int>& fl = flat[t];
+        fl.reserve(static_cast<size_t>(a.rp[std::min(n, (t + 1) * rch)] - a.rp[std::min(n, t * rch)]) * 2);
+        for (int i = t * rch; i < std::min(n, (t + 1) * rch); ++i) {
             c.assign(a.col.begin() + a.rp[i], a.col.begin() + a.rp[i + 1]);
             if (!std::binary_search(c.begin(), c.end(), i)) c.insert(std::lower_bound(c.begin(), c.end(), i), i);
             for (int j : c) mark[j] = i;
@@ -140,16 +154,9 @@ bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nth
                     }
                 }
             }
-            l.assign(c.size(), 0);
-            if (c.size() > orig) {  // merge the fill (level 1) into the sorted original pattern
-                std::vector<std::pair<int, int>> e(c.size());
-                for (size_t x = 0; x < c.size(); ++x) e[x] = {c[x], x < orig ? 0 : 1};
-                std::sort(e.begin(), e.end());
-                for (size_t x = 0; x < e.size(); ++x) {
-                    c[x] = e[x].first;
-                    l[x] = e[x].second;
-                }
-            }
+            if (c.size() > orig) std::sort(c.begin(), c.end());  // merge the fill (level 1), columns distinct
+            fl.insert(fl.end(), c.begin(), c.end());
+            rlen[i] = static_cast<int>(c.size());
         }
     };
     {
@@ -157,18 +164,27 @@ bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nth
         for (int t = 0; t < nthreads; ++t) th.emplace_back(worker_sym, t);
         for (auto& t : th) t.join();
     }
+    sc.mark("ilu symbolic");
     out.n = n;
     out.rp.assign(n + 1, 0);
-    for (int i = 0; i < n; ++i) out.rp[i + 1] = out.rp[i] + static_cast<int>(rc[i].size());
+    for (int i = 0; i < n; ++i) out.rp[i + 1] = out.rp[i] + rlen[i];
     out.col.resize(out.rp[n]);
     out.val.assign(out.rp[n], 0.0);
     std::vector<int> diag(n, -1);
-    for (int i = 0; i < n; ++i) {
-        std::copy(rc[i].begin(), rc[i].end(), out.col.begin() + out.rp[i]);
-        diag[i] = out.rp[i] + static_cast<int>(std::lower_bound(rc[i].begin(), rc[i].end(), i) - rc[i].begin());
-        std::vector<int>().swap(rc[i]);
-        std::vector<int>().swap(rl[i]);
+    {  // each thread places its block of rows and locates their diagonals
+        std::vector<std::thread> th;
+        for (int t = 0; t < nthreads; ++t)
+            th.emplace_back([&, t] {
+                const int i0 = std::min(n, t * rch), i1 = std::min(n, (t + 1) * rch);
+                if (i0 < i1) std::copy(flat[t].begin(), flat[t].end(), out.col.begin() + out.rp[i0]);
+                std::vector<int>().swap(flat[t]);
+                for (int i = i0; i < i1; ++i)
+                    diag[i] = static_cast<int>(std::lower_bound(out.col.begin() + out.rp[i], out.col.begin() + out.rp[i + 1], i) -
+                                               out.col.begin());
+            });
+        for (auto& x : th) x.join();
     }
+    sc.mark("ilu csr assembly");
     // levels of the final lower pattern
     std::vector<int> lev(n, 0);
     int nlev = 0;
@@ -185,6 +201,7 @@ bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nth
         std::vector<int> fill(lptr.begin(), lptr.end() - 1);
         for (int i = 0; i < n; ++i) rows[fill[lev[i]]++] = i;
     }
+    sc.mark("ilu levels");
     std::atomic<bool> broke{false};
     SpinBarrier bar(nthreads);
     auto worker_num = [&](int t) {
@@ -221,6 +238,7 @@ bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nth
         for (int t = 0; t < nthreads; ++t) th.emplace_back(worker_num, t);
         for (auto& t : th) t.join();
     }
+    sc.mark("ilu numeric");
     return !broke;
 }
 
@@ -356,42 +374,65 @@ void pack(const std::vector<int>& level, int n_levels, TriSchedule& t,
             });
         for (auto& x : th) x.join();
     }
+    StageClock sc;
     for (int p = 0; p < t.n_pos; ++p) t.rp[p + 1] += t.rp[p];
     t.col.resize(t.rp[t.n_pos]);
     t.val.resize(t.rp[t.n_pos]);
-    for (int k = 0; k < nthr; ++k) {
-        const int p0 = std::min(t.n_pos, k * pchunk);
-        std::copy(pc[k].begin(), pc[k].end(), t.col.begin() + t.rp[p0]);
-        std::copy(pv[k].begin(), pv[k].end(), t.val.begin() + t.rp[p0]);
-    }
-    t.maxd = 0;
-    for (int p = 0; p < t.n_pos; ++p) t.maxd = std::max(t.maxd, t.rp[p + 1] - t.rp[p]);
-    t.ell_col.assign(static_cast<size_t>(t.maxd) * t.n_pos, -1);
-    t.ell_val.assign(static_cast<size_t>(t.maxd) * t.n_pos, 0.0);
     t.pos.assign(n, -1);
-    for (int p = 0; p < t.n_pos; ++p)
-        if (t.order[p] >= 0) t.pos[t.order[p]] = p;
-    t.ell_pcol.assign(static_cast<size_t>(t.maxd) * t.n_pos, -1);
-    // ELL transposition: entry k of position p at k * n_pos + p; threads own position ranges
+    std::vector<int> maxd(nthr, 0);
+    {  // each thread places its own position range (and its rows' positions)
+        std::vector<std::thread> th;
+        for (int k = 0; k < nthr; ++k)
+            th.emplace_back([&, k] {
+                const int p0 = std::min(t.n_pos, k * pchunk), p1 = std::min(t.n_pos, (k + 1) * pchunk);
+                std::copy(pc[k].begin(), pc[k].end(), t.col.begin() + t.rp[p0]);
+                std::copy(pv[k].begin(), pv[k].end(), t.val.begin() + t.rp[p0]);
+                std::vector<int>().swap(pc[k]);
+                std::vector<double>().swap(pv[k]);
+                for (int p = p0; p < p1; ++p) {
+                    maxd[k] = std::max(maxd[k], t.rp[p + 1] - t.rp[p]);
+                    if (t.order[p] >= 0) t.pos[t.order[p]] = p;
+                }
+            });
+        for (auto& x : th) x.join();
+    }
+    t.maxd = *std::max_element(maxd.begin(), maxd.end());
+    const size_t ne = static_cast<size_t>(t.maxd) * t.n_pos;
+    // ELL transposition: entry k of position p at k * n_pos + p (padding -1 / 0); threads own
+    // position ranges and write every slot of them, so the arrays need no prior fill
+    t.ell_col.resize(ne);
+    t.ell_val.resize(ne);
+    t.ell_pcol.resize(ne);
+    sc.mark("pack concat + pos");
     const int nth = host_threads();
     auto ell = [&](int p0, int p1) {
-        for (int p = p0; p < p1; ++p)
-            for (int q = t.rp[p]; q < t.rp[p + 1]; ++q) {
-                const size_t x = static_cast<size_t>(q - t.rp[p]) * t.n_pos + p;
-                t.ell_col[x] = t.col[q];
-                t.ell_val[x] = t.val[q];
-                t.ell_pcol[x] = t.pos[t.col[q]];
+        for (int p = p0; p < p1; ++p) {
+            const int b = t.rp[p], len = t.rp[p + 1] - b;
+            for (int k = 0; k < t.maxd; ++k) {
+                const size_t x = static_cast<size_t>(k) * t.n_pos + p;
+                if (k < len) {
+                    t.ell_col[x] = t.col[b + k];
+                    t.ell_val[x] = t.val[b + k];
+                    t.ell_pcol[x] = t.pos[t.col[b + k]];
+                } else {
+                    t.ell_col[x] = -1;
+                    t.ell_val[x] = 0.0;
+                    t.ell_pcol[x] = -1;
+                }
             }
+        }
     };
     std::vector<std::thread> th;
     const int chunk = (t.n_pos + nth - 1) / nth;
     for (int k = 0; k < nth; ++k) th.emplace_back(ell, std::min(t.n_pos, k * chunk), std::min(t.n_pos, (k + 1) * chunk));
     for (auto& x : th) x.join();
+    sc.mark("pack ell");
 }
 
 }  // namespace
 
 void schedule_lower(const ScalarCsr& lu, TriSchedule& t) {
+    StageClock sc;
     const int n = lu.n;
     std::vector<int> level(n, 0);
     int n_levels = 0;
@@ -401,6 +442,7 @@ void schedule_lower(const ScalarCsr& lu, TriSchedule& t) {
         level[i] = l;
         n_levels = std::max(n_levels, l + 1);
     }
+    sc.mark("lower levels");
     // forward row: entries col < i in ascending column order (linalg.cpp:304-306)
     pack(level, n_levels, t, [&](int i, std::vector<int>& c, std::vector<double>& v, double&) {
         for (int p = lu.rp[i]; p < lu.rp[i + 1] && lu.col[p] < i; ++p) {
@@ -602,7 +644,8 @@ std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out) {
 
 namespace sfv {
 
-bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, std::vector<StreamRecord>& out) {
+bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed) {
+    StageClock sc;
     if (t.maxd > 8) return false;
     const int np = t.n_pos;
     std::vector<int> owner(np, 0), ordinal(np, 0), level_of(np, 0);
@@ -620,20 +663,41 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
             level_of[p] = l;
         }
     }
-    out.assign(np, StreamRecord{});
+    sc.mark("records owners");
+    // device chunk layout (precond_host.h): per 32 positions val[8][32], diag[32], dep[8][32],
+    // own[32]; positions are whole chunks (levels padded to 32), every byte written below
+    const size_t nchunk = (static_cast<size_t>(np) + 31) / 32;
+    packed.resize(nchunk * kChunkBytes);
+    sc.mark("records alloc");
     long long n_dep = 0, n_local = 0, n_near = 0, n_near_remote = 0;
     // positions are independent: threads own position ranges; statistics only when asked
     const bool stats = std::getenv("SFV_STREAM_STATS") != nullptr;
     const int nthr = stats ? 1 : host_threads();
     std::atomic<bool> bad{false};
-    auto body = [&](int p0, int p1) {
-    for (int p = p0; p < p1 && !bad; ++p) {
-        StreamRecord& rec = out[p];
-        rec.own = static_cast<uint16_t>(ordinal[p] % ring);
-        rec.diag = t.diag[p];
+    auto body = [&](int c0, int c1) {  // chunk ranges
+    for (int ch = c0; ch < c1 && !bad; ++ch) {
+        unsigned char* cb = packed.data() + static_cast<size_t>(ch) * kChunkBytes;
+        double* cval = reinterpret_cast<double*>(cb);
+        double* cdiag = reinterpret_cast<double*>(cb + 2048);
+        uint16_t* cdep = reinterpret_cast<uint16_t*>(cb + 2304);
+        uint16_t* cown = reinterpret_cast<uint16_t*>(cb + 2816);
+        std::memset(cb + 2880, 0, kChunkBytes - 2880);
+    for (int l = 0; l < 32; ++l) {
+        const int p = ch * 32 + l;
+        if (p >= np) {  // tail: no dependencies
+            for (int k = 0; k < 8; ++k) {
+                cval[k * 32 + l] = 0.0;
+                cdep[k * 32 + l] = 0xffff;
+            }
+            cdiag[l] = 0.0;
+            cown[l] = 0;
+            continue;
+        }
+        cown[l] = static_cast<uint16_t>(ordinal[p] % ring);
+        cdiag[l] = t.diag[p];
         for (int k = 0; k < 8; ++k) {
-            rec.dep[k] = 0xffff;
-            rec.val[k] = 0.0;
+            cdep[k * 32 + l] = 0xffff;
+            cval[k * 32 + l] = 0.0;
             if (k >= t.maxd) continue;
             const int q = t.ell_pcol[static_cast<size_t>(k) * np + p];
             if (q < 0) continue;
@@ -644,8 +708,8 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
                 bad = true;
                 return;
             }
-            rec.dep[k] = static_cast<uint16_t>((r << 12) | (ordinal[q] % ring));
-            rec.val[k] = t.ell_val[static_cast<size_t>(k) * np + p];
+            cdep[k * 32 + l] = static_cast<uint16_t>((r << 12) | (ordinal[q] % ring));
+            cval[k * 32 + l] = t.ell_val[static_cast<size_t>(k) * np + p];
             if (stats) {
                 ++n_dep;
                 if (r == owner[p]) ++n_local;
@@ -656,11 +720,13 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
             }
         }
     }
+    }
     };
     {
         std::vector<std::thread> th;
-        const int ch = (np + nthr - 1) / nthr;
-        for (int k = 0; k < nthr; ++k) th.emplace_back(body, std::min(np, k * ch), std::min(np, (k + 1) * ch));
+        const int nch = static_cast<int>(nchunk);
+        const int ch = (nch + nthr - 1) / nthr;
+        for (int k = 0; k < nthr; ++k) th.emplace_back(body, std::min(nch, k * ch), std::min(nch, (k + 1) * ch));
         for (auto& x : th) x.join();
     }
     if (bad) return false;
@@ -815,38 +881,5 @@ bool build_pipe(const ScalarCsr& lu, bool upper, int blocks, int ring, PipeSched
     return true;
 }
 
-void pack_stream_chunks(const std::vector<StreamRecord>& recs, std::vector<unsigned char>& out) {
-    const size_t nchunk = (recs.size() + 31) / 32;
-    out.assign(nchunk * kChunkBytes, 0);
-    const int nthr = host_threads();
-    auto body = [&](size_t c0, size_t c1) {
-        for (size_t ch = c0; ch < c1; ++ch) {
-            unsigned char* c = out.data() + ch * kChunkBytes;
-            double* val = reinterpret_cast<double*>(c);
-            double* diag = reinterpret_cast<double*>(c + 2048);
-            uint16_t* dep = reinterpret_cast<uint16_t*>(c + 2304);
-            uint16_t* own = reinterpret_cast<uint16_t*>(c + 2816);
-            for (size_t l = 0; l < 32; ++l) {
-                const size_t p = ch * 32 + l;
-                if (p >= recs.size()) {  // padding rows: no dependencies
-                    for (int q = 0; q < 8; ++q) dep[q * 32 + l] = 0xffff;
-                    continue;
-                }
-                const StreamRecord& r = recs[p];
-                for (int q = 0; q < 8; ++q) {
-                    val[q * 32 + l] = r.val[q];
-                    dep[q * 32 + l] = r.dep[q];
-                }
-                diag[l] = r.diag;
-                own[l] = r.own;
-            }
-        }
-    };
-    std::vector<std::thread> th;
-    const size_t cpt = (nchunk + nthr - 1) / nthr;
-    for (int k = 0; k < nthr; ++k)
-        th.emplace_back(body, std::min(nchunk, k * cpt), std::min(nchunk, (k + 1) * cpt));
-    for (auto& x : th) x.join();
-}
 
 }  // namespace sfv

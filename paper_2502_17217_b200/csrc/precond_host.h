@@ -2,7 +2,10 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
+#include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "host_mesh.h"
@@ -26,16 +29,41 @@ std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar,
 // IluBreakdown message.  The factor is the combined LU in one CSR pattern.
 std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& lu);
 
+// Allocator that leaves resized elements uninitialised: the large setup arrays below are
+// written completely by parallel passes, which then also do the first touch of the pages.
+template <class T>
+struct NoInit : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = NoInit<U>;
+    };
+    NoInit() = default;
+    template <class U>
+    NoInit(const NoInit<U>&) noexcept {}
+    template <class U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using rawvec = std::vector<T, NoInit<T>>;
+
 // One triangular sweep in dependency-level order, levels padded to whole warps.
 struct TriSchedule {
     int n_pos = 0, n_levels = 0;
-    std::vector<int> order, rp, col, level_ptr;
-    std::vector<double> val, diag;
+    std::vector<int> order, rp, level_ptr;
+    rawvec<int> col;
+    rawvec<double> val;
+    std::vector<double> diag;
     int maxd = 0;
-    std::vector<int> ell_col;   // [maxd * n_pos], entry k of position p at k * n_pos + p
-    std::vector<int> ell_pcol;  // the same columns as positions of this schedule
-    std::vector<double> ell_val;
-    std::vector<int> pos;       // row -> position
+    rawvec<int> ell_col;   // [maxd * n_pos], entry k of position p at k * n_pos + p
+    rawvec<int> ell_pcol;  // the same columns as positions of this schedule
+    rawvec<double> ell_val;
+    std::vector<int> pos;  // row -> position
 };
 void schedule_lower(const ScalarCsr& lu, TriSchedule& t);
 void schedule_upper(const ScalarCsr& lu, TriSchedule& t);
@@ -62,13 +90,14 @@ struct StreamRecord {
     double diag;
 };
 static_assert(sizeof(StreamRecord) == 96, "record layout");
-bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, std::vector<StreamRecord>& out);
+// Built directly in the device chunk layout below (every byte written by the parallel pass).
+bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed);
 // Device layout of the records: per chunk of 32 positions (levels are padded to 32), the
 // fields as arrays over the 32 positions — val[8][32], diag[32], dep[8][32], own[32],
 // 3072 bytes — so that a warp reading one field of 32 consecutive rows from shared
 // memory is bank-conflict free (the 96-byte AoS record was read at a 96-byte lane stride).
 constexpr int kChunkBytes = 3072;
-void pack_stream_chunks(const std::vector<StreamRecord>& recs, std::vector<unsigned char>& out);
+
 
 // Block-pipelined sweep (precond_pipe.cu): the rows, in sweep order, are cut into `blocks`
 // contiguous blocks, one CTA each; CTA b walks only the dependency levels present in its
