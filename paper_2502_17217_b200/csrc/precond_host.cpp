@@ -20,32 +20,36 @@ namespace sfv {
 std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar, bool transient, double rho,
                           double dt, std::vector<ScalarCsr>& comps) {
     const int nc = m.n_cells;
-    // pattern: diagonal plus one entry per internal face side, columns sorted (discretisation.cpp:223-236)
-    std::vector<int> rp(nc + 1, 1);
-    rp[0] = 0;
-    for (int f = 0; f < m.n_internal; ++f) {
-        ++rp[m.owner[f] + 1];
-        ++rp[m.neighbour[f] + 1];
-    }
-    for (int c = 0; c < nc; ++c) rp[c + 1] += rp[c];
-    std::vector<int> col(rp[nc]);
-    std::vector<int> fill(rp.begin(), rp.end() - 1);
-    for (int c = 0; c < nc; ++c) col[fill[c]++] = c;
-    for (int f = 0; f < m.n_internal; ++f) {
-        col[fill[m.owner[f]]++] = m.neighbour[f];
-        col[fill[m.neighbour[f]]++] = m.owner[f];
-    }
-    {  // rows sort independently
-        const int nth = host_threads();
+    // pattern: diagonal plus one entry per internal face side, columns sorted
+    // (discretisation.cpp:223-236); built per cell from its face list, rows in parallel
+    std::vector<int> rp(nc + 1, 0);
+    const int nthp = host_threads();
+    auto prows = [&](const std::function<void(int, int)>& body) {
         std::vector<std::thread> th;
-        const int ch = (nc + nth - 1) / nth;
-        for (int k = 0; k < nth; ++k)
-            th.emplace_back([&, k] {
-                for (int c = k * ch; c < std::min(nc, (k + 1) * ch); ++c)
-                    std::sort(col.begin() + rp[c], col.begin() + rp[c + 1]);
-            });
+        const int ch = (nc + nthp - 1) / nthp;
+        for (int k = 0; k < nthp; ++k) th.emplace_back(body, std::min(nc, k * ch), std::min(nc, (k + 1) * ch));
         for (auto& x : th) x.join();
-    }
+    };
+    prows([&](int c0, int c1) {
+        for (int c = c0; c < c1; ++c) {
+            int k = 1;
+            for (int q = m.cf_off[c]; q < m.cf_off[c + 1]; ++q) k += m.cf[q] < m.n_internal;
+            rp[c + 1] = k;
+        }
+    });
+    for (int c = 0; c < nc; ++c) rp[c + 1] += rp[c];
+    rawvec<int> col(rp[nc]);
+    prows([&](int c0, int c1) {
+        for (int c = c0; c < c1; ++c) {
+            int x = rp[c];
+            col[x++] = c;
+            for (int q = m.cf_off[c]; q < m.cf_off[c + 1]; ++q) {
+                const int f = m.cf[q];
+                if (f < m.n_internal) col[x++] = m.owner[f] == c ? m.neighbour[f] : m.owner[f];
+            }
+            std::sort(col.begin() + rp[c], col.begin() + rp[c + 1]);
+        }
+    });
     bool sym = false;
     for (int f = m.n_internal; f < m.n_faces(); ++f)
         if (m.patches[m.face_patch[f]].kind == SFV_PATCH_SYMMETRY) {
@@ -169,14 +173,17 @@ bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nth
     out.rp.assign(n + 1, 0);
     for (int i = 0; i < n; ++i) out.rp[i + 1] = out.rp[i] + rlen[i];
     out.col.resize(out.rp[n]);
-    out.val.assign(out.rp[n], 0.0);
+    out.val.resize(out.rp[n]);  // zeroed per row block below (fill entries start at 0)
     std::vector<int> diag(n, -1);
     {  // each thread places its block of rows and locates their diagonals
         std::vector<std::thread> th;
         for (int t = 0; t < nthreads; ++t)
             th.emplace_back([&, t] {
                 const int i0 = std::min(n, t * rch), i1 = std::min(n, (t + 1) * rch);
-                if (i0 < i1) std::copy(flat[t].begin(), flat[t].end(), out.col.begin() + out.rp[i0]);
+                if (i0 < i1) {
+                    std::copy(flat[t].begin(), flat[t].end(), out.col.begin() + out.rp[i0]);
+                    std::fill(out.val.begin() + out.rp[i0], out.val.begin() + out.rp[i1], 0.0);
+                }
                 std::vector<int>().swap(flat[t]);
                 for (int i = i0; i < i1; ++i)
                     diag[i] = static_cast<int>(std::lower_bound(out.col.begin() + out.rp[i], out.col.begin() + out.rp[i + 1], i) -
@@ -467,8 +474,8 @@ bool ic0_factor(const ScalarCsr& a, ScalarCsr& L) {
         L.rp[i + 1] = static_cast<int>(L.col.size());
     }
     const std::vector<int>& rp = L.rp;
-    const std::vector<int>& col = L.col;
-    std::vector<double>& val = L.val;
+    const auto& col = L.col;
+    auto& val = L.val;
     for (int i = 0; i < n; ++i) {
         const int diag_p = rp[i + 1] - 1;
         if (diag_p < rp[i] || col[diag_p] != i) return false;

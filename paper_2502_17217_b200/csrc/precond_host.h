@@ -12,23 +12,6 @@
 
 namespace sfv {
 
-struct ScalarCsr {
-    int n = 0;
-    std::vector<int> rp, col;  // columns ascending per row
-    std::vector<double> val;
-};
-
-// Per-component scalar matrices of assemble_approximate_jacobian
-// (/root/reference/proj/src/discretisation.cpp:216-262), accumulated entry by entry in
-// the reference's face order.  ncomp = 1 when every block is c*I (no symmetry faces),
-// 3 when blocks are diagonal (axis-aligned symmetry faces).  Returns "" or an error.
-std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar, bool transient, double rho,
-                          double dt, std::vector<ScalarCsr>& comps);
-
-// IlukPrecond ctor (linalg.cpp:251-300) on a scalar matrix: returns "" or the
-// IluBreakdown message.  The factor is the combined LU in one CSR pattern.
-std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& lu);
-
 // Allocator that leaves resized elements uninitialised: the large setup arrays below are
 // written completely by parallel passes, which then also do the first touch of the pages.
 template <class T>
@@ -51,6 +34,26 @@ struct NoInit : std::allocator<T> {
 };
 template <class T>
 using rawvec = std::vector<T, NoInit<T>>;
+
+struct ScalarCsr {
+    int n = 0;
+    std::vector<int> rp;
+    rawvec<int> col;  // columns ascending per row
+    rawvec<double> val;
+};
+
+// Per-component scalar matrices of assemble_approximate_jacobian
+// (/root/reference/proj/src/discretisation.cpp:216-262), accumulated entry by entry in
+// the reference's face order.  ncomp = 1 when every block is c*I (no symmetry faces),
+// 3 when blocks are diagonal (axis-aligned symmetry faces).  Returns "" or an error.
+std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar, bool transient, double rho,
+                          double dt, std::vector<ScalarCsr>& comps);
+
+// IlukPrecond ctor (linalg.cpp:251-300) on a scalar matrix: returns "" or the
+// IluBreakdown message.  The factor is the combined LU in one CSR pattern.
+std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& lu);
+
+
 
 // One triangular sweep in dependency-level order, levels padded to whole warps.
 struct TriSchedule {
