@@ -414,3 +414,20 @@ def test_segregated_symmetry_vs_oracle():
     assert abs(a - b) <= max(2, 0.02 * b)
     f = f.cpu().numpy()
     assert np.abs(f[0] - fo[0]).max() <= 1e-6 * np.abs(fo[0]).max()
+
+
+@pytest.mark.parametrize("path", ["fused", "twopass"])
+def test_alternative_jv_paths_bitwise(path, monkeypatch):
+    """The measured-and-rejected J.v kernels kept as switches (SFV_JV=fused: one persistent
+    face-once kernel; twopass: cell-centric two-pass kernels) still give the default path's
+    bits: R(u) and J.v at fixed eps against the oracle."""
+    sv = _sv()
+    monkeypatch.setenv("SFV_JV", path)
+    mesh = sv.box_mesh((1.0, 1.2, 0.8), (9, 7, 6), [D, T, T, T, T, T], distort=0.15, seed=42)
+    ev, orc = _pair(mesh, _phys())
+    u, v = cases.jv_inputs(mesh, seed=2)
+    r = orc.residual(u)
+    assert np.array_equal(ev.residual(u).cpu().numpy(), r)
+    eps = 3e-8
+    assert np.array_equal(sv.jacobian_vector_product(ev, u, r, v, eps=eps).cpu().numpy(),
+                          (orc.residual(u + eps * v) - r) / eps)
