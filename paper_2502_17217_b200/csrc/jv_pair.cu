@@ -64,6 +64,10 @@ __device__ __forceinline__ dm3 ldG(const double* __restrict__ r) {
     return a;
 }
 
+#ifndef SFV_GEN_CTAS
+#define SFV_GEN_CTAS 2  // resident 6-warp CTAs per SM the non-Hooke / TL face pass is compiled for
+#endif
+
 // programmatic dependent launch (see launch_win)
 __device__ __forceinline__ void wait_predecessor() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 #ifndef SFV_PDL_EARLY
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
 // INLB (Hooke, small strain, no symmetry patch): boundary faces are evaluated here, from the
 // cell's own gradient, instead of by boundary_kernel.
 template <bool PERT, int S, bool GEN, bool INLB>
-__global__ void __launch_bounds__(kCells* S, GEN ? 12 / S : 24 / S)
+__global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : 24 / S)
     flux_pair_kernel(DevMesh m, Physics ph, PatchTable pt, History hist, const double* __restrict__ wg,
                      const double* __restrict__ eps_p, const double* __restrict__ sig,
                      const double* __restrict__ bres, const double* __restrict__ r_u, double* __restrict__ out,
