@@ -64,6 +64,9 @@ __device__ __forceinline__ dm3 ldG(const double* __restrict__ r) {
     return a;
 }
 
+#ifndef SFV_HOOKE_CTAS
+#define SFV_HOOKE_CTAS 4  // resident 6-warp CTAs per SM the Hooke face pass is compiled for
+#endif
 #ifndef SFV_GEN_CTAS
 #define SFV_GEN_CTAS 2  // resident 6-warp CTAs per SM the non-Hooke / TL face pass is compiled for
 #endif
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
 // INLB (Hooke, small strain, no symmetry patch): boundary faces are evaluated here, from the
 // cell's own gradient, instead of by boundary_kernel.
 template <bool PERT, int S, bool GEN, bool INLB>
-__global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : 24 / S)
+__global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HOOKE_CTAS * 6 / S)
     flux_pair_kernel(DevMesh m, Physics ph, PatchTable pt, History hist, const double* __restrict__ wg,
                      const double* __restrict__ eps_p, const double* __restrict__ sig,
                      const double* __restrict__ bres, const double* __restrict__ r_u, double* __restrict__ out,
