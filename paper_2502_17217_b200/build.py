@@ -60,7 +60,8 @@ def build(verbose: bool = False) -> str:
         with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
             list(ex.map(_run, jobs))
     if _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-L/usr/local/cuda/lib64", "-lcusolver",
+              "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
     return LIB
 
 

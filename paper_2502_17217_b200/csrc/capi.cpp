@@ -1121,16 +1121,29 @@ int precond_create(sfv_ctx* c, int kind) {
     pt.mark("cell_jacobian");
     if (kind == SFV_PRECOND_LU) {
         for (size_t a = 0; a < comps.size(); ++a) {
+            // ordering and band on the host; the factorisation on the device (cuSOLVER dense
+            // Cholesky, SFV_HOST_LU=1: the host band factorisation)
             BandChol bc;
-            const std::string m2 = band_cholesky_neg(comps[a], bc);
+            const bool host_lu = std::getenv("SFV_HOST_LU") != nullptr;
+            const std::string m2 = band_cholesky_neg(comps[a], bc, host_lu);
             if (!m2.empty()) return c->fail(SFV_ERR_LU_SINGULAR, -1, m2);
+            pt.mark(host_lu ? "lu order + host factor" : "lu order + band");
             DevBuf<double> band;
             if (!band.upload(bc.l) || !c->dense_perm[a].upload(bc.perm) ||
                 !c->dense_w[a].alloc(static_cast<size_t>(bc.n) * bc.n))
                 return c->fail(SFV_ERR_CUDA, -1, "lu: out of device memory");
-            launch_band_inverse(band.p, bc.n, bc.bw, c->dense_w[a].p, c->stream);
-            ++c->launches;
-            if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->cuda_check("lu setup");
+            if (!host_lu) {  // factor and explicit inverse on the device
+                if (const std::string m3 = device_band_cholesky(band.p, bc.n, bc.bw, c->stream, c->dense_w[a].p);
+                    !m3.empty())
+                    return c->fail(m3.rfind("lu: factorisation", 0) == 0 ? SFV_ERR_LU_SINGULAR : SFV_ERR_CUDA, -1, m3);
+                c->launches += 3;
+                pt.mark("lu device factor + inverse");
+            } else {  // host band factor, inverse column by column on the device
+                launch_band_inverse(band.p, bc.n, bc.bw, c->dense_w[a].p, c->stream);
+                ++c->launches;
+                if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->cuda_check("lu setup");
+                pt.mark("lu inverse");
+            }
         }
         c->pc_kind = SFV_PRECOND_LU;
         return SFV_OK;

@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 
 #include <cuda_runtime.h>
 
@@ -314,6 +315,10 @@ void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double*
 void launch_dense_apply(const double* inv, int n, const double* r, double* z, cudaStream_t s);
 // Small-system exact preconditioner: W = (L L^T)^{-1} from a band Cholesky of -K, and
 // z = K^{-1} r = -P W P^T r applied to 3 interleaved components.
+// The band of -A (permuted, BandChol layout) factored by cuSOLVER dense Cholesky (potrf): with
+// W null the band becomes that of the factor (in place); with W the explicit inverse (potri)
+// is written to W (row-major n x n).  "" or the reference-style error text.
+std::string device_band_cholesky(double* band, int n, int bw, cudaStream_t s, double* W = nullptr);
 void launch_band_inverse(const double* l, int n, int bw, double* W, cudaStream_t s);
 // comp < 0: all three components with one W; comp = k: component k only
 void launch_dense_apply_perm(const double* W, int n, const int* perm, const double* r, double* z, int comp,

@@ -20,6 +20,10 @@
 
 #include <algorithm>
 
+#include <cusolverDn.h>
+
+#include <string>
+
 #include "device.h"
 
 namespace cg = cooperative_groups;
@@ -501,6 +505,75 @@ __global__ void __launch_bounds__(256) dense_apply_perm_kernel(const double* __r
 }
 
 }  // namespace
+
+// Dense Cholesky of the (permuted) band of -A by cuSOLVER: the band is scattered into a dense
+// column-major matrix, factored in place (lower), and the band of L read back out — Cholesky
+// does not fill outside the band.  Replaces the host band factorisation for the small-system
+// exact preconditioner (parity there is "any exact solve").
+__global__ void band_to_dense_kernel(const double* __restrict__ l, int n, int bw, double* __restrict__ D) {
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int w = bw + 1;
+    if (idx >= static_cast<size_t>(n) * w) return;
+    const int i = static_cast<int>(idx / w), k = static_cast<int>(idx % w);
+    const int j = i - bw + k;
+    if (j < 0) return;
+    D[static_cast<size_t>(j) * n + i] = l[idx];  // column-major, lower triangle (row i >= column j)
+}
+__global__ void dense_to_band_kernel(const double* __restrict__ D, int n, int bw, double* __restrict__ l) {
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int w = bw + 1;
+    if (idx >= static_cast<size_t>(n) * w) return;
+    const int i = static_cast<int>(idx / w), k = static_cast<int>(idx % w);
+    const int j = i - bw + k;
+    l[idx] = j < 0 ? 0.0 : D[static_cast<size_t>(j) * n + i];
+}
+
+__global__ void identity_kernel(int n, double* __restrict__ W) {
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx < static_cast<size_t>(n) * n) W[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
+}
+std::string device_band_cholesky(double* band, int n, int bw, cudaStream_t s, double* W) {
+    cusolverDnHandle_t h = nullptr;
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) return "lu: cusolver unavailable";
+    cusolverDnSetStream(h, s);
+    double* D = nullptr;
+    double* work = nullptr;
+    int* info = nullptr;
+    std::string err;
+    int lwork = 0, hinfo = 0;
+    const size_t nn = static_cast<size_t>(n) * n, nb = static_cast<size_t>(n) * (bw + 1);
+    if (cudaMalloc(&D, sizeof(double) * nn) != cudaSuccess || cudaMalloc(&info, sizeof(int)) != cudaSuccess) {
+        err = "lu: out of device memory";
+    } else {
+        cudaMemsetAsync(D, 0, sizeof(double) * nn, s);
+        band_to_dense_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, s>>>(band, n, bw, D);
+        if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, n, D, n, &lwork) != CUSOLVER_STATUS_SUCCESS ||
+            cudaMalloc(&work, sizeof(double) * (lwork > 0 ? lwork : 1)) != cudaSuccess) {
+            err = "lu: cusolver workspace";
+        } else if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, n, D, n, work, lwork, info) != CUSOLVER_STATUS_SUCCESS ||
+                   cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                   cudaStreamSynchronize(s) != cudaSuccess) {
+            err = "lu: factorisation failed";
+        } else if (hinfo != 0) {
+            err = "lu: factorisation failed";
+        } else if (!W) {
+            dense_to_band_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, s>>>(D, n, bw, band);
+            if (cudaStreamSynchronize(s) != cudaSuccess) err = "lu: factorisation failed";
+        } else {  // the explicit inverse: L L^T X = I by potrs (two TRSMs over n right-hand sides)
+            // X is symmetric, so its column-major image is the row-major W the apply reads
+            identity_kernel<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, s>>>(n, W);
+            if (cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, n, n, D, n, W, n, info) != CUSOLVER_STATUS_SUCCESS ||
+                cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess || hinfo != 0)
+                err = "lu: factorisation failed";
+        }
+    }
+    cudaFree(D);
+    cudaFree(work);
+    cudaFree(info);
+    cusolverDnDestroy(h);
+    return err;
+}
 
 void launch_band_inverse(const double* l, int n, int bw, double* W, cudaStream_t s) {
     band_inverse_kernel<<<(n + 127) / 128, 128, 0, s>>>(l, n, bw, W);

@@ -574,7 +574,7 @@ void schedule_upper(const ScalarCsr& lu, TriSchedule& t) {
     });
 }
 
-std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out) {
+std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out, bool factor) {
     const int n = a.n;
     // reverse Cuthill-McKee ordering of the symmetric pattern
     std::vector<int> deg(n);
@@ -631,6 +631,7 @@ std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out) {
             const int bi = inv[i], bj = inv[a.col[p]];
             if (bj <= bi) L(bi, bj) = -a.val[p];  // -A is symmetric positive definite
         }
+    if (!factor) return "";
     for (int i = 0; i < n; ++i) {
         const int j0 = std::max(0, i - bw);
         for (int j = j0; j < i; ++j) {

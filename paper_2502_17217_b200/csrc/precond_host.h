@@ -133,6 +133,7 @@ struct BandChol {
     std::vector<int> perm;  // band index -> original row
     std::vector<double> l;  // n * (bw + 1), l[i*(bw+1) + (j - i + bw)]
 };
-std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out);
+// factor = false: only the ordering (perm, bw) and the band of -A in l (not factored)
+std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out, bool factor = true);
 
 }  // namespace sfv

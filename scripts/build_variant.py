@@ -26,7 +26,8 @@ def main():
     lib_dir = os.path.join(ROOT, "scripts", "probes", "variants")
     os.makedirs(lib_dir, exist_ok=True)
     lib = os.path.join(lib_dir, f"libsfv_{name}.so")
-    B._run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o", lib, *objs])
+    B._run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o", lib, *objs, "-L/usr/local/cuda/lib64", "-lcusolver",
+            "-Xlinker", "-rpath=/usr/local/cuda/lib64"])
     print(lib)
 
 
