@@ -41,14 +41,11 @@ int main(int argc, char** argv) {
     mark("schedule_lower");
     schedule_upper(lu, tu);
     mark("schedule_upper");
-    std::vector<StreamRecord> recs;
     int max_rows = 32;
     for (int l = 0; l < tl.n_levels; ++l)
         max_rows = std::max(max_rows, ((tl.level_ptr[l + 1] - tl.level_ptr[l]) / 32 + 15) / 16 * 32);
-    const bool ok = build_stream_records(tl, 16, 3072, max_rows, recs);
+    rawvec<unsigned char> packed;
+    const bool ok = build_stream_records(tl, 16, 3072, max_rows, packed);
     mark(ok ? "stream records (L)" : "stream records FAILED");
-    std::vector<unsigned char> packed;
-    pack_stream_chunks(recs, packed);
-    mark("pack chunks (L)");
     return 0;
 }
