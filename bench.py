@@ -155,8 +155,9 @@ def run_reference(args):
     ref.set_time(1.0)
     r_u = ref.residual(u)
     # the reference is single-threaded; the K steps are spread over all host
-    # threads as concurrent independent J.v calls on the same (const) evaluator
-    threads = min(os.cpu_count() or 1, 32, max(1, args.steps)) if ref_available() else 1
+    # threads as concurrent independent J.v calls on the same (const) evaluator — every
+    # thread runs at least one, so a small K still uses all the cores
+    threads = min(os.cpu_count() or 1, 32) if ref_available() else 1
     per_thread = max(1, -(-args.steps // threads))
     warm = max(1, -(-args.warmup // threads))
     if ref_available():
