@@ -1151,8 +1151,10 @@ int precond_create(sfv_ctx* c, int kind) {
     const int level = kind == SFV_PRECOND_ILU0 ? 0 : kind == SFV_PRECOND_ILU1 ? 1 : 2;
     std::vector<ScalarCsr> lus(comps.size());
     bool broke = false;
+    // SFV_DEVICE_ILU=1: the numeric phase of ILU(0)/ILU(1) on the device (bit-identical factor)
+    const IluNumericFn numeric = std::getenv("SFV_DEVICE_ILU") ? device_ilu_numeric : nullptr;
     for (size_t a = 0; a < comps.size(); ++a)
-        if (!iluk_factor(comps[a], level, lus[a]).empty()) broke = true;
+        if (!iluk_factor(comps[a], level, lus[a], numeric).empty()) broke = true;
     if (broke) {  // one retry with a 1e-12 |diag| shift over the expanded diagonal (nonlinear.cpp:357-369)
         double dn = 0.0;
         for (int i = 0; i < c->nc; ++i)

@@ -20,6 +20,8 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 namespace sfv {
 
 constexpr int kMaxPatches = 16;
@@ -319,6 +321,9 @@ void launch_dense_apply(const double* inv, int n, const double* r, double* z, cu
 // W null the band becomes that of the factor (in place); with W the explicit inverse (potri)
 // is written to W (row-major n x n).  "" or the reference-style error text.
 std::string device_band_cholesky(double* band, int n, int bw, cudaStream_t s, double* W = nullptr);
+// ILU(<=1) numeric phase on the device (precond.cu; the IluNumericFn of precond_host.h)
+struct ScalarCsr;
+bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows);
 void launch_band_inverse(const double* l, int n, int bw, double* W, cudaStream_t s);
 // comp < 0: all three components with one W; comp = k: component k only
 void launch_dense_apply_perm(const double* W, int n, const int* perm, const double* r, double* z, int comp,

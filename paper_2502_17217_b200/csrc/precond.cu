@@ -699,3 +699,123 @@ void launch_dense_apply(const double* inv, int n, const double* r, double* z, cu
 namespace sfv {
 int ilu_ring_window() { return kRingPerCta * kDsCluster; }
 }  // namespace sfv
+
+// ---------------------------------------------------------------- ILU(<=1) numeric phase
+// IlukPrecond's IKJ elimination (linalg.cpp:283-299) on the device, one warp per row, rows in
+// dependency-level order over a persistent grid (every awaited row is held by a resident
+// warp at an earlier position, so the waits terminate).  Row i waits for row k (flag
+// published with release semantics after the row is final), l_ik = a_ik / u_kk by lane 0,
+// then the lanes take row k's upper entries and update the matching entries of row i
+// (binary search in the sorted row) — each entry of row i sees the same subtractions in the
+// same k order as the host loop, so the factor is bit-identical (-fmad=false).
+#include "host_threads.h"
+#include "precond_host.h"
+
+namespace sfv {
+namespace {
+
+__global__ void __launch_bounds__(256) ilu_numeric_kernel(int n, const int* __restrict__ rows,
+                                                          const int* __restrict__ rp, const int* __restrict__ col,
+                                                          const int* __restrict__ diag, double* val, int* done,
+                                                          int* broke) {
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < n; x += nw) {
+        const int i = rows[x];
+        const int r1 = rp[i + 1];
+        for (int p = rp[i]; p < r1; ++p) {
+            const int k = col[p];
+            if (k >= i) break;
+            if (lane == 0) {
+                int f;
+                do {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(done + k) : "memory");
+                } while (f == 0);
+            }
+            __syncwarp();
+            const double pivot = __ldcg(val + diag[k]);
+            if (pivot == 0.0 || !isfinite(pivot)) {
+                if (lane == 0) atomicExch(broke, 1);
+                break;
+            }
+            double lik = 0.0;
+            if (lane == 0) {
+                lik = val[p] / pivot;
+                val[p] = lik;
+            }
+            lik = __shfl_sync(0xffffffffu, lik, 0);
+            const int k1 = rp[k + 1];
+            for (int q = diag[k] + 1 + lane; q < k1; q += 32) {
+                const int j = col[q];
+                int lo = p + 1, hi = r1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (col[mid] < j) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo < r1 && col[lo] == j) val[lo] -= lik * __ldcg(val + q);
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const double d = val[diag[i]];
+            if (d == 0.0 || !isfinite(d)) atomicExch(broke, 1);
+            __threadfence();
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(done + i), "r"(1) : "memory");
+        }
+    }
+}
+
+template <typename T>
+T* dev_copy(const T* h, size_t n) {
+    T* d = nullptr;
+    if (cudaMalloc(&d, sizeof(T) * (n ? n : 1)) != cudaSuccess) return nullptr;
+    if (n) cudaMemcpy(d, h, sizeof(T) * n, cudaMemcpyHostToDevice);
+    return d;
+}
+
+}  // namespace
+
+bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows) {
+    StageClock sc;
+    const int n = out.n;
+    const size_t nnz = static_cast<size_t>(out.rp[n]);
+    int* d_rows = dev_copy(rows.data(), rows.size());
+    int* d_rp = dev_copy(out.rp.data(), out.rp.size());
+    int* d_col = dev_copy(out.col.data(), nnz);
+    int* d_diag = dev_copy(diag.data(), diag.size());
+    double* d_val = dev_copy(out.val.data(), nnz);
+    int* d_flags = nullptr;  // done[n] + broke
+    const bool alloc = d_rows && d_rp && d_col && d_diag && d_val &&
+                       cudaMalloc(&d_flags, sizeof(int) * (n + 1)) == cudaSuccess;
+    bool ok = false;
+    if (alloc) {
+        cudaMemset(d_flags, 0, sizeof(int) * (n + 1));
+        cudaDeviceSynchronize();
+        sc.mark("ilu device upload");
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ilu_numeric_kernel, 256, 0);
+        const int grid = std::max(1, std::min(sms * std::max(per, 1), (n + 7) / 8));
+        ilu_numeric_kernel<<<grid, 256>>>(n, d_rows, d_rp, d_col, d_diag, d_val, d_flags, d_flags + n);
+        cudaDeviceSynchronize();
+        sc.mark("ilu device kernel");
+        int broke = 1;
+        if (cudaMemcpy(&broke, d_flags + n, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess &&
+            cudaMemcpy(out.val.data(), d_val, sizeof(double) * nnz, cudaMemcpyDeviceToHost) == cudaSuccess)
+            ok = broke == 0;
+        sc.mark("ilu device download");
+    }
+    cudaFree(d_rows);
+    cudaFree(d_rp);
+    cudaFree(d_col);
+    cudaFree(d_diag);
+    cudaFree(d_val);
+    cudaFree(d_flags);
+    cudaGetLastError();  // a failed allocation falls back to the host factor, no sticky state
+    return ok;
+}
+
+}  // namespace sfv

@@ -130,7 +130,7 @@ struct SpinBarrier {
 // (levels of the final lower pattern) with each row's operations in the sequential order:
 // the factor is bit-identical.  Returns false on a breakdown (the caller reruns the
 // sequential code for the reference's exact message).
-bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nthreads) {
+bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nthreads, IluNumericFn numeric) {
     StageClock sc;
     const int n = a.n;
     // symbolic phase: each thread builds a contiguous block of rows into one flat buffer
@@ -209,6 +209,23 @@ bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nth
         for (int i = 0; i < n; ++i) rows[fill[lev[i]]++] = i;
     }
     sc.mark("ilu levels");
+    if (numeric) {  // A at the pattern positions (row blocks in parallel), then the device numeric phase
+        std::vector<std::thread> th;
+        for (int t = 0; t < nthreads; ++t)
+            th.emplace_back([&, t] {
+                std::vector<int> pos(n, 0);
+                for (int i = std::min(n, t * rch); i < std::min(n, (t + 1) * rch); ++i) {
+                    for (int q = out.rp[i]; q < out.rp[i + 1]; ++q) pos[out.col[q]] = q + 1;
+                    for (int p = a.rp[i]; p < a.rp[i + 1]; ++p) out.val[pos[a.col[p]] - 1] = a.val[p];
+                    for (int q = out.rp[i]; q < out.rp[i + 1]; ++q) pos[out.col[q]] = 0;
+                }
+            });
+        for (auto& x : th) x.join();
+        sc.mark("ilu scatter A");
+        const bool ok = numeric(out, diag, rows);
+        sc.mark("ilu numeric (device)");
+        return ok;
+    }
     std::atomic<bool> broke{false};
     SpinBarrier bar(nthreads);
     auto worker_num = [&](int t) {
@@ -251,11 +268,11 @@ bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nth
 
 }  // namespace
 
-std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& out) {
+std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& out, IluNumericFn numeric) {
     const int n = a.n;
     const int nthreads = host_threads();
-    if (level <= 1 && n >= 65536 && nthreads > 1 && !std::getenv("SFV_ILU_SERIAL") &&
-        iluk_factor_parallel(a, level, out, nthreads))
+    if (level <= 1 && n >= 65536 && (nthreads > 1 || numeric) && !std::getenv("SFV_ILU_SERIAL") &&
+        iluk_factor_parallel(a, level, out, nthreads, numeric))
         return "";
     // symbolic phase: level-of-fill row merge in ascending column order (linalg.cpp:252-269)
     out.n = n;

@@ -51,7 +51,12 @@ std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar,
 
 // IlukPrecond ctor (linalg.cpp:251-300) on a scalar matrix: returns "" or the
 // IluBreakdown message.  The factor is the combined LU in one CSR pattern.
-std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& lu);
+// Numeric phase of the ILU(<=1) factorisation on another engine (the device): out holds the
+// final pattern with A at its positions (fill entries 0), diag the diagonal positions and
+// rows the rows in dependency-level order; factors out.val in place with the reference's
+// per-entry operations, false on a breakdown (the caller reruns the sequential code).
+using IluNumericFn = bool (*)(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows);
+std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& lu, IluNumericFn numeric = nullptr);
 
 
 

@@ -193,6 +193,24 @@ def test_ilu_parallel_factorisation_bitwise(monkeypatch):
     assert np.array_equal(z_par, orc.precond_apply(r))
 
 
+@pytest.mark.parametrize("kind,code", [("ilu1", 3), ("ilu0", 2)])
+def test_ilu_device_numeric_bitwise(kind, code, monkeypatch):
+    """SFV_DEVICE_ILU=1: the numeric phase of the factorisation runs on the device (one warp
+    per row, rows in level order, release/acquire row flags); the factor must equal the host
+    one bit for bit (compared through the apply) and the reference's (through the oracle)."""
+    sv = _sv()
+    case = cases.config("c2", n=42)  # 74088 cells: above the parallel-factorisation threshold
+    mesh = case.mesh()
+    ev, orc = _pair(mesh, case.physics)
+    r = cases.uniform(9, 3 * mesh.n_cells)
+    z_host = sv.make_preconditioner(ev, kind).solve(r).cpu().numpy()
+    monkeypatch.setenv("SFV_DEVICE_ILU", "1")
+    z_dev = sv.make_preconditioner(ev, kind).solve(r).cpu().numpy()
+    assert np.array_equal(z_dev, z_host)
+    orc.precond_create(code)
+    assert np.array_equal(z_dev, orc.precond_apply(r))
+
+
 def test_ilu_apply_transient_bitwise():
     sv = _sv()
     case = cases.config("c4", n=8)
