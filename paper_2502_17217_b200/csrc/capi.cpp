@@ -1809,10 +1809,23 @@ int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v,
     cudaMemcpyAsync(c->ucand.p, u, bytes, cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(c->rcand.p, r_u, bytes, cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(c->tv.p, v, bytes, cudaMemcpyHostToDevice, c->stream);
-    const int e = sfv_jv(c, c->ucand.p, c->rcand.p, c->tv.p, c->wv.p, cell);
-    if (e) return e;
+    if (c->singular_cell >= 0) {  // sfv_jv's GradientFailure / zero-direction rule
+        const int e = sfv_jv(c, c->ucand.p, c->rcand.p, c->tv.p, c->wv.p, cell);
+        if (e) return e;
+        cudaMemcpyAsync(out, c->wv.p, bytes, cudaMemcpyDeviceToHost, c->stream);
+        return cudaStreamSynchronize(c->stream) == cudaSuccess ? SFV_OK : c->cuda_check("jv_host");
+    }
+    // one host synchronisation: the result copy is queued before the error words are read
+    // (on an error, out holds the failed product, as the reference leaves its output undefined)
+    if (cell) *cell = -1;
+    reset_err(c);
+    jv_async(c, c->ucand.p, c->rcand.p, c->tv.p, c->wv.p, false);
     cudaMemcpyAsync(out, c->wv.p, bytes, cudaMemcpyDeviceToHost, c->stream);
-    return cudaStreamSynchronize(c->stream) == cudaSuccess ? SFV_OK : c->cuda_check("jv_host");
+    if (int e = c->cuda_check("jv_host")) return e;
+    if (int e = fetch(c, 0)) return e;
+    const int e = decode_residual_errors(c, true);
+    if (cell) *cell = e ? c->last.cell : -1;
+    return e;
 }
 
 int sfv_precond_create(sfv_ctx* c, int kind) { return precond_create(c, kind); }
