@@ -173,11 +173,17 @@ struct sfv_ctx {
     int v_cap = 0;
     long long launches = 0;
     SfvError last{0, -1, ""};
+    // host-buffer J.v: r_u uploaded on a copy stream while the ε and gradient passes run
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_uv = nullptr, ev_ru = nullptr;
     ~sfv_ctx() {
         free_device_geometry(dgeo);
         if (ps.ev_w) cudaEventDestroy(ps.ev_w);
         if (ps.ev_b) cudaEventDestroy(ps.ev_b);
         if (ps.side) cudaStreamDestroy(ps.side);
+        if (ev_uv) cudaEventDestroy(ev_uv);
+        if (ev_ru) cudaEventDestroy(ev_ru);
+        if (copy) cudaStreamDestroy(copy);
     }
 
     int fail(int code, int cell, const std::string& msg) {
@@ -1806,10 +1812,20 @@ int sfv_residual_host(sfv_ctx* c, const double* u, double* r, int* cell) {
 int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out, int* cell) {
     const size_t bytes = sizeof(double) * c->n;
     if (!ensure_krylov(c, 1)) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
+    if (!c->copy && (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&c->ev_uv, cudaEventDisableTiming) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&c->ev_ru, cudaEventDisableTiming) != cudaSuccess))
+        return c->cuda_check("jv_host streams");
+    // u and v first (the ε and gradient passes need them); r_u, read only by the face pass,
+    // follows on the copy stream while those passes run
     cudaMemcpyAsync(c->ucand.p, u, bytes, cudaMemcpyHostToDevice, c->stream);
-    cudaMemcpyAsync(c->rcand.p, r_u, bytes, cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(c->tv.p, v, bytes, cudaMemcpyHostToDevice, c->stream);
-    if (c->singular_cell >= 0) {  // sfv_jv's GradientFailure / zero-direction rule
+    cudaEventRecord(c->ev_uv, c->stream);
+    cudaStreamWaitEvent(c->copy, c->ev_uv, 0);
+    cudaMemcpyAsync(c->rcand.p, r_u, bytes, cudaMemcpyHostToDevice, c->copy);
+    cudaEventRecord(c->ev_ru, c->copy);
+    if (c->singular_cell >= 0) {
+        cudaStreamWaitEvent(c->stream, c->ev_ru, 0);  // sfv_jv's GradientFailure / zero-direction rule
         const int e = sfv_jv(c, c->ucand.p, c->rcand.p, c->tv.p, c->wv.p, cell);
         if (e) return e;
         cudaMemcpyAsync(out, c->wv.p, bytes, cudaMemcpyDeviceToHost, c->stream);
@@ -1819,7 +1835,11 @@ int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v,
     // (on an error, out holds the failed product, as the reference leaves its output undefined)
     if (cell) *cell = -1;
     reset_err(c);
+    if (c->use_fused || c->jv_path != 0) cudaStreamWaitEvent(c->stream, c->ev_ru, 0);  // no in-pass wait
+    c->ps.ru_ready = c->ev_ru;
     jv_async(c, c->ucand.p, c->rcand.p, c->tv.p, c->wv.p, false);
+    c->ps.ru_ready = nullptr;
+    cudaStreamWaitEvent(c->stream, c->ev_ru, 0);  // also when the product short-circuits
     cudaMemcpyAsync(out, c->wv.p, bytes, cudaMemcpyDeviceToHost, c->stream);
     if (int e = c->cuda_check("jv_host")) return e;
     if (int e = fetch(c, 0)) return e;

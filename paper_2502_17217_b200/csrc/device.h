@@ -116,6 +116,8 @@ struct PairScratch {
     // boundary pass on a side stream, beside the gradient pass (null: in line)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_w = nullptr, ev_b = nullptr;
+    // optional: r_u arrives on another stream (host-buffer J.v); the face pass waits for it
+    cudaEvent_t ru_ready = nullptr;
     const double* partials = nullptr;  // block partials (or, with bar, the fused pass's scratch)
     int npart = 0;
     // set: eps_perturb_kernel reduces the norms itself (grid barrier on this counter) and

@@ -758,6 +758,7 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     }
     if (ps.marks) cudaEventRecord(ps.marks[2], st);
     const int ntiles = (m.nc + kCells - 1) / kCells;
+    if (ps.ru_ready) cudaStreamWaitEvent(st, ps.ru_ready, 0);
     const double* cwg = wg;
     const double* sg = ps.sig;
     const double* br = ps.bres;

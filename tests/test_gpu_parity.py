@@ -449,3 +449,26 @@ def test_alternative_jv_paths_bitwise(path, monkeypatch):
     eps = 3e-8
     assert np.array_equal(sv.jacobian_vector_product(ev, u, r, v, eps=eps).cpu().numpy(),
                           (orc.residual(u + eps * v) - r) / eps)
+
+
+def test_jv_host_buffers_bitwise():
+    """sfv_jv_host (host buffers; r_u uploaded on a copy stream while the first passes run)
+    returns the device-resident J.v bit for bit, repeatedly."""
+    import ctypes as C
+    sv = _sv()
+    case = cases.config("c2", n=24)
+    mesh = case.mesh()
+    ev = sv.ResidualEvaluator(mesh, case.physics)
+    ev.set_time(1.0)
+    u, v = cases.jv_inputs(mesh)
+    r_u = ev.residual(u).cpu().numpy()
+    ref = sv.jacobian_vector_product(ev, u, r_u, v).cpu().numpy()
+    dp = C.POINTER(C.c_double)
+    hu, hr, hv = (np.ascontiguousarray(x, dtype=np.float64) for x in (u, r_u, v))
+    for _ in range(3):
+        out = np.empty_like(hu)
+        cell = C.c_int(-1)
+        rc = ev.L.sfv_jv_host(ev.h, hu.ctypes.data_as(dp), hr.ctypes.data_as(dp), hv.ctypes.data_as(dp),
+                              out.ctypes.data_as(dp), C.byref(cell))
+        ev._check(rc, cell.value)
+        assert np.array_equal(out, ref)
