@@ -1158,7 +1158,11 @@ int precond_create(sfv_ctx* c, int kind) {
     std::vector<ScalarCsr> lus(comps.size());
     bool broke = false;
     // SFV_DEVICE_ILU=1: the numeric phase of ILU(0)/ILU(1) on the device (bit-identical factor)
-    const IluNumericFn numeric = std::getenv("SFV_DEVICE_ILU") ? device_ilu_numeric : nullptr;
+    IluNumericFn numeric;
+    if (std::getenv("SFV_DEVICE_ILU"))
+        numeric = [c](ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows) {
+            return device_ilu_numeric(out, diag, rows, c->stream);
+        };
     for (size_t a = 0; a < comps.size(); ++a)
         if (!iluk_factor(comps[a], level, lus[a], numeric).empty()) broke = true;
     if (broke) {  // one retry with a 1e-12 |diag| shift over the expanded diagonal (nonlinear.cpp:357-369)

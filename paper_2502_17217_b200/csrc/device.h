@@ -325,7 +325,8 @@ void launch_dense_apply(const double* inv, int n, const double* r, double* z, cu
 std::string device_band_cholesky(double* band, int n, int bw, cudaStream_t s, double* W = nullptr);
 // ILU(<=1) numeric phase on the device (precond.cu; the IluNumericFn of precond_host.h)
 struct ScalarCsr;
-bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows);
+bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows,
+                        cudaStream_t stream);
 void launch_band_inverse(const double* l, int n, int bw, double* W, cudaStream_t s);
 // comp < 0: all three components with one W; comp = k: component k only
 void launch_dense_apply_perm(const double* W, int n, const int* perm, const double* r, double* z, int comp,

@@ -18,6 +18,9 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "device.h"
 #include "face_math.cuh"
@@ -25,6 +28,8 @@
 
 namespace sfv {
 namespace {
+
+namespace cg = cooperative_groups;
 
 using namespace fm;
 
@@ -175,7 +180,6 @@ __global__ void __launch_bounds__(256) perturb_kernel(int nc, const double* __re
 // block partials, meets at a grid barrier, and every block finishes ε from the partials in
 // the same order (so all hold the same bits) and forms w.  u and v are read from HBM once;
 // the second read hits L2 (48 MB at 1M cells).  Replaces launch_norm_partials + perturb.
-// bar: monotonically increasing arrival counter, 64-bit (never wraps), same grid every call.
 // The reduction is the one of launch_norm_partials + perturb_kernel operation for operation
 // (same grid, per-thread strides, block trees and final partial sum), so ε — and with it
 // every Krylov and Newton decision — is bitwise what the two-launch path computes.
@@ -184,8 +188,7 @@ template <bool VEC>  // VEC: u and v 16-byte aligned (double2 loads)
 __global__ void __launch_bounds__(kEpT, 4) eps_perturb_kernel(int nc, const double* __restrict__ u,
                                                           const double* __restrict__ v, double* __restrict__ eps_p,
                                                           double* __restrict__ wg, double* __restrict__ part,
-                                                          double* __restrict__ u_norm, bool cached,
-                                                          unsigned long long* __restrict__ bar) {
+                                                          double* __restrict__ u_norm, bool cached) {
     __shared__ double sh[2 * (kEpT / 32) + 2];
     release_early();
     wait_predecessor();  // u, v, and the previous pass that read w
@@ -259,17 +262,10 @@ __global__ void __launch_bounds__(kEpT, 4) eps_perturb_kernel(int nc, const doub
     if (threadIdx.x == 0) {
         __stcg(&part[2 * blockIdx.x], au);
         __stcg(&part[2 * blockIdx.x + 1], av);
-        // grid barrier (all CTAs are resident: the grid is sized to the occupancy)
-        __threadfence();
-        const unsigned long long old = atomicAdd(bar, 1ull);
-        const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
-        unsigned long long seen;
-        do {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(bar) : "memory");
-        } while (seen < target);
-        __threadfence();
     }
-    __syncthreads();
+    // grid barrier: the launch is cooperative (launch_eps_perturb), so every CTA is resident
+    // or the launch is refused; the barrier state is the runtime's, per launch
+    cg::this_grid().sync();
     // perturb_kernel's final sum ran on 256-thread blocks: threads >= 256 contribute +0.0
     // after the 8 warp sums, which leaves every value unchanged
     const double eps = eps_from_partials(part, gridDim.x, u_norm, cached, sh, 256);
@@ -707,6 +703,34 @@ void launch_win(void (*kern)(KArgs...), int grid, int block, cudaStream_t st, co
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// The fused ε + perturb pass: a cooperative launch (co-residency guaranteed, or the launch is
+// refused) chained to its predecessor by PDL.  Returns false — with the launch error cleared —
+// when the runtime refuses it; the caller then runs the two-launch path.
+template <typename... KArgs, typename... Args>
+bool launch_eps_perturb(void (*kern)(KArgs...), int grid, cudaStream_t st, Args... args) {
+    static int mode = [] {
+        const char* e = std::getenv("SFV_EPS_COOP");  // 0: never fused, 1: cooperative without PDL
+        return e ? std::atoi(e) : 2;
+    }();
+    while (mode > 0) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kEpT);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = mode == 2 ? 2 : 1;
+        if (cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...) == cudaSuccess) return true;
+        cudaGetLastError();
+        --mode;  // PDL + cooperative refused: cooperative alone; then never
+    }
+    return false;
+}
+
 template <int S>
 void launch_grad(const DevMesh& m, const Physics& ph, const PatchTable& pt, const PairScratch& ps, ErrWords* err,
                  cudaStream_t st) {
@@ -725,16 +749,21 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     double* wg = ps.wg;
     const int cb = (m.nc + 255) / 256;
     const int epg = PERT && ps.partials && ps.bar ? eps_perturb_grid(m.nc) : 0;
+    bool fused = false;
     if (epg > 0) {  // ε reduction and w in one launch
         const bool vec = ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
-        launch_win(vec ? eps_perturb_kernel<true> : eps_perturb_kernel<false>, epg, kEpT, st, ps,
-                   m.nc, u, v, const_cast<double*>(eps), wg, const_cast<double*>(ps.partials), ps.u_norm,
-                   ps.u_norm_cached, ps.bar);
-    } else {
+        fused = launch_eps_perturb(vec ? eps_perturb_kernel<true> : eps_perturb_kernel<false>, epg, st, m.nc, u, v,
+                                   const_cast<double*>(eps), wg, const_cast<double*>(ps.partials), ps.u_norm,
+                                   ps.u_norm_cached);
+    }
+    if (!fused) {
+        int np = ps.npart;
+        if (PERT && ps.partials && ps.bar)  // the fused launch was refused: the two-launch path
+            np = launch_norm_partials(u, v, 3 * m.nc, const_cast<double*>(ps.partials), ps.u_norm_cached, st);
         // with the ε reduction folded in, a grid of a few waves keeps the per-block partial sums cheap
         const int pgrid = ps.partials ? std::min(cb, 148 * 8) : cb;
         launch_win(perturb_kernel<PERT>, pgrid, 256, st, ps, m.nc, u, v, const_cast<double*>(eps), wg, ps.partials,
-                   ps.npart, ps.u_norm, ps.u_norm_cached);
+                   np, ps.u_norm, ps.u_norm_cached);
     }
     if (ps.marks) cudaEventRecord(ps.marks[0], st);
     const int nbf = m.nf - m.nint;

@@ -300,8 +300,11 @@ bool launch_arnoldi_fused(const double* w, const double* V, int n, int j, double
     const int grid = arnoldi_fused_grid(n, &chunk);
     if (!grid) return false;
     void* args[] = {&w, &V, &n, &j, &chunk, &h, &partial, &vnext};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_kernel), dim3(grid), dim3(kAT), args,
-                                       static_cast<size_t>(chunk) * 8, s) == cudaSuccess;
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_kernel), dim3(grid), dim3(kAT), args,
+                                    static_cast<size_t>(chunk) * 8, s) == cudaSuccess)
+        return true;
+    cudaGetLastError();  // a refused cooperative launch is not sticky: clear it so the unfused MGS runs
+    return false;
 }
 
 void launch_scale_div(const double* in, const double* divisor, double* out, int n, cudaStream_t s) {

@@ -777,7 +777,8 @@ T* dev_copy(const T* h, size_t n) {
 
 }  // namespace
 
-bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows) {
+bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows,
+                        cudaStream_t stream) {
     StageClock sc;
     const int n = out.n;
     const size_t nnz = static_cast<size_t>(out.rp[n]);
@@ -792,6 +793,7 @@ bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std:
     bool ok = false;
     if (alloc) {
         cudaMemset(d_flags, 0, sizeof(int) * (n + 1));
+        int* d_broke = d_flags + n;
         cudaDeviceSynchronize();
         sc.mark("ilu device upload");
         int dev = 0, sms = 0, per = 0;
@@ -799,11 +801,15 @@ bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std:
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ilu_numeric_kernel, 256, 0);
         const int grid = std::max(1, std::min(sms * std::max(per, 1), (n + 7) / 8));
-        ilu_numeric_kernel<<<grid, 256>>>(n, d_rows, d_rp, d_col, d_diag, d_val, d_flags, d_flags + n);
-        cudaDeviceSynchronize();
+        // warps spin on rows owned by other blocks: the grid must be co-resident, which only a
+        // cooperative launch guarantees (a refused launch falls back to the host factor)
+        void* args[] = {const_cast<int*>(&n), &d_rows, &d_rp, &d_col, &d_diag, &d_val, &d_flags, &d_broke};
+        const bool launched = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(ilu_numeric_kernel), dim3(grid),
+                                                          dim3(256), args, 0, stream) == cudaSuccess;
+        cudaStreamSynchronize(stream);
         sc.mark("ilu device kernel");
         int broke = 1;
-        if (cudaMemcpy(&broke, d_flags + n, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess &&
+        if (launched && cudaMemcpy(&broke, d_flags + n, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess &&
             cudaMemcpy(out.val.data(), d_val, sizeof(double) * nnz, cudaMemcpyDeviceToHost) == cudaSuccess)
             ok = broke == 0;
         sc.mark("ilu device download");

@@ -130,7 +130,7 @@ struct SpinBarrier {
 // (levels of the final lower pattern) with each row's operations in the sequential order:
 // the factor is bit-identical.  Returns false on a breakdown (the caller reruns the
 // sequential code for the reference's exact message).
-bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nthreads, IluNumericFn numeric) {
+bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nthreads, const IluNumericFn& numeric) {
     StageClock sc;
     const int n = a.n;
     // symbolic phase: each thread builds a contiguous block of rows into one flat buffer
@@ -268,7 +268,7 @@ bool iluk_factor_parallel(const ScalarCsr& a, int level, ScalarCsr& out, int nth
 
 }  // namespace
 
-std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& out, IluNumericFn numeric) {
+std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& out, const IluNumericFn& numeric) {
     const int n = a.n;
     const int nthreads = host_threads();
     if (level <= 1 && n >= 65536 && (nthreads > 1 || numeric) && !std::getenv("SFV_ILU_SERIAL") &&

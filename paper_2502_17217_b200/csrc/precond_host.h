@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <new>
 #include <string>
@@ -55,8 +56,8 @@ std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar,
 // final pattern with A at its positions (fill entries 0), diag the diagonal positions and
 // rows the rows in dependency-level order; factors out.val in place with the reference's
 // per-entry operations, false on a breakdown (the caller reruns the sequential code).
-using IluNumericFn = bool (*)(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows);
-std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& lu, IluNumericFn numeric = nullptr);
+using IluNumericFn = std::function<bool(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows)>;
+std::string iluk_factor(const ScalarCsr& a, int level, ScalarCsr& lu, const IluNumericFn& numeric = nullptr);
 
 
 

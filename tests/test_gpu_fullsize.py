@@ -93,3 +93,70 @@ def test_c5_full_size_linearity():
     rm = ev.residual(-u).cpu().numpy()
     scale = np.max(np.abs(rp - r0))
     assert np.max(np.abs((rp - r0) + (rm - r0))) <= 1e-9 * scale
+
+
+# ---------------------------------------------------------------- full-size run_steps parity
+# Fixtures from the REFERENCE itself at the BASELINE sizes (tests/golden/make_fullsize.py:
+# run_steps, nonlinear.cpp:382-446, automatic preconditioner: LU at C1, ILU(1) at C2-C4).
+# Bars (BASELINE north_star / SURVEY.md 8d): equal per-step status and Newton count,
+# per-Newton GMRES counts within +-1, converged field within 1e-8 relative.
+import os  # noqa: E402
+
+FULL = os.path.join(os.path.dirname(__file__), "golden")
+U_TOL = 1e-8
+
+
+def _full_fixture(name):
+    p = os.path.join(FULL, f"full_{name}.npz")
+    if not os.path.exists(p):
+        pytest.skip(f"{p} not generated yet (tests/golden/make_fullsize.py {name})")
+    return np.load(p)
+
+
+def _block_aggregates(x, nb):
+    c = x.reshape(-1, 3)
+    edges = np.linspace(0, c.shape[0], nb + 1).astype(np.int64)
+    return np.add.reduceat(c, edges[:-1], axis=0), np.add.reduceat(c * c, edges[:-1], axis=0), np.diff(edges)
+
+
+def _check_field(fx, prefix, x):
+    """Sampled cells element-wise, every cell through per-block sums / sums of squares."""
+    c = x.reshape(-1, 3)
+    ref_s = fx[f"{prefix}_sample"]
+    scale = float(fx[f"{prefix}_max"])
+    err = np.max(np.abs(c[fx["sample_idx"]] - ref_s)) / scale
+    assert err <= U_TOL, f"{prefix}: sampled cells differ by {err:.3e} of max|{prefix}|"
+    s, q, cnt = _block_aggregates(x, fx[f"{prefix}_block_sum"].shape[0])
+    rs, rq = fx[f"{prefix}_block_sum"], fx[f"{prefix}_block_sq"]
+    # |sum d| <= sqrt(n sum d^2): relative to the block's own magnitude
+    bound = U_TOL * np.sqrt(np.maximum(rq, 1e-300) * cnt[:, None])
+    assert np.all(np.abs(s - rs) <= bound + 1e-300), f"{prefix}: block sums differ"
+    assert np.all(np.abs(q - rq) <= 2 * U_TOL * rq + 1e-300), f"{prefix}: block sums of squares differ"
+    assert abs(np.linalg.norm(x) - float(fx[f"{prefix}_norm"])) <= U_TOL * float(fx[f"{prefix}_norm"])
+    return err
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_full_size_run_steps_matches_reference(name):
+    fx = _full_fixture(name)
+    from paper_2502_17217_b200 import solver as sv
+    case = cases.config(name)
+    mesh = case.mesh()
+    assert mesh.n_cells == int(fx["n_cells"])
+    ev = sv.ResidualEvaluator(mesh, case.physics)
+    f0 = case.initial_field(mesh)
+    f, reps, wall = sv.run_steps_host(ev, f0, case.solver(), case.n_steps)
+    status = np.array([r.status for r in reps])
+    newton = np.array([r.outer_iters for r in reps])
+    assert len(reps) == len(fx["newton"]), (len(reps), fx["newton"])
+    assert np.array_equal(status, fx["status"]), (status, fx["status"])
+    assert np.array_equal(newton, fx["newton"]), (newton, fx["newton"])
+    for i, r in enumerate(reps):
+        k = np.array(r.summary()["krylov_per_newton"])
+        kr = fx["krylov"][i][fx["krylov"][i] >= 0]
+        assert len(k) == len(kr) and np.all(np.abs(k - kr) <= 1), (i, k, kr)
+    err = _check_field(fx, "u", f[0])
+    if "v_old_sample" in fx.files:
+        _check_field(fx, "v_old", f[3])
+    print(f"{name}: newton {newton.tolist()}, u rel err {err:.2e}, solve {wall:.2f} s "
+          f"(reference {float(fx['ref_wall_seconds']):.1f} s on {fx['cpu_model']})")
