@@ -110,31 +110,76 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_reference_jv(case, mesh, u, r_u, v, seconds_budget=20.0, threads=None):
-    """The reference's own jacobian_vector_product (oracle/_ref) on host threads; falls
-    back to the C restatement when the reference build is absent."""
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_jv(case, mesh, u, r_u, v, n_jv: int, warm: int = 1):
+    """The reference's own jacobian_vector_product (oracle/_ref: /root/reference/proj/src
+    compiled by oracle/Makefile) on the host cores.  The reference is single-threaded
+    (SPEC.md:390), so n_jv independent J.v calls on the same const evaluator run spread over
+    all host threads (at most 32), each thread at least one.  ONE definition for both the
+    reference arm and the GPU arm's cpu_baseline: value = J.v completed / wall seconds of the
+    timed region, ms_per_step = wall ms / J.v completed (so steps * ms_per_step = the timed
+    region).  Falls back to the C restatement (1 thread) when the reference build is absent."""
     from oracle.bind import OracleCase, RefCase, ref_available
-    threads = threads or min(os.cpu_count() or 1, 32)
     if ref_available():
+        threads = min(os.cpu_count() or 1, 32)
         rc = RefCase(mesh, case.physics)
         rc.set_time(1.0)
-        t1 = rc.time_jv(u, r_u, v, 1, 1)  # one J.v on one core, to size the sample
-        reps = max(1, int(seconds_budget / max(t1, 1e-6) / 2))
-        reps = min(reps, 8)
-        secs = rc.time_jv(u, r_u, v, reps, threads)
-        total = reps * threads
-        return {"value": total / secs, "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": f"{total} J.v ({threads} threads x {reps}) of the reference's jacobian_vector_product "
-                          f"on the full {mesh.n_cells}-cell mesh; single-core J.v {t1:.3f} s",
-                "single_core_jv_s": t1}
-    oc = OracleCase(mesh, case.physics)
-    oc.set_time(1.0)
-    t1 = oc.time_jv(u, r_u, v, 1)
-    reps = max(1, min(8, int(seconds_budget / max(t1, 1e-6))))
-    secs = oc.time_jv(u, r_u, v, reps)
-    return {"value": reps / secs, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{reps} J.v of the C restatement (oracle/sfv_oracle.c) on the full mesh, 1 core",
-            "single_core_jv_s": t1}
+        per_thread = max(1, -(-n_jv // threads))
+        rc.time_jv(u, r_u, v, max(1, warm), threads)
+        secs = rc.time_jv(u, r_u, v, per_thread, threads)
+        done = per_thread * threads
+        kind, what = "reference", "the reference's jacobian_vector_product (oracle/_ref)"
+    else:
+        threads = 1
+        oc = OracleCase(mesh, case.physics)
+        oc.set_time(1.0)
+        oc.time_jv(u, r_u, v, 1)
+        done = max(1, min(n_jv, 20))
+        secs = oc.time_jv(u, r_u, v, done)
+        kind, what = "port", "the C restatement (oracle/sfv_oracle.c)"
+    return {"value": done / secs, "unit": UNIT, "cores": threads, "kind": kind, "jv_done": done,
+            "seconds": secs, "ms_per_jv": 1e3 * secs / done, "cpu_model": _cpu_model(),
+            "host_threads": os.cpu_count(),
+            "sample": f"{done} J.v of {what} on the full {mesh.n_cells}-cell mesh, {threads} host threads "
+                      f"running concurrent independent calls ({-(-done // threads)} each)"}
+
+
+def reference_jfnk_sample(case, mesh, cycles: int = 1):
+    """A bounded sample of the reference's JFNK solve at this config (nonlinear.cpp:173-266
+    with the automatic preconditioner of run_steps, nonlinear.cpp:382-446): the preconditioner
+    setup (J~ assembly + ILU(1) factor, timed alone) and the first `cycles` GMRES(30) restart
+    cycles of the first Newton step, timed through jfnk_solve.  The full solve time is
+    projected from them with the Krylov count of the full solve and, when a full reference
+    run on this kind of host was recorded (profiles/r02_ref_jfnk_<cfg>.json), quoted."""
+    from oracle.bind import RefCase, ref_available
+    from paper_2502_17217_b200.abi import solver_cfg
+    if not ref_available():
+        return None
+    ref = RefCase(mesh, case.physics)
+    ref.set_time(1.0 / case.n_steps)
+    kind = "lu" if 3 * mesh.n_cells <= 30000 else "ilu1"  # make_preconditioner's automatic rule
+    t0 = time.perf_counter()
+    ref.precond_create({"lu": 5, "ilu1": 3}[kind])
+    setup = time.perf_counter() - t0
+    kr = 30 * cycles
+    cfg = solver_cfg(r_tol=case.r_tol, max_outer=1, max_krylov=kr, preconditioner=kind)
+    u0 = case.initial_field(mesh)[0]
+    t0 = time.perf_counter()
+    _, rep = ref.jfnk_solve(u0, cfg)
+    t_it = time.perf_counter() - t0
+    iters = max(1, int(rep.krylov_iters))
+    # jfnk_solve's other work in the sample: R(u0) and one line-search residual (~2 J.v)
+    return {"precond": kind, "precond_setup_s": setup, "sample_krylov": iters, "sample_s": t_it,
+            "per_krylov_s": t_it / iters, "cores": 1, "cpu_model": _cpu_model()}
 
 
 def run_reference(args):
@@ -150,38 +195,42 @@ def run_reference(args):
     else:
         mesh = case.mesh()
     u, v = cases.jv_inputs(mesh, extent=case.mesh_args.get("extents"))
-    Cls = RefCase if ref_available() else OracleCase
-    ref = Cls(mesh, case.physics)
+    ref = (RefCase if ref_available() else OracleCase)(mesh, case.physics)
     ref.set_time(1.0)
     r_u = ref.residual(u)
-    # the reference is single-threaded; the K steps are spread over all host
-    # threads as concurrent independent J.v calls on the same (const) evaluator — every
-    # thread runs at least one, so a small K still uses all the cores
-    threads = min(os.cpu_count() or 1, 32) if ref_available() else 1
-    per_thread = max(1, -(-args.steps // threads))
-    warm = max(1, -(-args.warmup // threads))
-    if ref_available():
-        ref.time_jv(u, r_u, v, warm, threads)
-        total_t = ref.time_jv(u, r_u, v, per_thread, threads)
-    else:
-        ref.time_jv(u, r_u, v, 1)
-        total_t = ref.time_jv(u, r_u, v, min(args.steps, 20))
-        per_thread = min(args.steps, 20)
-    n_jv = per_thread * threads
-    per_step = threads
-    step_times = [total_t / n_jv] * n_jv
-    value = n_jv / total_t
+    del ref
+    jv = reference_jv(case, mesh, u, r_u, v, args.steps, args.warmup)
+    n_jv = jv["jv_done"]
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total_t * threads / n_jv, "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": jv["value"], "unit": UNIT, "n_gpus": ws, "steps": n_jv,
+        "warmup": args.warmup, "ms_per_step": jv["ms_per_jv"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {case.notes}", "cells": mesh.n_cells, "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": per_step,
-                         "kind": "reference" if ref_available() else "port",
-                         "sample": f"{n_jv} J.v of the full {mesh.n_cells}-cell mesh, {threads} host threads x {per_thread} concurrent reference jacobian_vector_product calls"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {k: jv[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "host_threads")},
+        "e2e": {"value": jv["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "steps_requested": args.steps,
     }
+    if not args.no_jfnk:
+        line["jfnk"] = reference_jfnk_summary(args.config, case, mesh)
     print(json.dumps(line), flush=True)
+
+
+def reference_jfnk_summary(cfg_name, case, mesh):
+    try:
+        s = reference_jfnk_sample(case, mesh)
+    except Exception as exc:  # reported, never required
+        return {"error": str(exc)}
+    if s is None:
+        return {"unavailable": "reference build absent"}
+    prof = os.path.join(ROOT, "profiles", f"r02_ref_jfnk_{cfg_name}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            full = json.load(f)
+        s["recorded_full_solve"] = full
+        kr = full.get("krylov_total")
+        if kr:
+            s["projected_solve_seconds"] = s["precond_setup_s"] + kr * s["per_krylov_s"]
+    return s
 
 
 def run_ours(args):
@@ -320,8 +369,10 @@ def run_ours(args):
                         "final_rel_residual": [x["final_residual"] / x["initial_residual"] for x in s],
                         "path": "sfv_run_steps_host (host buffers; includes preconditioner setup)"}
     if rank == 0 and not args.no_cpu and ws == 1:
-        try:
-            line["cpu_baseline"] = cpu_reference_jv(case, mesh, u_h, r_u.cpu().numpy(), v_h)
+        try:  # the same measurement as the reference arm (reference_jv)
+            jv = reference_jv(case, mesh, u_h, r_u.cpu().numpy(), v_h, args.cpu_jv, 1)
+            line["cpu_baseline"] = {k: jv[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                                         "host_threads")}
         except Exception as exc:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(exc)}
     if rank == 0:
@@ -340,6 +391,7 @@ def main():
     ap.add_argument("--no-jfnk", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--jfnk-steps", type=int, default=1)
+    ap.add_argument("--cpu-jv", type=int, default=32, help="J.v in the GPU arm's cpu_baseline sample")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
