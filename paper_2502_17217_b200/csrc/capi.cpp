@@ -1368,6 +1368,10 @@ int precond_create(sfv_ctx* c, int kind) {
         if (c->tri_cluster != kPipeMode && (c->L[a].view.maxd > 32 || c->U[a].view.maxd > 32)) c->tri_cluster = 0;
     c->pc_kind = kind;
     pt.mark("rest");
+    if (std::getenv("SFV_TIMING"))
+        std::fprintf(stderr, "[sfv] ilu sweep mode %d (stream: ring %d rows %d stages %d; levels L %d U %d)\n",
+                     c->tri_cluster, c->sL.ring, c->sL.max_rows, c->sL.stages, c->sL.t[0].n_levels,
+                     c->sU.t[0].n_levels);
     return c->cuda_check("ilu setup");
 }
 
