@@ -62,6 +62,12 @@ void sfv_destroy(sfv_ctx* ctx);
 int sfv_set_stream(sfv_ctx* ctx, void* cuda_stream);
 int sfv_n_cells(const sfv_ctx* ctx);
 const char* sfv_last_error(const sfv_ctx* ctx);
+/* Execution switches (no effect on the arithmetic of any result):
+ *   "gmres_graph" 1 (default) / 0: run each GMRES restart cycle as one CUDA graph whose
+ *   WHILE node holds the Arnoldi steps (J.v, preconditioner, MGS, Givens) on the device,
+ *   or drive the steps from the host.  Both give bit-identical iterates.
+ * Returns SFV_ERR_INVALID_ARGUMENT for an unknown name. */
+int sfv_set_option(sfv_ctx* ctx, const char* name, int value);
 /* number of device kernels this context has launched so far */
 long long sfv_launch_count(const sfv_ctx* ctx);
 /* bytes of device memory held by the context */

@@ -171,12 +171,40 @@ struct sfv_ctx {
     // krylov workspace
     DevBuf<double> V, wv, rv, tv, xv, bv, hdev, ydev, ucand, rcand, uscratch, rscratch, dzero;
     int v_cap = 0;
+    // device-resident GMRES cycle (gmres_graph): one CUDA graph whose WHILE node runs the
+    // Arnoldi steps of a restart cycle (J.v, preconditioner, MGS, Givens) without the host
+    DevBuf<unsigned char> gstate;
+    unsigned char* gstate_host = nullptr;  // pinned mirror
+    GmresDev gdev{};
+    int g_cap = 0;  // restart the state is sized for
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t gev0 = nullptr, gev1 = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<unsigned char> g_key;  // everything the graph captured by value (gmres_graph_key)
+    long long pc_gen = 0;              // bumped by every preconditioner (re)build
+    long long g_launches = 0;  // kernels per Arnoldi step in the graph
+    bool graph_broken = false;
+    bool graph_off = false;  // sfv_set_option("gmres_graph", 0)
+    bool vsel_failed = false;
     long long launches = 0;
     SfvError last{0, -1, ""};
     // host-buffer J.v: r_u uploaded on a copy stream while the ε and gradient passes run
     cudaStream_t copy = nullptr;
     cudaEvent_t ev_uv = nullptr, ev_ru = nullptr;
+    void drop_graph() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+        gexec = nullptr;
+        graph = nullptr;
+        g_key.clear();
+    }
     ~sfv_ctx() {
+        drop_graph();
+        if (gstate_host) cudaFreeHost(gstate_host);
+        if (gev0) cudaEventDestroy(gev0);
+        if (gev1) cudaEventDestroy(gev1);
+        if (gstream) cudaStreamDestroy(gstream);
         free_device_geometry(dgeo);
         if (ps.ev_w) cudaEventDestroy(ps.ev_w);
         if (ps.ev_b) cudaEventDestroy(ps.ev_b);
@@ -617,6 +645,145 @@ bool ensure_krylov(sfv_ctx* c, int restart) {
 
 enum { G_CONVERGED = 0, G_MAX_ITERS = 1, G_STAGNATED = 2 };
 
+size_t gstate_bytes(int m) {
+    return sizeof(GmresHdr) + sizeof(double) * (2 * static_cast<size_t>(m) + (m + 1) + static_cast<size_t>(m) * (m + 1));
+}
+GmresDev gstate_view(unsigned char* base, int m) {
+    GmresDev d;
+    d.hdr = reinterpret_cast<GmresHdr*>(base);
+    d.cs = reinterpret_cast<double*>(base + sizeof(GmresHdr));
+    d.sn = d.cs + m;
+    d.g = d.sn + m;
+    d.H = d.g + (m + 1);
+    return d;
+}
+
+// The cycle graph for op = J.v at (u, r_u): a WHILE node whose body is one Arnoldi step —
+// J.v of V[j] (the fused ε pass selects v on the device), the preconditioner, the fused MGS
+// step (j on the device) and givens_kernel, which sets the condition.  Built once per
+// (u, r_u, restart) and reused for every cycle; false when any piece cannot be captured
+// (then gmres keeps the host-driven loop).  SFV_GMRES_GRAPH=0 disables it.
+// Kernel arguments are captured by value: the patch values (set_time), the physics, the
+// history pointers, the preconditioner's buffers and every workspace pointer.  The graph is
+// reused only while all of them are unchanged.
+std::vector<unsigned char> gmres_graph_key(const sfv_ctx* c, const double* u, const double* r_u, int restart) {
+    std::vector<unsigned char> k;
+    auto put = [&](const void* p, size_t nb) {
+        const unsigned char* b = static_cast<const unsigned char*>(p);
+        k.insert(k.end(), b, b + nb);
+    };
+    const void* ptrs[] = {u, r_u, c->V.p, c->tv.p, c->wv.p, c->hdev.p, c->red.p, c->scal.p, c->err.p, c->pwg.p,
+                          c->gstate.p, c->stream};
+    put(ptrs, sizeof(ptrs));
+    put(&restart, sizeof(restart));
+    put(&c->pc_gen, sizeof(c->pc_gen));
+    put(&c->ph, sizeof(c->ph));
+    put(&c->pt, sizeof(c->pt));
+    put(&c->hist, sizeof(c->hist));
+    put(&c->dm, sizeof(c->dm));
+    return k;
+}
+
+bool gmres_graph_ready(sfv_ctx* c, const double* u, const double* r_u, int restart) {
+    static const bool off = [] {
+        const char* e = std::getenv("SFV_GMRES_GRAPH");
+        return e && std::atoi(e) == 0;
+    }();
+    if (off || c->graph_off || c->graph_broken || c->use_fused || c->jv_path != 0 || !c->ps.bar) return false;
+    int chunk = 0;
+    if (eps_perturb_grid_for(c->nc) == 0 || arnoldi_fused_grid(c->n, &chunk) == 0) return false;
+    if (c->gexec && c->g_key == gmres_graph_key(c, u, r_u, restart)) return true;
+    c->drop_graph();
+    auto broken = [&](const char* why) {
+        if (std::getenv("SFV_TIMING")) std::fprintf(stderr, "[sfv] gmres graph unavailable: %s\n", why);
+        cudaGetLastError();
+        c->drop_graph();
+        c->graph_broken = true;
+        return false;
+    };
+    if (c->g_cap < restart) {
+        if (c->gstate_host) cudaFreeHost(c->gstate_host);
+        c->gstate_host = nullptr;
+        if (!c->gstate.alloc(gstate_bytes(restart)) ||
+            cudaMallocHost(&c->gstate_host, gstate_bytes(restart)) != cudaSuccess)
+            return broken("state allocation");
+        c->g_cap = restart;
+    }
+    c->gdev = gstate_view(c->gstate.p, restart);
+    if (!c->gstream && (cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+                        cudaEventCreateWithFlags(&c->gev0, cudaEventDisableTiming) != cudaSuccess ||
+                        cudaEventCreateWithFlags(&c->gev1, cudaEventDisableTiming) != cudaSuccess))
+        return broken("stream");
+    cudaGraphConditionalHandle cond;
+    if (cudaGraphCreate(&c->graph, 0) != cudaSuccess ||
+        cudaGraphConditionalHandleCreate(&cond, c->graph, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+        return broken("conditional handle");
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (cudaGraphAddNode(&node, c->graph, nullptr, 0, &np) != cudaSuccess) return broken("while node");
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    const int n = c->n;
+    cudaStream_t saved = c->stream;
+    c->stream = c->gstream;
+    const long long l0 = c->launches;
+    c->vsel_failed = false;
+    bool ok = cudaStreamBeginCaptureToGraph(c->gstream, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+        c->ps.vsel_j = &c->gdev.hdr->j;
+        c->ps.vsel_stride = static_cast<size_t>(n);
+        c->ps.vsel_failed = &c->vsel_failed;
+        c->ps.partials = c->red.p;
+        c->ps.u_norm = c->scal.p + 1;
+        c->ps.u_norm_cached = true;
+        residual_pass(c, c->ph, u, c->V.p, c->scal.p, r_u, c->tv.p);
+        c->ps.partials = nullptr;
+        c->ps.vsel_j = nullptr;
+        c->ps.vsel_failed = nullptr;
+        if (std::getenv("SFV_GRAPH_NOPC"))  // debugging aid: identity preconditioner inside the graph
+            cudaMemcpyAsync(c->wv.p, c->tv.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->gstream);
+        else
+            ok = precond_apply_async(c, c->tv.p, c->wv.p) == SFV_OK;
+        ok = launch_arnoldi_fused_dev(c->wv.p, c->V.p, n, &c->gdev.hdr->j, c->v_cap, c->hdev.p, c->red.p,
+                                      c->gstream) && ok;
+        launch_givens(c->gdev, c->hdev.p, c->err.p, cond, c->gstream);
+        c->launches += 2;
+        cudaGraph_t out = nullptr;
+        ok = cudaStreamEndCapture(c->gstream, &out) == cudaSuccess && ok && !c->vsel_failed;
+    }
+    c->stream = saved;
+    c->g_launches = c->launches - l0;
+    c->launches = l0;
+    if (!ok) return broken("capture");
+    if (cudaGraphInstantiate(&c->gexec, c->graph, 0) != cudaSuccess) return broken("instantiate");
+    c->g_key = gmres_graph_key(c, u, r_u, restart);
+    return true;
+}
+
+// One restart cycle through the graph: state upload (j = 0, total, g[0] = beta, target),
+// the graph, and one fetch of the state and the error words.
+int gmres_graph_cycle(sfv_ctx* c, int total, int restart, int max_iters, double beta, double target) {
+    GmresDev hv = gstate_view(c->gstate_host, restart);
+    *hv.hdr = GmresHdr{0, total, restart, max_iters, 0, 0, target};
+    hv.g[0] = beta;
+    cudaMemcpyAsync(c->gstate.p, c->gstate_host, sizeof(GmresHdr), cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(c->gdev.g, hv.g, sizeof(double), cudaMemcpyHostToDevice, c->stream);
+    reset_err(c);
+    cudaEventRecord(c->gev0, c->stream);
+    cudaStreamWaitEvent(c->gstream, c->gev0, 0);
+    if (cudaGraphLaunch(c->gexec, c->gstream) != cudaSuccess) return c->cuda_check("gmres graph");
+    cudaEventRecord(c->gev1, c->gstream);
+    cudaStreamWaitEvent(c->stream, c->gev1, 0);
+    cudaMemcpyAsync(c->gstate_host, c->gstate.p, gstate_bytes(restart), cudaMemcpyDeviceToHost, c->stream);
+    if (int e = fetch(c, 0)) return e;
+    c->launches += c->g_launches * (hv.hdr->total - total);
+    return SFV_OK;
+}
+
 // gmres_solve, left preconditioned (/root/reference/proj/src/linalg.cpp:423-538), with
 // op = J.v at (u, r_u).  x_zero: x0 is all zeros, so op(x0) = 0 without evaluation
 // (jacobian_vector_product short-circuits |v| = 0, nonlinear.cpp:110).
@@ -699,6 +866,7 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
         const char* e = std::getenv("SFV_FUSED_MGS");
         return e && std::atoi(e) == 0;
     }();
+    const bool use_graph = gmres_graph_ready(c, u, r_u, restart);
     while (total < max_iters) {
         const double cycle_start = beta;
         launch_scale_div_host(r, beta, V, n, c->stream);  // v0 = r / beta
@@ -709,7 +877,19 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
         g.assign(1, beta);
         int j = 0;
         bool happy = false;
-        while (j < restart && total < max_iters) {
+        if (use_graph) {
+            if (!unorm_cached) op(V, tmp);  // |u| for this u, as the first in-loop J.v would compute it
+            if (int e = gmres_graph_cycle(c, total, restart, max_iters, beta, target)) return e;
+            if (int e = decode_residual_errors(c, true)) return e;
+            const GmresDev hv = gstate_view(c->gstate_host, restart);
+            j = hv.hdr->j;
+            total = hv.hdr->total;
+            happy = hv.hdr->happy != 0;
+            g.assign(hv.g, hv.g + j + 1);
+            for (int k = 0; k < j; ++k) H.emplace_back(hv.H + static_cast<size_t>(k) * (restart + 1),
+                                                     hv.H + static_cast<size_t>(k) * (restart + 1) + k + 2);
+        }
+        while (!use_graph && j < restart && total < max_iters) {
             double* vj = V + static_cast<size_t>(j) * n;
             if (tim.on) cudaEventRecord(tim.ev[0], c->stream);
             op(vj, tmp);
@@ -749,7 +929,7 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
                 hj[i + 1] = -sn[i] * hj[i] + cs[i] * hj[i + 1];
                 hj[i] = t;
             }
-            const double denom = std::hypot(hj[j], hj[j + 1]);
+            const double denom = sfv_hypot(hj[j], hj[j + 1]);
             const double cc = denom == 0.0 ? 1.0 : hj[j] / denom;
             const double ss = denom == 0.0 ? 0.0 : hj[j + 1] / denom;
             cs.push_back(cc);
@@ -1116,6 +1296,8 @@ struct PhaseTimer {
 };
 
 int precond_create(sfv_ctx* c, int kind) {
+    ++c->pc_gen;  // a cached GMRES graph holds the old preconditioner's buffers
+    c->drop_graph();
     PhaseTimer pt;
     c->pc_kind = SFV_PRECOND_NONE;
     if (kind == SFV_PRECOND_AUTO) kind = 3 * c->nc <= 30000 ? SFV_PRECOND_LU : SFV_PRECOND_ILU1;  // nonlinear.cpp:355-356
@@ -1547,6 +1729,15 @@ void sfv_destroy(sfv_ctx* c) {
 int sfv_set_stream(sfv_ctx* c, void* s) {
     c->stream = static_cast<cudaStream_t>(s);
     return SFV_OK;
+}
+
+int sfv_set_option(sfv_ctx* c, const char* name, int value) {
+    if (name && std::strcmp(name, "gmres_graph") == 0) {
+        c->graph_off = value == 0;
+        c->drop_graph();
+        return SFV_OK;
+    }
+    return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, std::string("sfv_set_option: unknown option ") + (name ? name : ""));
 }
 
 int sfv_n_cells(const sfv_ctx* c) { return c->nc; }

@@ -53,6 +53,45 @@ struct DevMesh {
     const double* tf9 = nullptr;   // [(f>>5)][9][32]: Gamma xyz, Delta xyz, |Delta|/|d|, |Gamma|, w
 };
 
+// hypot as the reference's C library computes it (glibc's non-FMA x86-64 path: one sqrt, then
+// Borges' correction step — "An Improved Algorithm for hypot(a, b)", 2019), so the Givens
+// rotations of gmres_solve (linalg.cpp:481) get the reference's bits on the host loop and in
+// the device cycle alike.  Checked against the host libm on 1e6 random pairs (see
+// tests/test_known_answers.py).  Power-of-two scaling keeps the squares finite.
+__host__ __device__ inline double sfv_hypot(double x, double y) {
+    double ax = x < 0.0 ? -x : x, ay = y < 0.0 ? -y : y;
+    if (ax < ay) {
+        const double t = ax;
+        ax = ay;
+        ay = t;
+    }
+    if (!(ax <= 1.79769313486231570815e308)) return ax == ax ? ax : (ay == ay ? ax : ay);  // inf / nan
+    if (ay == 0.0) return ax;
+    double scale = 1.0;
+    if (ax > 0x1p+511) {
+        ax *= 0x1p-600;
+        ay *= 0x1p-600;
+        scale = 0x1p+600;
+    } else if (ay < 0x1p-511) {
+        ax *= 0x1p+600;
+        ay *= 0x1p+600;
+        scale = 0x1p-600;
+    }
+    double h = sqrt(ax * ax + ay * ay);
+    double t1, t2;
+    if (h <= 2.0 * ay) {
+        const double delta = h - ay;
+        t1 = ax * (2.0 * delta - ax);
+        t2 = (delta - 2.0 * (ax - ay)) * delta;
+    } else {
+        const double delta = h - ax;
+        t1 = 2.0 * delta * (ax - 2.0 * ay);
+        t2 = (4.0 * delta - ay) * ay + delta * delta;
+    }
+    h -= (t1 + t2) / (2.0 * h);
+    return h * scale;
+}
+
 constexpr int kTileShift = 5;  // 32 cells (faces) per tile of the tiled tables
 __host__ __device__ __forceinline__ size_t tiled(int c, int nq) {
     return static_cast<size_t>(c >> kTileShift) * (static_cast<size_t>(nq) << kTileShift) + (c & 31);
@@ -126,6 +165,11 @@ struct PairScratch {
     bool sym = false;  // the mesh has a symmetry patch (boundary faces then need boundary_kernel)
     double* u_norm = nullptr;
     bool u_norm_cached = false;
+    // v = v + (*vsel_j) * vsel_stride, read on the device (the fused ε pass only): the GMRES
+    // cycle graph passes the basis V and its step index
+    const int* vsel_j = nullptr;
+    size_t vsel_stride = 0;
+    bool* vsel_failed = nullptr;  // set when the fused ε pass could not run (the other passes do not select)
     // L2 persisting window over [w | G]: both are gathered by the next pass,
     // and G is rewritten in place by the next J.v, so resident lines never reach HBM
     void* win_base = nullptr;
@@ -225,6 +269,27 @@ void launch_axpy_dot(double* w, const double* vi, const double* h, const double*
 // 2 * SMs doubles.  Returns false (nothing launched) when w does not fit on chip.
 bool launch_arnoldi_fused(const double* w, const double* V, int n, int j, double* h, double* partial, double* vnext,
                           cudaStream_t s);
+// The same with the step index read on the device (*jdev) and v_{j+1} written to V[j + 1]
+// when j + 1 < vcap (device-resident GMRES cycle).
+int arnoldi_fused_grid(int n, int* chunk_out);  // 0: w does not fit on chip
+bool launch_arnoldi_fused_dev(const double* w, const double* V, int n, const int* jdev, int vcap, double* h,
+                              double* partial, cudaStream_t s);
+// device-resident GMRES(m) cycle state: header + rotations, residual estimates, Hessenberg
+// columns (column j at H + j * (m + 1))
+struct GmresHdr {
+    int j, total, restart, max_iters, happy, pad;
+    double target;
+};
+struct GmresDev {
+    GmresHdr* hdr = nullptr;
+    double* cs = nullptr;
+    double* sn = nullptr;
+    double* g = nullptr;
+    double* H = nullptr;
+};
+// one thread: the host half of an Arnoldi step (rotations, tests), then the cycle's WHILE condition
+void launch_givens(const GmresDev& st, const double* h, const ErrWords* err, cudaGraphConditionalHandle cond,
+                   cudaStream_t s);
 void launch_scale_div(const double* in, const double* divisor, double* out, int n, cudaStream_t s);
 void launch_scale_div_host(const double* in, double divisor, double* out, int n, cudaStream_t s);
 void launch_update(double* x, const double* V, const double* y, int j, int n, cudaStream_t s);

@@ -188,10 +188,12 @@ template <bool VEC>  // VEC: u and v 16-byte aligned (double2 loads)
 __global__ void __launch_bounds__(kEpT, 4) eps_perturb_kernel(int nc, const double* __restrict__ u,
                                                           const double* __restrict__ v, double* __restrict__ eps_p,
                                                           double* __restrict__ wg, double* __restrict__ part,
-                                                          double* __restrict__ u_norm, bool cached) {
+                                                          double* __restrict__ u_norm, bool cached,
+                                                          const int* __restrict__ vj, long long vstride) {
     __shared__ double sh[2 * (kEpT / 32) + 2];
     release_early();
     wait_predecessor();  // u, v, and the previous pass that read w
+    if (vj) v += static_cast<size_t>(*vj) * vstride;  // v = V[j], j on the device (GMRES cycle graph)
     const int n2 = VEC ? 3 * nc / 2 : 0;  // double2 elements of u and v (3 nc is even, or the tail below)
     const double2* u2 = reinterpret_cast<const double2*>(u);
     const double2* v2 = reinterpret_cast<const double2*>(v);
@@ -751,10 +753,15 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     const int epg = PERT && ps.partials && ps.bar ? eps_perturb_grid(m.nc) : 0;
     bool fused = false;
     if (epg > 0) {  // ε reduction and w in one launch
-        const bool vec = ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+        const bool vec = ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
+                         (!ps.vsel_j || ps.vsel_stride % 2 == 0);
         fused = launch_eps_perturb(vec ? eps_perturb_kernel<true> : eps_perturb_kernel<false>, epg, st, m.nc, u, v,
                                    const_cast<double*>(eps), wg, const_cast<double*>(ps.partials), ps.u_norm,
-                                   ps.u_norm_cached);
+                                   ps.u_norm_cached, ps.vsel_j, static_cast<long long>(ps.vsel_stride));
+    }
+    if (!fused && ps.vsel_j) {  // only the fused pass reads v through the device index
+        if (ps.vsel_failed) *ps.vsel_failed = true;
+        return;
     }
     if (!fused) {
         int np = ps.npart;

@@ -197,7 +197,14 @@ constexpr int kAK = 24;  // elements of a basis vector per thread held in regist
 
 __global__ void __launch_bounds__(kAT, 1) arnoldi_kernel(const double* __restrict__ w_in, const double* __restrict__ V,
                                                         int n, int j, int chunk, double* __restrict__ h,
-                                                        double* __restrict__ partial, double* __restrict__ vnext) {
+                                                        double* __restrict__ partial, double* __restrict__ vnext,
+                                                        const int* __restrict__ jdev, int vcap) {
+    // device-resident cycle (gmres graph): the step index is the cycle state's, and
+    // v_{j+1} goes to V[j + 1] when the basis has room for it
+    if (jdev) {
+        j = *jdev;
+        vnext = j + 1 < vcap ? const_cast<double*>(V) + static_cast<size_t>(j + 1) * n : nullptr;
+    }
     extern __shared__ double wsh[];  // [chunk]
     __shared__ double sh[kAT / 32];
     __shared__ double bcast;
@@ -257,6 +264,45 @@ __global__ void __launch_bounds__(kAT, 1) arnoldi_kernel(const double* __restric
     }
 }
 
+// ---------------------------------------------------------------- device-resident GMRES step
+// The host part of one Arnoldi step of gmres_solve (linalg.cpp:474-498) on the device, one
+// thread: the new Hessenberg column from the Arnoldi kernel's h (h[j+1] = w.w), the stored
+// Givens rotations, the new rotation, the residual estimate g, the happy-breakdown and target
+// tests, the restart / budget limits, and any error word a J.v of this step raised.  It sets
+// the WHILE condition of the cycle graph (capi.cpp: gmres_graph), so the whole restart cycle
+// runs without a host round trip.  Same expressions as the host loop in capi.cpp: gmres.
+__global__ void givens_kernel(GmresDev st, const double* __restrict__ h, const ErrWords* __restrict__ err,
+                              cudaGraphConditionalHandle cond) {
+    GmresHdr& hd = *st.hdr;
+    const int j = hd.j, m = hd.restart;
+    double* col = st.H + static_cast<size_t>(j) * (m + 1);
+    for (int i = 0; i <= j; ++i) col[i] = h[i];
+    col[j + 1] = sqrt(h[j + 1]);
+    for (int i = 0; i < j; ++i) {  // apply stored rotations
+        const double t = st.cs[i] * col[i] + st.sn[i] * col[i + 1];
+        col[i + 1] = -st.sn[i] * col[i] + st.cs[i] * col[i + 1];
+        col[i] = t;
+    }
+    const double denom = sfv_hypot(col[j], col[j + 1]);
+    const double cc = denom == 0.0 ? 1.0 : col[j] / denom;
+    const double ss = denom == 0.0 ? 0.0 : col[j + 1] / denom;
+    st.cs[j] = cc;
+    st.sn[j] = ss;
+    st.g[j + 1] = -ss * st.g[j];
+    st.g[j] = cc * st.g[j];
+    col[j] = denom;
+    const double subdiag = col[j + 1];
+    col[j + 1] = 0.0;
+    hd.total += 1;
+    hd.j = j + 1;
+    constexpr int none = 0x7f7f7f7f;
+    const bool bad = err->nan_jv != none || err->nan_cell != none || err->inverted_cell != none ||
+                     err->inverted_face != none || err->overflow_cell != none || err->retmap_cell != none;
+    hd.happy = subdiag <= 1e-14 * fmax(denom, 1e-300) ? 1 : 0;
+    const bool stop = bad || hd.happy || fabs(st.g[j + 1]) <= hd.target || j + 1 >= m || hd.total >= hd.max_iters;
+    cudaGraphSetConditional(cond, stop ? 0u : 1u);
+}
+
 int grid_for(int n) {
     const int b = (n + 255) / 256;
     return b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16;
@@ -299,12 +345,34 @@ bool launch_arnoldi_fused(const double* w, const double* V, int n, int j, double
     int chunk = 0;
     const int grid = arnoldi_fused_grid(n, &chunk);
     if (!grid) return false;
-    void* args[] = {&w, &V, &n, &j, &chunk, &h, &partial, &vnext};
+    const int* jdev = nullptr;
+    int vcap = 0;
+    void* args[] = {&w, &V, &n, &j, &chunk, &h, &partial, &vnext, &jdev, &vcap};
     if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_kernel), dim3(grid), dim3(kAT), args,
                                     static_cast<size_t>(chunk) * 8, s) == cudaSuccess)
         return true;
     cudaGetLastError();  // a refused cooperative launch is not sticky: clear it so the unfused MGS runs
     return false;
+}
+
+bool launch_arnoldi_fused_dev(const double* w, const double* V, int n, const int* jdev, int vcap, double* h,
+                              double* partial, cudaStream_t s) {
+    int chunk = 0;
+    const int grid = arnoldi_fused_grid(n, &chunk);
+    if (!grid) return false;
+    int j = 0;
+    double* vnext = nullptr;
+    void* args[] = {&w, &V, &n, &j, &chunk, &h, &partial, &vnext, &jdev, &vcap};
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(arnoldi_kernel), dim3(grid), dim3(kAT), args,
+                                    static_cast<size_t>(chunk) * 8, s) == cudaSuccess)
+        return true;
+    cudaGetLastError();
+    return false;
+}
+
+void launch_givens(const GmresDev& st, const double* h, const ErrWords* err, cudaGraphConditionalHandle cond,
+                   cudaStream_t s) {
+    givens_kernel<<<1, 1, 0, s>>>(st, h, err, cond);
 }
 
 void launch_scale_div(const double* in, const double* divisor, double* out, int n, cudaStream_t s) {

@@ -66,6 +66,7 @@ def lib():
         "sfv_destroy": (None, [_vp]),
         "sfv_set_stream": (C.c_int, [_vp, _vp]),
         "sfv_n_cells": (C.c_int, [_vp]),
+        "sfv_set_option": (C.c_int, [_vp, C.c_char_p, C.c_int]),
         "sfv_last_error": (C.c_char_p, [_vp]),
         "sfv_launch_count": (C.c_longlong, [_vp]),
         "sfv_device_bytes": (C.c_size_t, [_vp]),
@@ -218,6 +219,10 @@ class ResidualEvaluator:
         return _torch().zeros(self.n, dtype=_torch().float64, device="cuda")
 
     # -- reference API
+    def set_option(self, name: str, value: int):
+        """Execution switches (sfv_set_option): "gmres_graph" 1/0."""
+        self._check(self.L.sfv_set_option(self.h, name.encode(), int(value)))
+
     def set_time(self, t: float):
         self._check(self.L.sfv_set_time(self.h, float(t)))
 

@@ -453,22 +453,58 @@ def test_alternative_jv_paths_bitwise(path, monkeypatch):
 
 def test_jv_host_buffers_bitwise():
     """sfv_jv_host (host buffers; r_u uploaded on a copy stream while the first passes run)
-    returns the device-resident J.v bit for bit, repeatedly."""
+    returns the device-resident J.v bit for bit.  Pinned buffers (the copies are truly
+    asynchronous, as in bench.py) and a different r_u on every call, so a face pass that read
+    r_u before its upload finished would see the previous call's values and fail."""
     import ctypes as C
+    import torch
     sv = _sv()
     case = cases.config("c2", n=24)
     mesh = case.mesh()
     ev = sv.ResidualEvaluator(mesh, case.physics)
     ev.set_time(1.0)
     u, v = cases.jv_inputs(mesh)
-    r_u = ev.residual(u).cpu().numpy()
-    ref = sv.jacobian_vector_product(ev, u, r_u, v).cpu().numpy()
+    r0 = ev.residual(u).cpu().numpy()
     dp = C.POINTER(C.c_double)
-    hu, hr, hv = (np.ascontiguousarray(x, dtype=np.float64) for x in (u, r_u, v))
-    for _ in range(3):
-        out = np.empty_like(hu)
+    hu = torch.from_numpy(np.ascontiguousarray(u)).pin_memory()
+    hv = torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+    hr = torch.empty(len(u), dtype=torch.float64).pin_memory()
+    ho = torch.empty(len(u), dtype=torch.float64).pin_memory()
+    for rep in range(4):
+        r_u = r0 * (1.0 + 0.25 * rep) + 1e3 * rep  # a different r_u every call
+        hr.copy_(torch.from_numpy(r_u))
+        ho.fill_(float("nan"))
+        ref = sv.jacobian_vector_product(ev, u, r_u, v).cpu().numpy()
         cell = C.c_int(-1)
-        rc = ev.L.sfv_jv_host(ev.h, hu.ctypes.data_as(dp), hr.ctypes.data_as(dp), hv.ctypes.data_as(dp),
-                              out.ctypes.data_as(dp), C.byref(cell))
+        rc = ev.L.sfv_jv_host(ev.h, C.cast(hu.data_ptr(), dp), C.cast(hr.data_ptr(), dp), C.cast(hv.data_ptr(), dp),
+                              C.cast(ho.data_ptr(), dp), C.byref(cell))
         ev._check(rc, cell.value)
-        assert np.array_equal(out, ref)
+        assert np.array_equal(ho.numpy(), ref), rep
+
+
+@pytest.mark.parametrize("cfgname,n,pc", [("c2", 12, "ilu1"), ("c1", 8, "auto"), ("c4", 8, "ilu1")])
+def test_gmres_graph_matches_host_loop(cfgname, n, pc):
+    """The device-resident GMRES cycle (one CUDA graph per restart cycle: J.v, preconditioner,
+    MGS and the Givens step on the device) reproduces the host-driven loop bit for bit: same
+    Newton and Krylov counts, same field.  The Givens step uses sfv_hypot on both sides."""
+    sv = _sv()
+    case = cases.config(cfgname, n=n)
+    mesh = case.mesh()
+    out = []
+    for graph in (1, 0):
+        ev = sv.ResidualEvaluator(mesh, case.physics)
+        ev.set_option("gmres_graph", graph)
+        f0 = case.initial_field(mesh)
+        l0 = ev.launch_count
+        f, reps, _ = sv.run_steps_host(ev, f0, case.solver(preconditioner=pc, restart=12), min(case.n_steps, 3))
+        out.append((f, [r.summary()["krylov_per_newton"] for r in reps], ev.launch_count - l0))
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
+
+
+def test_gmres_graph_option_rejects_unknown():
+    sv = _sv()
+    case = cases.config("c2", n=6)
+    ev = sv.ResidualEvaluator(case.mesh(), case.physics)
+    with pytest.raises(sv.SolidfvError):
+        ev.set_option("no_such_option", 1)

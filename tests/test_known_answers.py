@@ -193,3 +193,42 @@ def test_jfnk_small_box_converges_and_zero_load(backend):
     be0.set_time(1.0)
     _, rep0 = be0.jfnk(np.zeros(3 * mesh.n_cells), cfg)
     assert rep0.summary()["outer_iters"] == 0
+
+
+def _hypot_restated(x, y):
+    """sfv_hypot (paper_2502_17217_b200/csrc/device.h), line for line: glibc's non-FMA hypot
+    (one sqrt, then Borges' correction step), used by the host and the device Givens step."""
+    import math
+    ax, ay = abs(x), abs(y)
+    if ax < ay:
+        ax, ay = ay, ax
+    if ay == 0.0:
+        return ax
+    h = math.sqrt(ax * ax + ay * ay)
+    if h <= 2.0 * ay:
+        delta = h - ay
+        t1 = ax * (2.0 * delta - ax)
+        t2 = (delta - 2.0 * (ax - ay)) * delta
+    else:
+        delta = h - ax
+        t1 = 2.0 * delta * (ax - 2.0 * ay)
+        t2 = (4.0 * delta - ay) * ay + delta * delta
+    return h - (t1 + t2) / (2.0 * h)
+
+
+def test_hypot_matches_the_reference_libm():
+    """gmres_solve's Givens rotation calls std::hypot (linalg.cpp:481); the device cycle must
+    get the same bits, so sfv_hypot restates the C library's algorithm.  Checked against the
+    host libm on random pairs over 16 decades, including near-equal and very unequal pairs."""
+    import ctypes
+    libm = ctypes.CDLL("libm.so.6")
+    libm.hypot.restype = ctypes.c_double
+    libm.hypot.argtypes = [ctypes.c_double, ctypes.c_double]
+    rng = np.random.default_rng(5)
+    n = 100000
+    a = rng.uniform(-1, 1, n) * 10.0 ** rng.uniform(-8, 8, n)
+    b = rng.uniform(-1, 1, n) * 10.0 ** rng.uniform(-8, 8, n)
+    b[: n // 3] = a[: n // 3] * rng.uniform(0.3, 3.0, n // 3)
+    b[n // 3: n // 2] = a[n // 3: n // 2] * 10.0 ** rng.uniform(-9, -3, n // 2 - n // 3)
+    bad = sum(libm.hypot(float(x), float(y)) != _hypot_restated(float(x), float(y)) for x, y in zip(a, b))
+    assert bad == 0
