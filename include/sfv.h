@@ -87,6 +87,20 @@ int sfv_mesh_geometry(const sfv_mesh_desc* mesh, double* volume, double* centroi
                       int errlen);
 
 int sfv_set_time(sfv_ctx* ctx, double t);
+/* DiscretisationConfig::body_force (discretisation.hpp:24): f = body_force(centroid_c) for every
+ * cell (3 n_cells host doubles, interleaved; the centroids are sfv_geometry's, i.e. the
+ * reference's); R gains volume_c * f_c after the stabilisation terms (discretisation.cpp:160-161).
+ * NULL clears it. */
+int sfv_set_body_force(sfv_ctx* ctx, const double* f);
+/* Boundary values per face instead of per patch: values[3 i] is BoundaryCondition::value
+ * (face_centroid, t) of boundary face n_internal + i at the current time (ResidualEvaluator::
+ * bc_value, discretisation.cpp:82-85; 3 (n_faces - n_internal) host doubles).  NULL returns to
+ * the per-patch values of sfv_physics. */
+int sfv_set_boundary_values(sfv_ctx* ctx, const double* values);
+/* The same sampled on every sfv_set_time (and every step of sfv_run_steps): fn(user, t, values)
+ * fills the per-face values at time t.  fn NULL returns to the per-patch values. */
+typedef void (*sfv_bc_sampler)(void* user, double t, double* values);
+int sfv_set_boundary_sampler(sfv_ctx* ctx, sfv_bc_sampler fn, void* user);
 int sfv_set_history(sfv_ctx* ctx, const double* u_old_dev, const double* u_old_old_dev, const double* v_old_dev,
                     const double* v_old_old_dev);
 
@@ -128,6 +142,15 @@ int sfv_residual_host(sfv_ctx* ctx, const double* u, double* r, int* cell);
 int sfv_jv_host(sfv_ctx* ctx, const double* u, const double* r_u, const double* v, double* out, int* cell);
 
 int sfv_precond_create(sfv_ctx* ctx, int kind);
+/* assemble_approximate_jacobian (discretisation.hpp:94-99, discretisation.cpp:216-262) in block
+ * CSR on the cell graph: row_ptr[n_cells + 1], col[nnz], blocks[9 nnz] (3x3 row-major).  With
+ * col or blocks NULL only nnz is returned; otherwise the arrays are filled and nnz returned
+ * (< 0: an error code).  Blocks are diagonal (c I, or per-axis with axis-aligned symmetry). */
+int sfv_approximate_jacobian(const sfv_ctx* ctx, int* row_ptr, int* col, double* blocks);
+/* line_search (nonlinear.hpp:81-90, nonlinear.cpp:140-163): success, the accepted s and
+ * its residual norm, and (when residual_dev is not NULL) the accepted residual. */
+int sfv_line_search(sfv_ctx* ctx, const double* u_dev, const double* du_dev, double r_norm0, int* success,
+                    double* s, double* r_norm, double* residual_dev);
 int sfv_precond_apply(sfv_ctx* ctx, const double* r_dev, double* z_dev);
 /* preconditioner facts: {kind_resolved, n_levels_fwd, n_levels_bwd, nnz_L, nnz_U} */
 int sfv_precond_info(const sfv_ctx* ctx, int info[5]);
@@ -136,8 +159,12 @@ int sfv_precond_info(const sfv_ctx* ctx, int info[5]);
  * the preconditioner is not ILU. */
 int sfv_precond_sweep(const sfv_ctx* ctx);
 
+/* gmres_solve(op = J.v at u, b, x0 = x_dev, precond = the context's, restart, rel_reduction,
+ * max_iters, right_preconditioned) (linalg.cpp:423-538); status 0 converged / 1 max_iters /
+ * 2 stagnated (GmresStatus).  Any restart >= 1. */
 int sfv_gmres_jv(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const double* b_dev, double* x_dev,
-                 int restart, double rel_reduction, int max_iters, int* iters, int* status, double* rel_residual);
+                 int restart, double rel_reduction, int max_iters, int right_preconditioned, int* iters, int* status,
+                 double* rel_residual);
 int sfv_jfnk_solve(sfv_ctx* ctx, double* u_dev, const sfv_solver_cfg* cfg, sfv_solve_report* report);
 /* segregated_solve (nonlinear.hpp:101-103; nonlinear.cpp:268-351): per outer iteration, each
  * displacement component by IC(0)-preconditioned CG on A = -J~ (Jacobi when IC(0) breaks

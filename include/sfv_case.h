@@ -112,6 +112,7 @@ typedef struct sfv_solver_cfg {
     int line_search;        /* 1 */
     int algorithm;          /* SFV_ALG_JFNK (default) or SFV_ALG_SEGREGATED (Algorithm, nonlinear.hpp:17) */
     double relaxation;      /* segregated update under-relaxation in (0, 1]; 0 => 1 */
+    int right_preconditioned; /* GMRES on A M^-1 (SolverConfig::right_preconditioned, nonlinear.hpp:37) */
 } sfv_solver_cfg;
 
 enum { SFV_ALG_JFNK = 0, SFV_ALG_SEGREGATED = 1 };
@@ -137,6 +138,11 @@ typedef struct sfv_solve_report {
     sfv_iteration_record records[64];
     char detail[SFV_DETAIL_LEN];
     int cg_diag_fallback; /* segregated: an IC(0) breakdown fell back to Jacobi (SolveReport) */
+    /* SolveReport::iterations is unbounded (nonlinear.hpp:64): when the caller sets
+     * all_records, every record (n_records of them, up to all_capacity) is written there
+     * too; records[] keeps the first 64.  Both fields survive the solver's reset. */
+    sfv_iteration_record* all_records;
+    int all_capacity;
 } sfv_solve_report;
 
 #ifdef __cplusplus

@@ -56,6 +56,8 @@ def _load(path: str, prefix: str):
     else:
         lib.orc_commit.argtypes = [C.c_void_p, _dp]
         lib.orc_law_state.argtypes = [C.c_void_p, _dp]
+    getattr(lib, p + "set_body_force").argtypes = [C.c_void_p, _dp]
+    getattr(lib, p + "set_face_bc").argtypes = [C.c_void_p, _dp]
     getattr(lib, p + "jv").argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _ip]
     getattr(lib, p + "precond_create").argtypes = [C.c_void_p, C.c_int]
     getattr(lib, p + "precond_apply").argtypes = [C.c_void_p, _dp, _dp]
@@ -75,7 +77,7 @@ def _load(path: str, prefix: str):
     else:
         lib.orc_time_jv.restype = C.c_double
         lib.orc_time_jv.argtypes = [C.c_void_p, _dp, _dp, _dp, C.c_int]
-        lib.orc_gmres_jv.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, C.c_int, C.c_double, C.c_int,
+        lib.orc_gmres_jv.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, C.c_int, C.c_double, C.c_int, C.c_int,
                                      _ip, _ip, _dp]
     _libs[path] = lib
     return lib
@@ -120,6 +122,16 @@ class _CpuCase:
     def set_history(self, u_old, u_old_old, v_old, v_old_old):
         arrs = [np.ascontiguousarray(a, dtype=np.float64).reshape(-1) for a in (u_old, u_old_old, v_old, v_old_old)]
         self._f("set_history")(self.h, *[dptr(a) for a in arrs])
+
+    def set_body_force(self, f):
+        """DiscretisationConfig::body_force sampled at the cell centroids (3 nc) or None."""
+        arr = None if f is None else np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
+        self._check(self._f("set_body_force")(self.h, None if arr is None else dptr(arr)))
+
+    def set_face_bc(self, v):
+        """Per boundary face BC values at the current time (3 (nf - nint))."""
+        arr = np.ascontiguousarray(v, dtype=np.float64).reshape(-1)
+        self._check(self._f("set_face_bc")(self.h, dptr(arr)))
 
     def residual(self, u):
         u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
@@ -214,12 +226,13 @@ class OracleCase(_CpuCase):
         u, r_u, v = (np.ascontiguousarray(a, dtype=np.float64).reshape(-1) for a in (u, r_u, v))
         return self.lib.orc_time_jv(self.h, dptr(u), dptr(r_u), dptr(v), int(reps))
 
-    def gmres_jv(self, u, r_u, b, restart=30, rel_reduction=1e-3, max_iters=300):
+    def gmres_jv(self, u, r_u, b, restart=30, rel_reduction=1e-3, max_iters=300, right=False):
         u, r_u, b = (np.ascontiguousarray(a, dtype=np.float64).reshape(-1) for a in (u, r_u, b))
         x = self.vec()
         it, st, rel = C.c_int(0), C.c_int(0), C.c_double(0)
         self._check(self.lib.orc_gmres_jv(self.h, dptr(u), dptr(r_u), dptr(b), dptr(x), restart,
-                                          rel_reduction, max_iters, C.byref(it), C.byref(st), C.byref(rel)))
+                                          rel_reduction, max_iters, int(bool(right)), C.byref(it), C.byref(st),
+                                          C.byref(rel)))
         return x, it.value, st.value, rel.value
 
 

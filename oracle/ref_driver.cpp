@@ -15,6 +15,8 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <array>
+#include <map>
 #include <memory>
 #include <thread>
 #include <vector>
@@ -33,6 +35,10 @@ namespace {
 struct RefCase {
     Mesh mesh;
     MeshGeometry geom;
+    // what the evaluator was built from (rebuilt when the body force or the BC values change)
+    std::shared_ptr<MechanicalLaw> law;
+    BoundaryConditions bcs;
+    DiscretisationConfig dc;
     std::unique_ptr<ResidualEvaluator> eval;
     std::unique_ptr<Preconditioner> precond;
     std::string last_error;
@@ -146,6 +152,7 @@ SolverConfig solver_of(const sfv_solver_cfg* c) {
     s.line_search = c->line_search != 0;
     s.algorithm = c->algorithm == SFV_ALG_SEGREGATED ? Algorithm::segregated : Algorithm::jfnk;
     s.relaxation = c->relaxation > 0.0 ? c->relaxation : 1.0;
+    s.right_preconditioned = c->right_preconditioned != 0;
     return s;
 }
 
@@ -268,12 +275,57 @@ void* ref_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, int 
         dc.transient = ph->transient != 0;
         dc.dt = ph->dt;
         dc.rho = ph->rho;
+        rc->law = law;
+        rc->bcs = bcs;
+        rc->dc = dc;
         rc->eval = std::make_unique<ResidualEvaluator>(rc->mesh, rc->geom, bcs, law, dc);
     } catch (const std::exception& e) {
         if (err) std::snprintf(err, errlen, "%s", e.what());
         return nullptr;
     }
     return rc.release();
+}
+
+using PointMap = std::map<std::array<double, 3>, Vec3>;
+static std::array<double, 3> key_of(const Vec3& x) { return {x.x, x.y, x.z}; }
+
+// DiscretisationConfig::body_force (discretisation.hpp:24) as a function of position that
+// returns the given per-cell values at the cell centroids (where the residual samples it,
+// discretisation.cpp:160-161); f NULL clears it.  The evaluator is rebuilt.
+int ref_set_body_force(void* h, const double* f) {
+    RefCase* rc = static_cast<RefCase*>(h);
+    return guarded(rc, nullptr, [&] {
+        if (!f) {
+            rc->dc.body_force = nullptr;
+        } else {
+            auto map = std::make_shared<PointMap>();
+            for (int c = 0; c < rc->mesh.n_cells; ++c)
+                (*map)[key_of(rc->geom.centroid[c])] = Vec3{f[3 * c], f[3 * c + 1], f[3 * c + 2]};
+            rc->dc.body_force = [map](const Vec3& x) { return map->at(key_of(x)); };
+        }
+        const double t = rc->eval->time();
+        rc->eval = std::make_unique<ResidualEvaluator>(rc->mesh, rc->geom, rc->bcs, rc->law, rc->dc);
+        rc->eval->set_time(t);
+    });
+}
+
+// BoundaryCondition::value (fields.hpp:16-19) as a function of position returning the given
+// per-boundary-face values (3 (n_faces - n_internal)) at the face centroids, where
+// ResidualEvaluator::bc_value samples it (discretisation.cpp:82-85).  The evaluator is rebuilt.
+int ref_set_face_bc(void* h, const double* v) {
+    RefCase* rc = static_cast<RefCase*>(h);
+    return guarded(rc, nullptr, [&] {
+        auto map = std::make_shared<PointMap>();
+        for (int f = rc->mesh.n_internal; f < rc->mesh.n_faces(); ++f) {
+            const int i = f - rc->mesh.n_internal;
+            (*map)[key_of(rc->geom.face_centroid[f])] = Vec3{v[3 * i], v[3 * i + 1], v[3 * i + 2]};
+        }
+        for (BoundaryCondition& bc : rc->bcs)
+            if (bc.kind != PatchKind::symmetry) bc.value = [map](const Vec3& x, double) { return map->at(key_of(x)); };
+        const double t = rc->eval->time();
+        rc->eval = std::make_unique<ResidualEvaluator>(rc->mesh, rc->geom, rc->bcs, rc->law, rc->dc);
+        rc->eval->set_time(t);
+    });
 }
 
 void ref_destroy(void* h) { delete static_cast<RefCase*>(h); }

@@ -187,6 +187,8 @@ struct orc_case {
     int* bc_ramp;
     double time;
     v3 *u_old, *u_old_old, *v_old, *v_old_old;
+    v3* body_vol; /* volume * body_force(centroid) per cell, NULL = none */
+    v3* face_bc;  /* per boundary face value(face_centroid, t), NULL = per patch */
     /* scratch */
     m3 *grad, *sigma, *fdef;
     /* preconditioner */
@@ -476,7 +478,7 @@ void orc_destroy(orc_case* h) {
                     h->centroid, h->g_inv, h->g_singular, h->face_centroid, h->area, h->area_mag,
                     h->normal, h->d, h->d_mag, h->w, h->delta, h->delta_mag, h->reflect, h->ls,
                     h->bc_value, h->bc_ramp, h->u_old, h->u_old_old, h->v_old, h->v_old_old,
-                    h->grad, h->sigma, h->fdef, h->j2_bbar, h->j2_F, h->j2_eps};
+                    h->grad, h->sigma, h->fdef, h->j2_bbar, h->j2_F, h->j2_eps, h->body_vol, h->face_bc};
     for (size_t i = 0; i < sizeof ptrs / sizeof ptrs[0]; ++i) free(ptrs[i]);
     csr_free(&h->ilu);
     lu_free(h->lu);
@@ -537,7 +539,10 @@ void orc_set_history(orc_case* h, const double* u_old, const double* u_old_old, 
 /* ------------------------------------------------------------------ residual */
 
 /* ResidualEvaluator::bc_value with the config-built BC (io.cpp:278-279) */
+/* ResidualEvaluator::bc_value (discretisation.cpp:82-85): value(face_centroid, t) — the
+   caller's sampled per-face values when given, else the patch value (times t when ramped) */
 static v3 bc_value(const orc_case* h, int f) {
+    if (h->face_bc) return h->face_bc[f - h->nint];
     const int p = h->face_patch[f];
     return h->bc_ramp[p] ? vscale(h->bc_value[p], h->time) : h->bc_value[p];
 }
@@ -834,6 +839,8 @@ static int residual(orc_case* h, const v3* u, v3* r) {
         }
     }
     add_stabilisation(h, u, h->grad, r);
+    if (h->body_vol) /* discretisation.cpp:160-161 */
+        for (int c = 0; c < nc; ++c) r[c] = vadd(r[c], h->body_vol[c]);
     if (h->transient)
         for (int c = 0; c < nc; ++c) {
             const v3 a = bdf2_acc(u[c], h->u_old[c], h->u_old_old[c], h->v_old[c], h->v_old_old[c], h->dt);
@@ -1504,9 +1511,10 @@ static int op_apply(jv_op* op, const double* v, double* out) {
 
 enum { G_CONVERGED = 0, G_MAX_ITERS = 1, G_STAGNATED = 2 };
 
-/* gmres_solve, left preconditioned (linalg.cpp:423-538) */
+/* gmres_solve (linalg.cpp:423-538): left preconditioned, or right preconditioned (right != 0:
+   residuals unpreconditioned :437, w = op(M^-1 v_j) :466-467, dx = M^-1 (V y) :514) */
 static int gmres(jv_op* op, const double* b, double* x, int n, int restart, double rel_reduction,
-                 int max_iters, int* iters_out, int* status_out, double* rel_out) {
+                 int max_iters, int right, int* iters_out, int* status_out, double* rel_out) {
     orc_case* h = op->h;
     double* r = xcalloc(n, sizeof(double));
     double* tmp = xcalloc(n, sizeof(double));
@@ -1525,7 +1533,10 @@ static int gmres(jv_op* op, const double* b, double* x, int n, int restart, doub
         rc = op_apply(op, (xx), tmp);                                  \
         if (rc) goto done;                                             \
         for (int i = 0; i < n; ++i) tmp[i] = b[i] - tmp[i];            \
-        precond_solve(h, tmp, r, n);                                   \
+        if (right)                                                     \
+            for (int i = 0; i < n; ++i) r[i] = tmp[i];                 \
+        else                                                           \
+            precond_solve(h, tmp, r, n);                               \
     } while (0)
     RESID(x);
     const double r0 = dnorm(r, n);
@@ -1542,9 +1553,14 @@ static int gmres(jv_op* op, const double* b, double* x, int n, int restart, doub
         g[0] = beta;
         int j = 0, happy = 0;
         while (j < restart && total < max_iters) {
-            rc = op_apply(op, V + (size_t)j * n, tmp);
+            if (right) {
+                precond_solve(h, V + (size_t)j * n, tmp, n);
+                rc = op_apply(op, tmp, w);
+            } else {
+                rc = op_apply(op, V + (size_t)j * n, tmp);
+                if (!rc) precond_solve(h, tmp, w, n);
+            }
             if (rc) goto done;
-            precond_solve(h, tmp, w, n);
             double* hj = H + (size_t)j * (restart + 1);
             for (int i = 0; i <= j + 1; ++i) hj[i] = 0.0;
             for (int i = 0; i <= j; ++i) {
@@ -1581,6 +1597,10 @@ static int gmres(jv_op* op, const double* b, double* x, int n, int restart, doub
         }
         for (int i = 0; i < n; ++i) dx[i] = 0.0;
         for (int i = 0; i < j; ++i) daxpy(y[i], V + (size_t)i * n, dx, n);
+        if (right) {
+            precond_solve(h, dx, tmp, n);
+            for (int i = 0; i < n; ++i) dx[i] = tmp[i];
+        }
         daxpy(1.0, dx, x, n);
         RESID(x);
         beta = dnorm(r, n);
@@ -1600,10 +1620,11 @@ done:
 }
 
 int orc_gmres_jv(orc_case* h, const double* u, const double* r_u, const double* b, double* x,
-                 int restart, double rel_reduction, int max_iters, int* iters, int* status,
+                 int restart, double rel_reduction, int max_iters, int right, int* iters, int* status,
                  double* rel_residual) {
     jv_op op = {h, u, r_u, xcalloc(h->nc, sizeof(v3)), xcalloc(h->nc, sizeof(v3))};
-    const int rc = gmres(&op, b, x, 3 * h->nc, restart, rel_reduction, max_iters, iters, status, rel_residual);
+    const int rc = gmres(&op, b, x, 3 * h->nc, restart, rel_reduction, max_iters, right, iters, status,
+                         rel_residual);
     free(op.s1);
     free(op.s2);
     return rc;
@@ -1670,7 +1691,8 @@ static int jfnk(orc_case* h, v3* u, const sfv_solver_cfg* cfg, sfv_solve_report*
         for (int i = 0; i < n; ++i) { rhs[i] = -rflat[i]; x[i] = 0.0; }
         int iters = 0, status = 0;
         double rel = 0.0;
-        err = gmres(&op, rhs, x, n, cfg->restart, inner, cfg->max_krylov, &iters, &status, &rel);
+        err = gmres(&op, rhs, x, n, cfg->restart, inner, cfg->max_krylov, cfg->right_preconditioned, &iters,
+                    &status, &rel);
         if (err == SFV_ERR_JVP_NAN) {
             rep->status = SFV_DIVERGED;
             snprintf(rep->detail, SFV_DETAIL_LEN, "%s", h->err.msg);
@@ -2046,4 +2068,30 @@ int orc_run_steps(orc_case* h, double* field, const sfv_solver_cfg* cfg, int n_s
     for (int c = 0; c < 3; ++c) csr_free(&comps[c]);
     *wall = now_s() - t0;
     return rc;
+}
+
+/* DiscretisationConfig::body_force (discretisation.hpp:24): f = body_force(centroid_c) per
+   cell (3 nc, interleaved; NULL clears); the residual adds volume_c * f_c (discretisation.cpp:160-161) */
+int orc_set_body_force(orc_case* h, const double* f) {
+    free(h->body_vol);
+    h->body_vol = NULL;
+    if (!f) return SFV_OK;
+    h->body_vol = xcalloc(h->nc, sizeof(v3));
+    for (int c = 0; c < h->nc; ++c) {
+        const v3 fc = {f[3 * c], f[3 * c + 1], f[3 * c + 2]};
+        h->body_vol[c] = vscale(fc, h->volume[c]);
+    }
+    return SFV_OK;
+}
+
+/* per boundary face values (3 (nf - nint), face nint + i; NULL = per patch): the sampled
+   BoundaryCondition::value(face_centroid, t) of the current time */
+int orc_set_face_bc(orc_case* h, const double* v) {
+    free(h->face_bc);
+    h->face_bc = NULL;
+    if (!v) return SFV_OK;
+    const int nb = h->nf - h->nint;
+    h->face_bc = xcalloc(nb > 0 ? nb : 1, sizeof(v3));
+    for (int i = 0; i < nb; ++i) h->face_bc[i] = (v3){v[3 * i], v[3 * i + 1], v[3 * i + 2]};
+    return SFV_OK;
 }

@@ -57,10 +57,15 @@ int orc_run_steps(orc_case* h, double* field, const sfv_solver_cfg* cfg, int n_s
 
 /* GMRES on the J.v operator at u (used by the Krylov parity tests). */
 int orc_gmres_jv(orc_case* h, const double* u, const double* r_u, const double* b, double* x,
-                 int restart, double rel_reduction, int max_iters, int* iters, int* status,
+                 int restart, double rel_reduction, int max_iters, int right, int* iters, int* status,
                  double* rel_residual);
 
 double orc_time_jv(orc_case* h, const double* u, const double* r_u, const double* v, int reps);
+
+/* DiscretisationConfig::body_force sampled at the cell centroids (3 nc; NULL clears) */
+int orc_set_body_force(orc_case* h, const double* f);
+/* per boundary face BC values (3 (nf - nint); NULL = per patch values) */
+int orc_set_face_bc(orc_case* h, const double* v);
 
 #ifdef __cplusplus
 }

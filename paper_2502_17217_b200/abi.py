@@ -91,6 +91,7 @@ class SolverCfg(C.Structure):
         ("line_search", C.c_int),
         ("algorithm", C.c_int),
         ("relaxation", C.c_double),
+        ("right_preconditioned", C.c_int),
     ]
 
 
@@ -117,10 +118,26 @@ class SolveReport(C.Structure):
         ("records", IterationRecord * 64),
         ("detail", C.c_char * 160),
         ("cg_diag_fallback", C.c_int),
+        ("all_records", C.POINTER(IterationRecord)),
+        ("all_capacity", C.c_int),
     ]
 
+    def attach_history(self, capacity: int = 4096):
+        """Unbounded SolveReport::iterations (nonlinear.hpp:64): the solver writes every
+        record into a caller buffer as well as the first 64 into records[]."""
+        self._hist = (IterationRecord * capacity)()
+        self.all_records = C.cast(self._hist, C.POINTER(IterationRecord))
+        self.all_capacity = capacity
+        return self
+
+    def record_list(self) -> list:
+        if self.all_records and self.all_capacity:
+            return [self.all_records[i] for i in range(min(self.n_records, self.all_capacity))]
+        return [self.records[i] for i in range(min(self.n_records, 64))]
+
     def summary(self) -> dict:
-        n = min(self.n_records, 64)
+        recs = self.record_list()
+        n = len(recs)
         return {
             "status": STATUS_NAME.get(self.status, str(self.status)),
             "step": self.step,
@@ -129,9 +146,9 @@ class SolveReport(C.Structure):
             "initial_residual": self.initial_residual,
             "final_residual": self.final_residual,
             "wall_seconds": self.wall_seconds,
-            "krylov_per_newton": [self.records[i].krylov_iters for i in range(1, n)],
-            "r_norms": [self.records[i].r_norm for i in range(n)],
-            "s": [self.records[i].s for i in range(1, n)],
+            "krylov_per_newton": [recs[i].krylov_iters for i in range(1, n)],
+            "r_norms": [recs[i].r_norm for i in range(n)],
+            "s": [recs[i].s for i in range(1, n)],
             "cg_diag_fallback": bool(self.cg_diag_fallback),
             "detail": self.detail.decode(errors="replace"),
         }
@@ -256,7 +273,7 @@ class Physics:
 
 def solver_cfg(r_tol=1e-6, a_tol=1e-50, s_tol=0.0, max_outer=0, inner_reduction=0.0, restart=30,
                max_krylov=300, preconditioner="auto", line_search=True, algorithm="jfnk",
-               relaxation=1.0) -> SolverCfg:
+               relaxation=1.0, right_preconditioned=False) -> SolverCfg:
     """SolverConfig defaults (nonlinear.hpp:27-44); algorithm "jfnk" or "segregated"."""
     c = SolverCfg()
     c.algorithm = {"jfnk": 0, "segregated": 1}[algorithm] if isinstance(algorithm, str) else int(algorithm)
@@ -266,4 +283,5 @@ def solver_cfg(r_tol=1e-6, a_tol=1e-50, s_tol=0.0, max_outer=0, inner_reduction=
     c.restart, c.max_krylov = restart, max_krylov
     c.preconditioner = PRECOND[preconditioner] if isinstance(preconditioner, str) else int(preconditioner)
     c.line_search = int(bool(line_search))
+    c.right_preconditioned = int(bool(right_preconditioned))
     return c

@@ -58,7 +58,8 @@ struct DevBuf {
 
 struct Status {  // pinned host mirror of the device scalars read per control decision
     ErrWords err;
-    double h[72];
+    double* h;  // pinned, hcap doubles: the Hessenberg column of an Arnoldi step (restart + 2)
+    int hcap;
 };
 
 struct TriDev {
@@ -164,6 +165,12 @@ struct sfv_ctx {
     // residual / J.v kernels: 0 = jv_pair.cu (default), 1 = jv_fused.cu, 2 = residual.cu
     int jv_path = 0;
     bool use_fused = false;
+    // body force and per-face boundary values (DiscretisationConfig::body_force,
+    // BoundaryCondition::value sampled at the face centroids)
+    DevBuf<double> body_dev, face_bc_dev;
+    std::vector<double> face_bc_host;
+    sfv_bc_sampler bc_sampler = nullptr;
+    void* bc_user = nullptr;
     FusedLayout fl;
     DevBuf<int> f_tfp, f_own, f_oth, f_slots, f_index, f_flags, f_ticket;
     DevBuf<double> f_geo, f_gring, f_fring;
@@ -229,11 +236,35 @@ namespace {
 
 constexpr int kNone = 0x7f7f7f7f;
 
-void update_patch_values(sfv_ctx* c) {
+int upload_face_values(sfv_ctx* c, const double* v);
+
+int update_patch_values(sfv_ctx* c) {
     // config-built BC: ramp ? v * t : v (io.cpp:278-279)
     for (int p = 0; p < c->pt.n; ++p)
         for (int k = 0; k < 3; ++k)
             c->pt.value[p][k] = c->bc_ramp[p] ? c->bc_raw[3 * p + k] * c->time : c->bc_raw[3 * p + k];
+    if (c->bc_sampler) {  // BoundaryCondition::value(face_centroid, t) for every boundary face
+        c->face_bc_host.assign(3 * static_cast<size_t>(c->mesh.n_faces() - c->mesh.n_internal), 0.0);
+        c->bc_sampler(c->bc_user, c->time, c->face_bc_host.data());
+        return upload_face_values(c, c->face_bc_host.data());
+    }
+    return SFV_OK;
+}
+
+// per boundary face values on the device (null: the patch table)
+int upload_face_values(sfv_ctx* c, const double* v) {
+    if (!v) {
+        c->pt.face_value = nullptr;
+        return SFV_OK;
+    }
+    const size_t nb = 3 * static_cast<size_t>(c->mesh.n_faces() - c->mesh.n_internal);
+    if (c->face_bc_dev.n != nb && !c->face_bc_dev.alloc(nb)) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
+    // ordered on the context stream: earlier kernels still reading the old values finish first
+    cudaStreamSynchronize(c->stream);
+    if (nb && cudaMemcpy(c->face_bc_dev.p, v, sizeof(double) * nb, cudaMemcpyHostToDevice) != cudaSuccess)
+        return c->cuda_check("boundary values");
+    c->pt.face_value = c->face_bc_dev.p;
+    return SFV_OK;
 }
 
 std::string build_layout(sfv_ctx* c) {
@@ -636,8 +667,19 @@ int precond_apply_async(sfv_ctx* c, const double* r, double* z) {
 bool ensure_krylov(sfv_ctx* c, int restart) {
     const size_t n = static_cast<size_t>(c->n);
     if (c->v_cap >= restart + 1 && c->wv.p) return true;
+    c->drop_graph();  // the basis and workspace pointers change
+    if (restart + 2 > c->st->hcap) {  // Hessenberg column of an Arnoldi step: restart + 2 doubles
+        double* h = nullptr;
+        if (cudaMallocHost(&h, sizeof(double) * (restart + 2)) != cudaSuccess || !c->hdev.alloc(restart + 2)) {
+            if (h) cudaFreeHost(h);
+            return false;
+        }
+        cudaFreeHost(c->st->h);
+        c->st->h = h;
+        c->st->hcap = restart + 2;
+    }
     bool ok = c->V.alloc(n * (restart + 1)) && c->wv.alloc(n) && c->rv.alloc(n) && c->tv.alloc(n) &&
-              c->xv.alloc(n) && c->bv.alloc(n) && c->ydev.alloc(64) && c->ucand.alloc(n) && c->rcand.alloc(n) &&
+              c->xv.alloc(n) && c->bv.alloc(n) && c->ydev.alloc(restart + 1) && c->ucand.alloc(n) && c->rcand.alloc(n) &&
               c->uscratch.alloc(n) && c->rscratch.alloc(n);
     c->v_cap = ok ? restart + 1 : 0;
     return ok;
@@ -784,13 +826,15 @@ int gmres_graph_cycle(sfv_ctx* c, int total, int restart, int max_iters, double 
     return SFV_OK;
 }
 
-// gmres_solve, left preconditioned (/root/reference/proj/src/linalg.cpp:423-538), with
-// op = J.v at (u, r_u).  x_zero: x0 is all zeros, so op(x0) = 0 without evaluation
-// (jacobian_vector_product short-circuits |v| = 0, nonlinear.cpp:110).
+// gmres_solve (/root/reference/proj/src/linalg.cpp:423-538), with op = J.v at (u, r_u),
+// left preconditioned or, with `right`, right preconditioned (residuals unpreconditioned
+// :437, w = op(M^-1 v_j) :466-467, dx = M^-1 V y :514).  x_zero: x0 is all zeros, so
+// op(x0) = 0 without evaluation (jacobian_vector_product short-circuits |v| = 0,
+// nonlinear.cpp:110).  Any restart >= 1 (the basis is sized to it).
 int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, double* x, bool x_zero, int restart,
-          double rel_reduction, int max_iters, int* iters_out, int* status_out, double* rel_out) {
+          double rel_reduction, int max_iters, int* iters_out, int* status_out, double* rel_out, bool right = false) {
     const int n = c->n;
-    if (restart > 64) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "gmres: restart > 64 unsupported");
+    if (restart < 1) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "gmres: restart must be >= 1");
     if (!ensure_krylov(c, restart)) return c->fail(SFV_ERR_CUDA, -1, "gmres: out of device memory");
     double* V = c->V.p;
     double* w = c->wv.p;
@@ -805,14 +849,16 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
     };
     // residual(x): r = M^-1 (b - op(x))  (linalg.cpp:434-439)
     auto residual_of_x = [&](bool zero) -> int {
+        double* res = right ? r : tmp;  // b - op(x); left: then M^-1
         if (zero) {
-            cudaMemcpyAsync(tmp, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
+            cudaMemcpyAsync(res, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
         } else {
-            op(x, tmp);
-            launch_sub_from(b, tmp, n, c->stream);
+            op(x, res);
+            launch_sub_from(b, res, n, c->stream);
             ++c->launches;
         }
-        if (int e = precond_apply_async(c, tmp, r)) return e;
+        if (!right)
+            if (int e = precond_apply_async(c, tmp, r)) return e;
         launch_dot(r, r, n, c->hdev.p, c->red.p, c->counter.p, c->stream);
         ++c->launches;
         if (int e = fetch(c, 1)) return e;
@@ -866,7 +912,7 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
         const char* e = std::getenv("SFV_FUSED_MGS");
         return e && std::atoi(e) == 0;
     }();
-    const bool use_graph = gmres_graph_ready(c, u, r_u, restart);
+    const bool use_graph = !right && gmres_graph_ready(c, u, r_u, restart);
     while (total < max_iters) {
         const double cycle_start = beta;
         launch_scale_div_host(r, beta, V, n, c->stream);  // v0 = r / beta
@@ -892,9 +938,15 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
         while (!use_graph && j < restart && total < max_iters) {
             double* vj = V + static_cast<size_t>(j) * n;
             if (tim.on) cudaEventRecord(tim.ev[0], c->stream);
-            op(vj, tmp);
-            if (tim.on) cudaEventRecord(tim.ev[1], c->stream);
-            if (int e = precond_apply_async(c, tmp, w)) return e;
+            if (right) {  // w = op(M^-1 v_j)
+                if (int e = precond_apply_async(c, vj, tmp)) return e;
+                if (tim.on) cudaEventRecord(tim.ev[1], c->stream);
+                op(tmp, w);
+            } else {  // w = M^-1 op(v_j)
+                op(vj, tmp);
+                if (tim.on) cudaEventRecord(tim.ev[1], c->stream);
+                if (int e = precond_apply_async(c, tmp, w)) return e;
+            }
             if (tim.on) cudaEventRecord(tim.ev[2], c->stream);
             // modified Gram-Schmidt (linalg.cpp:469-473).  Fused: one cooperative launch with
             // w in shared memory, also writing v_{j+1} = w / |w|.  Otherwise h_0 = w.v_0, then
@@ -960,8 +1012,15 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
             y[i] = s / H[i][i];
         }
         cudaMemcpyAsync(c->ydev.p, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, c->stream);
-        launch_update(x, V, c->ydev.p, j, n, c->stream);
-        ++c->launches;
+        if (right) {  // dx = M^-1 (V y); x += 1.0 * dx
+            launch_basis_combination(tmp, V, c->ydev.p, j, n, c->stream);
+            if (int e = precond_apply_async(c, tmp, w)) return e;
+            launch_axpy_host(x, 1.0, w, n, c->stream);
+            c->launches += 2;
+        } else {
+            launch_update(x, V, c->ydev.p, j, n, c->stream);
+            ++c->launches;
+        }
         x_zero = false;
         if (int e = residual_of_x(false)) return e;  // explicit restart residual (:518-519)
         beta = std::sqrt(c->st->h[0]);
@@ -983,8 +1042,19 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
 
 void push_record(sfv_solve_report* rep, int iter, double r_norm, int kry, double s) {
     const int cap = static_cast<int>(sizeof(rep->records) / sizeof(rep->records[0]));
-    if (rep->n_records < cap) rep->records[rep->n_records] = {0, iter, r_norm, kry, s};
+    const sfv_iteration_record rec{0, iter, r_norm, kry, s};
+    if (rep->n_records < cap) rep->records[rep->n_records] = rec;
+    if (rep->all_records && rep->n_records < rep->all_capacity) rep->all_records[rep->n_records] = rec;
     ++rep->n_records;
+}
+
+// memset a report, keeping the caller's unbounded-history buffer
+void clear_report(sfv_solve_report* rep) {
+    sfv_iteration_record* all = rep->all_records;
+    const int cap = rep->all_capacity;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->all_records = all;
+    rep->all_capacity = cap;
 }
 
 // jfnk_solve (nonlinear.cpp:173-266) with line_search (:140-163) and check_convergence
@@ -1096,7 +1166,7 @@ int segregated(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_repor
     const int max_outer = cfg->max_outer > 0 ? cfg->max_outer : 2000;
     const double inner = cfg->inner_reduction > 0.0 ? cfg->inner_reduction : 0.9;
     const double relax = cfg->relaxation > 0.0 ? cfg->relaxation : 1.0;
-    std::memset(rep, 0, sizeof(*rep));
+    clear_report(rep);
     rep->status = SFV_MAX_ITERS;
     auto wall = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     if (!ensure_krylov(c, std::max(cfg->restart, 1))) return c->fail(SFV_ERR_CUDA, -1, "segregated: out of device memory");
@@ -1171,12 +1241,37 @@ int segregated(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_repor
     return SFV_OK;
 }
 
+// line_search (nonlinear.cpp:140-163): s = 1, 1/2, ... 1/32; the first candidate u + s du
+// whose residual norm is strictly below r_norm0 wins (an invalid trial state — a law or
+// NaN error in R — rejects that step length).  The accepted candidate and its residual are
+// left in ucand / rcand.
+int line_search(sfv_ctx* c, const double* u, const double* du, double r_norm0, bool* ok, double* s_out,
+                double* rn_out) {
+    const int n = c->n;
+    double ss = 1.0, rn = 0.0;
+    *ok = false;
+    if (!ensure_krylov(c, 1)) return c->fail(SFV_ERR_CUDA, -1, "line_search: out of device memory");
+    for (int attempt = 0; attempt < 6; ++attempt, ss *= 0.5) {
+        launch_lincomb(c->ucand.p, u, ss, du, n, c->stream);
+        ++c->launches;
+        if (residual_sync(c, c->ucand.p, c->rcand.p)) continue;  // invalid trial state rejects the step
+        if (int e = norm_host(c, c->rcand.p, &rn)) return e;
+        if (rn < r_norm0) {
+            *ok = true;
+            break;
+        }
+    }
+    *s_out = ss;
+    *rn_out = rn;
+    return SFV_OK;
+}
+
 int jfnk(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep) {
     const auto t0 = std::chrono::steady_clock::now();
     const int n = c->n;
     const int max_outer = cfg->max_outer > 0 ? cfg->max_outer : 50;
     const double inner = cfg->inner_reduction > 0.0 ? cfg->inner_reduction : 1e-3;
-    std::memset(rep, 0, sizeof(*rep));
+    clear_report(rep);
     rep->status = SFV_MAX_ITERS;
     auto wall = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     if (!ensure_krylov(c, std::max(cfg->restart, 1))) return c->fail(SFV_ERR_CUDA, -1, "jfnk: out of device memory");
@@ -1206,7 +1301,8 @@ int jfnk(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep
         ++c->launches;
         int iters = 0, status = 0;
         double rel = 0.0;
-        e = gmres(c, u, r, rhs, x, true, cfg->restart, inner, cfg->max_krylov, &iters, &status, &rel);
+        e = gmres(c, u, r, rhs, x, true, cfg->restart, inner, cfg->max_krylov, &iters, &status, &rel,
+                  cfg->right_preconditioned != 0);
         if (e == SFV_ERR_JVP_NAN) {
             rep->status = SFV_DIVERGED;
             std::snprintf(rep->detail, SFV_DETAIL_LEN, "%s", c->last.msg.c_str());
@@ -1231,16 +1327,7 @@ int jfnk(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep
         if (cfg->line_search) {
             bool ok = false;
             double ss = 1.0, rn = 0.0;
-            for (int attempt = 0; attempt < 6; ++attempt, ss *= 0.5) {
-                launch_lincomb(c->ucand.p, u, ss, x, n, c->stream);
-                ++c->launches;
-                if (residual_sync(c, c->ucand.p, c->rcand.p)) continue;  // invalid trial state rejects the step
-                if ((e = norm_host(c, c->rcand.p, &rn))) return e;
-                if (rn < r_norm) {
-                    ok = true;
-                    break;
-                }
-            }
+            if ((e = line_search(c, u, x, r_norm, &ok, &ss, &rn))) return e;
             if (!ok) {
                 rep->status = SFV_DIVERGED;
                 std::snprintf(rep->detail, SFV_DETAIL_LEN, "line search found no residual decrease");
@@ -1716,13 +1803,19 @@ sfv_ctx* sfv_create(const sfv_mesh_desc* md, const sfv_physics* ph, char* err, i
         c->hist.u_old = c->hist.u_old_old = c->hist.v_old = c->hist.v_old_old = c->dzero.p;
     }
     if (cudaMallocHost(&c->st, sizeof(Status)) != cudaSuccess) return fail("cuda: pinned allocation failed");
+    c->st->hcap = 72;
+    if (cudaMallocHost(&c->st->h, sizeof(double) * c->st->hcap) != cudaSuccess)
+        return fail("cuda: pinned allocation failed");
     if (cudaDeviceSynchronize() != cudaSuccess) return fail("cuda: setup failed");
     return c.release();
 }
 
 void sfv_destroy(sfv_ctx* c) {
     if (!c) return;
-    if (c->st) cudaFreeHost(c->st);
+    if (c->st) {
+        if (c->st->h) cudaFreeHost(c->st->h);
+        cudaFreeHost(c->st);
+    }
     delete c;
 }
 
@@ -1815,8 +1908,41 @@ int sfv_geometry(const sfv_ctx* c, double* volume, double* centroid, double* fac
 
 int sfv_set_time(sfv_ctx* c, double t) {
     c->time = t;
-    update_patch_values(c);
+    return update_patch_values(c);
+}
+
+int sfv_set_body_force(sfv_ctx* c, const double* f) {
+    if (c->jv_path != 0 || c->use_fused)
+        return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "body force: only on the default residual path");
+    if (!f) {
+        c->hist.body = nullptr;
+        return SFV_OK;
+    }
+    // volume_c * body_force(centroid_c): the reference's product (discretisation.cpp:161)
+    std::vector<double> bv(3 * static_cast<size_t>(c->nc));
+    if (!download_geometry(c->dgeo, c->geom).empty()) return c->fail(SFV_ERR_CUDA, -1, "body force: geometry");
+    const auto& vol = c->geom.volume;
+    for (int cc = 0; cc < c->nc; ++cc)
+        for (int k = 0; k < 3; ++k) bv[3 * cc + k] = vol[cc] * f[3 * cc + k];
+    if (!c->body_dev.upload(bv)) return c->fail(SFV_ERR_CUDA, -1, "body force: out of device memory");
+    c->hist.body = c->body_dev.p;
     return SFV_OK;
+}
+
+int sfv_set_boundary_values(sfv_ctx* c, const double* values) {
+    if (c->jv_path != 0 || c->use_fused)
+        return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "boundary values: only on the default residual path");
+    c->bc_sampler = nullptr;
+    return upload_face_values(c, values);
+}
+
+int sfv_set_boundary_sampler(sfv_ctx* c, sfv_bc_sampler fn, void* user) {
+    if (c->jv_path != 0 || c->use_fused)
+        return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "boundary values: only on the default residual path");
+    c->bc_sampler = fn;
+    c->bc_user = user;
+    if (!fn) return upload_face_values(c, nullptr);
+    return update_patch_values(c);
 }
 
 int sfv_set_history(sfv_ctx* c, const double* uo, const double* uoo, const double* vo, const double* voo) {
@@ -2049,6 +2175,37 @@ int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v,
 
 int sfv_precond_create(sfv_ctx* c, int kind) { return precond_create(c, kind); }
 
+int sfv_line_search(sfv_ctx* c, const double* u, const double* du, double r_norm0, int* success, double* s,
+                    double* r_norm, double* residual) {
+    if (c->singular_cell >= 0) return gradient_failure(c);
+    bool ok = false;
+    double ss = 1.0, rn = 0.0;
+    if (int e = line_search(c, u, du, r_norm0, &ok, &ss, &rn)) return e;
+    *success = ok ? 1 : 0;
+    *s = ok ? ss : 0.0;
+    *r_norm = ok ? rn : 0.0;
+    if (ok && residual) cudaMemcpyAsync(residual, c->rcand.p, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->cuda_check("line_search");
+    return SFV_OK;
+}
+
+int sfv_approximate_jacobian(const sfv_ctx* c, int* row_ptr, int* col, double* blocks) {
+    std::vector<ScalarCsr> comps;
+    const std::string msg = cell_jacobian(c->mesh, c->geom, c->ph.kbar, c->ph.transient != 0, c->ph.rho, c->ph.dt, comps);
+    if (!msg.empty()) return const_cast<sfv_ctx*>(c)->fail(SFV_ERR_INVALID_ARGUMENT, -1, msg);
+    const ScalarCsr& a0 = comps[0];
+    const int nnz = a0.rp[a0.n];
+    if (!col || !blocks) return nnz;  // size query
+    for (int i = 0; i <= a0.n; ++i) row_ptr[i] = a0.rp[i];
+    for (int k = 0; k < nnz; ++k) {
+        col[k] = a0.col[k];
+        double* b = blocks + 9 * static_cast<size_t>(k);
+        for (int q = 0; q < 9; ++q) b[q] = 0.0;
+        for (int a = 0; a < 3; ++a) b[4 * a] = comps[comps.size() == 1 ? 0 : a].val[k];
+    }
+    return nnz;
+}
+
 int sfv_precond_apply(sfv_ctx* c, const double* r, double* z) {
     if (int e = precond_apply_async(c, r, z)) return e;
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->cuda_check("precond_apply");
@@ -2070,10 +2227,12 @@ int sfv_precond_sweep(const sfv_ctx* c) {
 }
 
 int sfv_gmres_jv(sfv_ctx* c, const double* u, const double* r_u, const double* b, double* x, int restart,
-                 double rel_reduction, int max_iters, int* iters, int* status, double* rel_residual) {
+                 double rel_reduction, int max_iters, int right_preconditioned, int* iters, int* status,
+                 double* rel_residual) {
     if (c->singular_cell >= 0) return gradient_failure(c);
     // x is the initial guess; a nonzero guess costs one extra J.v as in the reference
-    return gmres(c, u, r_u, b, x, false, restart, rel_reduction, max_iters, iters, status, rel_residual);
+    return gmres(c, u, r_u, b, x, false, restart, rel_reduction, max_iters, iters, status, rel_residual,
+                 right_preconditioned != 0);
 }
 
 int sfv_jfnk_solve(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep) {
@@ -2116,15 +2275,21 @@ int sfv_run_steps(sfv_ctx* c, double* field, const sfv_solver_cfg* cfg, int n_st
         } else {
             cudaMemcpyAsync(u, fu, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
         }
-        sfv_solve_report rep;
+        sfv_solve_report rep{};
+        if (*n_reports < cap) {  // the caller's unbounded-history buffer for this step
+            rep.all_records = reports[*n_reports].all_records;
+            rep.all_capacity = reports[*n_reports].all_capacity;
+        }
         const int e = seg ? segregated(c, u, cfg, &rep) : jfnk(c, u, cfg, &rep);
         if (e) {
-            std::memset(&rep, 0, sizeof(rep));
+            clear_report(&rep);
             rep.status = SFV_DIVERGED;
             std::snprintf(rep.detail, SFV_DETAIL_LEN, "%s", c->last.msg.c_str());
         }
         rep.step = step;
         for (int i = 0; i < std::min(rep.n_records, 64); ++i) rep.records[i].step = step;
+        if (rep.all_records)
+            for (int i = 0; i < std::min(rep.n_records, rep.all_capacity); ++i) rep.all_records[i].step = step;
         if (*n_reports < cap) reports[*n_reports] = rep;
         ++*n_reports;
         if (rep.status != SFV_CONVERGED) break;

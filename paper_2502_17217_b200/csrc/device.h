@@ -31,7 +31,24 @@ struct PatchTable {
     int n;
     int kind[kMaxPatches];
     double value[kMaxPatches][3];
+    // per boundary face values (face nint + i at 3 i), sampled from BoundaryCondition::value at
+    // the face centroids and the current time (ResidualEvaluator::bc_value,
+    // discretisation.cpp:82-85); null: the patch values above
+    const double* face_value = nullptr;
 };
+// prescribed value of boundary face f (patch `patch`)
+__host__ __device__ inline void bc_of(const PatchTable& pt, int patch, int f, int nint, double v[3]) {
+    if (pt.face_value) {
+        const double* q = pt.face_value + 3 * static_cast<size_t>(f - nint);
+        v[0] = q[0];
+        v[1] = q[1];
+        v[2] = q[2];
+    } else {
+        v[0] = pt.value[patch][0];
+        v[1] = pt.value[patch][1];
+        v[2] = pt.value[patch][2];
+    }
+}
 
 struct DevMesh {
     int nc = 0, nf = 0, nint = 0, slots = 0;
@@ -133,6 +150,8 @@ struct History {
     const double* u_old_old = nullptr;
     const double* v_old = nullptr;
     const double* v_old_old = nullptr;
+    // volume_c * body_force(centroid_c), interleaved (discretisation.cpp:160-161); null: none
+    const double* body = nullptr;
 };
 
 // ---- residual.cu
@@ -293,6 +312,7 @@ void launch_givens(const GmresDev& st, const double* h, const ErrWords* err, cud
 void launch_scale_div(const double* in, const double* divisor, double* out, int n, cudaStream_t s);
 void launch_scale_div_host(const double* in, double divisor, double* out, int n, cudaStream_t s);
 void launch_update(double* x, const double* V, const double* y, int j, int n, cudaStream_t s);
+void launch_basis_combination(double* dx, const double* V, const double* y, int j, int n, cudaStream_t s);
 void launch_sub_from(const double* b, double* r, int n, cudaStream_t s);  // r = b - r
 void launch_negate(const double* a, double* out, int n, cudaStream_t s);
 void launch_axpy_host(double* y, double alpha, const double* x, int n, cudaStream_t s);  // y += alpha x

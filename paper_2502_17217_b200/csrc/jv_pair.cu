@@ -437,7 +437,9 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, Physics ph, Pa
     const int f = m.nint + fb;
     const int patch = -m.tslot[tiled(c, 2 * m.spad) + 32 * (m.spad + s)] - 2;
     const int pk = pt.kind[patch];
-    const d3 bc = {pt.value[patch][0], pt.value[patch][1], pt.value[patch][2]};
+    double bv[3];
+    bc_of(pt, patch, f, m.nint, bv);
+    const d3 bc = {bv[0], bv[1], bv[2]};
     const double* fr = face_rec(m, f);
     const d3 gam = ld3(fr);
     // rhie_chow()'s per-face constants |Delta| / |d| and |Gamma|, precomputed on the host with
@@ -580,7 +582,9 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
                 // (discretisation.cpp:151-154, no stabilisation term, :204-205), displacement
                 // Gamma . sigma_P and the Rhie-Chow term towards the prescribed value (:136-140, :189-193)
                 const int patch = -o - 2;
-                const d3 bc = {pt.value[patch][0], pt.value[patch][1], pt.value[patch][2]};
+                double bv[3];
+                bc_of(pt, patch, f, m.nint, bv);
+                const d3 bc = {bv[0], bv[1], bv[2]};
                 const double* rf = face_rec(m, f);
                 const double gmag = rf[224];
                 if (pt.kind[patch] == SFV_PATCH_TRACTION) {
@@ -631,6 +635,7 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
 #pragma unroll
                 for (int t = 0; t < S; ++t)
                     if (((kw >> (8 * t)) & 0xff) == 2) r += res[t][3 + k][lane];
+                if (hist.body && !ph.stab_only) r = r + hist.body[ik];  // body force (discretisation.cpp:160-161)
                 if (ph.transient && !ph.stab_only) {  // BDF2 inertia (discretisation.cpp:48-57, :163-169)
                     const double uc = wg[tiled(c, kWG) + 32 * k];
                     const double idt = 1.0 / (2.0 * ph.dt);

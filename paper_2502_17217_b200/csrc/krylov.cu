@@ -112,15 +112,18 @@ __global__ void scale_div_kernel(const double* __restrict__ in, const double* __
 }
 
 // dx = sum_i y_i v_i accumulated in i order from zero, then x += dx (linalg.cpp:512-515)
-__global__ void update_kernel(double* __restrict__ x, const double* __restrict__ V, const double* __restrict__ y, int j,
-                              int n) {
-    __shared__ double ys[64];
+// dx = sum_i y_i v_i in the reference's axpy order (linalg.cpp:513), then x += 1.0 * dx
+// (:515), or dx alone into dx_out (right preconditioning applies M^-1 to it first, :514)
+__global__ void update_kernel(double* __restrict__ x, double* __restrict__ dx_out, const double* __restrict__ V,
+                              const double* __restrict__ y, int j, int n) {
+    extern __shared__ double ys[];  // [j]
     for (int i = threadIdx.x; i < j; i += blockDim.x) ys[i] = y[i];
     __syncthreads();
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
         double dx = 0.0;
         for (int i = 0; i < j; ++i) dx += ys[i] * V[static_cast<size_t>(i) * n + e];
-        x[e] += 1.0 * dx;
+        if (dx_out) dx_out[e] = dx;
+        else x[e] += 1.0 * dx;
     }
 }
 
@@ -384,7 +387,11 @@ void launch_scale_div_host(const double* in, double divisor, double* out, int n,
 }
 
 void launch_update(double* x, const double* V, const double* y, int j, int n, cudaStream_t s) {
-    update_kernel<<<grid_for(n), 256, 0, s>>>(x, V, y, j, n);
+    update_kernel<<<grid_for(n), 256, sizeof(double) * (j > 0 ? j : 1), s>>>(x, nullptr, V, y, j, n);
+}
+
+void launch_basis_combination(double* dx, const double* V, const double* y, int j, int n, cudaStream_t s) {
+    update_kernel<<<grid_for(n), 256, sizeof(double) * (j > 0 ? j : 1), s>>>(nullptr, dx, V, y, j, n);
 }
 
 void launch_sub_from(const double* b, double* r, int n, cudaStream_t s) {

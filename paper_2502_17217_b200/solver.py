@@ -28,6 +28,8 @@ import os
 
 import numpy as np
 
+_SAMPLER = C.CFUNCTYPE(None, C.c_void_p, C.c_double, C.POINTER(C.c_double))
+
 from .abi import ERR, Mesh, MeshDesc, Physics, PhysicsDesc, SolveReport, SolverCfg, dptr, iptr, solver_cfg
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -73,6 +75,9 @@ def lib():
         "sfv_jv_bytes": (C.c_double, [_vp]),
         "sfv_geometry": (C.c_int, [_vp] + [_dp] * 9 + [C.POINTER(C.c_byte), _ip, _ip, _dp]),
         "sfv_set_time": (C.c_int, [_vp, C.c_double]),
+        "sfv_set_body_force": (C.c_int, [_vp, _dp]),
+        "sfv_set_boundary_values": (C.c_int, [_vp, _dp]),
+        "sfv_set_boundary_sampler": (C.c_int, [_vp, _vp, _vp]),
         "sfv_set_history": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
         "sfv_residual": (C.c_int, [_vp, _vp, _vp, _ip]),
         "sfv_stabilisation": (C.c_int, [_vp, _vp, _vp, _ip]),
@@ -88,10 +93,12 @@ def lib():
         "sfv_residual_host": (C.c_int, [_vp, _dp, _dp, _ip]),
         "sfv_jv_host": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _ip]),
         "sfv_precond_create": (C.c_int, [_vp, C.c_int]),
+        "sfv_approximate_jacobian": (C.c_int, [_vp, _ip, _ip, _dp]),
+        "sfv_line_search": (C.c_int, [_vp, _vp, _vp, C.c_double, _ip, _dp, _dp, _vp]),
         "sfv_precond_apply": (C.c_int, [_vp, _vp, _vp]),
         "sfv_precond_info": (C.c_int, [_vp, _ip]),
         "sfv_precond_sweep": (C.c_int, [_vp]),
-        "sfv_gmres_jv": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_double, C.c_int, _ip, _ip, _dp]),
+        "sfv_gmres_jv": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_double, C.c_int, C.c_int, _ip, _ip, _dp]),
         "sfv_jfnk_solve": (C.c_int, [_vp, _vp, C.POINTER(SolverCfg), C.POINTER(SolveReport)]),
         "sfv_run_steps": (C.c_int, [_vp, _vp, C.POINTER(SolverCfg), C.c_int, C.POINTER(SolveReport), C.c_int,
                                     _ip, _dp]),
@@ -226,6 +233,38 @@ class ResidualEvaluator:
     def set_time(self, t: float):
         self._check(self.L.sfv_set_time(self.h, float(t)))
 
+    def set_body_force(self, f):
+        """DiscretisationConfig::body_force sampled at the cell centroids: (3*n_cells,) or None."""
+        if f is None:
+            self._check(self.L.sfv_set_body_force(self.h, None))
+            return
+        self._body = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
+        self._check(self.L.sfv_set_body_force(self.h, dptr(self._body)))
+
+    def set_boundary_values(self, values):
+        """Per boundary face BC values (3*(n_faces - n_internal),) at the current time, or None."""
+        if values is None:
+            self._check(self.L.sfv_set_boundary_values(self.h, None))
+            return
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        self._check(self.L.sfv_set_boundary_values(self.h, dptr(v)))
+
+    def set_boundary_sampler(self, fn):
+        """fn(t) -> (3*(n_faces - n_internal),) per-face BC values; sampled on every set_time and
+        every step of run_steps (BoundaryCondition::value at the face centroids).  None clears."""
+        if fn is None:
+            self._sampler = None
+            self._check(self.L.sfv_set_boundary_sampler(self.h, None, None))
+            return
+        nb = 3 * (self.mesh.n_faces - self.mesh.n_internal)
+
+        def cb(_user, t, out):
+            vals = np.ascontiguousarray(fn(t), dtype=np.float64).reshape(-1)
+            C.memmove(out, vals.ctypes.data, 8 * nb)
+
+        self._sampler = _SAMPLER(cb)
+        self._check(self.L.sfv_set_boundary_sampler(self.h, C.cast(self._sampler, _vp), None))
+
     def set_history(self, u_old, u_old_old, v_old, v_old_old):
         self._hist = [to_device(a) for a in (u_old, u_old_old, v_old, v_old_old)]
         self._check(self.L.sfv_set_history(self.h, *[_ptr(t) for t in self._hist]))
@@ -325,13 +364,40 @@ def make_preconditioner(ev: ResidualEvaluator, kind: str = "auto") -> Preconditi
     return Preconditioner(ev, kind)
 
 
-def gmres_jv(ev: ResidualEvaluator, u, r_u, b, x0=None, restart=30, rel_reduction=1e-3, max_iters=300):
-    """gmres_solve with op = J.v at u, left preconditioned by the current preconditioner."""
+def approximate_jacobian(ev: ResidualEvaluator):
+    """assemble_approximate_jacobian (discretisation.cpp:216-262): (row_ptr, col, blocks[nnz, 3, 3])."""
+    nnz = ev.L.sfv_approximate_jacobian(ev.h, None, None, None)
+    if nnz < 0:
+        ev._check(nnz)
+    rp = np.zeros(ev.n_cells + 1, dtype=np.int32)
+    col = np.zeros(nnz, dtype=np.int32)
+    blocks = np.zeros(9 * nnz)
+    r = ev.L.sfv_approximate_jacobian(ev.h, iptr(rp), iptr(col), dptr(blocks))
+    if r < 0:
+        ev._check(r)
+    return rp, col, blocks.reshape(nnz, 3, 3)
+
+
+def line_search(ev: ResidualEvaluator, u, du, r_norm0: float):
+    """line_search (nonlinear.cpp:140-163): (success, s, r_norm, residual or None)."""
+    ud, dd = to_device(u), to_device(du)
+    res = ev.empty()
+    ok, s, rn = C.c_int(0), C.c_double(0.0), C.c_double(0.0)
+    ev._check(ev.L.sfv_line_search(ev.h, _ptr(ud), _ptr(dd), float(r_norm0), C.byref(ok), C.byref(s), C.byref(rn),
+                                   _ptr(res)))
+    return bool(ok.value), s.value, rn.value, (res if ok.value else None)
+
+
+def gmres_jv(ev: ResidualEvaluator, u, r_u, b, x0=None, restart=30, rel_reduction=1e-3, max_iters=300,
+             right_preconditioned=False):
+    """gmres_solve (linalg.cpp:423-538) with op = J.v at u and the context's preconditioner,
+    left (default) or right preconditioned."""
     ud, rd, bd = to_device(u), to_device(r_u), to_device(b)
     x = ev.empty() if x0 is None else to_device(x0).clone()
     it, st, rel = C.c_int(0), C.c_int(0), C.c_double(0.0)
     ev._check(ev.L.sfv_gmres_jv(ev.h, _ptr(ud), _ptr(rd), _ptr(bd), _ptr(x), int(restart), float(rel_reduction),
-                                int(max_iters), C.byref(it), C.byref(st), C.byref(rel)))
+                                int(max_iters), int(bool(right_preconditioned)), C.byref(it), C.byref(st),
+                                C.byref(rel)))
     return x, it.value, ["converged", "max-iters", "stagnated"][st.value], rel.value
 
 
