@@ -152,6 +152,8 @@ int sfv_approximate_jacobian(const sfv_ctx* ctx, int* row_ptr, int* col, double*
 int sfv_line_search(sfv_ctx* ctx, const double* u_dev, const double* du_dev, double r_norm0, int* success,
                     double* s, double* r_norm, double* residual_dev);
 int sfv_precond_apply(sfv_ctx* ctx, const double* r_dev, double* z_dev);
+/* the same with host buffers (Preconditioner::solve, linalg.hpp:53-59) */
+int sfv_precond_apply_host(sfv_ctx* ctx, const double* r, double* z);
 /* preconditioner facts: {kind_resolved, n_levels_fwd, n_levels_bwd, nnz_L, nnz_U} */
 int sfv_precond_info(const sfv_ctx* ctx, int info[5]);
 /* Device sweep of the ILU apply: 200 streamed level-synchronous (default), 300 block-
@@ -166,11 +168,18 @@ int sfv_gmres_jv(sfv_ctx* ctx, const double* u_dev, const double* r_u_dev, const
                  int restart, double rel_reduction, int max_iters, int right_preconditioned, int* iters, int* status,
                  double* rel_residual);
 int sfv_jfnk_solve(sfv_ctx* ctx, double* u_dev, const sfv_solver_cfg* cfg, sfv_solve_report* report);
+/* the same with u in host memory (initial guess in, final iterate out) */
+int sfv_jfnk_solve_host(sfv_ctx* ctx, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* report);
 /* segregated_solve (nonlinear.hpp:101-103; nonlinear.cpp:268-351): per outer iteration, each
  * displacement component by IC(0)-preconditioned CG on A = -J~ (Jacobi when IC(0) breaks
  * down), then u += relaxation (u_next - u).  cfg->algorithm is ignored here; sfv_run_steps
  * dispatches on it (SFV_ALG_SEGREGATED) as run_steps does. */
 int sfv_segregated_solve(sfv_ctx* ctx, double* u_dev, const sfv_solver_cfg* cfg, sfv_solve_report* report);
+/* StepCallback (nonlinear.hpp:106-107): when set, sfv_run_steps calls fn(user, step, field)
+ * after every converged step with the field (6 x 3 n_cells doubles, the layout below) on the
+ * host.  fn NULL clears it. */
+typedef void (*sfv_step_callback)(void* user, int step, const double* field);
+int sfv_set_step_callback(sfv_ctx* ctx, sfv_step_callback fn, void* user);
 /* field_dev: 6 consecutive device arrays of 3*n_cells doubles:
  * u, u_old, u_old_old, v_old, v_old_old, a_old (VectorField, fields.hpp:29-42) */
 int sfv_run_steps(sfv_ctx* ctx, double* field_dev, const sfv_solver_cfg* cfg, int n_steps,

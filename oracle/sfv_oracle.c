@@ -1489,6 +1489,23 @@ int orc_precond_apply(orc_case* h, const double* r, double* z) {
 /* ------------------------------------------------------------------ GMRES */
 
 static double ddot(const double* a, const double* b, int n) { /* std::inner_product */
+    /* ORC_DOT_BLOCK=k (experiments only, scripts/order_sensitivity.py): sequential sums of k
+       consecutive products, then of the block sums — another valid evaluation order */
+    static int blk = -1;
+    if (blk < 0) {
+        const char* e = getenv("ORC_DOT_BLOCK");
+        blk = e ? atoi(e) : 0;
+    }
+    if (blk > 0) {
+        double t = 0.0;
+        for (int i0 = 0; i0 < n; i0 += blk) {
+            double s = 0.0;
+            const int i1 = i0 + blk < n ? i0 + blk : n;
+            for (int i = i0; i < i1; ++i) s = s + a[i] * b[i];
+            t = t + s;
+        }
+        return t;
+    }
     double s = 0.0;
     for (int i = 0; i < n; ++i) s = s + a[i] * b[i];
     return s;

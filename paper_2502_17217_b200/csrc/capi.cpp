@@ -171,6 +171,10 @@ struct sfv_ctx {
     std::vector<double> face_bc_host;
     sfv_bc_sampler bc_sampler = nullptr;
     void* bc_user = nullptr;
+    // run_steps' StepCallback (nonlinear.hpp:106-107): the field on the host after every step
+    sfv_step_callback step_fn = nullptr;
+    void* step_user = nullptr;
+    std::vector<double> step_field;
     FusedLayout fl;
     DevBuf<int> f_tfp, f_own, f_oth, f_slots, f_index, f_flags, f_ticket;
     DevBuf<double> f_geo, f_gring, f_fring;
@@ -2123,6 +2127,18 @@ int sfv_check_errors(sfv_ctx* c, int* cell) {
     return e;
 }
 
+int sfv_jfnk_solve_host(sfv_ctx* c, double* u, const sfv_solver_cfg* cfg, sfv_solve_report* rep) {
+    const size_t bytes = sizeof(double) * c->n;
+    double* d = nullptr;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
+    cudaMemcpyAsync(d, u, bytes, cudaMemcpyHostToDevice, c->stream);
+    const int e = jfnk(c, d, cfg, rep);
+    cudaMemcpyAsync(u, d, bytes, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(d);
+    return e;
+}
+
 int sfv_residual_host(sfv_ctx* c, const double* u, double* r, int* cell) {
     const size_t bytes = sizeof(double) * c->n;
     if (!ensure_krylov(c, 1)) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
@@ -2174,6 +2190,22 @@ int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v,
 }
 
 int sfv_precond_create(sfv_ctx* c, int kind) { return precond_create(c, kind); }
+
+int sfv_set_step_callback(sfv_ctx* c, sfv_step_callback fn, void* user) {
+    c->step_fn = fn;
+    c->step_user = user;
+    return SFV_OK;
+}
+
+int sfv_precond_apply_host(sfv_ctx* c, const double* r, double* z) {
+    const size_t bytes = sizeof(double) * c->n;
+    if (!ensure_krylov(c, 1)) return c->fail(SFV_ERR_CUDA, -1, "out of device memory");
+    cudaMemcpyAsync(c->tv.p, r, bytes, cudaMemcpyHostToDevice, c->stream);
+    if (int e = precond_apply_async(c, c->tv.p, c->wv.p)) return e;
+    cudaMemcpyAsync(z, c->wv.p, bytes, cudaMemcpyDeviceToHost, c->stream);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->cuda_check("precond_apply");
+    return SFV_OK;
+}
 
 int sfv_line_search(sfv_ctx* c, const double* u, const double* du, double r_norm0, int* success, double* s,
                     double* r_norm, double* residual) {
@@ -2301,6 +2333,12 @@ int sfv_run_steps(sfv_ctx* c, double* field, const sfv_solver_cfg* cfg, int n_st
             cudaMemcpyAsync(fuo, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
         }
         cudaMemcpyAsync(fu, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream);
+        if (c->step_fn) {  // on_step(step, field) (nonlinear.cpp:442)
+            c->step_field.resize(6 * static_cast<size_t>(n));
+            cudaMemcpyAsync(c->step_field.data(), field, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, c->stream);
+            if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->cuda_check("run_steps");
+            c->step_fn(c->step_user, step, c->step_field.data());
+        }
     }
     if (*n_reports > cap) *n_reports = cap;
     if (transient) sfv_set_history(c, c->dzero.p, c->dzero.p, c->dzero.p, c->dzero.p);
