@@ -357,9 +357,15 @@ int ilu_ring_window();
 
 // ---- precond_stream.cu: streamed sweep (default; records built by build_stream_records)
 constexpr int kStreamMode = 200;
-constexpr int kStreamCluster = 16;
+#ifndef SFV_STREAM_CLUSTER
+#define SFV_STREAM_CLUSTER 16
+#endif
+#ifndef SFV_STREAM_MAX_ROWS
+#define SFV_STREAM_MAX_ROWS 256
+#endif
+constexpr int kStreamCluster = SFV_STREAM_CLUSTER;
 constexpr int kStreamRing = 3072;    // 32-byte value slots per CTA
-constexpr int kStreamMaxRows = 256;  // positions per CTA per level
+constexpr int kStreamMaxRows = SFV_STREAM_MAX_ROWS;  // positions per CTA per level
 struct DevStream {
     int n_levels = 0;
     const int* level_ptr = nullptr;  // position-space level boundaries (same as DevTri)

@@ -38,11 +38,17 @@ namespace cg = cooperative_groups;
 #define SFV_TS_PROBE 0
 #endif
 #define TSP(b) (!(SFV_TS_PROBE & (b)))
+#ifndef SFV_DIV_CORR
+#define SFV_DIV_CORR 1  // 0: plain division in the U sweep
+#endif
 
 namespace sfv {
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef SFV_STREAM_THREADS
+#define SFV_STREAM_THREADS 256
+#endif
+constexpr int kThreads = SFV_STREAM_THREADS;
 constexpr int kLvl = 1024;
 
 // field offsets inside a 3072-byte chunk of 32 records (precond_host.h: pack_stream_chunks)
@@ -160,6 +166,13 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 const int ln = j % 32;
                 const double* rval = reinterpret_cast<const double*>(ch) + ln;  // [q * 32]
                 const unsigned short* rdep = reinterpret_cast<const unsigned short*>(ch + kOffDep) + ln;  // [q * 32]
+                // U: the pivot's reciprocal is computed while the dependencies are in flight, and
+                // z / dg is finished after them by one correction step (SFV_DIV_CORR, below)
+                double dg = 1.0, rdg = 1.0;
+                if (UPPER) {
+                    dg = reinterpret_cast<const double*>(ch + kOffDiag)[ln];
+                    if (SFV_DIV_CORR) rdg = 1.0 / dg;
+                }
                 unsigned short dep[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) dep[q] = rdep[q * 32];
@@ -191,9 +204,19 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
 #pragma unroll
                     for (int k = 0; k < NRHS; ++k) z[k] -= vq[q] * dv[q][k];
                 if (UPPER) {
-                    const double dg = reinterpret_cast<const double*>(ch + kOffDiag)[ln];
 #pragma unroll
-                    for (int k = 0; k < NRHS; ++k) z[k] /= dg;
+                    for (int k = 0; k < NRHS; ++k) {
+                        if (SFV_DIV_CORR) {
+                            // Markstein's correction: with rdg = RN(1 / dg) and q0 = RN(z rdg),
+                            // the residual e = z - q0 dg is exact (fma) and RN(q0 + e rdg) is
+                            // RN(z / dg) — the same bits as the division, off its latency
+                            const double q0 = z[k] * rdg;
+                            const double e = __fma_rn(-q0, dg, z[k]);
+                            z[k] = __fma_rn(e, rdg, q0);
+                        } else {
+                            z[k] /= dg;
+                        }
+                    }
                 }
                 const int own = reinterpret_cast<const unsigned short*>(ch + kOffOwn)[ln];
 #pragma unroll

@@ -232,3 +232,46 @@ def test_hypot_matches_the_reference_libm():
     b[n // 3: n // 2] = a[n // 3: n // 2] * 10.0 ** rng.uniform(-9, -3, n // 2 - n // 3)
     bad = sum(libm.hypot(float(x), float(y)) != _hypot_restated(float(x), float(y)) for x, y in zip(a, b))
     assert bad == 0
+
+
+def test_division_correction_is_the_division(tmp_path):
+    """The U sweep (precond_stream.cu) replaces z / d by q0 = z * RN(1/d), e = fma(-q0, d, z),
+    RN(q0 + e * RN(1/d)) — Markstein's correction, which returns the correctly rounded
+    quotient.  Checked here against IEEE division on 2e7 random pairs over 120 binades,
+    a quarter of them with divisor mantissas next to all-ones."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    src = tmp_path / "mk.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include <stdint.h>
+#include <string.h>
+#include <math.h>
+static uint64_t s = 88172645463325252ULL;
+static uint64_t xr(void) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; return s; }
+static double rnd(int e0, int e1) {
+    uint64_t m = xr() & ((1ULL << 52) - 1);
+    int e = e0 + (int)(xr() % (uint64_t)(e1 - e0));
+    uint64_t b = ((uint64_t)(e + 1023) << 52) | m;
+    double d;
+    memcpy(&d, &b, 8);
+    return (xr() & 1) ? -d : d;
+}
+int main(void) {
+    long bad = 0;
+    for (long i = 0; i < 20000000; ++i) {
+        double a = rnd(-60, 60), b = rnd(-60, 60);
+        if (i % 4 == 0) { uint64_t bb; memcpy(&bb, &b, 8); bb |= ((1ULL << 52) - 1) ^ (xr() & 0xff); memcpy(&b, &bb, 8); }
+        double r = 1.0 / b, q0 = a * r, e = fma(-q0, b, a), q = fma(e, r, q0);
+        bad += q != a / b;
+    }
+    printf("%ld\n", bad);
+    return 0;
+}
+''')
+    exe = tmp_path / "mk"
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-o", str(exe), str(src), "-lm"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.strip()
+    assert out == "0"
