@@ -62,10 +62,17 @@ void sfv_destroy(sfv_ctx* ctx);
 int sfv_set_stream(sfv_ctx* ctx, void* cuda_stream);
 int sfv_n_cells(const sfv_ctx* ctx);
 const char* sfv_last_error(const sfv_ctx* ctx);
-/* Execution switches (no effect on the arithmetic of any result):
+/* Execution switches:
  *   "gmres_graph" 1 (default) / 0: run each GMRES restart cycle as one CUDA graph whose
  *   WHILE node holds the Arnoldi steps (J.v, preconditioner, MGS, Givens) on the device,
  *   or drive the steps from the host.  Both give bit-identical iterates.
+ *   "sequential_reductions" 0 (default) / 1 (also SFV_SEQ_REDUCE=1): sum every inner product
+ *   and norm of the solve (the J.v's |u| and |v|, MGS, GMRES and Newton norms) left to right
+ *   from 0.0, as std::inner_product does in the reference (linalg.cpp:18-22,
+ *   nonlinear.cpp:13-24), instead of a fixed-order parallel tree.  With every other step
+ *   already bit-identical, a JFNK solve with an ILU(k) preconditioner then reproduces the
+ *   reference's run bit for bit (residual histories, Krylov counts, field).  ~13 ms per
+ *   3M-term sum: a reproducibility / verification mode, not the fast path.
  * Returns SFV_ERR_INVALID_ARGUMENT for an unknown name. */
 int sfv_set_option(sfv_ctx* ctx, const char* name, int value);
 /* number of device kernels this context has launched so far */

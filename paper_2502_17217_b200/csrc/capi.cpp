@@ -197,6 +197,13 @@ struct sfv_ctx {
     long long g_launches = 0;  // kernels per Arnoldi step in the graph
     bool graph_broken = false;
     bool graph_off = false;  // sfv_set_option("gmres_graph", 0)
+    // sfv_set_option("sequential_reductions", 1) / SFV_SEQ_REDUCE=1: every inner product and
+    // norm summed left to right as the reference does (launch_seq_dot), so the Krylov and Newton
+    // decisions are bit-identical to the CPU reference's; ~13 ms per 3M-term sum
+    bool seq_reduce = [] {
+        const char* e = std::getenv("SFV_SEQ_REDUCE");
+        return e && std::atoi(e) != 0;
+    }();
     bool vsel_failed = false;
     long long launches = 0;
     SfvError last{0, -1, ""};
@@ -601,8 +608,21 @@ void residual_async(sfv_ctx* c, const double* u, double* r) {
     residual_pass(c, c->ph, u, nullptr, nullptr, nullptr, r);
 }
 
+// *out = a.b on the device: a fixed-order tree, or the reference's left-to-right chain
+void dot_async(sfv_ctx* c, const double* a, const double* b, int n, double* out) {
+    if (c->seq_reduce) launch_seq_dot(a, b, n, out, c->stream);
+    else launch_dot(a, b, n, out, c->red.p, c->counter.p, c->stream);
+}
+
 // J.v (async).  u_norm_cached: *scal[1] already holds |u| for this u.
 void jv_async(sfv_ctx* c, const double* u, const double* r_u, const double* v, double* out, bool u_norm_cached) {
+    if (c->seq_reduce) {  // reference-order |v|, |u| and ε (nonlinear.cpp:109-115), then w = u + εv
+        launch_seq_eps(u, v, c->n, c->red.p, c->scal.p, c->scal.p + 1, u_norm_cached, c->stream);
+        c->ps.partials = nullptr;
+        residual_pass(c, c->ph, u, v, c->scal.p, r_u, out);
+        c->launches += 2;
+        return;
+    }
     if (c->jv_path == 0) {  // norms as block partials; eps finished inside the perturb pass
         if (!c->ps.bar) {
             c->ps.npart = launch_norm_partials(u, v, c->n, c->red.p, u_norm_cached, c->stream);
@@ -631,7 +651,7 @@ int residual_sync(sfv_ctx* c, const double* u, double* r) {
 
 // squared-norm on the device, returned on the host (one sync)
 int norm_host(sfv_ctx* c, const double* a, double* out) {
-    launch_dot(a, a, c->n, c->hdev.p, c->red.p, c->counter.p, c->stream);
+    dot_async(c, a, a, c->n, c->hdev.p);
     c->launches += 1;
     if (int e = fetch(c, 1)) return e;
     *out = std::sqrt(c->st->h[0]);
@@ -863,7 +883,7 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
         }
         if (!right)
             if (int e = precond_apply_async(c, tmp, r)) return e;
-        launch_dot(r, r, n, c->hdev.p, c->red.p, c->counter.p, c->stream);
+        dot_async(c, r, r, n, c->hdev.p);
         ++c->launches;
         if (int e = fetch(c, 1)) return e;
         if (!zero)
@@ -916,7 +936,7 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
         const char* e = std::getenv("SFV_FUSED_MGS");
         return e && std::atoi(e) == 0;
     }();
-    const bool use_graph = !right && gmres_graph_ready(c, u, r_u, restart);
+    const bool use_graph = !right && !c->seq_reduce && gmres_graph_ready(c, u, r_u, restart);
     while (total < max_iters) {
         const double cycle_start = beta;
         launch_scale_div_host(r, beta, V, n, c->stream);  // v0 = r / beta
@@ -955,19 +975,23 @@ int gmres(sfv_ctx* c, const double* u, const double* r_u, const double* b, doubl
             // modified Gram-Schmidt (linalg.cpp:469-473).  Fused: one cooperative launch with
             // w in shared memory, also writing v_{j+1} = w / |w|.  Otherwise h_0 = w.v_0, then
             // w -= h_i v_i fused with h_{i+1} = w.v_{i+1}; the last pass yields w.w
-            bool fused = !no_fused_mgs &&
+            bool fused = !no_fused_mgs && !c->seq_reduce &&
                          launch_arnoldi_fused(w, V, n, j, c->hdev.p, c->red.p,
                                               j + 1 < restart + 1 ? V + static_cast<size_t>(j + 1) * n : nullptr,
                                               c->stream);
             if (fused) {
                 ++c->launches;
             } else {
-                launch_dot(w, V, n, c->hdev.p, c->red.p, c->counter.p, c->stream);
+                dot_async(c, w, V, n, c->hdev.p);
                 ++c->launches;
                 for (int i = 0; i <= j; ++i) {
                     const double* vnext = i < j ? V + static_cast<size_t>(i + 1) * n : nullptr;
-                    launch_axpy_dot(w, V + static_cast<size_t>(i) * n, c->hdev.p + i, vnext, n, c->hdev.p + i + 1,
-                                    c->red.p, c->counter.p, c->stream);
+                    if (c->seq_reduce)
+                        launch_seq_axpy_dot(w, V + static_cast<size_t>(i) * n, c->hdev.p + i, vnext, n,
+                                            c->hdev.p + i + 1, c->stream);
+                    else
+                        launch_axpy_dot(w, V + static_cast<size_t>(i) * n, c->hdev.p + i, vnext, n,
+                                        c->hdev.p + i + 1, c->red.p, c->counter.p, c->stream);
                     ++c->launches;
                 }
             }
@@ -1107,7 +1131,7 @@ int seg_create(sfv_ctx* c) {
 
 // dot product of two device vectors of length n, on the host (fixed-order reduction, one sync)
 int dot_host(sfv_ctx* c, const double* a, const double* b, int n, double* out) {
-    launch_dot(a, b, n, c->hdev.p, c->red.p, c->counter.p, c->stream);
+    dot_async(c, a, b, n, c->hdev.p);
     c->launches += 1;
     if (int e = fetch(c, 1)) return e;
     *out = c->st->h[0];
@@ -1829,6 +1853,11 @@ int sfv_set_stream(sfv_ctx* c, void* s) {
 }
 
 int sfv_set_option(sfv_ctx* c, const char* name, int value) {
+    if (name && std::strcmp(name, "sequential_reductions") == 0) {
+        c->seq_reduce = value != 0;
+        c->drop_graph();
+        return SFV_OK;
+    }
     if (name && std::strcmp(name, "gmres_graph") == 0) {
         c->graph_off = value == 0;
         c->drop_graph();

@@ -283,6 +283,15 @@ void launch_dot(const double* a, const double* b, int n, double* out, double* sc
 // w -= (*h) * vi ; then *out = dot(w, vnext) (vnext == nullptr: *out = dot(w, w))
 void launch_axpy_dot(double* w, const double* vi, const double* h, const double* vnext, int n, double* out,
                      double* scratch, unsigned* counter, cudaStream_t s);
+// Reference-order sums (opt-in "sequential_reductions"): the left-to-right chain of
+// std::inner_product, one CTA, ~13 ms per 3M terms.  seq_axpy_dot: w -= (*h) vi, then the
+// chain of w.vnext (or w.w).  seq_eps: sums[0] = v.v, sums[1] = u.u (unless cached), then
+// eps_out = the reference's ε and u_norm = |u|.
+void launch_seq_dot(const double* a, const double* b, int n, double* out, cudaStream_t s);
+void launch_seq_axpy_dot(double* w, const double* vi, const double* h, const double* vnext, int n, double* out,
+                         cudaStream_t s);
+void launch_seq_eps(const double* u, const double* v, int n, double* sums, double* eps_out, double* u_norm,
+                    bool cached, cudaStream_t s);
 // Fused Arnoldi step (cooperative, w held in shared memory): h[0..j] = MGS projections of
 // w on V[0..j], h[j+1] = w.w after them, vnext (if not null) = w / sqrt(h[j+1]).  partial:
 // 2 * SMs doubles.  Returns false (nothing launched) when w does not fit on chip.

@@ -6,6 +6,8 @@
 // Newton/stepping vector updates of nonlinear.cpp.  Every reduction is a fixed-order
 // two-level tree (block partials, then one last block in block order), so results are
 // run-to-run deterministic; the scalar h_i never leaves the device between passes.
+#include <cfloat>
+
 #include <cooperative_groups.h>
 
 #include "device.h"
@@ -103,6 +105,90 @@ __global__ void __launch_bounds__(kT) axpy_dot_kernel(double* __restrict__ w, co
     }
     const double part = block_sum(acc, sh);
     if (publish_partial(part, partial, counter)) finish_sum(partial, counter, out, sh);
+}
+
+// ---------------------------------------------------------------- reference-order sums
+// The reference sums every inner product left to right from 0.0 (std::inner_product,
+// linalg.cpp:18-22; vec_norm / field_norm, nonlinear.cpp:13-24): s = RN(s + RN(a_i b_i)).
+// That chain cannot be re-associated without changing the bits, so these kernels run it as
+// the chain it is: one CTA, warps 1.. form the products of the next chunk in shared memory
+// while thread 0 adds the current chunk in index order (one dependent DADD per term, ~13 ms
+// per 3M-term sum on B200).  Two sums may share the launch (two independent chains
+// interleaved in thread 0: the J.v's |v| and |u|).  Opt-in (sfv_set_option
+// "sequential_reductions"): it makes every Krylov and Newton decision bit-identical to the
+// CPU reference's, at full size, where a parallel tree differs in the last bits.
+constexpr int kSeqT = 512;
+constexpr int kSeqChunk = 1024;  // 2 stages x 2 sums x 8 KB of static shared memory
+
+__global__ void __launch_bounds__(kSeqT, 1) seq_dot2_kernel(const double* __restrict__ a1, const double* __restrict__ b1,
+                                                          const double* __restrict__ a2, const double* __restrict__ b2,
+                                                          int n, double* __restrict__ out1, double* __restrict__ out2) {
+    __shared__ double buf[2][2][kSeqChunk];  // [stage][sum][term]
+    const bool two = a2 != nullptr;
+    const int nch = (n + kSeqChunk - 1) / kSeqChunk;
+    auto produce = [&](int k, int t0, int nt) {
+        const int base = k * kSeqChunk;
+        const int m = min(kSeqChunk, n - base);
+        double* p1 = buf[k & 1][0];
+        double* p2 = buf[k & 1][1];
+        for (int i = t0; i < m; i += nt) {
+            p1[i] = __dmul_rn(a1[base + i], b1[base + i]);
+            if (two) p2[i] = __dmul_rn(a2[base + i], b2[base + i]);
+        }
+    };
+    if (nch > 0) produce(0, threadIdx.x, kSeqT);
+    __syncthreads();
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < nch; ++k) {
+        if (threadIdx.x == 0) {
+            const int m = min(kSeqChunk, n - k * kSeqChunk);
+            const double* p1 = buf[k & 1][0];
+            const double* p2 = buf[k & 1][1];
+            int i = 0;
+            for (; i + 8 <= m; i += 8) {
+                double x[8], y[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    x[q] = p1[i + q];
+                    y[q] = two ? p2[i + q] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    s1 = __dadd_rn(s1, x[q]);
+                    if (two) s2 = __dadd_rn(s2, y[q]);
+                }
+            }
+            for (; i < m; ++i) {
+                s1 = __dadd_rn(s1, p1[i]);
+                if (two) s2 = __dadd_rn(s2, p2[i]);
+            }
+        } else if (threadIdx.x >= 32 && k + 1 < nch) {
+            produce(k + 1, threadIdx.x - 32, kSeqT - 32);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *out1 = s1;
+        if (two) *out2 = s2;
+    }
+}
+
+// ε of jacobian_vector_product (nonlinear.cpp:109-115) from reference-order |v| and |u|:
+// eps_out[0] = ε (0 when |v| = 0), u_norm = |u| (read instead when cached)
+__global__ void seq_eps_finish_kernel(const double* __restrict__ sums, double* __restrict__ eps_out,
+                                      double* __restrict__ u_norm, bool cached) {
+    const double vn = sqrt(sums[0]);
+    const double un = cached ? *u_norm : sqrt(sums[1]);
+    *eps_out = vn == 0.0 ? 0.0 : sqrt(DBL_EPSILON) * sqrt(1.0 + un) / vn;
+    if (!cached) *u_norm = un;
+}
+
+// w += (-h) v  (axpy(-h_i, v_i, w), linalg.cpp:471), h on the device
+__global__ void axpy_neg_dev_kernel(double* __restrict__ w, const double* __restrict__ vi, const double* __restrict__ h,
+                                    int n) {
+    const double hi = *h;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        w[i] = w[i] + (-hi) * vi[i];
 }
 
 __global__ void scale_div_kernel(const double* __restrict__ in, const double* __restrict__ d, double dh,
@@ -326,6 +412,22 @@ void launch_dot(const double* a, const double* b, int n, double* out, double* sc
 void launch_axpy_dot(double* w, const double* vi, const double* h, const double* vnext, int n, double* out,
                      double* scratch, unsigned* counter, cudaStream_t s) {
     axpy_dot_kernel<<<reduce_blocks(n), kT, 0, s>>>(w, vi, h, vnext, n, out, scratch, counter);
+}
+
+void launch_seq_dot(const double* a, const double* b, int n, double* out, cudaStream_t s) {
+    seq_dot2_kernel<<<1, kSeqT, 0, s>>>(a, b, nullptr, nullptr, n, out, nullptr);
+}
+
+void launch_seq_axpy_dot(double* w, const double* vi, const double* h, const double* vnext, int n, double* out,
+                         cudaStream_t s) {
+    axpy_neg_dev_kernel<<<grid_for(n), 256, 0, s>>>(w, vi, h, n);
+    seq_dot2_kernel<<<1, kSeqT, 0, s>>>(w, vnext ? vnext : w, nullptr, nullptr, n, out, nullptr);
+}
+
+void launch_seq_eps(const double* u, const double* v, int n, double* sums, double* eps_out, double* u_norm,
+                    bool cached, cudaStream_t s) {
+    seq_dot2_kernel<<<1, kSeqT, 0, s>>>(v, v, cached ? nullptr : u, cached ? nullptr : u, n, sums, sums + 1);
+    seq_eps_finish_kernel<<<1, 1, 0, s>>>(sums, eps_out, u_norm, cached);
 }
 
 int arnoldi_fused_grid(int n, int* chunk_out) {

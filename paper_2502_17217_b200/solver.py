@@ -227,7 +227,7 @@ class ResidualEvaluator:
 
     # -- reference API
     def set_option(self, name: str, value: int):
-        """Execution switches (sfv_set_option): "gmres_graph" 1/0."""
+        """Execution switches (sfv_set_option): "gmres_graph" 1/0, "sequential_reductions" 0/1."""
         self._check(self.L.sfv_set_option(self.h, name.encode(), int(value)))
 
     def set_time(self, t: float):
