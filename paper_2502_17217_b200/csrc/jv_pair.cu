@@ -314,7 +314,9 @@ int eps_perturb_grid(int nc) {
 // J2: the stress is the radial return from the cell's committed state (J2PlasticLaw::stress,
 // laws.cpp:201-212); with ph.commit set the trial state replaces it (ResidualEvaluator::commit,
 // discretisation.cpp:91-95 — each cell reads and writes only its own record).
-template <int S, bool GEN, bool J2 = false>
+// HOIST: the least-squares vectors (the largest stream, independent of the predecessor) are
+// loaded before griddepcontrol.wait, together with the slot indices.
+template <int S, bool GEN, bool J2 = false, bool HOIST = false>
 __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt, Physics ph, double* __restrict__ wg,
                                                         double* __restrict__ sig, double* __restrict__ lawst,
                                                         ErrWords* __restrict__ err) {
@@ -326,6 +328,12 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
     int o[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) o[s] = __ldcs(ts + 32 * (S + s));  // padding slots hold -1
+    d3 lsv[HOIST ? S : 1];
+    if constexpr (HOIST) {
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            lsv[s] = {__ldcs(tl + 32 * (3 * s)), __ldcs(tl + 32 * (3 * s + 1)), __ldcs(tl + 32 * (3 * s + 2))};
+    }
     wait_predecessor();  // w
     double* rc = wg + tiled(c, kWG);
     const d3 wc = ld3(rc);
@@ -346,7 +354,9 @@ __global__ void __launch_bounds__(256) grad_cell_kernel(DevMesh m, PatchTable pt
         } else {
             continue;  // traction / displacement faces are not in the stencil; padding
         }
-        const d3 ls = {__ldcs(tl + 32 * (3 * s)), __ldcs(tl + 32 * (3 * s + 1)), __ldcs(tl + 32 * (3 * s + 2))};
+        d3 ls;
+        if constexpr (HOIST) ls = lsv[s];
+        else ls = {__ldcs(tl + 32 * (3 * s)), __ldcs(tl + 32 * (3 * s + 1)), __ldcs(tl + 32 * (3 * s + 2))};
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -738,6 +748,14 @@ bool launch_eps_perturb(void (*kern)(KArgs...), int grid, cudaStream_t st, Args.
     return false;
 }
 
+bool grad_hoist() {
+    static const bool v = [] {
+        const char* e = std::getenv("SFV_GRAD_HOIST");
+        return e && std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 template <int S>
 void launch_grad(const DevMesh& m, const Physics& ph, const PatchTable& pt, const PairScratch& ps, ErrWords* err,
                  cudaStream_t st) {
@@ -746,6 +764,8 @@ void launch_grad(const DevMesh& m, const Physics& ph, const PatchTable& pt, cons
     if (ph.law == SFV_LAW_J2)
         launch_win(grad_cell_kernel<S, true, true>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, ps.lawst, err);
     else if (gen) launch_win(grad_cell_kernel<S, true>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, ps.lawst, err);
+    else if (grad_hoist())
+        launch_win(grad_cell_kernel<S, false, false, true>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, ps.lawst, err);
     else launch_win(grad_cell_kernel<S, false>, cb, 256, st, ps, m, pt, ph, ps.wg, ps.sig, ps.lawst, err);
 }
 
