@@ -80,80 +80,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
         : "memory");
 }
 
-// one position's row held in registers (the prefetching schedule)
-template <int NRHS>
-struct Row {
-    int a = 0, n = 0;  // the level slice: first position, count
-    unsigned short dep[8];
-    unsigned short own;
-    double vq[8];
-    double dg, rdg;
-    double z[NRHS];
-};
-template <bool UPPER, int NRHS>
-__device__ __forceinline__ void fill_row(Row<NRHS>& R, const unsigned char* stage_rec, const double* stage_src, int j,
-                                         int comp) {
-    const unsigned char* ch = stage_rec + (j / 32) * kChunk;
-    const int ln = j % 32;
-    const double* rval = reinterpret_cast<const double*>(ch) + ln;
-    const unsigned short* rdep = reinterpret_cast<const unsigned short*>(ch + kOffDep) + ln;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) R.dep[q] = rdep[q * 32];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) R.vq[q] = rval[q * 32];
-    R.dg = 1.0;
-    R.rdg = 1.0;
-    if (UPPER) {
-        R.dg = reinterpret_cast<const double*>(ch + kOffDiag)[ln];
-        R.rdg = 1.0 / R.dg;
-    }
-#pragma unroll
-    for (int k = 0; k < NRHS; ++k) R.z[k] = stage_src[j * 3 + comp + k];
-    R.own = reinterpret_cast<const unsigned short*>(ch + kOffOwn)[ln];
-}
-// the dependent half: DSMEM loads, the reference's subtraction order, the pivot, the stores
-template <bool UPPER, int NRHS>
-__device__ __forceinline__ void finish_row(const Row<NRHS>& R, double* ring, int ring_n, uint32_t ring_base,
-                                           uint32_t zero_addr, int rank, double* __restrict__ dst, int j, int comp) {
-    double dv[8][NRHS];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const unsigned d = R.dep[q];
-        const uint32_t ad = d != 0xffffu ? mapa(ring_base + (d & 0xfffu) * 8u, static_cast<int>(d >> 12)) : zero_addr;
-#pragma unroll
-        for (int k = 0; k < NRHS; ++k)
-            asm("ld.shared::cluster.f64 %0, [%1];"
-                : "=d"(dv[q][k])
-                : "r"(ad + (d != 0xffffu ? static_cast<uint32_t>(k * ring_n * 8) : 0u))
-                : "memory");
-    }
-    double z[NRHS];
-#pragma unroll
-    for (int k = 0; k < NRHS; ++k) z[k] = R.z[k];
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-#pragma unroll
-        for (int k = 0; k < NRHS; ++k) z[k] -= R.vq[q] * dv[q][k];
-    if (UPPER) {
-#pragma unroll
-        for (int k = 0; k < NRHS; ++k) {
-            const double q0 = z[k] * R.rdg;
-            const double e = __fma_rn(-q0, R.dg, z[k]);
-            z[k] = __fma_rn(e, R.rdg, q0);
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < NRHS; ++k) {
-        ring[k * ring_n + R.own] = z[k];
-        dst[3 * static_cast<size_t>(R.a + j) + comp + k] = z[k];
-    }
-}
-
 // kThreads compute threads + one producer warp whose lane 0 streams the records kStages - 1
 // levels ahead: a CTA's slice of a level is contiguous in position space, so it is two TMA
 // bulk copies (records, right-hand side) completing on the stage's mbarrier (expect_tx).
 // The per-level critical path is: wait stage -> rows -> cluster barrier.
-template <bool UPPER, int NRHS, int kStages, bool PF>
+template <bool UPPER, int NRHS, int kStages>
 __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet set, const double* __restrict__ src,
                                                                       double* __restrict__ dst) {
     const int kMaxRows = set.max_rows;  // rows per CTA per level (stage stride)
@@ -214,148 +145,104 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     (void)ph;
     (void)t0;
     (void)t1;
-    if constexpr (PF) {
-        // Prefetching schedule: a compute thread's first row of level l + 1 (dependency
-        // addresses, factor values, pivot, right-hand side — nothing that depends on level l)
-        // is loaded into registers between the cluster arrive and wait of level l, so after
-        // the wait only the dependency loads, the FP64 chain and the stores remain.
-        Row<NRHS> cur, nxt;
-        auto load_row = [&](int l, Row<NRHS>& R) {
-            R.n = 0;
-            if (l >= t.n_levels) return;
-            int a, b;
-            slice(l, a, b);
-            R.a = a;
-            R.n = b - a;
-            if (threadIdx.x >= R.n) return;
+    for (int l = 0; l < t.n_levels; ++l) {
+        if (!TSP(32)) t0 = clock64();
+        if (l + kStages - 1 + 1 - lbase > kLvl) stage_levels(l);  // keep lp[] covering the issue window
+        if (producer) {
+            // stage (l - 1) % kStages was consumed before the barrier that ended level l - 1
+            issue(l + kStages - 1);
+        } else {
             mbar_wait(mbar_base + 8u * (l % kStages), static_cast<uint32_t>((l / kStages) & 1));
-            fill_row<UPPER, NRHS>(R, stage_rec + static_cast<size_t>(l % kStages) * kMaxRows * 96,
-                                  stage_src + (l % kStages) * kMaxRows * 3, threadIdx.x, comp);
-        };
-        if (!producer) load_row(0, cur);
-        for (int l = 0; l < t.n_levels; ++l) {
-            if (l + kStages - 1 + 1 - lbase > kLvl) stage_levels(l);
-            if (producer) {
-                issue(l + kStages - 1);
-            } else {
-                const int s = l % kStages;
-                if (threadIdx.x < cur.n)
-                    finish_row<UPPER, NRHS>(cur, ring, ring_n, ring_base, zero_addr, rank, dst, threadIdx.x, comp);
-                // the rare rows beyond kThreads: the plain path
-                for (int j = threadIdx.x + kThreads; j < cur.n; j += kThreads) {
-                    Row<NRHS> R;
-                    R.a = cur.a;
-                    fill_row<UPPER, NRHS>(R, stage_rec + static_cast<size_t>(s) * kMaxRows * 96,
-                                          stage_src + s * kMaxRows * 3, j, comp);
-                    finish_row<UPPER, NRHS>(R, ring, ring_n, ring_base, zero_addr, rank, dst, j, comp);
-                }
-                asm volatile("fence.acq_rel.cta;" ::: "memory");
-            }
-            asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-            if (!producer) load_row(l + 1, nxt);
-            asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-            cur = nxt;
-        }
-    } else {
-        for (int l = 0; l < t.n_levels; ++l) {
-            if (!TSP(32)) t0 = clock64();
-            if (l + kStages - 1 + 1 - lbase > kLvl) stage_levels(l);  // keep lp[] covering the issue window
-            if (producer) {
-                // stage (l - 1) % kStages was consumed before the barrier that ended level l - 1
-                issue(l + kStages - 1);
-            } else {
-                mbar_wait(mbar_base + 8u * (l % kStages), static_cast<uint32_t>((l / kStages) & 1));
-                if (!TSP(32)) {
-                    t1 = clock64();
-                    ph[1] += t1 - t0;
-                    t0 = t1;
-                }
-                int a, b;
-                slice(l, a, b);
-                const int s = l % kStages;
-                for (int j = threadIdx.x; TSP(16) && j < b - a; j += kThreads) {
-                    const unsigned char* ch = stage_rec + static_cast<size_t>(s) * kMaxRows * 96 + (j / 32) * kChunk;
-                    const int ln = j % 32;
-                    const double* rval = reinterpret_cast<const double*>(ch) + ln;  // [q * 32]
-                    const unsigned short* rdep = reinterpret_cast<const unsigned short*>(ch + kOffDep) + ln;  // [q * 32]
-                    // U: the pivot's reciprocal is computed while the dependencies are in flight, and
-                    // z / dg is finished after them by one correction step (SFV_DIV_CORR, below)
-                    double dg = 1.0, rdg = 1.0;
-                    if (UPPER) {
-                        dg = reinterpret_cast<const double*>(ch + kOffDiag)[ln];
-                        if (SFV_DIV_CORR) rdg = 1.0 / dg;
-                    }
-                    unsigned short dep[8];
-    #pragma unroll
-                    for (int q = 0; q < 8; ++q) dep[q] = rdep[q * 32];
-                    double z[NRHS];
-    #pragma unroll
-                    for (int k = 0; k < NRHS; ++k) z[k] = stage_src[(s * kMaxRows + j) * 3 + comp + k];
-                    // Branch-free: an absent dependency (0xffff) reads a zero slot with factor value
-                    // 0, and z - 0*0 is z bit for bit (also for -0, inf, NaN), as the reference's
-                    // skipping it.  Every dependency load is issued before the first use.
-                    double dv[8][NRHS];
-    #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const unsigned d = dep[q];
-                        const uint32_t ad = d != 0xffffu && TSP(8)
-                                                ? mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank)
-                                                : zero_addr;
-    #pragma unroll
-                        for (int k = 0; k < NRHS; ++k)
-                            asm("ld.shared::cluster.f64 %0, [%1];"
-                                : "=d"(dv[q][k])
-                                : "r"(ad + (d != 0xffffu ? static_cast<uint32_t>(k * ring_n * 8) : 0u))
-                                : "memory");
-                    }
-                    double vq[8];
-    #pragma unroll
-                    for (int q = 0; q < 8; ++q) vq[q] = rval[q * 32];
-    #pragma unroll
-                    for (int q = 0; q < 8; ++q)  // the reference's order of subtraction
-    #pragma unroll
-                        for (int k = 0; k < NRHS; ++k) z[k] -= vq[q] * dv[q][k];
-                    if (UPPER) {
-    #pragma unroll
-                        for (int k = 0; k < NRHS; ++k) {
-                            if (SFV_DIV_CORR) {
-                                // Markstein's correction: with rdg = RN(1 / dg) and q0 = RN(z rdg),
-                                // the residual e = z - q0 dg is exact (fma) and RN(q0 + e rdg) is
-                                // RN(z / dg) — the same bits as the division, off its latency
-                                const double q0 = z[k] * rdg;
-                                const double e = __fma_rn(-q0, dg, z[k]);
-                                z[k] = __fma_rn(e, rdg, q0);
-                            } else {
-                                z[k] /= dg;
-                            }
-                        }
-                    }
-                    const int own = reinterpret_cast<const unsigned short*>(ch + kOffOwn)[ln];
-    #pragma unroll
-                    for (int k = 0; k < NRHS; ++k) {
-                        ring[k * ring_n + own] = z[k];
-                        if (TSP(2)) dst[3 * static_cast<size_t>(a + j) + comp + k] = z[k];
-                    }
-                }
-                if (!TSP(32)) {
-                    t1 = clock64();
-                    ph[2] += t1 - t0;
-                    t0 = t1;
-                }
-                // hand the level over: CTA-scope fence (the values live in this CTA's shared memory)
-                if (TSP(1)) asm volatile("fence.acq_rel.cta;" ::: "memory");
-            }
-            asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
             if (!TSP(32)) {
                 t1 = clock64();
-                ph[3] += t1 - t0;
+                ph[1] += t1 - t0;
                 t0 = t1;
             }
-            asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+            int a, b;
+            slice(l, a, b);
+            const int s = l % kStages;
+            for (int j = threadIdx.x; TSP(16) && j < b - a; j += kThreads) {
+                const unsigned char* ch = stage_rec + static_cast<size_t>(s) * kMaxRows * 96 + (j / 32) * kChunk;
+                const int ln = j % 32;
+                const double* rval = reinterpret_cast<const double*>(ch) + ln;  // [q * 32]
+                const unsigned short* rdep = reinterpret_cast<const unsigned short*>(ch + kOffDep) + ln;  // [q * 32]
+                // U: the pivot's reciprocal is computed while the dependencies are in flight, and
+                // z / dg is finished after them by one correction step (SFV_DIV_CORR, below)
+                double dg = 1.0, rdg = 1.0;
+                if (UPPER) {
+                    dg = reinterpret_cast<const double*>(ch + kOffDiag)[ln];
+                    if (SFV_DIV_CORR) rdg = 1.0 / dg;
+                }
+                unsigned short dep[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dep[q] = rdep[q * 32];
+                double z[NRHS];
+#pragma unroll
+                for (int k = 0; k < NRHS; ++k) z[k] = stage_src[(s * kMaxRows + j) * 3 + comp + k];
+                // Branch-free: an absent dependency (0xffff) reads a zero slot with factor value
+                // 0, and z - 0*0 is z bit for bit (also for -0, inf, NaN), as the reference's
+                // skipping it.  Every dependency load is issued before the first use.
+                double dv[8][NRHS];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const unsigned d = dep[q];
+                    const uint32_t ad = d != 0xffffu && TSP(8)
+                                            ? mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank)
+                                            : zero_addr;
+#pragma unroll
+                    for (int k = 0; k < NRHS; ++k)
+                        asm("ld.shared::cluster.f64 %0, [%1];"
+                            : "=d"(dv[q][k])
+                            : "r"(ad + (d != 0xffffu ? static_cast<uint32_t>(k * ring_n * 8) : 0u))
+                            : "memory");
+                }
+                double vq[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) vq[q] = rval[q * 32];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)  // the reference's order of subtraction
+#pragma unroll
+                    for (int k = 0; k < NRHS; ++k) z[k] -= vq[q] * dv[q][k];
+                if (UPPER) {
+#pragma unroll
+                    for (int k = 0; k < NRHS; ++k) {
+                        if (SFV_DIV_CORR) {
+                            // Markstein's correction: with rdg = RN(1 / dg) and q0 = RN(z rdg),
+                            // the residual e = z - q0 dg is exact (fma) and RN(q0 + e rdg) is
+                            // RN(z / dg) — the same bits as the division, off its latency
+                            const double q0 = z[k] * rdg;
+                            const double e = __fma_rn(-q0, dg, z[k]);
+                            z[k] = __fma_rn(e, rdg, q0);
+                        } else {
+                            z[k] /= dg;
+                        }
+                    }
+                }
+                const int own = reinterpret_cast<const unsigned short*>(ch + kOffOwn)[ln];
+#pragma unroll
+                for (int k = 0; k < NRHS; ++k) {
+                    ring[k * ring_n + own] = z[k];
+                    if (TSP(2)) dst[3 * static_cast<size_t>(a + j) + comp + k] = z[k];
+                }
+            }
             if (!TSP(32)) {
                 t1 = clock64();
-                ph[4] += t1 - t0;
+                ph[2] += t1 - t0;
+                t0 = t1;
             }
+            // hand the level over: CTA-scope fence (the values live in this CTA's shared memory)
+            if (TSP(1)) asm volatile("fence.acq_rel.cta;" ::: "memory");
+        }
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+        if (!TSP(32)) {
+            t1 = clock64();
+            ph[3] += t1 - t0;
+            t0 = t1;
+        }
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+        if (!TSP(32)) {
+            t1 = clock64();
+            ph[4] += t1 - t0;
         }
     }
     if (!TSP(32) && (threadIdx.x == 0 || threadIdx.x == kThreads) && (rank == 0 || rank == 15))
@@ -365,16 +252,9 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                ph[3] / t.n_levels, ph[4] / t.n_levels);
 }
 
-#ifndef SFV_TS_PREFETCH
-#define SFV_TS_PREFETCH 0
-#endif
 template <bool UPPER, int NRHS, int ST>
 cudaError_t launch_st(const StreamSet& set, int ncomp, const double* src, double* dst, cudaStream_t s) {
-    static const bool pf = [] {
-        const char* e = std::getenv("SFV_TS_PREFETCH");
-        return e ? std::atoi(e) != 0 : SFV_TS_PREFETCH != 0;
-    }();
-    auto kern = pf ? tri_stream_kernel<UPPER, NRHS, ST, true> : tri_stream_kernel<UPPER, NRHS, ST, false>;
+    auto kern = tri_stream_kernel<UPPER, NRHS, ST>;
     const int smem = stream_smem_bytes(set.ring, set.max_rows, ST);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
