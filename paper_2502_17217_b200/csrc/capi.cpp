@@ -22,6 +22,7 @@
 #include "host_threads.h"
 #include "device.h"
 #include "host_mesh.h"
+#include "precond_dev.h"
 #include "precond_host.h"
 #include "sfv.h"
 
@@ -54,6 +55,11 @@ struct DevBuf {
         return h.empty() || cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     }
     size_t bytes() const { return sizeof(T) * n; }
+    void adopt(T* q, size_t count) {  // take ownership of a cudaMalloc'd array
+        release();
+        p = q;
+        n = count;
+    }
 };
 
 struct Status {  // pinned host mirror of the device scalars read per control decision
@@ -1410,6 +1416,82 @@ struct PhaseTimer {
     }
 };
 
+// ILU(0) / ILU(1) set up on the device: J~, the factor, both sweeps' schedules and the
+// streamed sweep's records never visit the host (precond_dev.cu).  "" or why not.
+std::string precond_create_device(sfv_ctx* c, int level) {
+    DevIluSetup ds;
+    double tm[5] = {0, 0, 0, 0, 0};
+    const bool timing = std::getenv("SFV_TIMING") != nullptr;
+    std::string why = device_ilu_setup(device_topo(c->dgeo), c->ph.kbar, c->ph.transient != 0, c->ph.rho, c->ph.dt,
+                                       level, c->stream, ds, timing ? tm : nullptr);
+    cudaGetLastError();
+    if (!why.empty()) return why;
+    const int smem_cap = 232448;
+    const int stages = std::min(8, (smem_cap - stream_smem_bytes(ds.ring, ds.max_rows, 0)) / (ds.max_rows * 120));
+    if (stages < 3) {
+        ds.release();
+        return "device ilu: shared memory holds fewer than 3 stages";
+    }
+    const int nc = c->nc;
+    auto adopt = [&](TriDev& td, DevSweep& sw) {
+        td.order.adopt(sw.order, sw.n_pos);
+        td.level_ptr.adopt(sw.level_ptr, sw.n_levels + 1);
+        td.rp.release();
+        td.col.release();
+        td.val.release();
+        td.diag.release();
+        td.ell_col.release();
+        td.ell_val.release();
+        td.ell_pcol.release();
+        td.view = DevTri{};
+        td.view.n = sw.n_pos;
+        td.view.n_rows = nc;
+        td.view.n_levels = sw.n_levels;
+        td.view.order = td.order.p;
+        td.view.level_ptr = td.level_ptr.p;
+        td.n_levels = sw.n_levels;
+        td.nnz = 0;
+        sw.order = nullptr;
+        sw.level_ptr = nullptr;
+    };
+    adopt(c->L[0], ds.L);
+    adopt(c->U[0], ds.U);
+    c->L[0].nnz = static_cast<size_t>(ds.nnz_L);
+    c->U[0].nnz = static_cast<size_t>(ds.nnz_U);
+    c->U[0].u2l.adopt(ds.U.u2l, ds.U.n_pos);
+    c->U[0].view.u2l = c->U[0].u2l.p;
+    ds.U.u2l = nullptr;
+    c->srec[0].adopt(ds.L.rec, (static_cast<size_t>(ds.L.n_pos) + 31) / 32 * 3072);
+    c->srec[3].adopt(ds.U.rec, (static_cast<size_t>(ds.U.n_pos) + 31) / 32 * 3072);
+    ds.L.rec = ds.U.rec = nullptr;
+    c->sL.t[0] = DevStream{ds.L.n_levels, c->L[0].view.level_ptr, c->srec[0].p};
+    c->sU.t[0] = DevStream{ds.U.n_levels, c->U[0].view.level_ptr, c->srec[3].p};
+    for (StreamSet* ss : {&c->sL, &c->sU}) {
+        ss->ring = ds.ring;
+        ss->max_rows = ds.max_rows;
+        ss->stages = stages;
+    }
+    const int max_pos = std::max(ds.L.n_pos, ds.U.n_pos);
+    if (!c->ily.alloc(c->n) || !c->ipa.alloc(3 * static_cast<size_t>(max_pos)) ||
+        !c->ipb.alloc(3 * static_cast<size_t>(max_pos))) {
+        c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
+        return "ilu: out of device memory";
+    }
+    c->pc_ncomp = 1;
+    c->ring_ok = false;
+    c->stream_ok = true;
+    c->pipe_ok = false;
+    c->tri_cluster = kStreamMode;
+    c->pc_kind = level == 0 ? SFV_PRECOND_ILU0 : SFV_PRECOND_ILU1;
+    c->launches += 20;
+    if (timing)
+        std::fprintf(stderr,
+                     "[sfv] device ilu setup: J~ %.1f  pattern %.1f  schedules %.1f  numeric %.1f  records %.1f ms "
+                     "(ring %d rows %d stages %d; levels L %d U %d)\n",
+                     tm[0], tm[1], tm[2], tm[3], tm[4], ds.ring, ds.max_rows, stages, ds.L.n_levels, ds.U.n_levels);
+    return "";
+}
+
 int precond_create(sfv_ctx* c, int kind) {
     ++c->pc_gen;  // a cached GMRES graph holds the old preconditioner's buffers
     c->drop_graph();
@@ -1417,6 +1499,15 @@ int precond_create(sfv_ctx* c, int kind) {
     c->pc_kind = SFV_PRECOND_NONE;
     if (kind == SFV_PRECOND_AUTO) kind = 3 * c->nc <= 30000 ? SFV_PRECOND_LU : SFV_PRECOND_ILU1;  // nonlinear.cpp:355-356
     if (kind == SFV_PRECOND_NONE) return SFV_OK;
+    // (the host-built sweeps and the host factorisation switches keep the host setup)
+    if ((kind == SFV_PRECOND_ILU0 || kind == SFV_PRECOND_ILU1) && c->dgeo && !std::getenv("SFV_HOST_PRECOND") &&
+        !std::getenv("SFV_PIPE") && !std::getenv("SFV_TRI_CLUSTER") && !std::getenv("SFV_ILU_SERIAL") &&
+        !std::getenv("SFV_DEVICE_ILU")) {
+        // the whole setup on the device (precond_dev.cu); the host path below when it declines
+        const std::string why = precond_create_device(c, kind == SFV_PRECOND_ILU0 ? 0 : 1);
+        if (why.empty()) return c->cuda_check("ilu device setup");
+        if (pt.on) std::fprintf(stderr, "[sfv] device ilu setup declined: %s\n", why.c_str());
+    }
     std::vector<ScalarCsr> comps;
     const std::string msg = cell_jacobian(c->mesh, c->geom, c->ph.kbar, c->ph.transient != 0, c->ph.rho, c->ph.dt, comps);
     if (!msg.empty()) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, msg);

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "host_mesh.h"
+#include "precond_dev.h"
 #include "sfv_case.h"
 
 namespace sfv {
@@ -286,6 +287,23 @@ struct DeviceGeometry {
 };
 
 void free_device_geometry(DeviceGeometry* g) { delete g; }
+
+DevTopoView device_topo(const DeviceGeometry* g) {
+    DevTopoView v;
+    v.nc = g->t.nc;
+    v.nf = g->t.nf;
+    v.nint = g->t.nint;
+    v.owner = g->t.owner;
+    v.neigh = g->t.neigh;
+    v.cf_off = g->t.cf_off;
+    v.cf = g->t.cf;
+    v.face_kind = g->t.face_kind;
+    v.amag = g->amag.p;
+    v.dmag = g->dmag.p;
+    v.delmag = g->delmag.p;
+    v.vol = g->vol.p;
+    return v;
+}
 
 std::string device_layout(const DeviceGeometry* dg, int spad, int* tsl, double* tls, double* f9, int* bnd) {
     const Topo& t = dg->t;

@@ -67,6 +67,8 @@ std::string compute_geometry(const HostMesh& m, HostGeometry& g);
 struct DeviceGeometry;
 std::string device_geometry(const HostMesh& m, HostGeometry& g, DeviceGeometry** keep = nullptr);
 void free_device_geometry(DeviceGeometry* g);
+struct DevTopoView;
+DevTopoView device_topo(const DeviceGeometry* g);  // precond_dev.h
 // With keep, device_geometry copies only |Gamma|, n, |d|, |Delta|, volumes and the singular
 // flags to the host; this copies the rest (no-op once done).
 std::string download_geometry(const DeviceGeometry* dg, HostGeometry& g);

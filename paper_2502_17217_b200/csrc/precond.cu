@@ -709,6 +709,7 @@ int ilu_ring_window() { return kRingPerCta * kDsCluster; }
 // (binary search in the sorted row) — each entry of row i sees the same subtractions in the
 // same k order as the host loop, so the factor is bit-identical (-fmad=false).
 #include "host_threads.h"
+#include "precond_dev.h"
 #include "precond_host.h"
 
 namespace sfv {
@@ -776,6 +777,32 @@ T* dev_copy(const T* h, size_t n) {
 }
 
 }  // namespace
+
+bool launch_ilu_numeric(int n, const int* rows, const int* rp, const int* col, const int* diag, double* val,
+                        cudaStream_t stream) {
+    int* d_flags = nullptr;  // done[n] + broke
+    if (cudaMalloc(&d_flags, sizeof(int) * (n + 1)) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaMemsetAsync(d_flags, 0, sizeof(int) * (n + 1), stream);
+    int* d_broke = d_flags + n;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ilu_numeric_kernel, 256, 0);
+    const int grid = std::max(1, std::min(sms * std::max(per, 1), (n + 7) / 8));
+    void* args[] = {&n, const_cast<int**>(&rows), const_cast<int**>(&rp), const_cast<int**>(&col),
+                    const_cast<int**>(&diag), &val, &d_flags, &d_broke};
+    const bool launched = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(ilu_numeric_kernel), dim3(grid),
+                                                      dim3(256), args, 0, stream) == cudaSuccess;
+    int broke = 1;
+    if (launched) cudaMemcpyAsync(&broke, d_broke, sizeof(int), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    cudaFree(d_flags);
+    cudaGetLastError();
+    return launched && broke == 0;
+}
 
 bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows,
                         cudaStream_t stream) {

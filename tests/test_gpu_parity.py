@@ -195,9 +195,9 @@ def test_ilu_parallel_factorisation_bitwise(monkeypatch):
 
 @pytest.mark.parametrize("kind,code", [("ilu1", 3), ("ilu0", 2)])
 def test_ilu_device_numeric_bitwise(kind, code, monkeypatch):
-    """SFV_DEVICE_ILU=1: the numeric phase of the factorisation runs on the device (one warp
-    per row, rows in level order, release/acquire row flags); the factor must equal the host
-    one bit for bit (compared through the apply) and the reference's (through the oracle)."""
+    """SFV_DEVICE_ILU=1: the host setup with only the numeric phase on the device (one warp
+    per row, rows in level order, release/acquire row flags) against the default whole-device
+    setup; both must equal the reference's factor bit for bit (through the oracle)."""
     sv = _sv()
     case = cases.config("c2", n=42)  # 74088 cells: above the parallel-factorisation threshold
     mesh = case.mesh()
@@ -209,6 +209,60 @@ def test_ilu_device_numeric_bitwise(kind, code, monkeypatch):
     assert np.array_equal(z_dev, z_host)
     orc.precond_create(code)
     assert np.array_equal(z_dev, orc.precond_apply(r))
+
+
+@pytest.mark.parametrize("name,n,kind", [("c2", 24, "ilu1"), ("c2", 24, "ilu0"), ("c4", 24, "ilu1"),
+                                         ("c3", 48, "ilu1"), ("c5", 12, "ilu1")])
+def test_ilu_device_setup_bitwise(name, n, kind, monkeypatch):
+    """The default ILU setup runs on the device (precond_dev.cu: J~, pattern, levels, numeric
+    phase, positions, streamed-sweep records); its apply must equal the host setup's
+    (SFV_HOST_PRECOND=1) and the reference's bit for bit, with the same level counts and
+    factor sizes."""
+    sv = _sv()
+    case = cases.config(name, n=n)
+    mesh = case.mesh()
+    ev, orc = _pair(mesh, case.physics)
+    pc = sv.make_preconditioner(ev, kind)
+    info_dev = pc.info()
+    if name != "c5":  # (tets: ILU(1) rows may exceed the streamed sweep's 8 dependencies)
+        assert info_dev["sweep"] == 200
+    rs = [cases.uniform(seed, 3 * mesh.n_cells) for seed in (11, 12)]
+    z_dev = [pc.solve(r).cpu().numpy() for r in rs]
+    monkeypatch.setenv("SFV_HOST_PRECOND", "1")
+    pc_h = sv.make_preconditioner(ev, kind)
+    info_host = pc_h.info()
+    z_host = [pc_h.solve(r).cpu().numpy() for r in rs]
+    for k in ("levels_fwd", "levels_bwd", "nnz_L", "nnz_U"):
+        assert info_dev[k] == info_host[k], (k, info_dev, info_host)
+    for a, b in zip(z_dev, z_host):
+        assert np.array_equal(a, b)
+    orc.precond_create({"ilu0": 2, "ilu1": 3}[kind])
+    assert np.array_equal(z_dev[0], orc.precond_apply(rs[0]))
+
+
+def test_ilu_device_setup_full_size(monkeypatch):
+    """C2 at 1M cells: the device setup against the host setup, through the apply (bit for bit)."""
+    import time
+    import torch
+    sv = _sv()
+    case = cases.config("c2")
+    mesh = case.mesh()
+    ev = sv.ResidualEvaluator(mesh, case.physics)
+    r = sv.to_device(cases.uniform(21, 3 * mesh.n_cells))
+    t0 = time.time()
+    pc = sv.make_preconditioner(ev, "ilu1")
+    torch.cuda.synchronize()
+    t_dev = time.time() - t0
+    z_dev = pc.solve(r).cpu().numpy()
+    info_dev = pc.info()
+    monkeypatch.setenv("SFV_HOST_PRECOND", "1")
+    t0 = time.time()
+    pc_h = sv.make_preconditioner(ev, "ilu1")
+    torch.cuda.synchronize()
+    t_host = time.time() - t0
+    assert np.array_equal(z_dev, pc_h.solve(r).cpu().numpy())
+    assert info_dev["levels_fwd"] == pc_h.info()["levels_fwd"] and info_dev["nnz_L"] == pc_h.info()["nnz_L"]
+    print(f"c2 ilu1 setup: device {t_dev:.3f} s, host {t_host:.3f} s; apply bit-identical")
 
 
 def test_ilu_apply_transient_bitwise():
