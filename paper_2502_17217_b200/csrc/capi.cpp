@@ -1613,7 +1613,9 @@ int precond_create(sfv_ctx* c, int kind) {
                 std::vector<std::thread> th;
                 for (size_t x = 0; x < scheds.size(); ++x)
                     th.emplace_back([&, x] {
-                        ok[x] = build_stream_records(scheds[x], kStreamCluster, cand, s_rows, packed[x]);
+                        // forward sweep of component a: values go to its backward-sweep positions
+                        ok[x] = build_stream_records(scheds[x], kStreamCluster, cand, s_rows, packed[x],
+                                                     x % 2 ? nullptr : &scheds[x + 1].pos);
                     });
                 for (auto& t : th) t.join();
                 if (std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; })) {

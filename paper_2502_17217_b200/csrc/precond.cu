@@ -664,13 +664,16 @@ void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double*
         const int per = ncomp == 1 ? 3 : 1;
         for (int c = 0; c < ncomp; ++c)  // r -> L positions
             gather_pos_kernel<<<592, 256, 0, s>>>(L.t[c].order, L.t[c].n, c, per, r, pa);
-        if (cluster == kStreamMode) launch_tri_stream(*SL, false, ncomp, pa, pb, s);
-        else if (ncomp == 1) launch_cluster<false, 3>(L, 1, cluster, pa, pb, s);
+        if (cluster == kStreamMode) {  // the forward sweep stores in U positions, the backward one in rows
+            launch_tri_stream(*SL, false, ncomp, pa, pb, s);
+            launch_tri_stream(*SU, true, ncomp, pb, z, s);
+            return;
+        }
+        if (ncomp == 1) launch_cluster<false, 3>(L, 1, cluster, pa, pb, s);
         else launch_cluster<false, 1>(L, 3, cluster, pa, pb, s);
         for (int c = 0; c < ncomp; ++c)  // y: L positions -> U positions
             permute_pos_kernel<<<592, 256, 0, s>>>(U.t[c].u2l, U.t[c].n, c, per, pb, pa);
-        if (cluster == kStreamMode) launch_tri_stream(*SU, true, ncomp, pa, pb, s);
-        else if (ncomp == 1) launch_cluster<true, 3>(U, 1, cluster, pa, pb, s);
+        if (ncomp == 1) launch_cluster<true, 3>(U, 1, cluster, pa, pb, s);
         else launch_cluster<true, 1>(U, 3, cluster, pa, pb, s);
         for (int c = 0; c < ncomp; ++c)  // U positions -> rows
             scatter_pos_kernel<<<592, 256, 0, s>>>(U.t[c].order, U.t[c].n, c, per, pb, z);

@@ -319,10 +319,12 @@ __global__ void ring_need_kernel(Slicing s, const int* __restrict__ order, const
 
 // pass 2: the records in the device chunk layout (precond_host.h: val[8][32], diag[32],
 // dep[8][32], own[32], zero tail; 3072 bytes per 32 positions)
+// out (kOffOut): the forward sweep stores each value at its row's backward-sweep position
+// (out_pos), the backward sweep at its row
 template <bool UPPER>
 __global__ void records_kernel(Slicing s, const int* __restrict__ order, const int* __restrict__ pos,
                                const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ val,
-                               unsigned char* __restrict__ rec) {
+                               const int* __restrict__ out_pos, unsigned char* __restrict__ rec) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const int nchunk = (s.np + 31) / 32;
     if (p >= nchunk * 32) return;
@@ -331,8 +333,10 @@ __global__ void records_kernel(Slicing s, const int* __restrict__ order, const i
     double* cdiag = reinterpret_cast<double*>(cb + 2048);
     uint16_t* cdep = reinterpret_cast<uint16_t*>(cb + 2304);
     uint16_t* cown = reinterpret_cast<uint16_t*>(cb + 2816);
+    int* cout = reinterpret_cast<int*>(cb + 2880);
     const int ln = p & 31;
     if (ln < 24) reinterpret_cast<uint64_t*>(cb + 2880)[ln] = 0ull;  // bytes 2880..3071
+    __syncwarp();
     for (int k = 0; k < 8; ++k) {
         cval[k * 32 + ln] = 0.0;
         cdep[k * 32 + ln] = 0xffff;
@@ -340,6 +344,7 @@ __global__ void records_kernel(Slicing s, const int* __restrict__ order, const i
     if (p >= s.np) {  // tail of the last chunk
         cdiag[ln] = 0.0;
         cown[ln] = 0;
+        cout[ln] = -1;
         return;
     }
     const int l = level_of(s, p);
@@ -348,6 +353,7 @@ __global__ void records_kernel(Slicing s, const int* __restrict__ order, const i
     cown[ln] = static_cast<uint16_t>(o % s.ring);
     cdiag[ln] = 1.0;
     const int i = order[p];
+    cout[ln] = i < 0 ? -1 : out_pos ? out_pos[i] : i;
     if (i < 0) return;  // level padding: no dependencies, unit pivot
     int dq[8], dk[8], dpos;
     const int m = row_deps<UPPER>(i, rp, col, dq, dk, dpos);
@@ -644,8 +650,8 @@ std::string device_ilu_setup(const DevTopoView& t, double kbar, bool transient, 
             return "device ilu: out of memory";
         }
         const int gp = static_cast<int>((nchunk * 32 + 255) / 256);
-        if (w) records_kernel<true><<<gp, 256, 0, s>>>(su, out.U.order, upos, rp, col, val, sw.rec);
-        else records_kernel<false><<<gp, 256, 0, s>>>(sl, out.L.order, lpos, rp, col, val, sw.rec);
+        if (w) records_kernel<true><<<gp, 256, 0, s>>>(su, out.U.order, upos, rp, col, val, nullptr, sw.rec);
+        else records_kernel<false><<<gp, 256, 0, s>>>(sl, out.L.order, lpos, rp, col, val, upos, sw.rec);
     }
     if (cudaStreamSynchronize(s) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
         out.release();

@@ -669,7 +669,8 @@ std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out, bool factor) {
 
 namespace sfv {
 
-bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed) {
+bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed,
+                          const std::vector<int>* out_pos) {
     StageClock sc;
     if (t.maxd > 8) return false;
     const int np = t.n_pos;
@@ -706,6 +707,7 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
         double* cdiag = reinterpret_cast<double*>(cb + 2048);
         uint16_t* cdep = reinterpret_cast<uint16_t*>(cb + 2304);
         uint16_t* cown = reinterpret_cast<uint16_t*>(cb + 2816);
+        int32_t* cout = reinterpret_cast<int32_t*>(cb + kOffOut);
         std::memset(cb + 2880, 0, kChunkBytes - 2880);
     for (int l = 0; l < 32; ++l) {
         const int p = ch * 32 + l;
@@ -716,9 +718,13 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
             }
             cdiag[l] = 0.0;
             cown[l] = 0;
+            cout[l] = -1;
             continue;
         }
         cown[l] = static_cast<uint16_t>(ordinal[p] % ring);
+        // where the sweep stores this position's value: the row (backward sweep), or the row's
+        // backward-sweep position (forward sweep, out_pos = that schedule's row -> position)
+        cout[l] = t.order[p] < 0 ? -1 : out_pos ? (*out_pos)[t.order[p]] : t.order[p];
         cdiag[l] = t.diag[p];
         for (int k = 0; k < 8; ++k) {
             cdep[k * 32 + l] = 0xffff;

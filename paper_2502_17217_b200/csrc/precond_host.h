@@ -100,12 +100,17 @@ struct StreamRecord {
 };
 static_assert(sizeof(StreamRecord) == 96, "record layout");
 // Built directly in the device chunk layout below (every byte written by the parallel pass).
-bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed);
+bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed,
+                          const std::vector<int>* out_pos = nullptr);
 // Device layout of the records: per chunk of 32 positions (levels are padded to 32), the
 // fields as arrays over the 32 positions — val[8][32], diag[32], dep[8][32], own[32],
 // 3072 bytes — so that a warp reading one field of 32 consecutive rows from shared
 // memory is bank-conflict free (the 96-byte AoS record was read at a 96-byte lane stride).
+// Bytes 2880..3007: out[32] (int32), where the sweep stores the position's value: the forward
+// sweep writes in the backward sweep's position order, the backward sweep writes rows, so no
+// permute or scatter pass runs between or after them (-1: level padding, nothing stored).
 constexpr int kChunkBytes = 3072;
+constexpr int kOffOut = 2880;
 
 
 // Block-pipelined sweep (precond_pipe.cu): the rows, in sweep order, are cut into `blocks`

@@ -52,7 +52,7 @@ constexpr int kThreads = SFV_STREAM_THREADS;
 constexpr int kLvl = 1024;
 
 // field offsets inside a 3072-byte chunk of 32 records (precond_host.h: pack_stream_chunks)
-constexpr int kChunk = 3072, kOffDiag = 2048, kOffDep = 2304, kOffOwn = 2816;
+constexpr int kChunk = 3072, kOffDiag = 2048, kOffDep = 2304, kOffOwn = 2816, kOffOutIdx = 2880;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = static_cast<int>(cluster.block_rank());
     const int comp = NRHS == 3 ? 0 : static_cast<int>(blockIdx.x / kStreamCluster);
-    const DevStream& t = set.t[comp];
+    // constant indices: the parameter is read from the constant bank, not copied to local memory
+    const DevStream t = comp == 0 ? set.t[0] : comp == 1 ? set.t[1] : set.t[2];
     const bool producer = threadIdx.x >= kThreads;
     const int ptid = threadIdx.x - kThreads;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -166,13 +167,6 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 const int ln = j % 32;
                 const double* rval = reinterpret_cast<const double*>(ch) + ln;  // [q * 32]
                 const unsigned short* rdep = reinterpret_cast<const unsigned short*>(ch + kOffDep) + ln;  // [q * 32]
-                // U: the pivot's reciprocal is computed while the dependencies are in flight, and
-                // z / dg is finished after them by one correction step (SFV_DIV_CORR, below)
-                double dg = 1.0, rdg = 1.0;
-                if (UPPER) {
-                    dg = reinterpret_cast<const double*>(ch + kOffDiag)[ln];
-                    if (SFV_DIV_CORR) rdg = 1.0 / dg;
-                }
                 unsigned short dep[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) dep[q] = rdep[q * 32];
@@ -181,20 +175,48 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 for (int k = 0; k < NRHS; ++k) z[k] = stage_src[(s * kMaxRows + j) * 3 + comp + k];
                 // Branch-free: an absent dependency (0xffff) reads a zero slot with factor value
                 // 0, and z - 0*0 is z bit for bit (also for -0, inf, NaN), as the reference's
-                // skipping it.  Every dependency load is issued before the first use.
-                double dv[8][NRHS];
+                // skipping it.  The eight loads of a right-hand side are one asm statement, so they
+                // leave back to back (compiled separately, the scheduler put the eighth after the
+                // pivot reciprocal, ~40 instructions later, on the level's critical path).
+                uint32_t ad[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const unsigned d = dep[q];
-                    const uint32_t ad = d != 0xffffu && TSP(8)
-                                            ? mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank)
-                                            : zero_addr;
+                    ad[q] = d != 0xffffu && TSP(8)
+                                ? mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank)
+                                : zero_addr;
+                }
+                double dv[8][NRHS];
 #pragma unroll
-                    for (int k = 0; k < NRHS; ++k)
-                        asm("ld.shared::cluster.f64 %0, [%1];"
-                            : "=d"(dv[q][k])
-                            : "r"(ad + (d != 0xffffu ? static_cast<uint32_t>(k * ring_n * 8) : 0u))
-                            : "memory");
+                for (int k = 0; k < NRHS; ++k) {
+                    uint32_t a8[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        a8[q] = ad[q] + (dep[q] != 0xffffu ? static_cast<uint32_t>(k * ring_n * 8) : 0u);
+                    asm volatile(
+                        "ld.shared::cluster.f64 %0, [%8];\n\t"
+                        "ld.shared::cluster.f64 %1, [%9];\n\t"
+                        "ld.shared::cluster.f64 %2, [%10];\n\t"
+                        "ld.shared::cluster.f64 %3, [%11];\n\t"
+                        "ld.shared::cluster.f64 %4, [%12];\n\t"
+                        "ld.shared::cluster.f64 %5, [%13];\n\t"
+                        "ld.shared::cluster.f64 %6, [%14];\n\t"
+                        "ld.shared::cluster.f64 %7, [%15];"
+                        : "=d"(dv[0][k]), "=d"(dv[1][k]), "=d"(dv[2][k]), "=d"(dv[3][k]), "=d"(dv[4][k]),
+                          "=d"(dv[5][k]), "=d"(dv[6][k]), "=d"(dv[7][k])
+                        : "r"(a8[0]), "r"(a8[1]), "r"(a8[2]), "r"(a8[3]), "r"(a8[4]), "r"(a8[5]), "r"(a8[6]),
+                          "r"(a8[7])
+                        : "memory");
+                }
+                // U: the pivot (read after the loads are out) and its reciprocal overlap their
+                // latency; z / dg is finished after them by one correction step (SFV_DIV_CORR)
+                double dg = 1.0, rdg = 1.0;
+                if (UPPER) {
+                    asm volatile("ld.shared.f64 %0, [%1];"
+                                 : "=d"(dg)
+                                 : "r"(smem_u32(reinterpret_cast<const double*>(ch + kOffDiag) + ln))
+                                 : "memory");
+                    if (SFV_DIV_CORR) rdg = 1.0 / dg;
                 }
                 double vq[8];
 #pragma unroll
@@ -219,10 +241,13 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                     }
                 }
                 const int own = reinterpret_cast<const unsigned short*>(ch + kOffOwn)[ln];
+                // the backward sweep's position (forward) or the row (backward): no permute /
+                // scatter pass after the sweep
+                const int oi = reinterpret_cast<const int*>(ch + kOffOutIdx)[ln];
 #pragma unroll
                 for (int k = 0; k < NRHS; ++k) {
                     ring[k * ring_n + own] = z[k];
-                    if (TSP(2)) dst[3 * static_cast<size_t>(a + j) + comp + k] = z[k];
+                    if (TSP(2) && oi >= 0) dst[3 * static_cast<size_t>(oi) + comp + k] = z[k];
                 }
             }
             if (!TSP(32)) {
