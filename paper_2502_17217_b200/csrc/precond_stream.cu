@@ -277,165 +277,9 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                ph[3] / t.n_levels, ph[4] / t.n_levels);
 }
 
-// The same sweep for one right-hand side per cluster (the default split), with the next
-// level's row held in registers: between the cluster arrive and wait of level l each compute
-// thread waits for level l + 1's stage, reads its row's record (DSMEM addresses, factor values,
-// pivot, right-hand side, slot, output index) into plain registers, so after the wait only
-// the eight dependency loads, the subtraction chain, the pivot step and the stores remain.
-template <bool UPPER, int kStages>
-__global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_pf_kernel(StreamSet set, const double* __restrict__ src,
-                                                                         double* __restrict__ dst) {
-    const int kMaxRows = set.max_rows;
-    cg::cluster_group cluster = cg::this_cluster();
-    const int rank = static_cast<int>(cluster.block_rank());
-    const int comp = static_cast<int>(blockIdx.x / kStreamCluster);
-    const DevStream t = comp == 0 ? set.t[0] : comp == 1 ? set.t[1] : set.t[2];
-    const bool producer = threadIdx.x >= kThreads;
-    const int ptid = threadIdx.x - kThreads;
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int ring_n = set.ring;
-    double* ring = reinterpret_cast<double*>(smem);
-    unsigned char* stage_rec = smem + static_cast<size_t>(ring_n) * 24;
-    double* stage_src = reinterpret_cast<double*>(stage_rec + static_cast<size_t>(kStages) * kMaxRows * 96);
-    int* lp = reinterpret_cast<int*>(stage_src + kStages * kMaxRows * 3);
-    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(lp + kLvl + 2);
-    double* zero_slot = reinterpret_cast<double*>(mbar + kStages);
-    const uint32_t zero_addr = smem_u32(zero_slot);
-    const uint32_t ring_base = smem_u32(ring);
-    const uint32_t mbar_base = smem_u32(mbar);
-    int lbase = 0;
-    auto stage_levels = [&](int base) {
-        __syncthreads();
-        lbase = base;
-        for (int x = threadIdx.x; x < kLvl + 2; x += blockDim.x)
-            lp[x] = base + x <= t.n_levels ? t.level_ptr[base + x] : t.level_ptr[t.n_levels];
-        __syncthreads();
-    };
-    auto slice = [&](int l, int& a, int& b) {
-        const int la = lp[l - lbase], lb = lp[l - lbase + 1];
-        const int nch = (lb - la) >> 5, per = (nch + kStreamCluster - 1) / kStreamCluster;
-        a = min(lb, la + rank * per * 32);
-        b = min(lb, a + per * 32);
-    };
-    auto issue = [&](int l) {
-        if (l >= t.n_levels || ptid != 0) return;
-        const int s = l % kStages;
-        int a, b;
-        slice(l, a, b);
-        const uint32_t bar = mbar_base + 8u * s;
-        mbar_expect(bar, static_cast<uint32_t>(b - a) * 120u);
-        if (b > a) {
-            bulk_copy(smem_u32(stage_rec + static_cast<size_t>(s) * kMaxRows * 96),
-                      reinterpret_cast<const unsigned char*>(t.rec) + static_cast<size_t>(a) * 96,
-                      static_cast<uint32_t>(b - a) * 96u, bar);
-            bulk_copy(smem_u32(stage_src + s * kMaxRows * 3), src + 3 * static_cast<size_t>(a),
-                      static_cast<uint32_t>(b - a) * 24u, bar);
-        }
-    };
-    // one row's record fields (position j of stage s) into registers
-    auto fetch = [&](int s, int j, uint32_t (&ad)[8], double (&vq)[8], double& z, double& dg, uint32_t& own,
-                     int& oi) {
-        const unsigned char* ch = stage_rec + static_cast<size_t>(s) * kMaxRows * 96 + (j / 32) * kChunk;
-        const int ln = j % 32;
-        const unsigned short* rdep = reinterpret_cast<const unsigned short*>(ch + kOffDep) + ln;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const unsigned d = rdep[q * 32];
-            ad[q] = d != 0xffffu ? mapa(ring_base + (d & 0xfffu) * 8u, static_cast<int>(d >> 12)) : zero_addr;
-        }
-        const double* rval = reinterpret_cast<const double*>(ch) + ln;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) vq[q] = rval[q * 32];
-        z = stage_src[(s * kMaxRows + j) * 3 + comp];
-        dg = UPPER ? reinterpret_cast<const double*>(ch + kOffDiag)[ln] : 1.0;
-        own = ring_base + 8u * reinterpret_cast<const unsigned short*>(ch + kOffOwn)[ln];
-        oi = reinterpret_cast<const int*>(ch + kOffOutIdx)[ln];
-    };
-    auto finish = [&](const uint32_t (&ad)[8], const double (&vq)[8], double z, double dg, uint32_t own, int oi) {
-        double dv[8];
-        asm volatile(
-            "ld.shared::cluster.f64 %0, [%8];\n\t"
-            "ld.shared::cluster.f64 %1, [%9];\n\t"
-            "ld.shared::cluster.f64 %2, [%10];\n\t"
-            "ld.shared::cluster.f64 %3, [%11];\n\t"
-            "ld.shared::cluster.f64 %4, [%12];\n\t"
-            "ld.shared::cluster.f64 %5, [%13];\n\t"
-            "ld.shared::cluster.f64 %6, [%14];\n\t"
-            "ld.shared::cluster.f64 %7, [%15];"
-            : "=d"(dv[0]), "=d"(dv[1]), "=d"(dv[2]), "=d"(dv[3]), "=d"(dv[4]), "=d"(dv[5]), "=d"(dv[6]), "=d"(dv[7])
-            : "r"(ad[0]), "r"(ad[1]), "r"(ad[2]), "r"(ad[3]), "r"(ad[4]), "r"(ad[5]), "r"(ad[6]), "r"(ad[7])
-            : "memory");
-        double rdg = 1.0;
-        if (UPPER) rdg = 1.0 / dg;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) z -= vq[q] * dv[q];  // the reference's order of subtraction
-        if (UPPER) {  // Markstein's correction: RN(z / dg) (see tri_stream_kernel)
-            const double q0 = z * rdg;
-            const double e = __fma_rn(-q0, dg, z);
-            z = __fma_rn(e, rdg, q0);
-        }
-        asm volatile("st.shared.f64 [%0], %1;" ::"r"(own), "d"(z) : "memory");
-        if (oi >= 0) dst[3 * static_cast<size_t>(oi) + comp] = z;
-    };
-    if (threadIdx.x < kStages) mbar_init(mbar_base + 8u * threadIdx.x, 1);
-    if (threadIdx.x == 0) *zero_slot = 0.0;
-    stage_levels(0);
-    if (producer)
-        for (int l = 0; l < kStages - 1; ++l) issue(l);
-    uint32_t ad[8];
-    double vq[8], z = 0.0, dg = 1.0;
-    uint32_t own = 0;
-    int oi = -1, n_cur = 0;
-    if (!producer) {  // level 0's row
-        int a, b;
-        slice(0, a, b);
-        n_cur = b - a;
-        if (threadIdx.x < n_cur) {
-            mbar_wait(mbar_base, 0u);
-            fetch(0, threadIdx.x, ad, vq, z, dg, own, oi);
-        }
-    }
-    for (int l = 0; l < t.n_levels; ++l) {
-        if (l + kStages - 1 + 1 - lbase > kLvl) stage_levels(l);
-        if (producer) {
-            issue(l + kStages - 1);
-        } else {
-            if (threadIdx.x < n_cur) finish(ad, vq, z, dg, own, oi);
-            for (int j = threadIdx.x + kThreads; j < n_cur; j += kThreads) {  // rows beyond kThreads
-                uint32_t ad2[8];
-                double vq2[8], z2, dg2;
-                uint32_t own2;
-                int oi2;
-                fetch(l % kStages, j, ad2, vq2, z2, dg2, own2, oi2);
-                finish(ad2, vq2, z2, dg2, own2, oi2);
-            }
-            asm volatile("fence.acq_rel.cta;" ::: "memory");
-        }
-        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-        if (!producer) {  // level l + 1's row, while the barrier completes
-            n_cur = 0;
-            if (l + 1 < t.n_levels) {
-                int a, b;
-                slice(l + 1, a, b);
-                n_cur = b - a;
-                if (threadIdx.x < n_cur) {
-                    const int s1 = (l + 1) % kStages;
-                    mbar_wait(mbar_base + 8u * s1, static_cast<uint32_t>(((l + 1) / kStages) & 1));
-                    fetch(s1, threadIdx.x, ad, vq, z, dg, own, oi);
-                }
-            }
-        }
-        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-    }
-}
-
 template <bool UPPER, int NRHS, int ST>
 cudaError_t launch_st(const StreamSet& set, int ncomp, const double* src, double* dst, cudaStream_t s) {
-    static const bool pf = [] {
-        const char* e = std::getenv("SFV_TS_PF");
-        return e && std::atoi(e) != 0;
-    }();
-    auto kern = NRHS == 1 && pf ? tri_stream_pf_kernel<UPPER, ST> : tri_stream_kernel<UPPER, NRHS, ST>;
+    auto kern = tri_stream_kernel<UPPER, NRHS, ST>;
     const int smem = stream_smem_bytes(set.ring, set.max_rows, ST);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
