@@ -45,11 +45,15 @@ extern "C" {
 typedef struct sfv_mesh sfv_mesh;
 typedef struct sfv_ctx sfv_ctx;
 
-/* ---- mesh generators (host) ---- */
+/* ---- mesh generators ---- */
 sfv_mesh* sfv_mesh_box(const double extents[3], const int divisions[3], const int patch_kinds[6],
                        double distort_factor, uint64_t seed, char* err, int errlen);
+/* The config-5 tet mesh (harness generator; on the device when one is present, else on the host
+ * — the same arrays either way). */
 sfv_mesh* sfv_mesh_kuhn_tets(const double extents[3], int n, const int patch_kinds[6], uint64_t perm_seed,
                              int permute, int rcm, char* err, int errlen);
+/* 1 when the mesh was built by a device generator */
+int sfv_mesh_built_on_device(const sfv_mesh* m);
 /* counts = {n_points, n_faces, n_face_points, n_cells, n_internal, n_patches} */
 void sfv_mesh_counts(const sfv_mesh* m, int counts[6]);
 void sfv_mesh_export(const sfv_mesh* m, double* points, int* face_offsets, int* face_points, int* owner,

@@ -179,6 +179,7 @@ class Mesh:
     patch_start: np.ndarray
     patch_count: np.ndarray
     _keep: list = field(default_factory=list, repr=False)
+    on_device: bool = False  # built by a device generator (sfv_mesh_built_on_device)
 
     @property
     def n_faces(self) -> int:

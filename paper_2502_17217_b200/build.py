@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INC = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 
 CU = ["residual.cu", "jv_fused.cu", "jv_pair.cu", "krylov.cu", "precond.cu", "precond_stream.cu", "precond_pipe.cu",
-      "geometry.cu", "segregated.cu", "precond_dev.cu"]
+      "geometry.cu", "segregated.cu", "precond_dev.cu", "mesh_dev.cu"]
 CPP = ["host_mesh.cpp", "precond_host.cpp", "capi.cpp"]
 HEADERS = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))] + [
     os.path.join(ROOT, "include", h) for h in ("sfv.h", "sfv_case.h")]

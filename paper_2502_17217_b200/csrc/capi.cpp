@@ -109,6 +109,7 @@ struct SfvError {
 
 struct sfv_mesh {
     HostMesh m;
+    bool on_device = false;  // built by a device generator
 };
 
 struct sfv_ctx {
@@ -1794,8 +1795,12 @@ sfv_mesh* sfv_mesh_kuhn_tets(const double extents[3], int n, const int patch_kin
         if (err) std::snprintf(err, errlen, "kuhn_tets: n must be >= 1");
         return nullptr;
     }
-    return new sfv_mesh{kuhn_tets(extents, n, patch_kinds, perm_seed, permute != 0, rcm != 0)};
+    bool dev = false;
+    HostMesh hm = kuhn_tets(extents, n, patch_kinds, perm_seed, permute != 0, rcm != 0, &dev);
+    return new sfv_mesh{std::move(hm), dev};
 }
+
+int sfv_mesh_built_on_device(const sfv_mesh* m) { return m && m->on_device ? 1 : 0; }
 
 void sfv_mesh_counts(const sfv_mesh* mm, int counts[6]) {
     const HostMesh& m = mm->m;

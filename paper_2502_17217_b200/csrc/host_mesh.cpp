@@ -546,7 +546,31 @@ struct FaceKey {
 
 }  // namespace
 
-HostMesh kuhn_tets(const double ext[3], int n, const int kinds[6], uint64_t perm_seed, bool permute, bool do_rcm) {
+HostMesh kuhn_tets(const double ext[3], int n, const int kinds[6], uint64_t perm_seed, bool permute, bool do_rcm,
+                   bool* on_device) {
+    if (on_device) *on_device = false;
+    // on the device when there is one (mesh_dev.cu, the same mesh array for array); the seeded
+    // Fisher-Yates permutation is a sequential chain of swaps and is drawn here
+    if (!std::getenv("SFV_HOST_MESH") && n >= 8) {
+        const long long ntl = 6LL * n * n * n;
+        std::vector<int> newid;
+        if (permute && ntl < (1LL << 28)) {
+            const int nt = static_cast<int>(ntl);
+            std::vector<int> perm(nt);
+            std::iota(perm.begin(), perm.end(), 0);
+            for (int i = nt - 1; i > 0; --i) {
+                const int r = static_cast<int>(splitmix_at(perm_seed, static_cast<uint64_t>(i)) % static_cast<uint64_t>(i + 1));
+                std::swap(perm[i], perm[r]);
+            }
+            newid.resize(nt);
+            for (int i = 0; i < nt; ++i) newid[perm[i]] = i;
+        }
+        HostMesh dm;
+        if (device_kuhn_tets(ext, n, kinds, permute ? &newid : nullptr, do_rcm, dm).empty()) {
+            if (on_device) *on_device = true;
+            return dm;
+        }
+    }
     const int np1 = n + 1;
     auto pid = [&](int i, int j, int k) { return i + np1 * (j + np1 * k); };
     HostMesh m;

@@ -57,13 +57,18 @@ std::string distort(HostMesh& m, double factor, uint64_t seed);
 // Config-5 generator: parity-mirrored Kuhn split of an n^3 box into 6 tets per hex,
 // optional seeded random cell permutation followed by reverse Cuthill-McKee,
 // faces rebuilt with internal faces first (owner < neighbour) and patches contiguous.
+// On the device when there is one (device_kuhn_tets; *on_device tells which path built it).
 HostMesh kuhn_tets(const double ext[3], int n, const int kinds[6], uint64_t perm_seed, bool permute,
-                   bool rcm);
+                   bool rcm, bool* on_device = nullptr);
 // compute_geometry (mesh.cpp:347-510).
 std::string compute_geometry(const HostMesh& m, HostGeometry& g);
 // The same on the device (geometry.cu): bit-identical results and error texts.  With keep,
 // the device-resident topology and geometry stay alive for device_layout (free with
 // free_device_geometry).
+// The config-5 tet mesh built on the device (mesh_dev.cu): "" or why the host must build it.
+// perm_newid: the seeded permutation's new ids (host Fisher-Yates), or null.
+std::string device_kuhn_tets(const double ext[3], int n, const int kinds[6], const std::vector<int>* perm_newid,
+                             bool do_rcm, HostMesh& m);
 struct DeviceGeometry;
 std::string device_geometry(const HostMesh& m, HostGeometry& g, DeviceGeometry** keep = nullptr);
 void free_device_geometry(DeviceGeometry* g);

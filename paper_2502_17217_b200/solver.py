@@ -61,6 +61,7 @@ def lib():
     sig = {
         "sfv_mesh_box": (_vp, [_dp, _ip, _ip, C.c_double, C.c_uint64, C.c_char_p, C.c_int]),
         "sfv_mesh_kuhn_tets": (_vp, [_dp, C.c_int, _ip, C.c_uint64, C.c_int, C.c_int, C.c_char_p, C.c_int]),
+        "sfv_mesh_built_on_device": (C.c_int, [_vp]),
         "sfv_mesh_counts": (None, [_vp, _ip]),
         "sfv_mesh_export": (None, [_vp, _dp] + [_ip] * 7),
         "sfv_mesh_free": (None, [_vp]),
@@ -153,7 +154,10 @@ def kuhn_tet_mesh(extents, n: int, kinds, perm_seed: int = 0, permute: bool = Tr
     h = lib().sfv_mesh_kuhn_tets(dptr(e), int(n), iptr(k), C.c_uint64(perm_seed), int(permute), int(rcm), err, 256)
     if not h:
         raise SolidfvError(1, -1, err.value.decode())
-    return _export_mesh(h)
+    on_dev = bool(lib().sfv_mesh_built_on_device(h))
+    m = _export_mesh(h)
+    m.on_device = on_dev
+    return m
 
 
 # ------------------------------------------------------------------ device arrays

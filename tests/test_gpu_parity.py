@@ -562,3 +562,35 @@ def test_gmres_graph_option_rejects_unknown():
     ev = sv.ResidualEvaluator(case.mesh(), case.physics)
     with pytest.raises(sv.SolidfvError):
         ev.set_option("no_such_option", 1)
+
+
+@pytest.mark.parametrize("n,permute,rcm", [(8, True, True), (12, True, True), (12, False, False), (26, True, True)])
+def test_device_tet_mesh_equals_host(n, permute, rcm, monkeypatch):
+    """The config-5 mesh is built on the device (mesh_dev.cu: Kuhn split, face sorts, pairing,
+    RCM as a level-synchronous breadth-first order, orientation); it must equal the host
+    generator's array for array (SFV_HOST_MESH=1)."""
+    sv = _sv()
+    D, T = 1, 2
+    args = ((1.0, 1.0, 1.0), n, [D, T, T, T, T, T], 42, permute, rcm)
+    md = sv.kuhn_tet_mesh(*args)
+    assert md.on_device
+    monkeypatch.setenv("SFV_HOST_MESH", "1")
+    mh = sv.kuhn_tet_mesh(*args)
+    assert not mh.on_device
+    for f in ("points", "face_offsets", "face_points", "owner", "neighbour", "patch_kind", "patch_start",
+              "patch_count"):
+        a, b = getattr(md, f), getattr(mh, f)
+        assert np.array_equal(a, b), f
+    assert md.n_cells == mh.n_cells and md.n_internal == mh.n_internal
+
+
+def test_device_tet_mesh_full_size_time(monkeypatch):
+    """C5 at n = 160 (24.6M tets): device generator time (the host one takes ~36 s)."""
+    import time
+    sv = _sv()
+    D, T = 1, 2
+    t0 = time.time()
+    m = sv.kuhn_tet_mesh((1.0, 1.0, 1.0), 160, [D, T, T, T, T, T], 42, True, True)
+    dt = time.time() - t0
+    assert m.n_cells == 6 * 160 ** 3 and m.on_device
+    print(f"c5 n=160 mesh on the device: {dt:.2f} s")
