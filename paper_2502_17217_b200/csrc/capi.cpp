@@ -217,6 +217,11 @@ struct sfv_ctx {
     // host-buffer J.v: r_u uploaded on a copy stream while the ε and gradient passes run
     cudaStream_t copy = nullptr;
     cudaEvent_t ev_uv = nullptr, ev_ru = nullptr;
+    // chunked host-buffer J.v: r_u arrives in kHostChunks pieces, the face pass runs per piece
+    // and each piece of the result leaves on d2h while the next is computed
+    static constexpr int kHostChunks = 4;
+    cudaStream_t d2h = nullptr;
+    cudaEvent_t ev_ruk[kHostChunks] = {}, ev_outk[kHostChunks] = {};
     void drop_graph() {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);
@@ -237,6 +242,11 @@ struct sfv_ctx {
         if (ev_uv) cudaEventDestroy(ev_uv);
         if (ev_ru) cudaEventDestroy(ev_ru);
         if (copy) cudaStreamDestroy(copy);
+        for (int k = 0; k < kHostChunks; ++k) {
+            if (ev_ruk[k]) cudaEventDestroy(ev_ruk[k]);
+            if (ev_outk[k]) cudaEventDestroy(ev_outk[k]);
+        }
+        if (d2h) cudaStreamDestroy(d2h);
     }
 
     int fail(int code, int cell, const std::string& msg) {
@@ -2286,12 +2296,20 @@ int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v,
         return c->cuda_check("jv_host streams");
     // u and v first (the ε and gradient passes need them); r_u, read only by the face pass,
     // follows on the copy stream while those passes run
+    static const bool chunked_off = [] {
+        const char* e = std::getenv("SFV_JV_HOST_CHUNKS");
+        return e && std::atoi(e) <= 1;
+    }();
+    const bool chunked = !chunked_off && !c->use_fused && c->jv_path == 0 && !c->seq_reduce && c->nc >= 4096 &&
+                         c->singular_cell < 0;
     cudaMemcpyAsync(c->ucand.p, u, bytes, cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(c->tv.p, v, bytes, cudaMemcpyHostToDevice, c->stream);
     cudaEventRecord(c->ev_uv, c->stream);
     cudaStreamWaitEvent(c->copy, c->ev_uv, 0);
-    cudaMemcpyAsync(c->rcand.p, r_u, bytes, cudaMemcpyHostToDevice, c->copy);
-    cudaEventRecord(c->ev_ru, c->copy);
+    if (!chunked) {
+        cudaMemcpyAsync(c->rcand.p, r_u, bytes, cudaMemcpyHostToDevice, c->copy);
+        cudaEventRecord(c->ev_ru, c->copy);
+    }
     if (c->singular_cell >= 0) {
         cudaStreamWaitEvent(c->stream, c->ev_ru, 0);  // sfv_jv's GradientFailure / zero-direction rule
         const int e = sfv_jv(c, c->ucand.p, c->rcand.p, c->tv.p, c->wv.p, cell);
@@ -2303,6 +2321,48 @@ int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v,
     // (on an error, out holds the failed product, as the reference leaves its output undefined)
     if (cell) *cell = -1;
     reset_err(c);
+    if (chunked && !c->d2h) {
+        bool ok = cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) == cudaSuccess;
+        for (int k = 0; k < sfv_ctx::kHostChunks && ok; ++k)
+            ok = cudaEventCreateWithFlags(&c->ev_ruk[k], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&c->ev_outk[k], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) return c->cuda_check("jv_host streams");
+    }
+    if (chunked) {
+        // r_u and the result in tile-aligned pieces: the face pass of piece k starts when its
+        // r_u has arrived, and its result goes back while piece k + 1 is computed, so the copy
+        // back overlaps the upload of the rest of r_u (the two PCIe directions are independent)
+        const int K = sfv_ctx::kHostChunks;
+        const int ntiles = (c->nc + 31) / 32;
+        size_t lo[sfv_ctx::kHostChunks + 1];
+        for (int k = 0; k <= K; ++k)
+            lo[k] = 3 * std::min<size_t>(static_cast<size_t>(c->nc),
+                                         32 * static_cast<size_t>(static_cast<long long>(ntiles) * k / K));
+        for (int k = 0; k < K; ++k) {
+            cudaMemcpyAsync(c->rcand.p + lo[k], r_u + lo[k], sizeof(double) * (lo[k + 1] - lo[k]),
+                            cudaMemcpyHostToDevice, c->copy);
+            cudaEventRecord(c->ev_ruk[k], c->copy);
+        }
+        c->ps.nchunk = K;
+        c->ps.ru_chunk = c->ev_ruk;
+        c->ps.out_chunk = c->ev_outk;
+        jv_async(c, c->ucand.p, c->rcand.p, c->tv.p, c->wv.p, false);
+        c->ps.nchunk = 0;
+        c->ps.ru_chunk = nullptr;
+        c->ps.out_chunk = nullptr;
+        for (int k = 0; k < K; ++k) {
+            cudaStreamWaitEvent(c->d2h, c->ev_outk[k], 0);
+            cudaMemcpyAsync(out + lo[k], c->wv.p + lo[k], sizeof(double) * (lo[k + 1] - lo[k]), cudaMemcpyDeviceToHost,
+                            c->d2h);
+        }
+        cudaEventRecord(c->ev_ru, c->d2h);  // (reused: the last piece is home)
+        cudaStreamWaitEvent(c->stream, c->ev_ru, 0);
+        if (int e = c->cuda_check("jv_host")) return e;
+        if (int e = fetch(c, 0)) return e;
+        const int e = decode_residual_errors(c, true);
+        if (cell) *cell = e ? c->last.cell : -1;
+        return e;
+    }
     if (c->use_fused || c->jv_path != 0) cudaStreamWaitEvent(c->stream, c->ev_ru, 0);  // no in-pass wait
     c->ps.ru_ready = c->ev_ru;
     jv_async(c, c->ucand.p, c->rcand.p, c->tv.p, c->wv.p, false);

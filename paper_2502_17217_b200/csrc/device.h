@@ -176,6 +176,11 @@ struct PairScratch {
     cudaEvent_t ev_w = nullptr, ev_b = nullptr;
     // optional: r_u arrives on another stream (host-buffer J.v); the face pass waits for it
     cudaEvent_t ru_ready = nullptr;
+    // optional (host-buffer J.v): the face pass runs in nchunk launches over consecutive tile
+    // ranges; launch k waits for ru_chunk[k] (its share of r_u) and records out_chunk[k]
+    int nchunk = 0;
+    const cudaEvent_t* ru_chunk = nullptr;
+    cudaEvent_t* out_chunk = nullptr;
     const double* partials = nullptr;  // block partials (or, with bar, the fused pass's scratch)
     int npart = 0;
     // set: eps_perturb_kernel reduces the norms itself (grid barrier on this counter) and

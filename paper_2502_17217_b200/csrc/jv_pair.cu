@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
     flux_pair_kernel(DevMesh m, Physics ph, PatchTable pt, History hist, const double* __restrict__ wg,
                      const double* __restrict__ eps_p, const double* __restrict__ sig,
                      const double* __restrict__ bres, const double* __restrict__ r_u, double* __restrict__ out,
-                     ErrWords* __restrict__ err) {
+                     ErrWords* __restrict__ err, int tile0, int tile1) {
     // double-buffered per-slot results: one barrier per tile; the sums of tile i (warps
     // s < 3) overlap the face work of tile i + 1, and the barrier of tile i + 1 orders
     // them before buffer i & 1 is rewritten by tile i + 2
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
     // slot kinds lane-major, 8 bytes per cell: the summing thread reads them in one 64-bit load
     __shared__ __align__(8) unsigned char kind_buf[2][kCells][8];
     const int lane = threadIdx.x % kCells, s = threadIdx.x / kCells;
-    const int ntiles = (m.nc + kCells - 1) / kCells;
+    const int ntiles = tile1;  // this launch covers tiles [tile0, tile1) (the host-buffer J.v runs chunks)
     // Persistent grid-stride loop over tiles of kCells cells (= the tiles of the tables).
     // The slot indices of a tile and the epilogue operand r_u of (component s, cell) —
     // threads s < 3 do the per-cell sums — are loaded one iteration ahead, so a tile's
@@ -541,12 +541,12 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
     };
     int fr_next, o_next;
     double ru_next;
-    fetch(blockIdx.x, fr_next, o_next, ru_next);
+    fetch(tile0 + blockIdx.x, fr_next, o_next, ru_next);
     wait_predecessor();  // bres (and through it G, w, eps)
     const double eps = PERT ? *eps_p : 0.0;
     const bool zero = PERT && eps == 0.0;  // |v| = 0 short-circuit (nonlinear.cpp:110)
     int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    for (int tile = tile0 + blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         double(*res)[6][kCells] = res_buf[it & 1];
         unsigned char(*kind)[8] = kind_buf[it & 1];
         const int fr = fr_next, o = o_next;
@@ -818,15 +818,24 @@ void launch_s(const DevMesh& m, const Physics& ph, const PatchTable& pt, const H
     const double* cwg = wg;
     const double* sg = ps.sig;
     const double* br = ps.bres;
-    if (gen)
-        launch_win(flux_pair_kernel<PERT, S, true, false>, flux_grid<PERT, S, true, false>(ntiles), kCells * S, st,
-                   ps, m, ph, pt, hist, cwg, eps, sg, br, r_u, out, err);
-    else if (inlb)
-        launch_win(flux_pair_kernel<PERT, S, false, true>, flux_grid<PERT, S, false, true>(ntiles), kCells * S, st,
-                   ps, m, ph, pt, hist, cwg, eps, sg, br, r_u, out, err);
-    else
-        launch_win(flux_pair_kernel<PERT, S, false, false>, flux_grid<PERT, S, false, false>(ntiles), kCells * S, st,
-                   ps, m, ph, pt, hist, cwg, eps, sg, br, r_u, out, err);
+    // one launch, or (host-buffer J.v) one per chunk of tiles, each after its share of r_u has
+    // arrived and followed by an event for the copy of its share of the result
+    const int nk = ps.nchunk > 1 ? ps.nchunk : 1;
+    for (int k = 0; k < nk; ++k) {
+        const int t0 = static_cast<int>(static_cast<long long>(ntiles) * k / nk);
+        const int t1 = static_cast<int>(static_cast<long long>(ntiles) * (k + 1) / nk);
+        if (nk > 1 && ps.ru_chunk) cudaStreamWaitEvent(st, ps.ru_chunk[k], 0);
+        if (gen)
+            launch_win(flux_pair_kernel<PERT, S, true, false>, flux_grid<PERT, S, true, false>(t1 - t0), kCells * S,
+                       st, ps, m, ph, pt, hist, cwg, eps, sg, br, r_u, out, err, t0, t1);
+        else if (inlb)
+            launch_win(flux_pair_kernel<PERT, S, false, true>, flux_grid<PERT, S, false, true>(t1 - t0), kCells * S,
+                       st, ps, m, ph, pt, hist, cwg, eps, sg, br, r_u, out, err, t0, t1);
+        else
+            launch_win(flux_pair_kernel<PERT, S, false, false>, flux_grid<PERT, S, false, false>(t1 - t0), kCells * S,
+                       st, ps, m, ph, pt, hist, cwg, eps, sg, br, r_u, out, err, t0, t1);
+        if (nk > 1 && ps.out_chunk) cudaEventRecord(ps.out_chunk[k], st);
+    }
 }
 
 }  // namespace

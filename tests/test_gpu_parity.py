@@ -505,15 +505,17 @@ def test_alternative_jv_paths_bitwise(path, monkeypatch):
                           (orc.residual(u + eps * v) - r) / eps)
 
 
-def test_jv_host_buffers_bitwise():
-    """sfv_jv_host (host buffers; r_u uploaded on a copy stream while the first passes run)
-    returns the device-resident J.v bit for bit.  Pinned buffers (the copies are truly
-    asynchronous, as in bench.py) and a different r_u on every call, so a face pass that read
-    r_u before its upload finished would see the previous call's values and fail."""
+@pytest.mark.parametrize("n", [24, 100])
+def test_jv_host_buffers_bitwise(n):
+    """sfv_jv_host (host buffers; r_u uploaded in pieces on a copy stream while the first passes
+    run, the face pass per piece, the result copied back piece by piece) returns the
+    device-resident J.v bit for bit.  Pinned buffers (the copies are truly asynchronous, as in
+    bench.py) and a different r_u on every call, so a face pass that read r_u before its upload
+    finished would see the previous call's values and fail."""
     import ctypes as C
     import torch
     sv = _sv()
-    case = cases.config("c2", n=24)
+    case = cases.config("c2", n=n)
     mesh = case.mesh()
     ev = sv.ResidualEvaluator(mesh, case.physics)
     ev.set_time(1.0)
