@@ -219,7 +219,7 @@ struct sfv_ctx {
     cudaEvent_t ev_uv = nullptr, ev_ru = nullptr;
     // chunked host-buffer J.v: r_u arrives in kHostChunks pieces, the face pass runs per piece
     // and each piece of the result leaves on d2h while the next is computed
-    static constexpr int kHostChunks = 4;
+    static constexpr int kHostChunks = 16;  // at most (SFV_JV_HOST_CHUNKS, default 8)
     cudaStream_t d2h = nullptr;
     cudaEvent_t ev_ruk[kHostChunks] = {}, ev_outk[kHostChunks] = {};
     void drop_graph() {
@@ -2296,11 +2296,11 @@ int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v,
         return c->cuda_check("jv_host streams");
     // u and v first (the ε and gradient passes need them); r_u, read only by the face pass,
     // follows on the copy stream while those passes run
-    static const bool chunked_off = [] {
+    static const int host_chunks = [] {
         const char* e = std::getenv("SFV_JV_HOST_CHUNKS");
-        return e && std::atoi(e) <= 1;
+        return std::max(1, std::min(sfv_ctx::kHostChunks, e ? std::atoi(e) : 8));
     }();
-    const bool chunked = !chunked_off && !c->use_fused && c->jv_path == 0 && !c->seq_reduce && c->nc >= 4096 &&
+    const bool chunked = host_chunks > 1 && !c->use_fused && c->jv_path == 0 && !c->seq_reduce && c->nc >= 4096 &&
                          c->singular_cell < 0;
     cudaMemcpyAsync(c->ucand.p, u, bytes, cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(c->tv.p, v, bytes, cudaMemcpyHostToDevice, c->stream);
@@ -2332,7 +2332,7 @@ int sfv_jv_host(sfv_ctx* c, const double* u, const double* r_u, const double* v,
         // r_u and the result in tile-aligned pieces: the face pass of piece k starts when its
         // r_u has arrived, and its result goes back while piece k + 1 is computed, so the copy
         // back overlaps the upload of the rest of r_u (the two PCIe directions are independent)
-        const int K = sfv_ctx::kHostChunks;
+        const int K = host_chunks;
         const int ntiles = (c->nc + 31) / 32;
         size_t lo[sfv_ctx::kHostChunks + 1];
         for (int k = 0; k <= K; ++k)
