@@ -300,7 +300,19 @@ __global__ void __launch_bounds__(kAT, 1) arnoldi_kernel(const double* __restric
     cg::grid_group grid = cg::this_grid();
     const int lo = blockIdx.x * chunk;
     const int cnt = max(0, min(chunk, n - lo));
-    for (int e = threadIdx.x; e < cnt; e += kAT) wsh[e] = w_in[lo + e];
+    {  // w into shared memory: all of this thread's loads in flight together
+        double x[kAK];
+#pragma unroll
+        for (int k = 0; k < kAK; ++k) {
+            const int e = threadIdx.x + k * kAT;
+            x[k] = e < cnt ? w_in[lo + e] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < kAK; ++k) {
+            const int e = threadIdx.x + k * kAT;
+            if (e < cnt) wsh[e] = x[k];
+        }
+    }
     __syncthreads();
     const int G = gridDim.x;
     for (int i = 0; i <= j + 1; ++i) {

@@ -192,15 +192,13 @@ __global__ void level_kernel(int n, const int* __restrict__ rp, const int* __res
         if (UPPER) {
             for (int p = rp[i + 1] - 1; p >= rp[i] && col[p] > i; --p) {
                 int v;
-                while ((v = ld_acq(lev + col[p])) < 0) {
-                }
+                while ((v = ld_acq(lev + col[p])) < 0) __nanosleep(64);  // back off: the polls share L2
                 l = max(l, v + 1);
             }
         } else {
             for (int p = rp[i]; p < rp[i + 1] && col[p] < i; ++p) {
                 int v;
-                while ((v = ld_acq(lev + col[p])) < 0) {
-                }
+                while ((v = ld_acq(lev + col[p])) < 0) __nanosleep(64);
                 l = max(l, v + 1);
             }
         }
