@@ -103,6 +103,9 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     int* lp = reinterpret_cast<int*>(stage_src + kStages * kMaxRows * 3);  // [kLvl + 2]
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(lp + kLvl + 2);  // [kStages], 8-aligned
     double* zero_slot = reinterpret_cast<double*>(mbar + kStages);  // 0.0: read by absent dependencies
+    // per stage: (first position, count) of this CTA's slice, written by the producer before
+    // the stage's mbarrier arrive, so a compute thread does not redo the slice arithmetic
+    int2* stage_hdr = reinterpret_cast<int2*>(zero_slot + 2);  // [kStages]
     const uint32_t zero_addr = smem_u32(zero_slot);
     const uint32_t ring_base = smem_u32(ring);
     const uint32_t mbar_base = smem_u32(mbar);
@@ -128,6 +131,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
         if (!TSP(4)) b = a;
         const uint32_t bar = mbar_base + 8u * s;
         // positions are chunk (32) aligned: both copies are 16-byte multiples at 16-byte addresses
+        stage_hdr[s] = make_int2(a, b - a);
         mbar_expect(bar, static_cast<uint32_t>(b - a) * 120u);
         if (b > a) {
             bulk_copy(smem_u32(stage_rec + static_cast<size_t>(s) * kMaxRows * 96),
@@ -159,9 +163,9 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 ph[1] += t1 - t0;
                 t0 = t1;
             }
-            int a, b;
-            slice(l, a, b);
             const int s = l % kStages;
+            const int2 hd = stage_hdr[s];
+            const int a = hd.x, b = hd.x + hd.y;
             for (int j = threadIdx.x; TSP(16) && j < b - a; j += kThreads) {
                 const unsigned char* ch = stage_rec + static_cast<size_t>(s) * kMaxRows * 96 + (j / 32) * kChunk;
                 const int ln = j % 32;
@@ -313,7 +317,7 @@ cudaError_t launch_one(const StreamSet& set, int ncomp, const double* src, doubl
 }  // namespace
 
 int stream_smem_bytes(int ring, int max_rows, int stages) {
-    return ring * 24 + stages * max_rows * (96 + 24) + (kLvl + 2) * 4 + 8 * 8 + 16;
+    return ring * 24 + stages * max_rows * (96 + 24) + (kLvl + 2) * 4 + 8 * 8 + 16 + 8 * 8;
 }
 
 cudaError_t launch_tri_stream(const StreamSet& set, bool upper, int ncomp, const double* src, double* dst,
