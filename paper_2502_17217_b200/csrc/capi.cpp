@@ -1619,7 +1619,7 @@ int precond_create(sfv_ctx* c, int kind) {
                 s_rows = std::max(s_rows, (nch + kStreamCluster - 1) / kStreamCluster * 32);
             }
         if (s_rows <= kStreamMaxRows)
-            for (int cand : {1024, 2048, 3072, 4096}) {
+            for (int cand : {1024, 2048, 3072, 4095}) {  // (slot 4095 at most: the +0.0 slot)
                 std::vector<char> ok(scheds.size(), 0);
                 std::vector<std::thread> th;
                 for (size_t x = 0; x < scheds.size(); ++x)

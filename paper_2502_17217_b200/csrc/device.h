@@ -391,6 +391,8 @@ struct StreamSet {
     int max_rows = 0;  // positions per CTA per level (multiple of 32)
     int stages = 3;    // cp.async pipeline depth (levels in flight + 1)
 };
+// value ring(s) incl. the +0.0 slot (3 right-hand sides of ring + 1 doubles), 128-byte rounded
+__host__ __device__ inline int stream_ring_bytes(int ring) { return ((ring + 1) * 24 + 127) & ~127; }
 int stream_smem_bytes(int ring, int max_rows, int stages);
 cudaError_t launch_tri_stream(const StreamSet& set, bool upper, int ncomp, const double* src, double* dst,
                               cudaStream_t s);

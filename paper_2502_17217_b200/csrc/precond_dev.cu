@@ -335,9 +335,14 @@ __global__ void records_kernel(Slicing s, const int* __restrict__ order, const i
     const int ln = p & 31;
     if (ln < 24) reinterpret_cast<uint64_t*>(cb + 2880)[ln] = 0ull;  // bytes 2880..3071
     __syncwarp();
+    int r = 0, o = 0, l = 0;
+    if (p < s.np) {
+        l = level_of(s, p);
+        owner_ordinal(s, p, l, r, o);
+    }
     for (int k = 0; k < 8; ++k) {
         cval[k * 32 + ln] = 0.0;
-        cdep[k * 32 + ln] = 0xffff;
+        cdep[k * 32 + ln] = static_cast<uint16_t>((r << 12) | s.ring);  // absent: the reader's +0.0 slot
     }
     if (p >= s.np) {  // tail of the last chunk
         cdiag[ln] = 0.0;
@@ -345,9 +350,6 @@ __global__ void records_kernel(Slicing s, const int* __restrict__ order, const i
         cout[ln] = -1;
         return;
     }
-    const int l = level_of(s, p);
-    int r, o;
-    owner_ordinal(s, p, l, r, o);
     cown[ln] = static_cast<uint16_t>(o % s.ring);
     cdiag[ln] = 1.0;
     const int i = order[p];
@@ -629,7 +631,7 @@ std::string device_ilu_setup(const DevTopoView& t, double kbar, bool transient, 
         return "device ilu: a row has more than 8 dependencies";
     }
     out.ring = 0;
-    for (int cand : {1024, 2048, 3072, 4096})
+    for (int cand : {1024, 2048, 3072, 4095})  // (the +0.0 slot is slot index `ring`, 12 bits)
         if (cand >= nh[0]) {
             out.ring = cand;
             break;

@@ -672,7 +672,7 @@ namespace sfv {
 bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed,
                           const std::vector<int>* out_pos) {
     StageClock sc;
-    if (t.maxd > 8) return false;
+    if (t.maxd > 8 || ring > 4095) return false;  // slot index ring (12 bits) is the +0.0 slot
     const int np = t.n_pos;
     std::vector<int> owner(np, 0), ordinal(np, 0), level_of(np, 0);
     std::vector<int> count(cs, 0);
@@ -714,7 +714,7 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
         if (p >= np) {  // tail: no dependencies
             for (int k = 0; k < 8; ++k) {
                 cval[k * 32 + l] = 0.0;
-                cdep[k * 32 + l] = 0xffff;
+                cdep[k * 32 + l] = static_cast<uint16_t>(ring);  // rank 0's +0.0 slot
             }
             cdiag[l] = 0.0;
             cown[l] = 0;
@@ -727,7 +727,8 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
         cout[l] = t.order[p] < 0 ? -1 : out_pos ? (*out_pos)[t.order[p]] : t.order[p];
         cdiag[l] = t.diag[p];
         for (int k = 0; k < 8; ++k) {
-            cdep[k * 32 + l] = 0xffff;
+            // an absent dependency reads the +0.0 slot of the reading CTA's ring
+            cdep[k * 32 + l] = static_cast<uint16_t>((owner[p] << 12) | ring);
             cval[k * 32 + l] = 0.0;
             if (k >= t.maxd) continue;
             const int q = t.ell_pcol[static_cast<size_t>(k) * np + p];

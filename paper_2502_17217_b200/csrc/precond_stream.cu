@@ -97,8 +97,11 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     const int ptid = threadIdx.x - kThreads;
     extern __shared__ __align__(16) unsigned char smem[];
     const int ring_n = set.ring;
-    double* ring = reinterpret_cast<double*>(smem);  // [NRHS][ring_n]
-    unsigned char* stage_rec = smem + static_cast<size_t>(ring_n) * 24;  // [kStages][kMaxRows / 32 chunks]
+    // [NRHS][ring_n + 1]: slot ring_n of each array holds +0.0 — the records point an absent
+    // dependency there (its factor value is 0), so the dependency loads need no predicate
+    const int ring_s = ring_n + 1;
+    double* ring = reinterpret_cast<double*>(smem);
+    unsigned char* stage_rec = smem + stream_ring_bytes(ring_n);  // [kStages][kMaxRows / 32 chunks]
     double* stage_src = reinterpret_cast<double*>(stage_rec + static_cast<size_t>(kStages) * kMaxRows * 96);  // [kStages][kMaxRows*3]
     int* lp = reinterpret_cast<int*>(stage_src + kStages * kMaxRows * 3);  // [kLvl + 2]
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(lp + kLvl + 2);  // [kStages], 8-aligned
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     };
     if (threadIdx.x < kStages) mbar_init(mbar_base + 8u * threadIdx.x, 1);
     if (threadIdx.x == 0) *zero_slot = 0.0;
+    if (threadIdx.x < NRHS) ring[threadIdx.x * ring_s + ring_n] = 0.0;
     stage_levels(0);  // its __syncthreads also publishes the mbarrier init
     if (producer)
         for (int l = 0; l < kStages - 1; ++l) issue(l);
@@ -177,26 +181,23 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 double z[NRHS];
 #pragma unroll
                 for (int k = 0; k < NRHS; ++k) z[k] = stage_src[(s * kMaxRows + j) * 3 + comp + k];
-                // Branch-free: an absent dependency (0xffff) reads a zero slot with factor value
-                // 0, and z - 0*0 is z bit for bit (also for -0, inf, NaN), as the reference's
-                // skipping it.  The eight loads of a right-hand side are one asm statement, so they
+                // Branch-free: an absent dependency reads the +0.0 slot with factor value 0, and
+                // z - 0*0 is z bit for bit (also for -0, inf, NaN), as the reference's skipping it.  The eight loads of a right-hand side are one asm statement, so they
                 // leave back to back (compiled separately, the scheduler put the eighth after the
                 // pivot reciprocal, ~40 instructions later, on the level's critical path).
                 uint32_t ad[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const unsigned d = dep[q];
-                    ad[q] = d != 0xffffu && TSP(8)
-                                ? mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank)
-                                : zero_addr;
+                    ad[q] = TSP(8) ? mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank)
+                                   : zero_addr;
                 }
                 double dv[8][NRHS];
 #pragma unroll
                 for (int k = 0; k < NRHS; ++k) {
                     uint32_t a8[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        a8[q] = ad[q] + (dep[q] != 0xffffu ? static_cast<uint32_t>(k * ring_n * 8) : 0u);
+                    for (int q = 0; q < 8; ++q) a8[q] = ad[q] + static_cast<uint32_t>(k * ring_s * 8);
                     asm volatile(
                         "ld.shared::cluster.f64 %0, [%8];\n\t"
                         "ld.shared::cluster.f64 %1, [%9];\n\t"
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 const int oi = reinterpret_cast<const int*>(ch + kOffOutIdx)[ln];
 #pragma unroll
                 for (int k = 0; k < NRHS; ++k) {
-                    ring[k * ring_n + own] = z[k];
+                    ring[k * ring_s + own] = z[k];
                     if (TSP(2) && oi >= 0) dst[3 * static_cast<size_t>(oi) + comp + k] = z[k];
                 }
             }
@@ -317,7 +318,7 @@ cudaError_t launch_one(const StreamSet& set, int ncomp, const double* src, doubl
 }  // namespace
 
 int stream_smem_bytes(int ring, int max_rows, int stages) {
-    return ring * 24 + stages * max_rows * (96 + 24) + (kLvl + 2) * 4 + 8 * 8 + 16 + 8 * 8;
+    return stream_ring_bytes(ring) + stages * max_rows * (96 + 24) + (kLvl + 2) * 4 + 8 * 8 + 16 + 8 * 8;
 }
 
 cudaError_t launch_tri_stream(const StreamSet& set, bool upper, int ncomp, const double* src, double* dst,
