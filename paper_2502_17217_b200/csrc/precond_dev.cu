@@ -316,7 +316,7 @@ __global__ void ring_need_kernel(Slicing s, const int* __restrict__ order, const
 }
 
 // pass 2: the records in the device chunk layout (precond_host.h: val[8][32], diag[32],
-// dep[8][32], own[32], zero tail; 3072 bytes per 32 positions)
+// dep[8][32], own[32], out[32], zero tail; 3072 bytes per 32 positions)
 // out (kOffOut): the forward sweep stores each value at its row's backward-sweep position
 // (out_pos), the backward sweep at its row
 template <bool UPPER>

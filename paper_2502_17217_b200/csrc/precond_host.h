@@ -92,7 +92,7 @@ void schedule_ic0(const ScalarCsr& L, TriSchedule& fwd, TriSchedule& bwd);
 // (owner << 12 | slot).  Returns false when a ring slot would be overwritten before its
 // last reader (then the caller keeps another sweep), or a slice exceeds max_rows.
 struct StreamRecord {
-    uint16_t dep[8];  // owner << 12 | slot, 0xffff = none; at most 8 entries per row
+    uint16_t dep[8];  // owner << 12 | slot; absent: the reader's +0.0 slot (slot = ring size)
     uint16_t own;     // this position's slot in its owner's ring
     uint16_t pad[3];
     double val[8];
