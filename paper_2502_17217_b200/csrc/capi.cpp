@@ -1438,7 +1438,8 @@ std::string precond_create_device(sfv_ctx* c, int level) {
     cudaGetLastError();
     if (!why.empty()) return why;
     const int smem_cap = 232448;
-    const int stages = std::min(8, (smem_cap - stream_smem_bytes(ds.ring, ds.max_rows, 0)) / (ds.max_rows * 120));
+    const int stages =
+        std::min(8, (smem_cap - stream_smem_bytes(ds.ring, ds.max_rows, 0)) / (ds.max_rows * (kStreamRec + 24)));
     if (stages < 3) {
         ds.release();
         return "device ilu: shared memory holds fewer than 3 stages";
@@ -1472,8 +1473,8 @@ std::string precond_create_device(sfv_ctx* c, int level) {
     c->U[0].u2l.adopt(ds.U.u2l, ds.U.n_pos);
     c->U[0].view.u2l = c->U[0].u2l.p;
     ds.U.u2l = nullptr;
-    c->srec[0].adopt(ds.L.rec, (static_cast<size_t>(ds.L.n_pos) + 31) / 32 * 3072);
-    c->srec[3].adopt(ds.U.rec, (static_cast<size_t>(ds.U.n_pos) + 31) / 32 * 3072);
+    c->srec[0].adopt(ds.L.rec, (static_cast<size_t>(ds.L.n_pos) + 31) / 32 * kStreamChunk);
+    c->srec[3].adopt(ds.U.rec, (static_cast<size_t>(ds.U.n_pos) + 31) / 32 * kStreamChunk);
     ds.L.rec = ds.U.rec = nullptr;
     c->sL.t[0] = DevStream{ds.L.n_levels, c->L[0].view.level_ptr, c->srec[0].p};
     c->sU.t[0] = DevStream{ds.U.n_levels, c->U[0].view.level_ptr, c->srec[3].p};
@@ -1635,7 +1636,8 @@ int precond_create(sfv_ctx* c, int kind) {
                 }
             }
         const int smem_cap = 232448;
-        s_stages = s_ring ? std::min(8, (smem_cap - stream_smem_bytes(s_ring, s_rows, 0)) / (s_rows * 120)) : 0;
+        s_stages = s_ring ? std::min(8, (smem_cap - stream_smem_bytes(s_ring, s_rows, 0)) / (s_rows * (kStreamRec + 24)))
+                          : 0;
         stream_ok_all = s_ring > 0 && s_stages >= 3;
     }
     pt.mark("stream records");

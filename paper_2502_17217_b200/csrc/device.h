@@ -15,6 +15,7 @@
 //   * per-patch BC values (already multiplied by t when ramped) are kernel arguments.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <string>
 
@@ -391,6 +392,18 @@ struct StreamSet {
     int max_rows = 0;  // positions per CTA per level (multiple of 32)
     int stages = 3;    // cp.async pipeline depth (levels in flight + 1)
 };
+// Streamed-sweep records, per chunk of 32 positions (field-major, bank-conflict-free reads):
+// val[8][32] doubles, diag[32], dep[8][32] u32, own[32] u16, out[32] i32, zero tail.  A dep word
+// is the dependency's shared::cluster window offset from the ring base: owner rank << 24 |
+// slot * 8 (the layout mapa.shared::cluster produces on sm_100, scripts/probes/mapa_probe.cu),
+// so the sweep forms each load address with one add; an absent dependency is the reading
+// CTA's +0.0 slot (slot = ring size).
+constexpr int kStreamChunk = 3584, kStreamRec = 112;
+constexpr int kStreamOffDiag = 2048, kStreamOffDep = 2304, kStreamOffOwn = 3328, kStreamOffOut = 3392,
+              kStreamOffEnd = 3520;
+__host__ __device__ inline uint32_t stream_dep(int rank, int slot) {
+    return (static_cast<uint32_t>(rank) << 24) | (static_cast<uint32_t>(slot) * 8u);
+}
 // value ring(s) incl. the +0.0 slot (3 right-hand sides of ring + 1 doubles), 128-byte rounded
 __host__ __device__ inline int stream_ring_bytes(int ring) { return ((ring + 1) * 24 + 127) & ~127; }
 int stream_smem_bytes(int ring, int max_rows, int stages);

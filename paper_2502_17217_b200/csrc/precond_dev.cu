@@ -14,7 +14,7 @@
 //   4. the IKJ numeric phase (linalg.cpp:283-299): ilu_numeric_kernel of precond.cu, rows in
 //      level order — the factor is bit-identical to the host's and the reference's;
 //   5. positions (rows grouped by level, ascending row within a level, levels padded to 32),
-//      the U -> L position map, and the streamed sweep's 96-byte records with the DSMEM
+//      the U -> L position map, and the streamed sweep's 112-byte records with the DSMEM
 //      owner / ring slot of every dependency (build_stream_records' layout and its ring check).
 // Position order does not change any result: a row's arithmetic is fixed by its entries.
 // Returns "" or the reason the caller falls back to the host setup (symmetry patches couple
@@ -315,8 +315,8 @@ __global__ void ring_need_kernel(Slicing s, const int* __restrict__ order, const
     atomicMax(need, req);
 }
 
-// pass 2: the records in the device chunk layout (precond_host.h: val[8][32], diag[32],
-// dep[8][32], own[32], out[32], zero tail; 3072 bytes per 32 positions)
+// pass 2: the records in the device chunk layout (device.h kStream*: val[8][32], diag[32],
+// dep[8][32], own[32], out[32], zero tail; 3584 bytes per 32 positions)
 // out (kOffOut): the forward sweep stores each value at its row's backward-sweep position
 // (out_pos), the backward sweep at its row
 template <bool UPPER>
@@ -326,15 +326,14 @@ __global__ void records_kernel(Slicing s, const int* __restrict__ order, const i
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const int nchunk = (s.np + 31) / 32;
     if (p >= nchunk * 32) return;
-    unsigned char* cb = rec + static_cast<size_t>(p >> 5) * 3072;
+    unsigned char* cb = rec + static_cast<size_t>(p >> 5) * kStreamChunk;
     double* cval = reinterpret_cast<double*>(cb);
-    double* cdiag = reinterpret_cast<double*>(cb + 2048);
-    uint16_t* cdep = reinterpret_cast<uint16_t*>(cb + 2304);
-    uint16_t* cown = reinterpret_cast<uint16_t*>(cb + 2816);
-    int* cout = reinterpret_cast<int*>(cb + 2880);
+    double* cdiag = reinterpret_cast<double*>(cb + kStreamOffDiag);
+    uint32_t* cdep = reinterpret_cast<uint32_t*>(cb + kStreamOffDep);
+    uint16_t* cown = reinterpret_cast<uint16_t*>(cb + kStreamOffOwn);
+    int* cout = reinterpret_cast<int*>(cb + kStreamOffOut);
     const int ln = p & 31;
-    if (ln < 24) reinterpret_cast<uint64_t*>(cb + 2880)[ln] = 0ull;  // bytes 2880..3071
-    __syncwarp();
+    if (ln < (kStreamChunk - kStreamOffEnd) / 8) reinterpret_cast<uint64_t*>(cb + kStreamOffEnd)[ln] = 0ull;
     int r = 0, o = 0, l = 0;
     if (p < s.np) {
         l = level_of(s, p);
@@ -342,7 +341,7 @@ __global__ void records_kernel(Slicing s, const int* __restrict__ order, const i
     }
     for (int k = 0; k < 8; ++k) {
         cval[k * 32 + ln] = 0.0;
-        cdep[k * 32 + ln] = static_cast<uint16_t>((r << 12) | s.ring);  // absent: the reader's +0.0 slot
+        cdep[k * 32 + ln] = stream_dep(r, s.ring);  // absent: the reader's +0.0 slot
     }
     if (p >= s.np) {  // tail of the last chunk
         cdiag[ln] = 0.0;
@@ -362,7 +361,7 @@ __global__ void records_kernel(Slicing s, const int* __restrict__ order, const i
         const int q = pos[dq[k]];
         int rq, oq;
         owner_ordinal(s, q, level_of(s, q), rq, oq);
-        cdep[k * 32 + ln] = static_cast<uint16_t>((rq << 12) | (oq % s.ring));
+        cdep[k * 32 + ln] = stream_dep(rq, oq % s.ring);
         cval[k * 32 + ln] = val[dk[k]];
     }
 }
@@ -644,7 +643,7 @@ std::string device_ilu_setup(const DevTopoView& t, double kbar, bool transient, 
     for (int w = 0; w < 2; ++w) {
         DevSweep& sw = w ? out.U : out.L;
         const size_t nchunk = (static_cast<size_t>(sw.n_pos) + 31) / 32;
-        sw.rec = keep_alloc<unsigned char>(nchunk * 3072);
+        sw.rec = keep_alloc<unsigned char>(nchunk * kStreamChunk);
         if (!sw.rec) {
             out.release();
             return "device ilu: out of memory";

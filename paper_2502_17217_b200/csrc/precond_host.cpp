@@ -1,6 +1,7 @@
 // precond_host.cpp — preconditioner setup on the host (once per run, as in the reference:
 // run_steps factors once and reuses the factor for every step, nonlinear.cpp:390-400).
 #include "host_threads.h"
+#include "device.h"
 #include "precond_host.h"
 
 #include <algorithm>
@@ -690,8 +691,8 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
         }
     }
     sc.mark("records owners");
-    // device chunk layout (precond_host.h): per 32 positions val[8][32], diag[32], dep[8][32],
-    // own[32]; positions are whole chunks (levels padded to 32), every byte written below
+    // device chunk layout (device.h kStream*): per 32 positions val[8][32], diag[32], dep[8][32],
+    // own[32], out[32]; positions are whole chunks (levels padded to 32), every byte written below
     const size_t nchunk = (static_cast<size_t>(np) + 31) / 32;
     packed.resize(nchunk * kChunkBytes);
     sc.mark("records alloc");
@@ -704,17 +705,17 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
     for (int ch = c0; ch < c1 && !bad; ++ch) {
         unsigned char* cb = packed.data() + static_cast<size_t>(ch) * kChunkBytes;
         double* cval = reinterpret_cast<double*>(cb);
-        double* cdiag = reinterpret_cast<double*>(cb + 2048);
-        uint16_t* cdep = reinterpret_cast<uint16_t*>(cb + 2304);
-        uint16_t* cown = reinterpret_cast<uint16_t*>(cb + 2816);
-        int32_t* cout = reinterpret_cast<int32_t*>(cb + kOffOut);
-        std::memset(cb + 2880, 0, kChunkBytes - 2880);
+        double* cdiag = reinterpret_cast<double*>(cb + kStreamOffDiag);
+        uint32_t* cdep = reinterpret_cast<uint32_t*>(cb + kStreamOffDep);
+        uint16_t* cown = reinterpret_cast<uint16_t*>(cb + kStreamOffOwn);
+        int32_t* cout = reinterpret_cast<int32_t*>(cb + kStreamOffOut);
+        std::memset(cb + kStreamOffEnd, 0, kChunkBytes - kStreamOffEnd);
     for (int l = 0; l < 32; ++l) {
         const int p = ch * 32 + l;
         if (p >= np) {  // tail: no dependencies
             for (int k = 0; k < 8; ++k) {
                 cval[k * 32 + l] = 0.0;
-                cdep[k * 32 + l] = static_cast<uint16_t>(ring);  // rank 0's +0.0 slot
+                cdep[k * 32 + l] = stream_dep(0, ring);  // rank 0's +0.0 slot
             }
             cdiag[l] = 0.0;
             cown[l] = 0;
@@ -728,7 +729,7 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
         cdiag[l] = t.diag[p];
         for (int k = 0; k < 8; ++k) {
             // an absent dependency reads the +0.0 slot of the reading CTA's ring
-            cdep[k * 32 + l] = static_cast<uint16_t>((owner[p] << 12) | ring);
+            cdep[k * 32 + l] = stream_dep(owner[p], ring);
             cval[k * 32 + l] = 0.0;
             if (k >= t.maxd) continue;
             const int q = t.ell_pcol[static_cast<size_t>(k) * np + p];
@@ -740,7 +741,7 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
                 bad = true;
                 return;
             }
-            cdep[k * 32 + l] = static_cast<uint16_t>((r << 12) | (ordinal[q] % ring));
+            cdep[k * 32 + l] = stream_dep(r, ordinal[q] % ring);
             cval[k * 32 + l] = t.ell_val[static_cast<size_t>(k) * np + p];
             if (stats) {
                 ++n_dep;

@@ -85,32 +85,32 @@ bool ic0_factor(const ScalarCsr& a, ScalarCsr& L);
 // z_i loses L_ji z_j for j descending, then / L_ii — both in dependency-level order.
 void schedule_ic0(const ScalarCsr& L, TriSchedule& fwd, TriSchedule& bwd);
 
-// Streamed-sweep records (precond.cu, tri_stream_kernel): one 96-byte record per position,
+// Streamed-sweep records (precond.cu, tri_stream_kernel): one 112-byte record per position,
 // position order.  Level l's positions are split into `cs` contiguous chunk-aligned slices
 // (CTA r of the cluster owns slice r); each CTA stores its positions' values in a ring of
 // `ring` slots in its shared memory, and every dependency is recorded as its DSMEM address
 // (owner << 12 | slot).  Returns false when a ring slot would be overwritten before its
 // last reader (then the caller keeps another sweep), or a slice exceeds max_rows.
-struct StreamRecord {
-    uint16_t dep[8];  // owner << 12 | slot; absent: the reader's +0.0 slot (slot = ring size)
+struct StreamRecord {  // (the logical record; stored field-major per chunk, device.h kStream*)
+    uint32_t dep[8];  // owner << 24 | slot * 8; absent: the reader's +0.0 slot (slot = ring size)
     uint16_t own;     // this position's slot in its owner's ring
-    uint16_t pad[3];
+    uint16_t pad;
+    int32_t out;      // where the sweep stores the value (-1: level padding)
     double val[8];
     double diag;
 };
-static_assert(sizeof(StreamRecord) == 96, "record layout");
+static_assert(sizeof(StreamRecord) == 112, "record layout");
 // Built directly in the device chunk layout below (every byte written by the parallel pass).
 bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed,
                           const std::vector<int>* out_pos = nullptr);
 // Device layout of the records: per chunk of 32 positions (levels are padded to 32), the
-// fields as arrays over the 32 positions — val[8][32], diag[32], dep[8][32], own[32],
-// 3072 bytes — so that a warp reading one field of 32 consecutive rows from shared
+// fields as arrays over the 32 positions — val[8][32], diag[32], dep[8][32] (u32), own[32],
+// out[32], 3584 bytes (device.h kStream*) — so that a warp reading one field of 32 consecutive rows from shared
 // memory is bank-conflict free (the 96-byte AoS record was read at a 96-byte lane stride).
-// Bytes 2880..3007: out[32] (int32), where the sweep stores the position's value: the forward
+// out[32] (int32): where the sweep stores the position's value: the forward
 // sweep writes in the backward sweep's position order, the backward sweep writes rows, so no
 // permute or scatter pass runs between or after them (-1: level padding, nothing stored).
-constexpr int kChunkBytes = 3072;
-constexpr int kOffOut = 2880;
+constexpr int kChunkBytes = 3584;  // = kStreamChunk (device.h)
 
 
 // Block-pipelined sweep (precond_pipe.cu): the rows, in sweep order, are cut into `blocks`

@@ -8,9 +8,9 @@
 //   * CTA r owns a contiguous chunk-aligned slice of the level's positions and computes
 //     them; their values go into CTA r's shared-memory ring, from where later levels read
 //     them over DSMEM (one ld.shared::cluster pair per dependency, ~200 cycles);
-//   * each position's factor row is a 96-byte record (16-bit DSMEM address of every
+//   * each position's factor row is a 112-byte record (32-bit DSMEM window offset of every
 //     dependency, its value, the pivot), stored field-major per chunk of 32 positions
-//     (pack_stream_chunks: bank-conflict-free shared-memory reads) and streamed kStages-1
+//     (device.h kStream*: bank-conflict-free shared-memory reads) and streamed kStages-1
 //     levels ahead with cp.async into shared-memory stages — the dependent chain per level
 //     is only DSMEM loads + FMA-free FP64 arithmetic, never an HBM round trip;
 //   * the value ring is one array per right-hand side ([NRHS][ring] doubles), so the 32
@@ -52,14 +52,10 @@ constexpr int kThreads = SFV_STREAM_THREADS;
 constexpr int kLvl = 1024;
 
 // field offsets inside a 3072-byte chunk of 32 records (precond_host.h: pack_stream_chunks)
-constexpr int kChunk = 3072, kOffDiag = 2048, kOffDep = 2304, kOffOwn = 2816, kOffOutIdx = 2880;
+constexpr int kChunk = kStreamChunk, kRec = kStreamRec, kOffDiag = kStreamOffDiag, kOffDep = kStreamOffDep,
+              kOffOwn = kStreamOffOwn, kOffOutIdx = kStreamOffOut;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
 
 __device__ __forceinline__ void mbar_init(uint32_t a, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -102,7 +98,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     const int ring_s = ring_n + 1;
     double* ring = reinterpret_cast<double*>(smem);
     unsigned char* stage_rec = smem + stream_ring_bytes(ring_n);  // [kStages][kMaxRows / 32 chunks]
-    double* stage_src = reinterpret_cast<double*>(stage_rec + static_cast<size_t>(kStages) * kMaxRows * 96);  // [kStages][kMaxRows*3]
+    double* stage_src = reinterpret_cast<double*>(stage_rec + static_cast<size_t>(kStages) * kMaxRows * kRec);  // [kStages][kMaxRows*3]
     int* lp = reinterpret_cast<int*>(stage_src + kStages * kMaxRows * 3);  // [kLvl + 2]
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(lp + kLvl + 2);  // [kStages], 8-aligned
     double* zero_slot = reinterpret_cast<double*>(mbar + kStages);  // 0.0: read by absent dependencies
@@ -111,6 +107,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     int2* stage_hdr = reinterpret_cast<int2*>(zero_slot + 2);  // [kStages]
     const uint32_t zero_addr = smem_u32(zero_slot);
     const uint32_t ring_base = smem_u32(ring);
+    const uint32_t ring_lo = ring_base & 0xffffffu;
     const uint32_t mbar_base = smem_u32(mbar);
     int lbase = 0;
     auto stage_levels = [&](int base) {
@@ -135,11 +132,11 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
         const uint32_t bar = mbar_base + 8u * s;
         // positions are chunk (32) aligned: both copies are 16-byte multiples at 16-byte addresses
         stage_hdr[s] = make_int2(a, b - a);
-        mbar_expect(bar, static_cast<uint32_t>(b - a) * 120u);
+        mbar_expect(bar, static_cast<uint32_t>(b - a) * (kRec + 24u));
         if (b > a) {
-            bulk_copy(smem_u32(stage_rec + static_cast<size_t>(s) * kMaxRows * 96),
-                      reinterpret_cast<const unsigned char*>(t.rec) + static_cast<size_t>(a) * 96,
-                      static_cast<uint32_t>(b - a) * 96u, bar);
+            bulk_copy(smem_u32(stage_rec + static_cast<size_t>(s) * kMaxRows * kRec),
+                      reinterpret_cast<const unsigned char*>(t.rec) + static_cast<size_t>(a) * kRec,
+                      static_cast<uint32_t>(b - a) * kRec, bar);
             bulk_copy(smem_u32(stage_src + s * kMaxRows * 3), src + 3 * static_cast<size_t>(a),
                       static_cast<uint32_t>(b - a) * 24u, bar);
         }
@@ -171,11 +168,11 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
             const int2 hd = stage_hdr[s];
             const int a = hd.x, b = hd.x + hd.y;
             for (int j = threadIdx.x; TSP(16) && j < b - a; j += kThreads) {
-                const unsigned char* ch = stage_rec + static_cast<size_t>(s) * kMaxRows * 96 + (j / 32) * kChunk;
+                const unsigned char* ch = stage_rec + static_cast<size_t>(s) * kMaxRows * kRec + (j / 32) * kChunk;
                 const int ln = j % 32;
                 const double* rval = reinterpret_cast<const double*>(ch) + ln;  // [q * 32]
-                const unsigned short* rdep = reinterpret_cast<const unsigned short*>(ch + kOffDep) + ln;  // [q * 32]
-                unsigned short dep[8];
+                const uint32_t* rdep = reinterpret_cast<const uint32_t*>(ch + kOffDep) + ln;  // [q * 32]
+                uint32_t dep[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) dep[q] = rdep[q * 32];
                 double z[NRHS];
@@ -185,12 +182,13 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 // z - 0*0 is z bit for bit (also for -0, inf, NaN), as the reference's skipping it.  The eight loads of a right-hand side are one asm statement, so they
                 // leave back to back (compiled separately, the scheduler put the eighth after the
                 // pivot reciprocal, ~40 instructions later, on the level's critical path).
+                // a dep word is the window offset from the ring base (owner << 24 | slot * 8): the
+                // load address is one add (ring_lo: the ring base without this CTA's rank byte)
                 uint32_t ad[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const unsigned d = dep[q];
-                    ad[q] = TSP(8) ? mapa(ring_base + (d & 0xfffu) * 8u, TSP(64) ? static_cast<int>(d >> 12) : rank)
-                                   : zero_addr;
+                    const uint32_t d = TSP(64) ? dep[q] : (dep[q] & 0xffffffu) | (static_cast<uint32_t>(rank) << 24);
+                    ad[q] = TSP(8) ? d + ring_lo : zero_addr;
                 }
                 double dv[8][NRHS];
 #pragma unroll
@@ -318,7 +316,7 @@ cudaError_t launch_one(const StreamSet& set, int ncomp, const double* src, doubl
 }  // namespace
 
 int stream_smem_bytes(int ring, int max_rows, int stages) {
-    return stream_ring_bytes(ring) + stages * max_rows * (96 + 24) + (kLvl + 2) * 4 + 8 * 8 + 16 + 8 * 8;
+    return stream_ring_bytes(ring) + stages * max_rows * (kRec + 24) + (kLvl + 2) * 4 + 8 * 8 + 16 + 8 * 8;
 }
 
 cudaError_t launch_tri_stream(const StreamSet& set, bool upper, int ncomp, const double* src, double* dst,
