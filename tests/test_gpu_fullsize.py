@@ -119,23 +119,22 @@ def _block_aggregates(x, nb):
     return np.add.reduceat(c, edges[:-1], axis=0), np.add.reduceat(c * c, edges[:-1], axis=0), np.diff(edges)
 
 
-def _check_field(fx, prefix, x, tol=U_TOL, blocks=True):
-    """Sampled cells element-wise, every cell through per-block sums / sums of squares
-    (blocks=False: the sample and the global norm only)."""
+def _check_field(fx, prefix, x, tol=U_TOL):
+    """"Within tol relative" as every cell within tol * max|field| of the reference: the sampled
+    cells element-wise, and every cell through per-block sums and sums of squares (a block whose
+    cells all lie within e of the reference has |sum d| <= n e and |sum (u^2 - u_ref^2)| <=
+    2 e sqrt(n sum u_ref^2) + n e^2)."""
     c = x.reshape(-1, 3)
     ref_s = fx[f"{prefix}_sample"]
     scale = float(fx[f"{prefix}_max"])
     err = np.max(np.abs(c[fx["sample_idx"]] - ref_s)) / scale
     assert err <= tol, f"{prefix}: sampled cells differ by {err:.3e} of max|{prefix}|"
-    if not blocks:
-        assert abs(np.linalg.norm(x) - float(fx[f"{prefix}_norm"])) <= tol * float(fx[f"{prefix}_norm"])
-        return err
     s, q, cnt = _block_aggregates(x, fx[f"{prefix}_block_sum"].shape[0])
     rs, rq = fx[f"{prefix}_block_sum"], fx[f"{prefix}_block_sq"]
-    # |sum d| <= sqrt(n sum d^2): relative to the block's own magnitude
-    bound = tol * np.sqrt(np.maximum(rq, 1e-300) * cnt[:, None])
-    assert np.all(np.abs(s - rs) <= bound + 1e-300), f"{prefix}: block sums differ"
-    assert np.all(np.abs(q - rq) <= 2 * tol * rq + 1e-300), f"{prefix}: block sums of squares differ"
+    e = tol * scale
+    n = cnt[:, None].astype(float)
+    assert np.all(np.abs(s - rs) <= n * e), f"{prefix}: block sums differ"
+    assert np.all(np.abs(q - rq) <= 2 * e * np.sqrt(n * rq) + n * e * e), f"{prefix}: block sums of squares differ"
     assert abs(np.linalg.norm(x) - float(fx[f"{prefix}_norm"])) <= tol * float(fx[f"{prefix}_norm"])
     return err
 
@@ -149,11 +148,9 @@ def _check_field(fx, prefix, x, tol=U_TOL, blocks=True):
 # sequentially (scripts/order_sensitivity.py, profiles/r02_c2_order_sensitivity_512.json).  A
 # parallel device reduction cannot reproduce a 3M-term sequential sum, so C2 is held to
 # Newton steps within 1, Krylov counts within 1 on the common steps, and the field within
-# 5e-8 of max|u| on the sampled cells and in the global norm (two solutions converged to
-# ~1e-8 residual, one Newton step apart; measured 3.3e-8).  The per-block aggregates are not
-# compared there: blocks near the clamped face hold |u| far below max|u|.  The bit-exact C2
-# check is test_sequential_reductions_c2_* below: with the reference's summation order the
-# device solve reproduces the reference's own run bit for bit.
+# 5e-8 of max|u| (two solutions converged to ~1e-8 residual, one Newton step apart; measured
+# 3.3e-8).  The bit-exact C2 check is test_sequential_reductions_* below: with the reference's
+# summation order the device solve reproduces the reference's own run bit for bit.
 ORDER_SENSITIVE = {"c2": {"newton": 1, "u_tol": 5e-8}}
 
 
@@ -178,9 +175,9 @@ def test_full_size_run_steps_matches_reference(name):
         kr = fx["krylov"][i][fx["krylov"][i] >= 0]
         m = min(len(k), len(kr))
         assert abs(len(k) - len(kr)) <= sens["newton"] and np.all(np.abs(k[:m] - kr[:m]) <= 1), (i, k, kr)
-    err = _check_field(fx, "u", f[0], sens["u_tol"], blocks=name not in ORDER_SENSITIVE)
+    err = _check_field(fx, "u", f[0], sens["u_tol"])
     if "v_old_sample" in fx.files:
-        _check_field(fx, "v_old", f[3], sens["u_tol"], blocks=name not in ORDER_SENSITIVE)
+        _check_field(fx, "v_old", f[3], sens["u_tol"])
     print(f"{name}: newton {newton.tolist()}, u rel err {err:.2e}, solve {wall:.2f} s "
           f"(reference {float(fx['ref_wall_seconds']):.1f} s on {fx['cpu_model']})")
 
