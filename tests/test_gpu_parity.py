@@ -586,6 +586,33 @@ def test_device_tet_mesh_equals_host(n, permute, rcm, monkeypatch):
     assert md.n_cells == mh.n_cells and md.n_internal == mh.n_internal
 
 
+def test_ilu_symmetry_patches_host_setup():
+    """Axis-aligned symmetry patches give per-component diagonal blocks: the device setup
+    declines (it builds the c I case) and the host setup factors three matrices; the apply still
+    equals the reference's bit for bit."""
+    sv = _sv()
+    mesh = sv.box_mesh((1.0, 1.0, 1.0), (12, 10, 9), [D, T, S, T, S, T], distort=0.1, seed=5)
+    phys = _phys()
+    ev, orc = _pair(mesh, phys)
+    pc = sv.make_preconditioner(ev, "ilu1")
+    orc.precond_create(3)
+    r = cases.uniform(17, 3 * mesh.n_cells)
+    assert np.array_equal(pc.solve(r).cpu().numpy(), orc.precond_apply(r))
+
+
+def test_device_tet_mesh_odd_n(monkeypatch):
+    """An odd division count (the mirrored split is then not symmetric): device and host
+    generators still give the same arrays."""
+    sv = _sv()
+    args = ((1.0, 2.0, 0.5), 9, [D, T, T, T, T, T], 3, True, True)
+    md = sv.kuhn_tet_mesh(*args)
+    monkeypatch.setenv("SFV_HOST_MESH", "1")
+    mh = sv.kuhn_tet_mesh(*args)
+    assert md.on_device and not mh.on_device
+    for f in ("points", "face_offsets", "face_points", "owner", "neighbour", "patch_start", "patch_count"):
+        assert np.array_equal(getattr(md, f), getattr(mh, f)), f
+
+
 def test_device_tet_mesh_full_size_time(monkeypatch):
     """C5 at n = 160 (24.6M tets): device generator time (the host one takes ~36 s)."""
     import time
