@@ -156,7 +156,12 @@ int sfv_precond_create(sfv_ctx* ctx, int kind);
 /* assemble_approximate_jacobian (discretisation.hpp:94-99, discretisation.cpp:216-262) in block
  * CSR on the cell graph: row_ptr[n_cells + 1], col[nnz], blocks[9 nnz] (3x3 row-major).  With
  * col or blocks NULL only nnz is returned; otherwise the arrays are filled and nnz returned
- * (< 0: an error code).  Blocks are diagonal (c I, or per-axis with axis-aligned symmetry). */
+ * (< 0: an error code).  Off-diagonal blocks are c I; a diagonal block is c I, per-axis with
+ * axis-aligned symmetry faces, or full (- coeff n (x) n, discretisation.cpp:250-251) when a symmetry
+ * face's normal is not axis-aligned.  In that last case sfv_precond_create factors the reference's
+ * expand_scalar() matrix (linalg.cpp:135-158: 3 n_cells rows, all nine entries of every block) as
+ * one system and sfv_precond_apply solves it with the sync-free sweep; the segregated solver
+ * refuses it as the reference does (scalar_component, linalg.cpp:120-133). */
 int sfv_approximate_jacobian(const sfv_ctx* ctx, int* row_ptr, int* col, double* blocks);
 /* line_search (nonlinear.hpp:81-90, nonlinear.cpp:140-163): success, the accepted s and
  * its residual norm, and (when residual_dev is not NULL) the accepted residual. */

@@ -154,6 +154,7 @@ struct sfv_ctx {
     // preconditioner
     int pc_kind = SFV_PRECOND_NONE;
     int pc_ncomp = 1;
+    bool pc_coupled = false;  // one factor over all 3n unknowns (symmetry plane not axis-aligned)
     TriDev L[3], U[3];
     DevBuf<double> ily, ipa, ipb;  // forward-sweep scratch, position-space scratch
     int tri_grid = 0;
@@ -687,15 +688,15 @@ int precond_apply_async(sfv_ctx* c, const double* r, double* z) {
                 Ls.t[a] = c->L[a].view;
                 Us.t[a] = c->U[a].view;
             }
-            launch_ilu_apply(Ls, Us, c->pc_ncomp, r, c->ily.p, z, c->tri_grid, c->tri_sleep, c->tri_cluster, c->ipa.p,
+            launch_ilu_apply(Ls, Us, c->pc_coupled ? -1 : c->pc_ncomp, r, c->ily.p, z, c->tri_grid, c->tri_sleep, c->tri_cluster, c->ipa.p,
                              c->ipb.p, &c->sL, &c->sU, c->stream, &c->pL, &c->pU);
             c->launches += c->tri_cluster == kPipeMode ? 11 : c->tri_cluster > 0 ? 2 : 4;
             return SFV_OK;
         }
         case SFV_PRECOND_LU:
             for (int a = 0; a < c->pc_ncomp; ++a) {
-                launch_dense_apply_perm(c->dense_w[a].p, c->nc, c->dense_perm[a].p, r, z, c->pc_ncomp == 1 ? -1 : a,
-                                        c->stream);
+                launch_dense_apply_perm(c->dense_w[a].p, c->pc_coupled ? c->n : c->nc, c->dense_perm[a].p, r, z,
+                                        c->pc_coupled ? kDenseCoupled : c->pc_ncomp == 1 ? -1 : a, c->stream);
                 c->launches += 1;
             }
             return SFV_OK;
@@ -1111,7 +1112,8 @@ int seg_create(sfv_ctx* c) {
     if (c->seg_ncomp) return SFV_OK;
     std::vector<ScalarCsr> comps;
     const std::string msg = cell_jacobian(c->mesh, c->geom, c->ph.kbar, c->ph.transient != 0, c->ph.rho, c->ph.dt, comps);
-    if (!msg.empty()) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "scalar_component: blocks are not diagonal");
+    if (!msg.empty() || comps[0].n != c->nc)  // scalar_component (linalg.cpp:120-133) refuses coupled blocks
+        return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, "scalar_component: blocks are not diagonal");
     const int n = c->nc;
     for (size_t a = 0; a < comps.size(); ++a) {
         ScalarCsr& A = comps[a];
@@ -1509,6 +1511,7 @@ int precond_create(sfv_ctx* c, int kind) {
     c->drop_graph();
     PhaseTimer pt;
     c->pc_kind = SFV_PRECOND_NONE;
+    c->pc_coupled = false;
     if (kind == SFV_PRECOND_AUTO) kind = 3 * c->nc <= 30000 ? SFV_PRECOND_LU : SFV_PRECOND_ILU1;  // nonlinear.cpp:355-356
     if (kind == SFV_PRECOND_NONE) return SFV_OK;
     // (the host-built sweeps and the host factorisation switches keep the host setup)
@@ -1524,6 +1527,9 @@ int precond_create(sfv_ctx* c, int kind) {
     const std::string msg = cell_jacobian(c->mesh, c->geom, c->ph.kbar, c->ph.transient != 0, c->ph.rho, c->ph.dt, comps);
     if (!msg.empty()) return c->fail(SFV_ERR_INVALID_ARGUMENT, -1, msg);
     c->pc_ncomp = static_cast<int>(comps.size());
+    // a symmetry plane that is not axis-aligned: the expanded 3n x 3n matrix, one factor
+    c->pc_coupled = comps.size() == 1 && comps[0].n == c->n && c->nc != c->n;
+    const int rows = c->pc_coupled ? c->n : c->nc;
     pt.mark("cell_jacobian");
     if (kind == SFV_PRECOND_LU) {
         for (size_t a = 0; a < comps.size(); ++a) {
@@ -1570,13 +1576,14 @@ int precond_create(sfv_ctx* c, int kind) {
         for (int i = 0; i < c->nc; ++i)
             for (int a = 0; a < 3; ++a) {
                 const ScalarCsr& s = comps[comps.size() == 1 ? 0 : a];
-                const int q = static_cast<int>(std::lower_bound(s.col.begin() + s.rp[i], s.col.begin() + s.rp[i + 1], i) -
+                const int ri = c->pc_coupled ? 3 * i + a : i;
+                const int q = static_cast<int>(std::lower_bound(s.col.begin() + s.rp[ri], s.col.begin() + s.rp[ri + 1], ri) -
                                                s.col.begin());
                 dn += s.val[q] * s.val[q];
             }
         dn = std::sqrt(dn);
         for (auto& s : comps)
-            for (int i = 0; i < c->nc; ++i) {
+            for (int i = 0; i < rows; ++i) {
                 const int q = static_cast<int>(std::lower_bound(s.col.begin() + s.rp[i], s.col.begin() + s.rp[i + 1], i) -
                                                s.col.begin());
                 s.val[q] += 1e-12 * dn;
@@ -1647,7 +1654,7 @@ int precond_create(sfv_ctx* c, int kind) {
     for (size_t a = 0; a < lus.size(); ++a) {
         const TriSchedule& tl = scheds[2 * a];
         const TriSchedule& tu = scheds[2 * a + 1];
-        if (!c->L[a].upload(tl, c->nc, full) || !c->U[a].upload(tu, c->nc, full) || !c->U[a].u2l.upload(u2ls[a]))
+        if (!c->L[a].upload(tl, rows, full) || !c->U[a].upload(tu, rows, full) || !c->U[a].u2l.upload(u2ls[a]))
             return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
         c->U[a].view.u2l = c->U[a].u2l.p;
         for (const TriSchedule* ts : {&tl, &tu}) {  // DSMEM ring admissibility
@@ -1702,7 +1709,7 @@ int precond_create(sfv_ctx* c, int kind) {
     // block-pipelined sweeps (precond_pipe.cu), opt-in with SFV_PIPE=1: bit-identical, but
     // slower than the streamed level-synchronous sweep at every size measured
     c->pipe_ok = false;
-    if (const char* pe = std::getenv("SFV_PIPE"); pe && std::atoi(pe) != 0) {
+    if (const char* pe = std::getenv("SFV_PIPE"); pe && std::atoi(pe) != 0 && !c->pc_coupled) {
         bool ok = true;
         int ring = 0;
         std::vector<PipeSchedule> ps(2 * lus.size());
@@ -1769,6 +1776,7 @@ int precond_create(sfv_ctx* c, int kind) {
     }
     for (int a = 0; a < c->pc_ncomp; ++a)  // the ELL cluster sweep holds rows of up to 32 entries
         if (c->tri_cluster != kPipeMode && (c->L[a].view.maxd > 32 || c->U[a].view.maxd > 32)) c->tri_cluster = 0;
+    if (c->pc_coupled) c->tri_cluster = 0;  // one factor over 3n unknowns: the sync-free sweep
     c->pc_kind = kind;
     pt.mark("rest");
     if (std::getenv("SFV_TIMING"))
@@ -2415,6 +2423,22 @@ int sfv_approximate_jacobian(const sfv_ctx* c, int* row_ptr, int* col, double* b
     const std::string msg = cell_jacobian(c->mesh, c->geom, c->ph.kbar, c->ph.transient != 0, c->ph.rho, c->ph.dt, comps);
     if (!msg.empty()) return const_cast<sfv_ctx*>(c)->fail(SFV_ERR_INVALID_ARGUMENT, -1, msg);
     const ScalarCsr& a0 = comps[0];
+    if (a0.n == 3 * c->nc && c->nc > 0) {  // coupled components: the expanded matrix back to 3 x 3 blocks
+        const int nnzb = a0.rp[a0.n] / 9;
+        if (!col || !blocks) return nnzb;
+        row_ptr[0] = 0;
+        for (int i = 0; i < c->nc; ++i) {
+            const int nb = (a0.rp[3 * i + 1] - a0.rp[3 * i]) / 3;
+            row_ptr[i + 1] = row_ptr[i] + nb;
+            for (int k = 0; k < nb; ++k) {
+                col[row_ptr[i] + k] = a0.col[a0.rp[3 * i] + 3 * k] / 3;
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b)
+                        blocks[9 * static_cast<size_t>(row_ptr[i] + k) + 3 * a + b] = a0.val[a0.rp[3 * i + a] + 3 * k + b];
+            }
+        }
+        return nnzb;
+    }
     const int nnz = a0.rp[a0.n];
     if (!col || !blocks) return nnz;  // size query
     for (int i = 0; i <= a0.n; ++i) row_ptr[i] = a0.rp[i];

@@ -361,7 +361,9 @@ struct TriSet {
     DevTri t[3];
 };
 // y is the forward-sweep scratch vector (3n); z receives M^{-1} r.  ncomp = 1: one
-// factor for all three components; ncomp = 3: factor t[k] for component k.
+// factor for all three components; ncomp = 3: factor t[k] for component k; ncomp = -1: t[0]
+// is one factor over all 3n unknowns (coupled components: a symmetry plane that is not
+// axis-aligned), applied by the sync-free sweep (cluster == 0).
 // cluster > 0: level-synchronous sweep by one cluster of that many CTAs per component;
 // cluster == 0: sync-free sentinel polling on a persistent grid of `grid` CTAs.
 // pa, pb: position-space scratch vectors of 3 * max positions (cluster > 0 path).
@@ -448,7 +450,9 @@ struct ScalarCsr;
 bool device_ilu_numeric(ScalarCsr& out, const std::vector<int>& diag, const std::vector<int>& rows,
                         cudaStream_t stream);
 void launch_band_inverse(const double* l, int n, int bw, double* W, cudaStream_t s);
-// comp < 0: all three components with one W; comp = k: component k only
+// comp < 0: all three components with one W; comp = k: component k only;
+// comp = kDenseCoupled: W spans all 3n unknowns (n = 3 x cells, coupled components)
+constexpr int kDenseCoupled = -2;
 void launch_dense_apply_perm(const double* W, int n, const int* perm, const double* r, double* z, int comp,
                              cudaStream_t s);
 

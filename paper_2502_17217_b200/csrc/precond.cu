@@ -70,7 +70,9 @@ __global__ void fill_sentinel_kernel(double* z, int n) {
 // (all CTAs resident), so every awaited row is owned by a running thread.
 // NRHS = 3: one factor shared by the three interleaved components (c*I blocks);
 // NRHS = 1: per-component factors (axis-aligned symmetry planes), component = blockIdx.y.
-template <bool UPPER, int NRHS>
+// RS = 1 (with NRHS = 1): one scalar factor over all 3n unknowns — the expanded matrix of a
+// symmetry plane that is not axis-aligned, whose blocks couple the components.
+template <bool UPPER, int NRHS, int RS = 3>
 __global__ void __launch_bounds__(256) tri_kernel(TriSet set, const double* __restrict__ src, double* dst,
                                                   int sleep_ns) {
     const int comp = NRHS == 3 ? 0 : static_cast<int>(blockIdx.y);
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(256) tri_kernel(TriSet set, const double* __re
         const int b = t.rp[p], e = t.rp[p + 1];
         double z[NRHS];
 #pragma unroll
-        for (int k = 0; k < NRHS; ++k) z[k] = src[3 * i + comp + k];
+        for (int k = 0; k < NRHS; ++k) z[k] = src[RS * i + comp + k];
         for (int q = b; q < e; ++q) {
             const int j = t.col[q];
             const double a = t.val[q];
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(256) tri_kernel(TriSet set, const double* __re
                 bool ready = true;
 #pragma unroll
                 for (int k = 0; k < NRHS; ++k) {
-                    wv[k] = ld_relaxed_u64(&dst[3 * j + comp + k]);
+                    wv[k] = ld_relaxed_u64(&dst[RS * j + comp + k]);
                     ready &= wv[k] != kSentinel;
                 }
                 if (ready) break;
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(256) tri_kernel(TriSet set, const double* __re
             for (int k = 0; k < NRHS; ++k) z[k] /= d;
         }
 #pragma unroll
-        for (int k = 0; k < NRHS; ++k) __stcg(&dst[3 * i + comp + k], publish(z[k]));
+        for (int k = 0; k < NRHS; ++k) __stcg(&dst[RS * i + comp + k], publish(z[k]));
     }
 }
 
@@ -475,8 +477,9 @@ __global__ void __launch_bounds__(128) band_inverse_kernel(const double* __restr
 }
 
 // z[perm[i]] = -sum_j W[i][j] r[perm[j]] (K = -A): NRHS = 3 applies one W to the three
-// interleaved components; NRHS = 1 applies it to component `comp` only.
-template <int NRHS>
+// interleaved components; NRHS = 1 applies it to component `comp` only; RS = 1: W spans all
+// 3n unknowns (coupled components).
+template <int NRHS, int RS = 3>
 __global__ void __launch_bounds__(256) dense_apply_perm_kernel(const double* __restrict__ W, int n,
                                                                const int* __restrict__ perm,
                                                                const double* __restrict__ r,
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(256) dense_apply_perm_kernel(const double* __r
         const double a = row[j];
         const int pj = perm[j];
 #pragma unroll
-        for (int k = 0; k < NRHS; ++k) acc[k] += a * r[3 * pj + comp + k];
+        for (int k = 0; k < NRHS; ++k) acc[k] += a * r[RS * pj + comp + k];
     }
 #pragma unroll
     for (int k = 0; k < NRHS; ++k)
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(256) dense_apply_perm_kernel(const double* __r
     if (lane == 0) {
         const int pi = perm[warp];
 #pragma unroll
-        for (int k = 0; k < NRHS; ++k) z[3 * pi + comp + k] = -acc[k];
+        for (int k = 0; k < NRHS; ++k) z[RS * pi + comp + k] = -acc[k];
     }
 }
 
@@ -581,7 +584,9 @@ void launch_band_inverse(const double* l, int n, int bw, double* W, cudaStream_t
 
 void launch_dense_apply_perm(const double* W, int n, const int* perm, const double* r, double* z, int comp,
                              cudaStream_t s) {
-    if (comp < 0)
+    if (comp == kDenseCoupled)  // W over all 3n unknowns (coupled components)
+        dense_apply_perm_kernel<1, 1><<<(n + 7) / 8, 256, 0, s>>>(W, n, perm, r, z, 0);
+    else if (comp < 0)
         dense_apply_perm_kernel<3><<<(n + 7) / 8, 256, 0, s>>>(W, n, perm, r, z, 0);
     else
         dense_apply_perm_kernel<1><<<(n + 7) / 8, 256, 0, s>>>(W, n, perm, r, z, comp);
@@ -679,10 +684,13 @@ void launch_ilu_apply(const TriSet& L, const TriSet& U, int ncomp, const double*
             scatter_pos_kernel<<<592, 256, 0, s>>>(U.t[c].order, U.t[c].n, c, per, pb, z);
         return;
     }
-    const int n3 = 3 * L.t[0].n_rows;  // sync-free sentinel polling (SFV_TRI_CLUSTER=0)
+    const int n3 = ncomp < 0 ? L.t[0].n_rows : 3 * L.t[0].n_rows;  // sync-free sentinel polling (SFV_TRI_CLUSTER=0)
     fill_sentinel_kernel<<<592, 256, 0, s>>>(y, n3);
     fill_sentinel_kernel<<<592, 256, 0, s>>>(z, n3);
-    if (ncomp == 1) {
+    if (ncomp < 0) {  // coupled components: one factor over the 3n unknowns
+        tri_kernel<false, 1, 1><<<grid, 256, 0, s>>>(L, r, y, sleep_ns);
+        tri_kernel<true, 1, 1><<<grid, 256, 0, s>>>(U, y, z, sleep_ns);
+    } else if (ncomp == 1) {
         tri_kernel<false, 3><<<grid, 256, 0, s>>>(L, r, y, sleep_ns);  // forward, unit lower: y
         tri_kernel<true, 3><<<grid, 256, 0, s>>>(U, y, z, sleep_ns);   // backward with U: z
     } else {

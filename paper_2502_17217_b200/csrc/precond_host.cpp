@@ -51,19 +51,74 @@ std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar,
             std::sort(col.begin() + rp[c], col.begin() + rp[c + 1]);
         }
     });
-    bool sym = false;
+    bool sym = false, coupled = false;
+    auto find = [&](int i, int j) {
+        return static_cast<int>(std::lower_bound(col.begin() + rp[i], col.begin() + rp[i + 1], j) - col.begin());
+    };
     for (int f = m.n_internal; f < m.n_faces(); ++f)
         if (m.patches[m.face_patch[f]].kind == SFV_PATCH_SYMMETRY) {
             sym = true;
             const V3 n = g.normal[f];
-            if (n.x * n.y != 0.0 || n.x * n.z != 0.0 || n.y * n.z != 0.0)
-                return "preconditioner: symmetry plane not axis-aligned couples the displacement components";
+            if (n.x * n.y != 0.0 || n.x * n.z != 0.0 || n.y * n.z != 0.0) coupled = true;
         }
+    if (coupled) {
+        // A symmetry plane that is not axis-aligned puts -coeff n (x) n with off-diagonal entries on
+        // the diagonal block (discretisation.cpp:250-251), so the components do not separate: the
+        // matrix is the reference's expand_scalar() (linalg.cpp:135-158) — rows 3 i + a, every
+        // block all nine entries (zeros included, they are part of the ILU pattern) — with each
+        // entry accumulated by the reference's own operations in its face order.
+        comps.assign(1, ScalarCsr{});
+        ScalarCsr& s = comps[0];
+        s.n = 3 * nc;
+        s.rp.assign(3 * static_cast<size_t>(nc) + 1, 0);
+        for (int i = 0; i < nc; ++i)
+            for (int a = 0; a < 3; ++a) s.rp[3 * i + a + 1] = 3 * (rp[i + 1] - rp[i]);
+        for (int r = 0; r < 3 * nc; ++r) s.rp[r + 1] += s.rp[r];
+        s.col.resize(s.rp[3 * nc]);
+        s.val.resize(s.rp[3 * nc]);
+        prows([&](int c0, int c1) {
+            for (int i = c0; i < c1; ++i) {
+                const int nb = rp[i + 1] - rp[i];
+                double* row[3];
+                for (int a = 0; a < 3; ++a) {
+                    row[a] = s.val.data() + s.rp[3 * i + a];
+                    int* cc = s.col.data() + s.rp[3 * i + a];
+                    for (int k = 0; k < nb; ++k)
+                        for (int b = 0; b < 3; ++b) {
+                            cc[3 * k + b] = 3 * col[rp[i] + k] + b;
+                            row[a][3 * k + b] = 0.0;
+                        }
+                }
+                const int kd = find(i, i) - rp[i];
+                auto add = [&](int k, double c, const double* nn) {  // block k of the row += c * M
+                    for (int a = 0; a < 3; ++a)
+                        for (int b = 0; b < 3; ++b)
+                            row[a][3 * k + b] += (nn ? nn[a] * nn[b] : (a == b ? 1.0 : 0.0)) * c;
+                };
+                for (int q = m.cf_off[i]; q < m.cf_off[i + 1]; ++q) {
+                    const int f = m.cf[q];
+                    const double coeff = kbar * g.delta_mag[f] / g.d_mag[f] * g.area_mag[f];
+                    if (f < m.n_internal) {
+                        const int o = m.owner[f] == i ? m.neighbour[f] : m.owner[f];
+                        add(find(i, o) - rp[i], coeff, nullptr);
+                        add(kd, -coeff, nullptr);
+                    } else {
+                        const int kind = m.patches[m.face_patch[f]].kind;
+                        if (kind == SFV_PATCH_DISPLACEMENT) {
+                            add(kd, -coeff, nullptr);
+                        } else if (kind == SFV_PATCH_SYMMETRY) {
+                            const double nn[3] = {g.normal[f].x, g.normal[f].y, g.normal[f].z};
+                            add(kd, -coeff, nn);
+                        }
+                    }
+                }
+                if (transient) add(kd, -2.25 * rho * g.volume[i] / (dt * dt), nullptr);
+            }
+        });
+        return "";
+    }
     const int ncomp = sym ? 3 : 1;
     comps.assign(ncomp, ScalarCsr{});
-    auto find = [&](int i, int j) {
-        return static_cast<int>(std::lower_bound(col.begin() + rp[i], col.begin() + rp[i + 1], j) - col.begin());
-    };
     for (int a = 0; a < ncomp; ++a) {
         ScalarCsr& s = comps[a];
         s.n = nc;
@@ -647,7 +702,9 @@ std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out, bool factor) {
     for (int i = 0; i < n; ++i)
         for (int p = a.rp[i]; p < a.rp[i + 1]; ++p) {
             const int bi = inv[i], bj = inv[a.col[p]];
-            if (bj <= bi) L(bi, bj) = -a.val[p];  // -A is symmetric positive definite
+            // -A is symmetric positive definite (explicit zeros of an expanded block pattern are
+            // outside the band computed above and stay out)
+            if (bj <= bi && a.val[p] != 0.0) L(bi, bj) = -a.val[p];
         }
     if (!factor) return "";
     for (int i = 0; i < n; ++i) {

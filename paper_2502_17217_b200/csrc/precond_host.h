@@ -46,7 +46,10 @@ struct ScalarCsr {
 // Per-component scalar matrices of assemble_approximate_jacobian
 // (/root/reference/proj/src/discretisation.cpp:216-262), accumulated entry by entry in
 // the reference's face order.  ncomp = 1 when every block is c*I (no symmetry faces),
-// 3 when blocks are diagonal (axis-aligned symmetry faces).  Returns "" or an error.
+// 3 when blocks are diagonal (axis-aligned symmetry faces).  A symmetry face whose normal is not
+// axis-aligned couples the components (-coeff n (x) n on the diagonal block): then comps holds ONE
+// matrix with n = 3 * cells, the reference's expand_scalar() (linalg.cpp:135-158) — rows 3 i + a,
+// all nine entries of every block in the pattern.  Returns "" or an error.
 std::string cell_jacobian(const HostMesh& m, const HostGeometry& g, double kbar, bool transient, double rho,
                           double dt, std::vector<ScalarCsr>& comps);
 

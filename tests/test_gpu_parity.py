@@ -623,3 +623,97 @@ def test_device_tet_mesh_full_size_time(monkeypatch):
     dt = time.time() - t0
     assert m.n_cells == 6 * 160 ** 3 and m.on_device
     print(f"c5 n=160 mesh on the device: {dt:.2f} s")
+
+
+def _turned(mesh, about_z=20.0, about_x=35.0):
+    """The same mesh turned about z and then x: no boundary plane stays axis-aligned, so a
+    symmetry patch gets a normal with three non-zero components."""
+    import dataclasses
+    a, b = np.deg2rad(about_z), np.deg2rad(about_x)
+    rz = np.array([[np.cos(a), -np.sin(a), 0.0], [np.sin(a), np.cos(a), 0.0], [0.0, 0.0, 1.0]])
+    rx = np.array([[1.0, 0.0, 0.0], [0.0, np.cos(b), -np.sin(b)], [0.0, np.sin(b), np.cos(b)]])
+    return dataclasses.replace(mesh, points=np.ascontiguousarray(mesh.points @ (rx @ rz).T), _keep=[])
+
+
+def test_residual_oblique_symmetry_bitwise():
+    """R(u) and J.v at fixed eps on a mesh whose symmetry planes are not axis-aligned."""
+    sv = _sv()
+    mesh = _turned(sv.box_mesh((1.0, 1.0, 1.0), (8, 6, 5), [D, T, S, T, S, T], distort=0.1, seed=3))
+    ev, orc = _pair(mesh, _phys())
+    u = 1e-4 * cases.uniform(31, 3 * mesh.n_cells)
+    assert np.array_equal(ev.residual(u).cpu().numpy(), orc.residual(u))
+
+
+@pytest.mark.parametrize("kind,code", [("ilu0", 2), ("ilu1", 3), ("ilu2", 4)])
+def test_ilu_oblique_symmetry_coupled_bitwise(kind, code):
+    """A symmetry plane that is not axis-aligned puts -coeff n (x) n with off-diagonal entries on
+    the diagonal blocks (discretisation.cpp:250-251): the components couple, and the factor is
+    the reference's ILU(k) of expand_scalar() (linalg.cpp:135-158, :249-334) — one 3n x 3n
+    scalar matrix with all nine entries of every block.  The apply equals it bit for bit."""
+    sv = _sv()
+    mesh = _turned(sv.box_mesh((1.0, 1.0, 1.0), (12, 10, 9), [D, T, S, T, S, T], distort=0.1, seed=5))
+    ev, orc = _pair(mesh, _phys())
+    pc = sv.make_preconditioner(ev, kind)
+    assert pc.info()["sweep"] == 0  # the sync-free sweep over the 3n unknowns
+    orc.precond_create(code)
+    for seed in (17, 18):
+        r = cases.uniform(seed, 3 * mesh.n_cells)
+        assert np.array_equal(pc.solve(r).cpu().numpy(), orc.precond_apply(r))
+
+
+def test_ilu_oblique_symmetry_coupled_large():
+    """The same at 3n >= 65536 rows, where the host factorisation takes its threaded path."""
+    sv = _sv()
+    mesh = _turned(sv.box_mesh((1.0, 1.0, 1.0), (28, 28, 28), [D, T, S, T, S, T], distort=0.1, seed=5))
+    ev, orc = _pair(mesh, _phys(transient=True))
+    pc = sv.make_preconditioner(ev, "ilu1")
+    orc.precond_create(3)
+    r = cases.uniform(19, 3 * mesh.n_cells)
+    assert np.array_equal(pc.solve(r).cpu().numpy(), orc.precond_apply(r))
+
+
+def test_oblique_symmetry_lu_jacobian_segregated():
+    """Coupled blocks with the exact preconditioner (LU of the expanded matrix), the exported
+    3 x 3 blocks, and the segregated solver's refusal (scalar_component, linalg.cpp:120-133)."""
+    sv = _sv()
+    mesh = _turned(sv.box_mesh((1.0, 1.0, 1.0), (8, 6, 5), [D, T, S, T, S, T], distort=0.1, seed=3))
+    ev, orc = _pair(mesh, _phys())
+    pc = sv.make_preconditioner(ev, "auto")  # 720 rows -> LU
+    orc.precond_create(0)
+    r = cases.uniform(4, 3 * mesh.n_cells)
+    z_gpu, z_orc = pc.solve(r).cpu().numpy(), orc.precond_apply(r)
+    assert np.linalg.norm(z_gpu - z_orc) / np.linalg.norm(z_orc) < 1e-11
+    rp, col, blocks = sv.approximate_jacobian(ev)
+    assert rp[-1] == len(col) == len(blocks) and len(rp) == mesh.n_cells + 1
+    off = blocks - np.einsum("kii->ki", blocks)[:, :, None] * np.eye(3)
+    coupled_rows = {int(np.searchsorted(rp, k, side="right") - 1) for k in np.nonzero(np.abs(off).max(axis=(1, 2)))[0]}
+    sym_faces = [f for p in (2, 4) for f in range(mesh.patch_start[p], mesh.patch_start[p] + mesh.patch_count[p])]
+    assert coupled_rows == {int(mesh.owner[f]) for f in sym_faces}
+    assert np.array_equal(blocks, blocks.transpose(0, 2, 1))  # every block symmetric (c I, or + c n (x) n)
+    # M^{-1} is the inverse of that matrix: J~ z = r
+    A = np.zeros((3 * mesh.n_cells, 3 * mesh.n_cells))
+    for i in range(mesh.n_cells):
+        for k in range(rp[i], rp[i + 1]):
+            A[3 * i:3 * i + 3, 3 * col[k]:3 * col[k] + 3] = blocks[k]
+    assert np.linalg.norm(A @ z_gpu - r) / np.linalg.norm(r) < 1e-9
+    with pytest.raises(sv.SolidfvError) as e:
+        sv.run_steps(ev, np.zeros((6, 3 * mesh.n_cells)), solver_cfg(algorithm="segregated"), 1)
+    assert "blocks are not diagonal" in str(e.value)
+
+
+def test_run_steps_oblique_symmetry_parity():
+    """run_steps with the coupled ILU(1) factor: Krylov counts within 1 and u within 1e-8 of the
+    oracle's."""
+    sv = _sv()
+    mesh = _turned(sv.box_mesh((1.0, 1.0, 1.0), (12, 10, 9), [D, T, S, T, S, T], distort=0.1, seed=5))
+    phys = _phys()
+    ev, orc = sv.ResidualEvaluator(mesh, phys), OracleCase(mesh, phys)
+    cfg = solver_cfg(preconditioner="ilu1")
+    f0 = np.zeros((6, 3 * mesh.n_cells))
+    fg, rg, _ = sv.run_steps(ev, f0, cfg, 2)
+    fo, ro, _ = orc.run_steps(f0, cfg, 2)
+    assert [r.status for r in rg] == [r.status for r in ro] == [0, 0]
+    for a, b in zip(_counts(rg), _counts(ro)):
+        assert len(a) == len(b) and all(abs(x - y) <= 1 for x, y in zip(a, b)), (_counts(rg), _counts(ro))
+    u_g, u_o = fg.cpu().numpy()[0], fo[0]
+    assert np.abs(u_g - u_o).max() <= 1e-8 * np.abs(u_o).max()
