@@ -39,6 +39,12 @@ namespace cg = cooperative_groups;
 #define SFV_TS_PROBE 0
 #endif
 #define TSP(b) (!(SFV_TS_PROBE & (b)))
+#ifndef SFV_STREAM_PWAIT
+#define SFV_STREAM_PWAIT 1  // 0: every compute thread tests the stage's mbarrier itself
+#endif
+#ifndef SFV_STREAM_PFENCE
+#define SFV_STREAM_PFENCE 1
+#endif
 #ifndef SFV_DIV_CORR
 #define SFV_DIV_CORR 1  // 0: plain division in the U sweep
 #endif
@@ -155,6 +161,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     const int A = t.solo_a < 0 ? 0 : t.solo_a, B = t.solo_a < 0 ? n_lv - 1 : t.solo_b;
     if (producer)
         for (int l = 0; l < kStages - 1; ++l) issue(l);
+#if SFV_STREAM_PWAIT
+    if (n_lv > 0) mbar_wait(mbar_base, 0u);  // level 0 (issued just above)
+    __syncthreads();
+#endif
     long long ph[5] = {0, 0, 0, 0, 0}, pl[5] = {0, 0, 0, 0, 0}, t0 = 0, t1 = 0;  // (pl: solo levels)
     (void)pl;
     (void)ph;
@@ -167,13 +177,23 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
         if (producer) {
             // stage (l - 1) % kStages was consumed before the barrier that ended level l - 1
             issue(l + kStages - 1);
+#if SFV_STREAM_PWAIT
+            // the producer, idle until the barrier, waits for the NEXT level's records: the barrier
+            // that ends this level then tells every thread they have landed (the TMA writes are in
+            // shared memory when the mbarrier completes), and no compute thread tests an mbarrier
+            if (l + 1 < n_lv) mbar_wait(mbar_base + 8u * ((l + 1) % kStages), static_cast<uint32_t>(((l + 1) / kStages) & 1));
+            // (as the compute threads do for the ring: CTA-scope fence, then the relaxed arrive)
+            if (!LOCAL && SFV_STREAM_PFENCE) asm volatile("fence.acq_rel.cta;" ::: "memory");
+#endif
             if (!TSP(32)) {
                 t1 = clock64();
                 (LOCAL ? pl : ph)[0] += t1 - t0;
                 t0 = t1;
             }
         } else {
+#if !SFV_STREAM_PWAIT
             mbar_wait(mbar_base + 8u * (l % kStages), static_cast<uint32_t>((l / kStages) & 1));
+#endif
             if (!TSP(32)) {
                 t1 = clock64();
                 (LOCAL ? pl : ph)[1] += t1 - t0;
