@@ -1478,8 +1478,8 @@ std::string precond_create_device(sfv_ctx* c, int level) {
     c->srec[0].adopt(ds.L.rec, (static_cast<size_t>(ds.L.n_pos) + 31) / 32 * kStreamChunk);
     c->srec[3].adopt(ds.U.rec, (static_cast<size_t>(ds.U.n_pos) + 31) / 32 * kStreamChunk);
     ds.L.rec = ds.U.rec = nullptr;
-    c->sL.t[0] = DevStream{ds.L.n_levels, c->L[0].view.level_ptr, c->srec[0].p, ds.L.solo_a, ds.L.solo_b};
-    c->sU.t[0] = DevStream{ds.U.n_levels, c->U[0].view.level_ptr, c->srec[3].p, ds.U.solo_a, ds.U.solo_b};
+    c->sL.t[0] = DevStream{ds.L.n_levels, c->L[0].view.level_ptr, c->srec[0].p};
+    c->sU.t[0] = DevStream{ds.U.n_levels, c->U[0].view.level_ptr, c->srec[3].p};
     for (StreamSet* ss : {&c->sL, &c->sU}) {
         ss->ring = ds.ring;
         ss->max_rows = ds.max_rows;
@@ -1620,11 +1620,11 @@ int precond_create(sfv_ctx* c, int kind) {
     // and as many cp.async stages as the remaining shared memory holds
     std::vector<rawvec<unsigned char>> packed(scheds.size());
     int s_ring = 0, s_rows = 32, s_stages = 0;
-    std::vector<int> spans(scheds.size(), 1 << 30);
     {
         for (const TriSchedule& ts : scheds)
             for (int l = 0; l < ts.n_levels; ++l) {
-                s_rows = std::max(s_rows, stream_per(ts.level_ptr[l + 1] - ts.level_ptr[l], kStreamCluster) * 32);
+                const int nch = (ts.level_ptr[l + 1] - ts.level_ptr[l]) / 32;
+                s_rows = std::max(s_rows, (nch + kStreamCluster - 1) / kStreamCluster * 32);
             }
         if (s_rows <= kStreamMaxRows)
             for (int cand : {1024, 2048, 3072, 4095}) {  // (slot 4095 at most: the +0.0 slot)
@@ -1634,7 +1634,7 @@ int precond_create(sfv_ctx* c, int kind) {
                     th.emplace_back([&, x] {
                         // forward sweep of component a: values go to its backward-sweep positions
                         ok[x] = build_stream_records(scheds[x], kStreamCluster, cand, s_rows, packed[x],
-                                                     x % 2 ? nullptr : &scheds[x + 1].pos, &spans[x]);
+                                                     x % 2 ? nullptr : &scheds[x + 1].pos);
                     });
                 for (auto& t : th) t.join();
                 if (std::all_of(ok.begin(), ok.end(), [](char v) { return v != 0; })) {
@@ -1677,7 +1677,6 @@ int precond_create(sfv_ctx* c, int kind) {
                 return c->fail(SFV_ERR_CUDA, -1, "ilu: out of device memory");
             const int a = static_cast<int>(x / 2);
             DevStream ds{scheds[x].n_levels, x % 2 ? c->U[a].view.level_ptr : c->L[a].view.level_ptr, b.p};
-            stream_ranges(scheds[x].level_ptr.data(), scheds[x].n_levels, spans[x], ds.solo_a, ds.solo_b);
             (x % 2 ? c->sU : c->sL).t[a] = ds;
         }
         for (StreamSet* ss : {&c->sL, &c->sU}) {

@@ -381,48 +381,13 @@ constexpr int kStreamMode = 200;
 #define SFV_STREAM_MAX_ROWS 256
 #endif
 constexpr int kStreamCluster = SFV_STREAM_CLUSTER;
-// Slicing of a level over the cluster (the one rule of the host and device record builders and
-// of the sweep): a level of n positions (a multiple of 32) is cut into cs contiguous slices of
-// stream_per(n, cs) chunks of 32.  A level of at most kStreamSolo positions is a "solo" level:
-// CTA 0 takes all of it, so a run of solo levels — the narrow wavefronts at both ends of a
-// sweep — needs no cluster barrier and no DSMEM traffic between its levels, only a CTA barrier.
-#ifndef SFV_STREAM_SOLO
-#define SFV_STREAM_SOLO 224
-#endif
-constexpr int kStreamSolo = SFV_STREAM_SOLO;  // (0: no solo levels)
-__host__ __device__ inline bool stream_solo(int n) { return n <= kStreamSolo; }
-__host__ __device__ inline int stream_per(int n, int cs) {
-    const int nch = n >> 5;
-    const int per = stream_solo(n) ? nch : (nch + cs - 1) / cs;
-    return per > 0 ? per : 1;
-}
 constexpr int kStreamRing = 3072;    // 32-byte value slots per CTA
 constexpr int kStreamMaxRows = SFV_STREAM_MAX_ROWS;  // positions per CTA per level
 struct DevStream {
     int n_levels = 0;
     const int* level_ptr = nullptr;  // position-space level boundaries (same as DevTri)
     const void* rec = nullptr;       // [n_pos] 112-byte records
-    // Level ranges of the sweep (stream_ranges below): [0, solo_a) and [solo_b, n_levels - 1) are
-    // runs of solo levels whose dependencies are all CTA 0's; -1: none (every level cluster-wide)
-    int solo_a = -1, solo_b = -1;
 };
-// [0, A) and [B, n - 1): the runs of solo levels at both ends of a sweep in which every dependency
-// is CTA 0's as well: A is the level before the first non-solo level (that level hands over to the
-// cluster), B lies `span` levels — the largest level distance of a dependency — after the last one.
-inline void stream_ranges(const int* level_ptr, int n, int span, int& A, int& B) {
-    int first = n, last = 0;
-    for (int l = 0; l < n; ++l)
-        if (!stream_solo(level_ptr[l + 1] - level_ptr[l])) {
-            if (first == n) first = l;
-            last = l + 1;
-        }
-    A = B = n - 1;
-    if (first < n) {
-        A = first - 1 > 0 ? first - 1 : 0;
-        const long long b = static_cast<long long>(last) + span;
-        B = b < n - 1 ? static_cast<int>(b) : n - 1;
-    }
-}
 struct StreamSet {
     DevStream t[3];
     int ring = 0;      // value slots per CTA

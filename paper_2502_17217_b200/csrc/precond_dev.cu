@@ -254,7 +254,7 @@ __device__ __forceinline__ int level_of(const Slicing& s, int p) {
 }
 __device__ __forceinline__ void owner_ordinal(const Slicing& s, int p, int l, int& r, int& ord) {
     const int la = s.lptr[l], lb = s.lptr[l + 1];
-    const int per = stream_per(lb - la, s.cs);
+    const int nch = (lb - la) >> 5, per = max(1, (nch + s.cs - 1) / s.cs);
     r = ((p - la) >> 5) / per;
     ord = s.cum[r * (s.nl + 1) + l] + (p - (la + r * per * 32));
 }
@@ -292,8 +292,7 @@ __device__ __forceinline__ int row_deps(int i, const int* __restrict__ rp, const
 // pass 1: the smallest ring with no slot rewritten before its last reader, and the row width
 template <bool UPPER>
 __global__ void ring_need_kernel(Slicing s, const int* __restrict__ order, const int* __restrict__ pos,
-                                 const int* __restrict__ rp, const int* __restrict__ col, int* need, int* wide,
-                                 int* span) {
+                                 const int* __restrict__ rp, const int* __restrict__ col, int* need, int* wide) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= s.np) return;
     const int i = order[p];
@@ -305,18 +304,15 @@ __global__ void ring_need_kernel(Slicing s, const int* __restrict__ order, const
         return;
     }
     const int l = level_of(s, p);
-    int req = 0, far = 0;
+    int req = 0;
     for (int k = 0; k < m; ++k) {
         const int q = pos[dq[k]];
         int r, o;
-        const int lq = level_of(s, q);
-        far = max(far, l - lq);
-        owner_ordinal(s, q, lq, r, o);
+        owner_ordinal(s, q, level_of(s, q), r, o);
         // the slot of q is rewritten by r's (o + ring)-th position: it must lie after level l
         req = max(req, s.cum[r * (s.nl + 1) + l + 1] - o);
     }
     atomicMax(need, req);
-    atomicMax(span, far);  // the largest level distance of a dependency
 }
 
 // pass 2: the records in the device chunk layout (device.h kStream*: val[8][32], diag[32],
@@ -500,7 +496,7 @@ std::vector<int> slice_cum(const std::vector<int>& lptr, int cs) {
     std::vector<int> cum(static_cast<size_t>(cs) * (nl + 1), 0);
     for (int l = 0; l < nl; ++l) {
         const int la = lptr[l], lb = lptr[l + 1];
-        const int per = stream_per(lb - la, cs);
+        const int nch = (lb - la) / 32, per = std::max(1, (nch + cs - 1) / cs);
         for (int r = 0; r < cs; ++r) {
             const int a = std::min(lb, la + r * per * 32), b = std::min(lb, a + per * 32);
             cum[static_cast<size_t>(r) * (nl + 1) + l + 1] = cum[static_cast<size_t>(r) * (nl + 1) + l] + (b - a);
@@ -603,8 +599,9 @@ std::string device_ilu_setup(const DevTopoView& t, double kbar, bool transient, 
     int rows_l = 32, rows_u = 32;
     for (auto* lp : {&lptr_l, &lptr_u})
         for (size_t l = 0; l + 1 < lp->size(); ++l) {
+            const int nch = ((*lp)[l + 1] - (*lp)[l]) / 32;
             (lp == &lptr_l ? rows_l : rows_u) =
-                std::max(lp == &lptr_l ? rows_l : rows_u, stream_per((*lp)[l + 1] - (*lp)[l], cs) * 32);
+                std::max(lp == &lptr_l ? rows_l : rows_u, (nch + cs - 1) / cs * 32);
         }
     out.max_rows = std::max(rows_l, rows_u);
     if (out.max_rows > kStreamMaxRows) {
@@ -613,23 +610,21 @@ std::string device_ilu_setup(const DevTopoView& t, double kbar, bool transient, 
     }
     const std::vector<int> cum_l = slice_cum(lptr_l, cs), cum_u = slice_cum(lptr_u, cs);
     int* dcum = tmp.get<int>(cum_l.size() + cum_u.size());
-    int* need = tmp.get<int>(4);
+    int* need = tmp.get<int>(2);
     if (!dcum || !need) {
         out.release();
         return "device ilu: out of memory";
     }
     cudaMemcpyAsync(dcum, cum_l.data(), sizeof(int) * cum_l.size(), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(dcum + cum_l.size(), cum_u.data(), sizeof(int) * cum_u.size(), cudaMemcpyHostToDevice, s);
-    cudaMemsetAsync(need, 0, sizeof(int) * 4, s);
+    cudaMemsetAsync(need, 0, sizeof(int) * 2, s);
     Slicing sl{out.L.n_pos, out.L.n_levels, cs, 0, out.L.level_ptr, dcum};
     Slicing su{out.U.n_pos, out.U.n_levels, cs, 0, out.U.level_ptr, dcum + cum_l.size()};
-    ring_need_kernel<false><<<(sl.np + 255) / 256, 256, 0, s>>>(sl, out.L.order, lpos, rp, col, need, need + 1, need + 2);
-    ring_need_kernel<true><<<(su.np + 255) / 256, 256, 0, s>>>(su, out.U.order, upos, rp, col, need, need + 1, need + 3);
-    int nh[4] = {0, 0, 0, 0};
+    ring_need_kernel<false><<<(sl.np + 255) / 256, 256, 0, s>>>(sl, out.L.order, lpos, rp, col, need, need + 1);
+    ring_need_kernel<true><<<(su.np + 255) / 256, 256, 0, s>>>(su, out.U.order, upos, rp, col, need, need + 1);
+    int nh[2] = {0, 0};
     cudaMemcpyAsync(nh, need, sizeof nh, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    stream_ranges(lptr_l.data(), out.L.n_levels, nh[2], out.L.solo_a, out.L.solo_b);
-    stream_ranges(lptr_u.data(), out.U.n_levels, nh[3], out.U.solo_a, out.U.solo_b);
     if (nh[1]) {
         out.release();
         return "device ilu: a row has more than 8 dependencies";

@@ -26,7 +26,6 @@ struct DevTopoView {
 // the backward sweep the backward -> forward position map); device memory owned by the caller
 struct DevSweep {
     int n_pos = 0, n_levels = 0;
-    int solo_a = -1, solo_b = -1;  // level ranges of the sweep (device.h stream_ranges)
     int* order = nullptr;          // [n_pos] position -> row (-1 padding)
     int* level_ptr = nullptr;      // [n_levels + 1]
     unsigned char* rec = nullptr;  // [n_pos / 32] chunks of 3072 bytes (precond_host.h layout)

@@ -728,7 +728,7 @@ std::string band_cholesky_neg(const ScalarCsr& a, BandChol& out, bool factor) {
 namespace sfv {
 
 bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed,
-                          const std::vector<int>* out_pos, int* span_out) {
+                          const std::vector<int>* out_pos) {
     StageClock sc;
     if (t.maxd > 8 || ring > 4095) return false;  // slot index ring (12 bits) is the +0.0 slot
     const int np = t.n_pos;
@@ -737,10 +737,10 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
     std::vector<std::vector<int>> ord_level(cs);  // per CTA: level of its k-th position
     for (int l = 0; l < t.n_levels; ++l) {
         const int a = t.level_ptr[l], b = t.level_ptr[l + 1];
-        const int per = stream_per(b - a, cs);
+        const int nch = (b - a) / 32, per = (nch + cs - 1) / cs;
         if (per * 32 > max_rows) return false;
         for (int p = a; p < b; ++p) {
-            const int r = ((p - a) / 32) / per;
+            const int r = ((p - a) / 32) / std::max(per, 1);
             owner[p] = r;
             ordinal[p] = count[r]++;
             ord_level[r].push_back(l);
@@ -758,17 +758,7 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
     const bool stats = std::getenv("SFV_STREAM_STATS") != nullptr;
     const int nthr = stats ? 1 : host_threads();
     std::atomic<bool> bad{false};
-    std::atomic<int> span{0};  // the largest level distance of a dependency
     auto body = [&](int c0, int c1) {  // chunk ranges
-    int span_local = 0;
-    struct Publish {
-        std::atomic<int>& g;
-        int& v;
-        ~Publish() {
-            int cur = g.load();
-            while (v > cur && !g.compare_exchange_weak(cur, v)) {}
-        }
-    } publish{span, span_local};
     for (int ch = c0; ch < c1 && !bad; ++ch) {
         unsigned char* cb = packed.data() + static_cast<size_t>(ch) * kChunkBytes;
         double* cval = reinterpret_cast<double*>(cb);
@@ -810,7 +800,6 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
             }
             cdep[k * 32 + l] = stream_dep(r, ordinal[q] % ring);
             cval[k * 32 + l] = t.ell_val[static_cast<size_t>(k) * np + p];
-            span_local = std::max(span_local, level_of[p] - level_of[q]);
             if (stats) {
                 ++n_dep;
                 if (r == owner[p]) ++n_local;
@@ -831,7 +820,6 @@ bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, 
         for (auto& x : th) x.join();
     }
     if (bad) return false;
-    if (span_out) *span_out = span.load();
     if (std::getenv("SFV_STREAM_STATS"))
         std::fprintf(stderr,
                      "stream records: %d positions, %d levels, %lld deps, %.1f%% in the reading CTA, %.1f%% from the "

@@ -104,9 +104,8 @@ struct StreamRecord {  // (the logical record; stored field-major per chunk, dev
 };
 static_assert(sizeof(StreamRecord) == 112, "record layout");
 // Built directly in the device chunk layout below (every byte written by the parallel pass).
-// span_out: the largest level distance between a position and one of its dependencies.
 bool build_stream_records(const TriSchedule& t, int cs, int ring, int max_rows, rawvec<unsigned char>& packed,
-                          const std::vector<int>* out_pos = nullptr, int* span_out = nullptr);
+                          const std::vector<int>* out_pos = nullptr);
 // Device layout of the records: per chunk of 32 positions (levels are padded to 32), the
 // fields as arrays over the 32 positions — val[8][32], diag[32], dep[8][32] (u32), own[32],
 // out[32], 3584 bytes (device.h kStream*) — so that a warp reading one field of 32 consecutive rows from shared

@@ -22,7 +22,6 @@
 // reader and that no level slice exceeds kMaxRows (build_stream_records); otherwise the
 // other sweeps in precond.cu are used.  Compiled with -fmad=false: bit-identical results.
 #include <cooperative_groups.h>
-#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -39,12 +38,6 @@ namespace cg = cooperative_groups;
 #define SFV_TS_PROBE 0
 #endif
 #define TSP(b) (!(SFV_TS_PROBE & (b)))
-#ifndef SFV_STREAM_PWAIT
-#define SFV_STREAM_PWAIT 1  // 0: every compute thread tests the stage's mbarrier itself
-#endif
-#ifndef SFV_STREAM_PFENCE
-#define SFV_STREAM_PFENCE 1
-#endif
 #ifndef SFV_DIV_CORR
 #define SFV_DIV_CORR 1  // 0: plain division in the U sweep
 #endif
@@ -126,7 +119,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     };
     auto slice = [&](int l, int& a, int& b) {  // this CTA's positions of level l
         const int la = lp[l - lbase], lb = lp[l - lbase + 1];
-        const int per = stream_per(lb - la, kStreamCluster);
+        const int nch = (lb - la) >> 5, per = (nch + kStreamCluster - 1) / kStreamCluster;
         a = min(lb, la + rank * per * 32);
         b = min(lb, a + per * 32);
     };
@@ -152,51 +145,23 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
     if (threadIdx.x == 0) *zero_slot = 0.0;
     if (threadIdx.x < NRHS) ring[threadIdx.x * ring_s + ring_n] = 0.0;
     stage_levels(0);  // its __syncthreads also publishes the mbarrier init
-    // Level ranges (device.h: CTA 0 owns every position of a solo level).  [0, A) and [B, n - 1)
-    // are runs of solo levels all of whose dependencies are CTA 0's too — the narrow wavefronts
-    // at both ends of a sweep: nothing crosses CTAs, so CTA 0 reads them with ld.shared and a level
-    // ends with a CTA barrier; the other CTAs pass through their empty slices and wait at the
-    // next cluster barrier.  [A, B) and the last level run the cluster-wide level below.
-    const int n_lv = t.n_levels;
-    const int A = t.solo_a < 0 ? 0 : t.solo_a, B = t.solo_a < 0 ? n_lv - 1 : t.solo_b;
     if (producer)
         for (int l = 0; l < kStages - 1; ++l) issue(l);
-#if SFV_STREAM_PWAIT
-    if (n_lv > 0) mbar_wait(mbar_base, 0u);  // level 0 (issued just above)
-    __syncthreads();
-#endif
-    long long ph[5] = {0, 0, 0, 0, 0}, pl[5] = {0, 0, 0, 0, 0}, t0 = 0, t1 = 0;  // (pl: solo levels)
-    (void)pl;
+    long long ph[5] = {0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
     (void)ph;
     (void)t0;
     (void)t1;
-    auto level = [&](const int l, auto local_tag) {
-        constexpr bool LOCAL = decltype(local_tag)::value;
+    for (int l = 0; l < t.n_levels; ++l) {
         if (!TSP(32)) t0 = clock64();
         if (l + kStages - 1 + 1 - lbase > kLvl) stage_levels(l);  // keep lp[] covering the issue window
         if (producer) {
             // stage (l - 1) % kStages was consumed before the barrier that ended level l - 1
             issue(l + kStages - 1);
-#if SFV_STREAM_PWAIT
-            // the producer, idle until the barrier, waits for the NEXT level's records: the barrier
-            // that ends this level then tells every thread they have landed (the TMA writes are in
-            // shared memory when the mbarrier completes), and no compute thread tests an mbarrier
-            if (l + 1 < n_lv) mbar_wait(mbar_base + 8u * ((l + 1) % kStages), static_cast<uint32_t>(((l + 1) / kStages) & 1));
-            // (as the compute threads do for the ring: CTA-scope fence, then the relaxed arrive)
-            if (!LOCAL && SFV_STREAM_PFENCE) asm volatile("fence.acq_rel.cta;" ::: "memory");
-#endif
-            if (!TSP(32)) {
-                t1 = clock64();
-                (LOCAL ? pl : ph)[0] += t1 - t0;
-                t0 = t1;
-            }
         } else {
-#if !SFV_STREAM_PWAIT
             mbar_wait(mbar_base + 8u * (l % kStages), static_cast<uint32_t>((l / kStages) & 1));
-#endif
             if (!TSP(32)) {
                 t1 = clock64();
-                (LOCAL ? pl : ph)[1] += t1 - t0;
+                ph[1] += t1 - t0;
                 t0 = t1;
             }
             const int s = l % kStages;
@@ -223,8 +188,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const uint32_t d = TSP(64) ? dep[q] : (dep[q] & 0xffffffu) | (static_cast<uint32_t>(rank) << 24);
-                    // (LOCAL: the owner byte is 0 = this CTA, the word is the byte offset in the ring)
-                    ad[q] = TSP(8) ? d + (LOCAL ? ring_base : ring_lo) : zero_addr;
+                    ad[q] = TSP(8) ? d + ring_lo : zero_addr;
                 }
                 double dv[8][NRHS];
 #pragma unroll
@@ -232,36 +196,20 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                     uint32_t a8[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) a8[q] = ad[q] + static_cast<uint32_t>(k * ring_s * 8);
-                    if constexpr (LOCAL)
-                        asm volatile(
-                            "ld.shared.f64 %0, [%8];\n\t"
-                            "ld.shared.f64 %1, [%9];\n\t"
-                            "ld.shared.f64 %2, [%10];\n\t"
-                            "ld.shared.f64 %3, [%11];\n\t"
-                            "ld.shared.f64 %4, [%12];\n\t"
-                            "ld.shared.f64 %5, [%13];\n\t"
-                            "ld.shared.f64 %6, [%14];\n\t"
-                            "ld.shared.f64 %7, [%15];"
-                            : "=d"(dv[0][k]), "=d"(dv[1][k]), "=d"(dv[2][k]), "=d"(dv[3][k]), "=d"(dv[4][k]),
-                              "=d"(dv[5][k]), "=d"(dv[6][k]), "=d"(dv[7][k])
-                            : "r"(a8[0]), "r"(a8[1]), "r"(a8[2]), "r"(a8[3]), "r"(a8[4]), "r"(a8[5]), "r"(a8[6]),
-                              "r"(a8[7])
-                            : "memory");
-                    else
-                        asm volatile(
-                            "ld.shared::cluster.f64 %0, [%8];\n\t"
-                            "ld.shared::cluster.f64 %1, [%9];\n\t"
-                            "ld.shared::cluster.f64 %2, [%10];\n\t"
-                            "ld.shared::cluster.f64 %3, [%11];\n\t"
-                            "ld.shared::cluster.f64 %4, [%12];\n\t"
-                            "ld.shared::cluster.f64 %5, [%13];\n\t"
-                            "ld.shared::cluster.f64 %6, [%14];\n\t"
-                            "ld.shared::cluster.f64 %7, [%15];"
-                            : "=d"(dv[0][k]), "=d"(dv[1][k]), "=d"(dv[2][k]), "=d"(dv[3][k]), "=d"(dv[4][k]),
-                              "=d"(dv[5][k]), "=d"(dv[6][k]), "=d"(dv[7][k])
-                            : "r"(a8[0]), "r"(a8[1]), "r"(a8[2]), "r"(a8[3]), "r"(a8[4]), "r"(a8[5]), "r"(a8[6]),
-                              "r"(a8[7])
-                            : "memory");
+                    asm volatile(
+                        "ld.shared::cluster.f64 %0, [%8];\n\t"
+                        "ld.shared::cluster.f64 %1, [%9];\n\t"
+                        "ld.shared::cluster.f64 %2, [%10];\n\t"
+                        "ld.shared::cluster.f64 %3, [%11];\n\t"
+                        "ld.shared::cluster.f64 %4, [%12];\n\t"
+                        "ld.shared::cluster.f64 %5, [%13];\n\t"
+                        "ld.shared::cluster.f64 %6, [%14];\n\t"
+                        "ld.shared::cluster.f64 %7, [%15];"
+                        : "=d"(dv[0][k]), "=d"(dv[1][k]), "=d"(dv[2][k]), "=d"(dv[3][k]), "=d"(dv[4][k]),
+                          "=d"(dv[5][k]), "=d"(dv[6][k]), "=d"(dv[7][k])
+                        : "r"(a8[0]), "r"(a8[1]), "r"(a8[2]), "r"(a8[3]), "r"(a8[4]), "r"(a8[5]), "r"(a8[6]),
+                          "r"(a8[7])
+                        : "memory");
                 }
                 // U: the pivot (read after the loads are out) and its reciprocal overlap their
                 // latency; z / dg is finished after them by one correction step (SFV_DIV_CORR)
@@ -307,16 +255,11 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
             }
             if (!TSP(32)) {
                 t1 = clock64();
-                (LOCAL ? pl : ph)[2] += t1 - t0;
+                ph[2] += t1 - t0;
                 t0 = t1;
             }
             // hand the level over: CTA-scope fence (the values live in this CTA's shared memory)
-            if (!LOCAL && TSP(1)) asm volatile("fence.acq_rel.cta;" ::: "memory");
-        }
-        if constexpr (LOCAL) {  // the next level reads only this CTA's values; the stage is consumed
-            __syncthreads();
-            if (!TSP(32)) pl[3] += clock64() - t0;
-            return;
+            if (TSP(1)) asm volatile("fence.acq_rel.cta;" ::: "memory");
         }
         asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
         if (!TSP(32)) {
@@ -329,23 +272,12 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
             t1 = clock64();
             ph[4] += t1 - t0;
         }
-    };
-    for (int l = 0; l < A; ++l) level(l, std::true_type{});
-    for (int l = A; l < B; ++l) level(l, std::false_type{});
-    for (int l = B; l < n_lv - 1; ++l) level(l, std::true_type{});
-    if (n_lv > 0) level(n_lv - 1, std::false_type{});  // (no CTA leaves while another may read its ring)
+    }
     if (!TSP(32) && (threadIdx.x == 0 || threadIdx.x == kThreads) && (rank == 0 || rank == 15))
         printf("tri_stream U=%d rank %d thr %d levels %d: stage-wait %lld rows %lld fence+arrive %lld "
                "barrier-wait %lld cycles/level\n",
                UPPER ? 1 : 0, rank, threadIdx.x, t.n_levels, ph[1] / t.n_levels, ph[2] / t.n_levels,
                ph[3] / t.n_levels, ph[4] / t.n_levels);
-    if (!TSP(32) && (threadIdx.x == 0 || threadIdx.x == kThreads) && (rank == 0 || rank == 15)) {
-        const int ns = max(1, A + max(0, n_lv - 1 - B)), nc = max(1, n_lv - ns);
-        printf("tri_stream U=%d rank %d thr %d: %d cluster levels: issue %lld stage-wait %lld rows %lld fence+arrive %lld "
-               "barrier-wait %lld | %d solo levels: issue %lld stage-wait %lld rows %lld cta-barrier %lld cycles/level\n",
-               UPPER ? 1 : 0, rank, threadIdx.x, nc, ph[0] / nc, ph[1] / nc, ph[2] / nc, ph[3] / nc, ph[4] / nc, ns,
-               pl[0] / ns, pl[1] / ns, pl[2] / ns, pl[3] / ns);
-    }
 }
 
 template <bool UPPER, int NRHS, int ST>

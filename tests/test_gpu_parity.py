@@ -717,3 +717,30 @@ def test_run_steps_oblique_symmetry_parity():
         assert len(a) == len(b) and all(abs(x - y) <= 1 for x, y in zip(a, b)), (_counts(rg), _counts(ro))
     u_g, u_o = fg.cpu().numpy()[0], fo[0]
     assert np.abs(u_g - u_o).max() <= 1e-8 * np.abs(u_o).max()
+
+
+def test_ilu_first_apply_after_setup_full_size(monkeypatch):
+    """C2 at 1M cells: the FIRST apply after each preconditioner setup (records cold in L2, so the
+    sweep really waits for its TMA stages) equals the sync-free sweep bit for bit, for device-built
+    and host-built records, several setups in a row.  (A sweep variant that passed every warm
+    repetition failed only here; scripts/probes/ilu_repeat.py is the longer soak.)"""
+    sv = _sv()
+    case = cases.config("c2")
+    mesh = case.mesh()
+    ev = sv.ResidualEvaluator(mesh, case.physics)
+    r = sv.to_device(cases.uniform(21, 3 * mesh.n_cells))
+    monkeypatch.setenv("SFV_HOST_PRECOND", "1")
+    monkeypatch.setenv("SFV_TRI_CLUSTER", "0")
+    pc = sv.make_preconditioner(ev, "ilu1")
+    assert pc.info()["sweep"] == 0
+    truth = pc.solve(r).cpu().numpy()
+    monkeypatch.delenv("SFV_TRI_CLUSTER")
+    for rnd in range(6):
+        for host in (False, True):
+            if host:
+                monkeypatch.setenv("SFV_HOST_PRECOND", "1")
+            else:
+                monkeypatch.delenv("SFV_HOST_PRECOND", raising=False)
+            pc = sv.make_preconditioner(ev, "ilu1")
+            assert pc.info()["sweep"] == 200
+            assert np.array_equal(pc.solve(r).cpu().numpy(), truth), (rnd, host)
