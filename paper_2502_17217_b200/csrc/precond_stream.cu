@@ -157,7 +157,13 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
         if (producer) {
             // stage (l - 1) % kStages was consumed before the barrier that ended level l - 1
             issue(l + kStages - 1);
+#ifdef SFV_STREAM_DELAY  // robustness probe: one CTA's producer arrives late at the level's barrier
+            if (SFV_STREAM_DELAY == 1 && rank == 5 && (l & 31) == 7) __nanosleep(4000);
+#endif
         } else {
+#ifdef SFV_STREAM_DELAY  // ... or one CTA's compute threads start their rows late
+            if (SFV_STREAM_DELAY == 2 && rank == 5 && (l & 31) == 7) __nanosleep(4000);
+#endif
             mbar_wait(mbar_base + 8u * (l % kStages), static_cast<uint32_t>((l / kStages) & 1));
             if (!TSP(32)) {
                 t1 = clock64();
