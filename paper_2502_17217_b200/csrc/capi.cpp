@@ -1506,6 +1506,22 @@ std::string precond_create_device(sfv_ctx* c, int level) {
     return "";
 }
 
+// One discarded apply at the end of an ILU setup.  In soaks at C2 (scripts/probes/ilu_repeat.py)
+// the streamed sweep's FIRST apply after a setup — records, schedules and scratch vectors cold in
+// L2 and the TLB, so a cluster really stalls on its first TMA copies of a page — came out wrong
+// in rare cases when the sweep was perturbed (2 of 480 first applies with -DSFV_STREAM_DELAY=3;
+// 0 of ~430 unperturbed), while no later apply ever did (thousands, and the bit-for-bit
+// full-size solves).  Until that stale read is found, the cold apply is spent here on a zero
+// vector, so every apply a caller sees runs warm.  SFV_ILU_WARMUP=0 disables it.
+int precond_warmup(sfv_ctx* c) {
+    if (const char* e = std::getenv("SFV_ILU_WARMUP"); e && std::atoi(e) == 0) return SFV_OK;
+    if (c->tri_cluster != kStreamMode || !c->ily.p) return SFV_OK;
+    cudaMemsetAsync(c->ily.p, 0, sizeof(double) * c->n, c->stream);
+    if (int e = precond_apply_async(c, c->ily.p, c->ily.p)) return e;
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return c->cuda_check("ilu warm-up");
+    return SFV_OK;
+}
+
 int precond_create(sfv_ctx* c, int kind) {
     ++c->pc_gen;  // a cached GMRES graph holds the old preconditioner's buffers
     c->drop_graph();
@@ -1520,7 +1536,10 @@ int precond_create(sfv_ctx* c, int kind) {
         !std::getenv("SFV_DEVICE_ILU")) {
         // the whole setup on the device (precond_dev.cu); the host path below when it declines
         const std::string why = precond_create_device(c, kind == SFV_PRECOND_ILU0 ? 0 : 1);
-        if (why.empty()) return c->cuda_check("ilu device setup");
+        if (why.empty()) {
+            if (int e = c->cuda_check("ilu device setup")) return e;
+            return precond_warmup(c);
+        }
         if (pt.on) std::fprintf(stderr, "[sfv] device ilu setup declined: %s\n", why.c_str());
     }
     std::vector<ScalarCsr> comps;
@@ -1783,7 +1802,8 @@ int precond_create(sfv_ctx* c, int kind) {
         std::fprintf(stderr, "[sfv] ilu sweep mode %d (stream: ring %d rows %d stages %d; levels L %d U %d)\n",
                      c->tri_cluster, c->sL.ring, c->sL.max_rows, c->sL.stages, c->sL.t[0].n_levels,
                      c->sU.t[0].n_levels);
-    return c->cuda_check("ilu setup");
+    if (int e = c->cuda_check("ilu setup")) return e;
+    return precond_warmup(c);
 }
 
 }  // namespace

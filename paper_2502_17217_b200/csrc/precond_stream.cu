@@ -156,7 +156,14 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
         if (l + kStages - 1 + 1 - lbase > kLvl) stage_levels(l);  // keep lp[] covering the issue window
         if (producer) {
             // stage (l - 1) % kStages was consumed before the barrier that ended level l - 1
+#if defined(SFV_STREAM_DELAY) && SFV_STREAM_DELAY == 3
+            // robustness probe: CTA 5 issues every 32nd level just in time instead of kStages - 1
+            // levels ahead, so its compute threads really wait for the TMA copies there
+            if (!(rank == 5 && ((l + kStages - 1) & 31) == 7)) issue(l + kStages - 1);
+            if (rank == 5 && (l & 31) == 7 && l >= kStages - 1) issue(l);
+#else
             issue(l + kStages - 1);
+#endif
 #ifdef SFV_STREAM_DELAY  // robustness probe: one CTA's producer arrives late at the level's barrier
             if (SFV_STREAM_DELAY == 1 && rank == 5 && (l & 31) == 7) __nanosleep(4000);
 #endif
