@@ -38,6 +38,11 @@ namespace cg = cooperative_groups;
 #define SFV_TS_PROBE 0
 #endif
 #define TSP(b) (!(SFV_TS_PROBE & (b)))
+// hand-over experiments (soak only): 1: cluster-scope fence before the arrive, 2: a
+// fence.proxy.async after the rows, 4: the slice recomputed instead of read from the stage header
+#ifndef SFV_STREAM_FIX
+#define SFV_STREAM_FIX 0
+#endif
 #ifndef SFV_DIV_CORR
 #define SFV_DIV_CORR 1  // 0: plain division in the U sweep
 #endif
@@ -82,7 +87,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
 // The per-level critical path is: wait stage -> rows -> cluster barrier.
 template <bool UPPER, int NRHS, int kStages>
 __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet set, const double* __restrict__ src,
-                                                                      double* __restrict__ dst) {
+                                                                      double* __restrict__ dst
+#if defined(SFV_STREAM_DELAY) && SFV_STREAM_DELAY >= 4
+                                                                      ,
+                                                                      double* tlb_probe  // cold pages, 2 MB apart
+#endif
+) {
     const int kMaxRows = set.max_rows;  // rows per CTA per level (stage stride)
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = static_cast<int>(cluster.block_rank());
@@ -161,6 +171,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
             // levels ahead, so its compute threads really wait for the TMA copies there
             if (!(rank == 5 && ((l + kStages - 1) & 31) == 7)) issue(l + kStages - 1);
             if (rank == 5 && (l & 31) == 7 && l >= kStages - 1) issue(l);
+#elif defined(SFV_STREAM_DELAY) && SFV_STREAM_DELAY == 6
+            // ... every CTA, every 8th level
+            if (((l + kStages - 1) & 7) != 7) issue(l + kStages - 1);
+            if ((l & 7) == 7 && l >= kStages - 1) issue(l);
 #else
             issue(l + kStages - 1);
 #endif
@@ -178,7 +192,12 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 t0 = t1;
             }
             const int s = l % kStages;
-            const int2 hd = stage_hdr[s];
+            int2 hd = stage_hdr[s];
+            if (SFV_STREAM_FIX & 4) {
+                int sa, sb;
+                slice(l, sa, sb);
+                hd = make_int2(sa, sb - sa);
+            }
             const int a = hd.x, b = hd.x + hd.y;
             for (int j = threadIdx.x; TSP(16) && j < b - a; j += kThreads) {
                 const unsigned char* ch = stage_rec + static_cast<size_t>(s) * kMaxRows * kRec + (j / 32) * kChunk;
@@ -260,11 +279,24 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 // the backward sweep's position (forward) or the row (backward): no permute /
                 // scatter pass after the sweep
                 const int oi = reinterpret_cast<const int*>(ch + kOffOutIdx)[ln];
+#if defined(SFV_STREAM_DELAY) && SFV_STREAM_DELAY >= 4
+                // robustness probe: one thread of CTA 5 stores to a page nobody has touched (a TLB
+                // miss in flight) just before the level's ring stores (4) or just after them (5)
+                // (7: warp 0 of every CTA, every 4th level, one page per lane)
+                const bool cold_store = SFV_STREAM_DELAY == 7 ? j < 32 && (l & 3) == 3 : rank == 5 && j == 0 && (l & 7) == 3;
+                double* cold = SFV_STREAM_DELAY == 7
+                                   ? tlb_probe + ((static_cast<size_t>(l >> 2) * 48 + comp * 16 + rank) * 32 + j) % (size_t(40) * 288) * (1u << 18)
+                                   : tlb_probe + (static_cast<size_t>(comp) * 96 + (l >> 3)) * (1u << 18);
+                if ((SFV_STREAM_DELAY == 4 || SFV_STREAM_DELAY == 7) && cold_store) *cold = z[0];
+#endif
 #pragma unroll
                 for (int k = 0; k < NRHS; ++k) {
                     ring[k * ring_s + own] = z[k];
                     if (TSP(2) && oi >= 0) dst[3 * static_cast<size_t>(oi) + comp + k] = z[k];
                 }
+#if defined(SFV_STREAM_DELAY) && SFV_STREAM_DELAY >= 4
+                if (SFV_STREAM_DELAY == 5 && cold_store) *cold = z[0];
+#endif
             }
             if (!TSP(32)) {
                 t1 = clock64();
@@ -272,7 +304,9 @@ __global__ void __launch_bounds__(kThreads + 32, 1) tri_stream_kernel(StreamSet 
                 t0 = t1;
             }
             // hand the level over: CTA-scope fence (the values live in this CTA's shared memory)
-            if (TSP(1)) asm volatile("fence.acq_rel.cta;" ::: "memory");
+            if (SFV_STREAM_FIX & 2) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (SFV_STREAM_FIX & 1) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            else if (TSP(1)) asm volatile("fence.acq_rel.cta;" ::: "memory");
         }
         asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
         if (!TSP(32)) {
@@ -311,7 +345,19 @@ cudaError_t launch_st(const StreamSet& set, int ncomp, const double* src, double
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+#if defined(SFV_STREAM_DELAY) && SFV_STREAM_DELAY >= 4
+    // 24 GB never written before: every launch gets its own 3 x 96 pages of 2 MB
+    static double* probe = [] {
+        double* p = nullptr;
+        cudaMalloc(&p, size_t(24) << 30);
+        return p;
+    }();
+    static size_t launch = 0;
+    double* mine = SFV_STREAM_DELAY == 7 ? probe : probe + (launch++ % 40) * 3 * 96 * (size_t(1) << 18);
+    return cudaLaunchKernelEx(&cfg, kern, set, src, dst, mine);
+#else
     return cudaLaunchKernelEx(&cfg, kern, set, src, dst);
+#endif
 }
 
 template <bool UPPER, int NRHS>
