@@ -72,6 +72,9 @@ __device__ __forceinline__ dm3 ldG(const double* __restrict__ r) {
 #ifndef SFV_HOOKE_CTAS
 #define SFV_HOOKE_CTAS 4  // resident 6-warp CTAs per SM the Hooke face pass is compiled for
 #endif
+#ifndef SFV_OWN_ASYNC
+#define SFV_OWN_ASYNC 0  // 1: a tile's own [w | G] records staged in shared memory (measured slower on hexes)
+#endif
 #ifndef SFV_GEN_CTAS
 #define SFV_GEN_CTAS 2  // resident 6-warp CTAs per SM the non-Hooke / TL face pass is compiled for
 #endif
@@ -521,8 +524,20 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
     __shared__ double res_buf[2][S][6][kCells];
     // slot kinds lane-major, 8 bytes per cell: the summing thread reads them in one 64-bit load
     __shared__ __align__(8) unsigned char kind_buf[2][kCells][8];
+    // Hooke: the tile's own [w | G] records — one contiguous 3072-byte block of the tiled table —
+    // are copied to shared memory one tile ahead (cp.async.cg, 16 bytes per thread, past L1), so
+    // the six slot warps read them from there instead of gathering them six times through L1
+    constexpr bool OWN = !GEN && SFV_OWN_ASYNC;
+    __shared__ __align__(16) double own_buf[OWN ? 2 : 1][OWN ? kWG : 1][kCells];
     const int lane = threadIdx.x % kCells, s = threadIdx.x / kCells;
     const int ntiles = tile1;  // this launch covers tiles [tile0, tile1) (the host-buffer J.v runs chunks)
+    auto stage_own = [&](int t, int b) {
+        if (!OWN || t >= ntiles) return;
+        const char* src = reinterpret_cast<const char*>(wg + static_cast<size_t>(t) * (kWG * kCells));
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&own_buf[b][0][0]));
+        for (int x = threadIdx.x; x < kWG * kCells / 2; x += kCells * S)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * x), "l"(src + 16 * x) : "memory");
+    };
     // Persistent grid-stride loop over tiles of kCells cells (= the tiles of the tables).
     // The slot indices of a tile and the epilogue operand r_u of (component s, cell) —
     // threads s < 3 do the per-cell sums — are loaded one iteration ahead, so a tile's
@@ -543,15 +558,24 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
     double ru_next;
     fetch(tile0 + blockIdx.x, fr_next, o_next, ru_next);
     wait_predecessor();  // bres (and through it G, w, eps)
+    if (OWN) {
+        stage_own(tile0 + blockIdx.x, 0);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    }
     const double eps = PERT ? *eps_p : 0.0;
     const bool zero = PERT && eps == 0.0;  // |v| = 0 short-circuit (nonlinear.cpp:110)
     int it = 0;
     for (int tile = tile0 + blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         double(*res)[6][kCells] = res_buf[it & 1];
         unsigned char(*kind)[8] = kind_buf[it & 1];
+        const double(*own)[kCells] = own_buf[OWN ? it & 1 : 0];
+        (void)own;
         const int fr = fr_next, o = o_next;
         const double ru = ru_next;
         fetch(tile + gridDim.x, fr_next, o_next, ru_next);
+        // buffer (it + 1) & 1 was last read in iteration it - 1, before that iteration's barrier
+        stage_own(tile + gridDim.x, (it + 1) & 1);
         const int c = tile * kCells + lane;
         unsigned char kd = 0;
         if (fr != -1 && !zero) {
@@ -565,13 +589,29 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
                 const double* rn = wg_rec(wg, in);
                 const d3 gam = ld3(rf), del = ld3(rf + 96);
                 const double cfac = rf[192], gmag = rf[224], wf = rf[256];
-                const d3 up = ld3(rp), un = ld3(rn);
-                if (!GEN) {
+                if (OWN) {
+                    // the other cell's record gathered, this cell's from the staged tile
+                    const double* rx = wg_rec(wg, o);
+                    const d3 ux = ld3(rx);
+                    double gx[9], gp[9], gn[9];
+                    ldg9(rx, gx);
+                    const d3 uo = {own[0][lane], own[1][lane], own[2][lane]};
+                    const d3 up = nb ? ux : uo, un = nb ? uo : ux;
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) {
+                        const double go = own[3 + q][lane];
+                        gp[q] = nb ? gx[q] : go;
+                        gn[q] = nb ? go : gx[q];
+                    }
+                    hooke_face(gp, gn, wf, ph.mu, ph.lam, gam, del, up, un, cfac, gmag, ph.alpha, ph.kbar, flux, st);
+                } else if (!GEN) {
+                    const d3 up = ld3(rp), un = ld3(rn);
                     double gp[9], gn[9];
                     ldg9(rp, gp);
                     ldg9(rn, gn);
                     hooke_face(gp, gn, wf, ph.mu, ph.lam, gam, del, up, un, cfac, gmag, ph.alpha, ph.kbar, flux, st);
                 } else {
+                    const d3 up = ld3(rp), un = ld3(rn);
                     const dm3 gp = ldG(rp), gn = ldG(rn);
                     const dm3 sp = ld_sig(sig + tiled(ip, kSig)), sn = ld_sig(sig + tiled(in, kSig));
                     d3 gm = gam;
@@ -606,8 +646,16 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
                     kd = 1;
                 } else {
                     const double* rc = wg_rec(wg, c);
-                    const dm3 gc = ldG(rc);
-                    const d3 uc = ld3(rc);
+                    dm3 gc;
+                    d3 uc;
+                    if (OWN) {
+#pragma unroll
+                        for (int q = 0; q < 9; ++q) gc.a[q / 3][q % 3] = own[3 + q][lane];
+                        uc = {own[0][lane], own[1][lane], own[2][lane]};
+                    } else {
+                        gc = ldG(rc);
+                        uc = ld3(rc);
+                    }
                     flux = dot_left(ld3(rf), hooke(gc, ph.mu, ph.lam));
                     const d3 compact = scl(sub(bc, uc), rf[192]);
                     st = scl(sub(compact, dot_left(ld3(rf + 96), gc)), ph.alpha * ph.kbar * gmag);
@@ -630,6 +678,7 @@ __global__ void __launch_bounds__(kCells* S, GEN ? SFV_GEN_CTAS * 6 / S : SFV_HO
             res[s][5][lane] = st.z;
         }
         kind[lane][s] = kd;
+        if (OWN) asm volatile("cp.async.wait_all;" ::: "memory");  // the next tile's records (issued a tile ago)
         __syncthreads();
         // (component k = s, cell c): the reference's per-cell summation order
         if (s < 3 && c < m.nc) {
